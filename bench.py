@@ -1,0 +1,297 @@
+"""GridShift hot-path benchmark (driver contract).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+
+A step = one engine.run over one batch of the workload's synthetic input.
+`value` is whole-job points/s with the points already resident in HBM (device outputs);
+`e2e` is the same metric through the C-ABI with pinned HOST buffers, the H2D copy of the
+points and the D2H copy of the labels inside the timed region.  Each timed step is bracketed
+by CUDA events on the engine's stream; the L2 is flushed (512 MiB write) before every step.
+Under torchrun each rank clusters its own independent image(s) (frame sharding, no
+collective on the data path) and the time is the max over ranks.
+`--impl reference` times the CPU oracle (the reference algorithm restated, oracle/) on all
+host threads instead, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("active-cell updates/sec (cells×iters/s) + end-to-end points/sec; "
+          "% HBM roofline")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [r for r in rows if r[6].isdigit() and int(r[6]) > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(int(r[0]) for r in busy),
+                "sm_max_mhz": max(int(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(busy)}
+
+
+def workload_input(name: str, rank: int):
+    from paper_2206_02200_b200 import configs as CF
+    cfg = CF.CONFIGS[name]
+    if name == "cfg2":   # each rank its own independent image (seeded per rank)
+        X = CF.voronoi_rgb(seed=2208 + 1000 * rank)[None]
+    elif name == "cfg4":
+        X = CF.generate("cfg4", frames=cfg.batch, frame0=rank * cfg.batch)
+    else:
+        X = CF.generate(name)
+    return cfg, X
+
+
+def cpu_baseline(name: str, X: np.ndarray, h: float, max_iter: int, budget_s: float = 10.0):
+    """The oracle (SPEC-literal build) on one host core over a bounded sample of the workload."""
+    from oracle import oracle as O
+    frames = X.shape[0]
+    times, pts = [], 0
+    t_end = time.perf_counter() + budget_s
+    f = 0
+    while True:
+        x = np.ascontiguousarray(X[f % frames], np.float64)
+        t0 = time.perf_counter()
+        O.run(x, h, max_iter, O.BUILD_SPEC)
+        times.append(time.perf_counter() - t0)
+        pts += x.shape[0]
+        f += 1
+        if time.perf_counter() > t_end:
+            break
+    return {"value": pts / sum(times), "unit": "points/s", "cores": 1, "kind": "port",
+            "sample": f"{f} oracle runs of {name} frames ({pts} points, {sum(times):.1f} s, "
+                      f"SPEC-literal build, 1 thread)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on all host threads, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2206_02200_b200 import configs as CF
+    cfg, X = workload_input(args.workload, 0)
+    threads = os.cpu_count() or 1
+    x0 = np.ascontiguousarray(X[0], np.float64)
+    n = x0.shape[0]
+
+    def one(_):
+        O.run(x0, cfg.h, cfg.max_iter, O.BUILD_SPEC)
+
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(threads)
+    step_times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        list(pool.map(one, range(threads)))
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            step_times.append(dt)
+    total = sum(step_times)
+    value = threads * n * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "n": n, "d": cfg.d, "h": cfg.h,
+                   "max_iter": cfg.max_iter, "batch": 1},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": f"per step {threads} concurrent independent oracle runs of "
+                                   f"one {args.workload} frame (SPEC-literal build)"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2206_02200_b200 import gridshift as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    eng = G.Engine(local, stream.cuda_stream)
+
+    cfg, X = workload_input(args.workload, rank)
+    B, n, d = X.shape
+    dt = G.GS_F32 if X.dtype == np.float32 else G.GS_F64
+    econf = G.EngineConfig(cfg.h, cfg.max_iter)
+    X_host = torch.from_numpy(X).pin_memory()
+    X_dev = X_host.to(dev)
+    labels_dev = torch.empty((B, n), dtype=torch.int32, device=dev)
+    labels_host = torch.empty((B, n), dtype=torch.int32).pin_memory()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step(device_resident: bool):
+        if device_resident:
+            eng.run_raw(X_dev.data_ptr(), n, d, dt, B, True, econf, labels_dev.data_ptr(),
+                        device_outputs=True)
+        else:
+            eng.run_raw(X_host.data_ptr(), n, d, dt, B, False, econf, labels_host.data_ptr())
+
+    def timed(device_resident: bool, steps: int):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        stats = []
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for s in range(steps):
+            flush.zero_()
+            ev[s][0].record(stream)
+            step(device_resident)
+            ev[s][1].record(stream)
+            stats.append(eng.stats())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = [a.elapsed_time(b) for a, b in ev]
+        return ms, stats
+
+    for _ in range(args.warmup):
+        step(True)
+        step(False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_dev, st_dev = timed(True, args.steps)
+    ms_e2e, st_e2e = timed(False, args.steps)
+    clk = clocks.stop()
+
+    tot_dev, tot_e2e = sum(ms_dev), sum(ms_e2e)
+    if world > 1:
+        t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_dev, tot_e2e = t.tolist()
+    pts_all = world * B * n * args.steps
+    value = pts_all / (tot_dev / 1e3)
+    e2e = pts_all / (tot_e2e / 1e3)
+    # cells x iterations (Σ m_t) per second over the iteration phase
+    s0 = st_dev[-1]
+    cells = sum(s["cells_swept"] for s in st_dev)
+    it_ms = sum(s["ms_iterate"] for s in st_dev)
+    launches = int(np.median([s["kernel_launches"] for s in st_dev]))
+    lib_calls = int(np.median([s["lib_calls"] for s in st_dev]))
+
+    # roofline of the n-scale binning kernel K2: algorithmic bytes = points read + slot write
+    peak, peak_kind = peaks()
+    s_in = 4 if dt == G.GS_F32 else 8
+    kbin_ms = float(np.mean([s["ms_k_bin"] for s in st_dev]))
+    kbin_bytes = B * n * (d * s_in + 4)
+    kbin_gbs = kbin_bytes / (kbin_ms / 1e3) / 1e9
+    phase = {k: float(np.mean([s[k] for s in st_dev]))
+             for k in ("ms_bin", "ms_iterate", "ms_label", "ms_k_bin", "ms_k_label")}
+    dominant = max(("binning phase (K1+K2+K3)", phase["ms_bin"]),
+                   ("iteration phase (K4+K5)", phase["ms_iterate"]),
+                   ("label phase (K7)", phase["ms_label"]), key=lambda x: x[1])[0]
+    out = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "desc": cfg.desc, "n": n, "d": d, "batch": B,
+                   "h": cfg.h, "max_iter": cfg.max_iter, "input_dtype": "f32" if s_in == 4 else "f64",
+                   "l2": "flushed (512 MiB write) before every timed step",
+                   "parallelism": f"frames x{world} (independent images per rank)"},
+        "cell_updates_per_s": cells / (it_ms / 1e3) if it_ms > 0 else None,
+        "cells_swept_per_step": s0["cells_swept"], "m0": s0["m0"], "k": s0["k_total"],
+        "iterations": s0["max_iterations"],
+        "phase_ms": phase, "dominant_phase": dominant,
+        "roofline": {"kernel": "k_bin (K2 binning)", "bound": "hbm", "achieved": kbin_gbs,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": kbin_gbs / peak, "traffic": None,
+                     "algorithmic_bytes": kbin_bytes},
+        "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
+                "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},
+        "gpu_launches": launches, "lib_calls": lib_calls,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload, X, cfg.h, cfg.max_iter, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(out))
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,149 @@
+/* gridshift_c.h — C-ABI of the B200-native GridShift engine (libgridshift_cuda.so).
+ *
+ * Drop-in boundary for the reference's engine API.  The reference exposes no FFI: its
+ * boundary is the C++ library call
+ *     gridshift::ClusterLabeling gridshift::run(const Dataset&, const EngineConfig&)
+ * specified at /root/reference/SPEC.md:135-143 (types SPEC.md:107-114, errors
+ * /root/reference/proj/include/gridshift/errors.hpp:9-72).  Each entry point below names the
+ * SPEC operation it replaces.  Only C types cross this boundary; the C++ wrapper
+ * (include/gridshift/gridshift.hpp) keeps the SPEC signature and rethrows status codes as the
+ * errors.hpp exception types.  The engine runs on an sm_100a GPU; there is no CPU fallback
+ * (a missing device is GS_E_NO_DEVICE, never a silent host path).
+ *
+ * Ownership: inputs are borrowed for the duration of the call; outputs go into caller buffers.
+ * Threading: a gs_ctx is not thread-safe; distinct contexts may run concurrently
+ * ("independent runs ... fully isolated state").
+ */
+#ifndef GRIDSHIFT_C_H_
+#define GRIDSHIFT_C_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_MAX_DIM 12 /* SPEC.md:96 documented limit d <= 12 */
+
+/* Status codes map 1:1 onto errors.hpp (see gridshift::throw_for_status). */
+typedef enum {
+  GS_OK = 0,
+  GS_E_INVALID_INPUT = 1,      /* InvalidInputError: non-finite coordinate  */
+  GS_E_INVALID_BANDWIDTH = 2,  /* InvalidBandwidthError: h <= 0 or non-finite     */
+  GS_E_EMPTY_INPUT = 3,        /* EmptyInputError: n == 0                         */
+  GS_E_INVALID_PARAMETER = 4,  /* InvalidParameterError: d, batch, max_iter, dtype out of range */
+  GS_E_INTERNAL_INVARIANT = 5, /* InternalInvariantError: partition/merge invariant broken      */
+  GS_E_KEY_RANGE = 6,          /* InvalidParameterError: key box exceeds the dense cell grid   */
+  GS_E_CUDA = 7,               /* Error: CUDA runtime failure                                   */
+  GS_E_OOM = 8,                /* Error: device allocation failed                               */
+  GS_E_NCCL = 9,               /* Error: collective failure (multi-GPU driver)                  */
+  GS_E_NO_DEVICE = 10          /* Error: no sm_100 device visible                               */
+} gs_status;
+
+typedef enum { GS_F32 = 0, GS_F64 = 1 } gs_dtype;
+
+/* A dataset: `batch` independent frames of n points each, d coordinates,
+ * row-major [batch][n][d].  Frames are clustered independently.  With
+ * on_device != 0, `points` is a device pointer on the context's device. */
+typedef struct {
+  const void* points;
+  int64_t n;      /* points per frame, >= 1 */
+  int32_t d;      /* 1 .. GS_MAX_DIM */
+  int32_t dtype;  /* gs_dtype */
+  int64_t batch;  /* frames, >= 1 */
+  int32_t on_device;
+  int32_t reserved;
+} gs_input;
+
+#define GS_RECORD_HISTORY 0x1u  /* keep per-iteration (m, max displacement)   */
+#define GS_DEVICE_OUTPUTS 0x2u  /* result.labels is a device pointer                          */
+
+/* EngineConfig. */
+typedef struct {
+  double h;          /* bandwidth = cell side, > 0 */
+  int32_t max_iter;  /* >= 1; SPEC default 1000 */
+  uint32_t flags;
+} gs_config;
+
+/* ClusterLabeling, per frame.  Caller-owned buffers:
+ *   labels      batch*n cluster ids; id = lexicographic rank of the final cell
+ *   k           batch entries: clusters per frame
+ *   iterations  batch entries: completed shift iterations (do-while, >= 1)
+ *   converged   batch entries: 0 = max_iter reached (warning, not an error) */
+typedef struct {
+  int32_t* labels;
+  int64_t* k;
+  int32_t* iterations;
+  int32_t* converged;
+} gs_result;
+
+typedef struct gs_ctx gs_ctx;
+
+/* Host-only argument validation with the same codes gs_run returns (no device needed). */
+gs_status gs_validate(const gs_input* in, const gs_config* cfg);
+
+/* Create an engine context on `device`; cuda_stream is a cudaStream_t (NULL = own stream). */
+gs_status gs_create(int device, void* cuda_stream, gs_ctx** out);
+void gs_destroy(gs_ctx* ctx);
+
+/* engine.run over every frame of `in`.  Synchronous w.r.t. the caller:
+ * on return the result buffers are filled. */
+gs_status gs_run(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out);
+
+/* Cluster centroids of `frame` from the last gs_run: k x d fp64 in cluster-id order. */
+gs_status gs_get_centroids(gs_ctx* ctx, int64_t frame, double* out, int64_t cap_k);
+
+/* History of `frame` from the last gs_run (needs GS_RECORD_HISTORY): m_t = active cells
+ * entering iteration t, maxdisp_t = max Euclidean sweep displacement.  Writes min(cap, iters). */
+gs_status gs_get_history(gs_ctx* ctx, int64_t frame, int64_t* m_t, double* maxdisp_t,
+                         int32_t cap);
+
+/* Per-run counters of the last gs_run (device-timed with CUDA events on the ctx stream). */
+typedef struct {
+  double ms_total;       /* first kernel to last kernel (device-resident input/outputs)   */
+  double ms_bin;         /* bounds + binning + compaction (n-scale)                        */
+  double ms_iterate;     /* the iteration phase (all iterations)                           */
+  double ms_label;       /* label propagation (n-scale)                                    */
+  double ms_h2d;         /* host->device copy of the points (0 when on_device)             */
+  double ms_d2h;         /* device->host copy of the labels (0 with GS_DEVICE_OUTPUTS)     */
+  int64_t cells_swept;   /* sum over frames and iterations of active cells (Σ m_t)         */
+  int64_t m0;            /* initial active cells (all frames)                              */
+  int64_t k_total;       /* final cells (all frames)                                       */
+  int64_t kernel_launches;
+  int32_t max_iterations;/* max over frames                                                */
+  int32_t fixed_shift;   /* F of the fixed-point cell sums                                 */
+  int64_t dense_cells;   /* size of the dense cell grid (all frames)                       */
+  double ms_k_bin;       /* the binning kernel K2 alone                                     */
+  double ms_k_label;     /* the label kernel K7 alone                                       */
+  int64_t lib_calls;     /* library (CUB) device calls, not counted in kernel_launches      */
+} gs_stats;
+gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out);
+
+const char* gs_last_error(const gs_ctx* ctx); /* valid until the next call on ctx */
+const char* gs_status_string(gs_status s);
+
+/* ---- test hooks (parity harness; not needed by callers) ---- */
+
+/* build_active_grid only on one frame: m0 cells in lex order.
+ * keys m0*d int64, counts m0, centroids m0*d, slot n (cell rank of each point). */
+gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_m,
+                         int64_t* m_out, int64_t* keys, int64_t* counts, double* centroids,
+                         int64_t* slot);
+
+/* One iterate_once on an injected lex-sorted state; outputs mirror
+ * oracle gso_iterate_once: new state, post-sweep centroids, parent ranks, flags. */
+gs_status gs_debug_iterate_once(gs_ctx* ctx, int32_t d, double h, int64_t m,
+                                const int64_t* keys, const int64_t* counts,
+                                const double* centroids, int64_t* m_out, int64_t* keys_out,
+                                int64_t* counts_out, double* centroids_out, double* swept_out,
+                                int64_t* parent_out, int32_t* changed_out,
+                                int32_t* converged_out, double* maxdisp_out);
+
+/* The fixed-point exponent F used for the binning sums of a frame of n points at bandwidth h. */
+int32_t gs_fixed_shift(int64_t n, double h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDSHIFT_C_H_ */

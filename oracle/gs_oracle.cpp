@@ -1,0 +1,449 @@
+// gs_oracle.cpp — CPU ORACLE for the GridShift hot path.  TEST INFRASTRUCTURE ONLY.
+//
+// This file is the parity checker, never the product: only tests/, __graft_entry__.smoke()
+// and bench.py's cpu_baseline / --impl reference legs may load liboracle.  The product
+// path (libgridshift_cuda.so) has no CPU fallback and never links this file.
+//
+// It restates, line by line, the reference specification of the path:
+//   grid-core  /root/reference/SPEC.md:17-100   (grid_index, neighborhood,
+//              build_active_grid, merge_into, invariants :77-81, ledger :83-87)
+//   engine     /root/reference/SPEC.md:102-181  (iterate_once :117-125, has_converged
+//              :126-134, run :135-143, ledger :161-167)
+//   Alg. 1     /root/reference/PAPER.md:83-118 read through SPEC's typo fixes SPEC.md:163-164,
+//              Eq. (3)-(5) PAPER.md:68-78, :124-130.
+// The reference ships no implementation code, so there is no `oracle/_ref`:
+// this restatement is pinned against every known-answer example the SPEC holds
+// (tests/golden/spec_kats.json, tests/test_oracle_kat.py).
+//
+// Pins the SPEC leaves open (DESIGN.md §"Oracle pins"):
+//   P1 grid_index is floor(RN(x/h)) with IEEE division, never x*(1/h)
+//   P2 sweep sum: num = 0.0; for v in lex order: num = num + (double)C'*S'; S = num/(double)ΣC'
+//      (no FMA: build with -ffp-contract=off)                                  SPEC.md:120(c), :52
+//   P3 a cell with no active neighbour other than itself keeps its centroid bit-for-bit
+//                                                                              SPEC.md:124
+//   P4 merge (Eq. 3) folded in visit order: s = ((double)c*s + (double)C'*S') / (double)(c+C')
+//                                                                              SPEC.md:70, :75
+//   P5 do-while loop: >= 1 iteration; exit on has_converged || !changed || iters == max_iter
+//                                                                              SPEC.md:138, :141, :164
+//   P6 build mode 0 ("spec"): incremental mean in point order (Alg. 1 line 5).
+//      build mode 1 ("fixed"): the GPU engine's deterministic fixed-point cell sums
+//      (DESIGN.md §"Fixed-point binning"); every later step is identical in both modes.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+constexpr int kMaxD = 12;  // SPEC.md:96 documented limit d <= 12
+
+// Status codes shared with include/gridshift_c.h (gs_status).
+enum {
+  OK = 0,
+  E_INVALID_INPUT = 1,
+  E_INVALID_BANDWIDTH = 2,
+  E_EMPTY_INPUT = 3,
+  E_INVALID_PARAMETER = 4,
+  E_INTERNAL_INVARIANT = 5,
+};
+
+using Key = std::array<int64_t, kMaxD>;  // GridIndex; unused tail is zero
+
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (int i = 0; i < kMaxD; ++i) {
+      h ^= (uint64_t)k[i] + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    }
+    return (size_t)h;
+  }
+};
+
+// CellRecord: centroid, count, member set.
+struct Cell {
+  Key key;
+  double c[kMaxD];
+  int64_t count;
+  std::vector<int64_t> members;
+};
+
+// grid_index: floor toward -inf of the IEEE quotient (pin P1).
+inline int64_t grid_coord(double x, double h) { return (int64_t)std::floor(x / h); }
+
+// Fixed-point scale exponent for build mode 1: |sum of offsets * 2^F| < 2^61 for any cell
+// of at most n points (offsets lie in [~0, h]).  Mirrors gs_fixed_shift() in the CUDA engine.
+int fixed_shift(int64_t n, double h) {
+  int ln = 0;
+  while ((int64_t(1) << ln) < n) ++ln;            // ceil(log2(n))
+  int eh = std::ilogb(h) + 1;                      // h < 2^eh
+  int F = 61 - ln - eh;
+  if (F > 1000) F = 1000;
+  if (F < -1000) F = -1000;
+  return F;
+}
+
+struct Engine {
+  int d;
+  double h;
+  std::vector<Cell> cells;  // kept sorted lexicographically by key between iterations
+
+  // neighborhood: the 3^d offsets in lexicographic order of v.
+  static std::vector<std::array<int8_t, kMaxD>> offsets(int d) {
+    std::vector<std::array<int8_t, kMaxD>> out;
+    int64_t total = 1;
+    for (int i = 0; i < d; ++i) total *= 3;
+    for (int64_t t = 0; t < total; ++t) {
+      std::array<int8_t, kMaxD> v{};
+      int64_t r = t;
+      for (int i = d - 1; i >= 0; --i) {  // dim 0 is the most significant digit
+        v[i] = (int8_t)(r % 3) - 1;
+        r /= 3;
+      }
+      out.push_back(v);
+    }
+    return out;
+  }
+
+  void sort_cells() {
+    std::sort(cells.begin(), cells.end(),
+              [](const Cell& a, const Cell& b) { return a.key < b.key; });
+  }
+
+  // build_active_grid.
+  int build(const double* X, int64_t n, int mode, int64_t* slot_out) {
+    std::unordered_map<Key, int64_t, KeyHash> index;
+    index.reserve((size_t)std::min<int64_t>(n, 1 << 22));
+    std::vector<int64_t> cell_of(n);
+    int F = fixed_shift(n, h);
+    double scale = std::ldexp(1.0, F);
+    std::vector<std::array<int64_t, kMaxD>> qsum;
+    for (int64_t i = 0; i < n; ++i) {
+      Key k{};
+      const double* x = X + i * d;
+      for (int c = 0; c < d; ++c) {
+        if (!std::isfinite(x[c])) return E_INVALID_INPUT;
+        k[c] = grid_coord(x[c], h);
+      }
+      auto it = index.find(k);
+      int64_t ci;
+      if (it == index.end()) {
+        ci = (int64_t)cells.size();
+        index.emplace(k, ci);
+        Cell cell;
+        cell.key = k;
+        for (int c = 0; c < d; ++c) cell.c[c] = x[c];  // Alg. 1 lines 8-10
+        cell.count = 1;
+        cells.push_back(std::move(cell));
+        qsum.push_back({});
+      } else {
+        ci = it->second;
+        Cell& cell = cells[ci];
+        for (int c = 0; c < d; ++c)  // Alg. 1 line 5: S <- (C*S + x)/(C+1)
+          cell.c[c] = ((double)cell.count * cell.c[c] + x[c]) / (double)(cell.count + 1);
+        cell.count += 1;
+      }
+      cells[ci].members.push_back(i);
+      cell_of[i] = ci;
+      if (mode == 1) {
+        for (int c = 0; c < d; ++c) {
+          double base = (double)k[c] * h;
+          double off = x[c] - base;
+          qsum[ci][c] += (int64_t)std::nearbyint(off * scale);
+        }
+      }
+    }
+    if (mode == 1) {
+      for (size_t ci = 0; ci < cells.size(); ++ci) {
+        Cell& cell = cells[ci];
+        for (int c = 0; c < d; ++c) {
+          double base = (double)cell.key[c] * h;
+          double mean_q = (double)qsum[ci][c] / (double)cell.count;
+          cell.c[c] = base + std::ldexp(mean_q, -F);
+        }
+      }
+    }
+    // Lex order, and remember each point's initial cell rank (slot) for the GPU K2 check.
+    std::vector<int64_t> perm(cells.size());
+    for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int64_t)i;
+    std::sort(perm.begin(), perm.end(),
+              [&](int64_t a, int64_t b) { return cells[a].key < cells[b].key; });
+    std::vector<int64_t> rank(cells.size());
+    for (size_t r = 0; r < perm.size(); ++r) rank[perm[r]] = (int64_t)r;
+    if (slot_out)
+      for (int64_t i = 0; i < n; ++i) slot_out[i] = rank[cell_of[i]];
+    sort_cells();
+    return OK;
+  }
+
+  // lookup of an OLD key among the lex-sorted snapshot (binary search; -1 if inactive).
+  int64_t find(const std::vector<Key>& keys, const Key& k) const {
+    auto it = std::lower_bound(keys.begin(), keys.end(), k);
+    if (it == keys.end() || *it != k) return -1;
+    return (int64_t)(it - keys.begin());
+  }
+
+  // iterate_once.  parent[i] = rank of the new cell that old cell i joined.
+  int iterate_once(bool* changed, double* maxdisp, std::vector<int64_t>* parent,
+                   std::vector<double>* swept) {
+    const int64_t m = (int64_t)cells.size();
+    const auto offs = offsets(d);
+    // (a) snapshot: C' counts and S' centroids (S' is then updated in place, Eq. 5)
+    std::vector<Key> keys(m);
+    std::vector<int64_t> Cs(m);
+    std::vector<double> S((size_t)m * d), S0((size_t)m * d);
+    for (int64_t i = 0; i < m; ++i) {
+      keys[i] = cells[i].key;
+      Cs[i] = cells[i].count;
+      for (int c = 0; c < d; ++c) S[i * d + c] = S0[i * d + c] = cells[i].c[c];
+    }
+    // (b)+(c) lexicographic in-place sweep
+    for (int64_t i = 0; i < m; ++i) {
+      double num[kMaxD];
+      for (int c = 0; c < d; ++c) num[c] = 0.0;
+      int64_t den = 0;
+      int others = 0;
+      for (size_t t = 0; t < offs.size(); ++t) {
+        Key k = keys[i];
+        bool self = true;
+        for (int c = 0; c < d; ++c) {
+          k[c] += offs[t][c];
+          if (offs[t][c] != 0) self = false;
+        }
+        int64_t nb = self ? i : find(keys, k);
+        if (nb < 0) continue;
+        double w = (double)Cs[nb];
+        for (int c = 0; c < d; ++c) num[c] = num[c] + w * S[nb * d + c];
+        den += Cs[nb];
+        if (!self) ++others;
+      }
+      if (others == 0) continue;  // pin P3
+      for (int c = 0; c < d; ++c) S[i * d + c] = num[c] / (double)den;
+    }
+    if (swept) *swept = S;
+    // displacement history and (e) changed
+    bool ch = false;
+    double md = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) {
+        double t = S[i * d + c] - S0[i * d + c];
+        acc = acc + t * t;
+        if (std::memcmp(&S[i * d + c], &S0[i * d + c], sizeof(double)) != 0) ch = true;
+      }
+      double disp = std::sqrt(acc);
+      if (disp > md) md = disp;
+    }
+    // (d) rehome each cell, in visit order, via merge_into (Eq. 3-4)
+    std::unordered_map<Key, int64_t, KeyHash> nidx;
+    std::vector<Cell> next;
+    std::vector<int64_t> par(m);
+    for (int64_t i = 0; i < m; ++i) {
+      Key k{};
+      for (int c = 0; c < d; ++c) k[c] = grid_coord(S[i * d + c], h);
+      if (k != keys[i]) ch = true;
+      auto it = nidx.find(k);
+      if (it == nidx.end()) {  // key absent -> inserted as-is
+        Cell cell;
+        cell.key = k;
+        for (int c = 0; c < d; ++c) cell.c[c] = S[i * d + c];
+        cell.count = Cs[i];
+        cell.members = std::move(cells[i].members);
+        par[i] = (int64_t)next.size();
+        nidx.emplace(k, par[i]);
+        next.push_back(std::move(cell));
+      } else {  // Eq. (3): count-weighted mean, counts add, member sets union
+        Cell& cell = next[it->second];
+        for (int c = 0; c < d; ++c)
+          cell.c[c] = ((double)cell.count * cell.c[c] + (double)Cs[i] * S[i * d + c]) /
+                      (double)(cell.count + Cs[i]);
+        cell.count += Cs[i];
+        cell.members.insert(cell.members.end(), cells[i].members.begin(),
+                            cells[i].members.end());
+        par[i] = it->second;
+      }
+    }
+    // re-rank new cells lexicographically
+    std::vector<int64_t> perm(next.size());
+    for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int64_t)i;
+    std::sort(perm.begin(), perm.end(),
+              [&](int64_t a, int64_t b) { return next[a].key < next[b].key; });
+    std::vector<int64_t> rank(next.size());
+    for (size_t r = 0; r < perm.size(); ++r) rank[perm[r]] = (int64_t)r;
+    for (int64_t i = 0; i < m; ++i) par[i] = rank[par[i]];
+    std::vector<Cell> sorted;
+    sorted.reserve(next.size());
+    for (size_t r = 0; r < perm.size(); ++r) sorted.push_back(std::move(next[perm[r]]));
+    cells = std::move(sorted);
+    if ((int64_t)cells.size() > m) return E_INTERNAL_INVARIANT;  // (f) |map'| <= |map|
+    if (parent) *parent = std::move(par);
+    *changed = ch;
+    *maxdisp = md;
+    return OK;
+  }
+
+  // has_converged: no active cell has another active cell in its 1-neighborhood.
+  bool has_converged() const {
+    const int64_t m = (int64_t)cells.size();
+    std::vector<Key> keys(m);
+    for (int64_t i = 0; i < m; ++i) keys[i] = cells[i].key;
+    const auto offs = offsets(d);
+    for (int64_t i = 0; i < m; ++i) {
+      for (const auto& v : offs) {
+        Key k = keys[i];
+        bool self = true;
+        for (int c = 0; c < d; ++c) {
+          k[c] += v[c];
+          if (v[c] != 0) self = false;
+        }
+        if (!self && find(keys, k) >= 0) return false;
+      }
+    }
+    return true;
+  }
+};
+
+int check_common(int64_t n, int d, double h) {
+  if (!(h > 0.0) || !std::isfinite(h)) return E_INVALID_BANDWIDTH;
+  if (n < 1) return E_EMPTY_INPUT;
+  if (d < 1 || d > kMaxD) return E_INVALID_PARAMETER;
+  return OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gso_version() { return 1; }
+
+int gso_fixed_shift(int64_t n, double h) { return fixed_shift(n, h); }
+
+// build_active_grid only: returns m0 and the lex-sorted cells; slot[i] = rank of point i's cell.
+// keys_out: m0*d int64; counts_out: m0; cent_out: m0*d; caller sizes them for n cells.
+int gso_build(const double* X, int64_t n, int32_t d, double h, int32_t mode, int64_t* m_out,
+              int64_t* keys_out, int64_t* counts_out, double* cent_out, int64_t* slot_out) {
+  int st = check_common(n, d, h);
+  if (st) return st;
+  Engine e{d, h, {}};
+  st = e.build(X, n, mode, slot_out);
+  if (st) return st;
+  *m_out = (int64_t)e.cells.size();
+  for (size_t i = 0; i < e.cells.size(); ++i) {
+    for (int c = 0; c < d; ++c) {
+      keys_out[i * d + c] = e.cells[i].key[c];
+      cent_out[i * d + c] = e.cells[i].c[c];
+    }
+    counts_out[i] = e.cells[i].count;
+  }
+  return OK;
+}
+
+// One iterate_once on an injected state (lex-sorted keys).  Outputs the new state, the
+// post-sweep centroids (pre-merge), parent ranks, changed and has_converged(new state).
+int gso_iterate_once(int32_t d, double h, int64_t m, const int64_t* keys, const int64_t* counts,
+                     const double* cent, int64_t* m_out, int64_t* keys_out,
+                     int64_t* counts_out, double* cent_out, double* swept_out,
+                     int64_t* parent_out, int32_t* changed_out, int32_t* converged_out,
+                     double* maxdisp_out) {
+  int st = check_common(m, d, h);
+  if (st) return st;
+  Engine e{d, h, {}};
+  e.cells.resize(m);
+  for (int64_t i = 0; i < m; ++i) {
+    Key k{};
+    for (int c = 0; c < d; ++c) {
+      k[c] = keys[i * d + c];
+      e.cells[i].c[c] = cent[i * d + c];
+    }
+    e.cells[i].key = k;
+    e.cells[i].count = counts[i];
+    e.cells[i].members = {i};
+    if (counts[i] < 1) return E_INVALID_INPUT;
+    if (i > 0 && !(e.cells[i - 1].key < k)) return E_INVALID_INPUT;  // must be strictly lex-sorted
+  }
+  bool changed;
+  double md;
+  std::vector<int64_t> parent;
+  std::vector<double> swept;
+  st = e.iterate_once(&changed, &md, &parent, &swept);
+  if (st) return st;
+  *m_out = (int64_t)e.cells.size();
+  for (size_t i = 0; i < e.cells.size(); ++i) {
+    for (int c = 0; c < d; ++c) {
+      keys_out[i * d + c] = e.cells[i].key[c];
+      cent_out[i * d + c] = e.cells[i].c[c];
+    }
+    counts_out[i] = e.cells[i].count;
+  }
+  for (int64_t i = 0; i < m; ++i) parent_out[i] = parent[i];
+  std::memcpy(swept_out, swept.data(), sizeof(double) * (size_t)m * d);
+  *changed_out = changed ? 1 : 0;
+  *converged_out = e.has_converged() ? 1 : 0;
+  *maxdisp_out = md;
+  return OK;
+}
+
+// has_converged on a given key set (lex order not required).
+int gso_has_converged(int32_t d, int64_t m, const int64_t* keys, int32_t* out) {
+  Engine e{d, 1.0, {}};
+  e.cells.resize(m);
+  for (int64_t i = 0; i < m; ++i) {
+    Key k{};
+    for (int c = 0; c < d; ++c) k[c] = keys[i * d + c];
+    e.cells[i].key = k;
+  }
+  e.sort_cells();
+  *out = e.has_converged() ? 1 : 0;
+  return OK;
+}
+
+// engine.run on one dataset (one frame).
+//   labels_out: n int32 cluster ids (lex rank of the final cell)
+//   cent_out:   capacity n*d; first k*d entries are the cluster centroids in id order
+//   hist_m / hist_disp: capacity max_iter; per-iteration active-cell count entering the
+//   iteration and max sweep displacement; *iters_out entries are written.
+int gso_run(const double* X, int64_t n, int32_t d, double h, int32_t max_iter, int32_t mode,
+            int32_t* labels_out, int64_t* k_out, int32_t* iters_out, int32_t* converged_out,
+            double* cent_out, int64_t* hist_m, double* hist_disp) {
+  int st = check_common(n, d, h);
+  if (st) return st;
+  if (max_iter < 1) return E_INVALID_PARAMETER;  // SPEC.md:112 positive integer
+  Engine e{d, h, {}};
+  st = e.build(X, n, mode, nullptr);
+  if (st) return st;
+  int iters = 0;
+  bool conv = false;
+  do {  // pin P5: do-while
+    int64_t m_t = (int64_t)e.cells.size();
+    bool changed;
+    double md;
+    st = e.iterate_once(&changed, &md, nullptr, nullptr);
+    if (st) return st;
+    if (hist_m) hist_m[iters] = m_t;
+    if (hist_disp) hist_disp[iters] = md;
+    ++iters;
+    if (e.has_converged() || !changed) {
+      conv = true;
+      break;
+    }
+  } while (iters < max_iter);
+  // ClusterLabeling: ids by lexicographic order of final keys (cells are kept sorted)
+  int64_t seen = 0;
+  for (size_t id = 0; id < e.cells.size(); ++id) {
+    for (int64_t p : e.cells[id].members) {
+      if (p < 0 || p >= n) return E_INTERNAL_INVARIANT;
+      labels_out[p] = (int32_t)id;
+      ++seen;
+    }
+    for (int c = 0; c < d; ++c) cent_out[id * d + c] = e.cells[id].c[c];
+  }
+  if (seen != n) return E_INTERNAL_INVARIANT;  // partition invariant SPEC.md:78
+  *k_out = (int64_t)e.cells.size();
+  *iters_out = iters;
+  *converged_out = conv ? 1 : 0;
+  return OK;
+}
+
+}  // extern "C"

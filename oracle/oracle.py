@@ -1,0 +1,116 @@
+"""ctypes binding of the CPU oracle (oracle/gs_oracle.cpp).  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline / ``--impl reference``
+legs may import this module; the product path never does.  The oracle restates
+/root/reference/SPEC.md:17-181 (grid-core + engine) — see the header of gs_oracle.cpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+BUILD_SPEC, BUILD_FIXED = 0, 1
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+        L.gso_build.argtypes = [P, I64, I32, D, I32, P, P, P, P, P]
+        L.gso_iterate_once.argtypes = [I32, D, I64, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.gso_has_converged.argtypes = [I32, I64, P, P]
+        L.gso_run.argtypes = [P, I64, I32, D, I32, I32, P, P, P, P, P, P, P]
+        L.gso_fixed_shift.argtypes = [I64, D]
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int):
+        super().__init__(f"oracle status {status}")
+        self.status = status
+
+
+def _chk(rc: int) -> None:
+    if rc != 0:
+        raise OracleError(rc)
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def build_grid(X: np.ndarray, h: float, mode: int = BUILD_FIXED):
+    """build_active_grid: lex-sorted keys, counts, centroids, point->rank."""
+    X = np.ascontiguousarray(X, np.float64)
+    n, d = X.shape
+    keys = np.zeros((n, d), np.int64)
+    cnt = np.zeros(n, np.int64)
+    cen = np.zeros((n, d), np.float64)
+    slot = np.zeros(n, np.int64)
+    m = C.c_int64()
+    _chk(lib().gso_build(_p(X), n, d, h, mode, C.byref(m), _p(keys), _p(cnt), _p(cen), _p(slot)))
+    m = m.value
+    return keys[:m], cnt[:m], cen[:m], slot
+
+
+def iterate_once(keys, counts, cent, h: float) -> dict:
+    """iterate_once on an injected lex-sorted state."""
+    keys = np.ascontiguousarray(keys, np.int64)
+    counts = np.ascontiguousarray(counts, np.int64)
+    cent = np.ascontiguousarray(cent, np.float64)
+    m, d = keys.shape
+    ko = np.zeros((m, d), np.int64)
+    co = np.zeros(m, np.int64)
+    so = np.zeros((m, d), np.float64)
+    sw = np.zeros((m, d), np.float64)
+    par = np.zeros(m, np.int64)
+    mo, ch, cv, md = C.c_int64(), C.c_int32(), C.c_int32(), C.c_double()
+    _chk(lib().gso_iterate_once(d, h, m, _p(keys), _p(counts), _p(cent), C.byref(mo), _p(ko),
+                                _p(co), _p(so), _p(sw), _p(par), C.byref(ch), C.byref(cv),
+                                C.byref(md)))
+    mn = mo.value
+    return dict(keys=ko[:mn], counts=co[:mn], centroids=so[:mn], swept=sw, parent=par,
+                changed=bool(ch.value), converged=bool(cv.value), maxdisp=md.value)
+
+
+def has_converged(keys) -> bool:
+    keys = np.ascontiguousarray(keys, np.int64)
+    m, d = keys.shape
+    out = C.c_int32()
+    _chk(lib().gso_has_converged(d, m, _p(keys), C.byref(out)))
+    return bool(out.value)
+
+
+def run(X: np.ndarray, h: float, max_iter: int = 1000, mode: int = BUILD_SPEC) -> dict:
+    """engine.run on one frame."""
+    X = np.ascontiguousarray(X, np.float64)
+    n, d = X.shape
+    labels = np.zeros(n, np.int32)
+    cen = np.zeros((n, d), np.float64)
+    hm = np.zeros(max(max_iter, 1), np.int64)
+    hd = np.zeros(max(max_iter, 1), np.float64)
+    k, it, cv = C.c_int64(), C.c_int32(), C.c_int32()
+    _chk(lib().gso_run(_p(X), n, d, h, max_iter, mode, _p(labels), C.byref(k), C.byref(it),
+                       C.byref(cv), _p(cen), _p(hm), _p(hd)))
+    k, it = k.value, it.value
+    return dict(labels=labels, k=k, iterations=it, converged=bool(cv.value), centroids=cen[:k],
+                history=[(int(hm[t]), float(hd[t])) for t in range(it)])
+
+
+def fixed_shift(n: int, h: float) -> int:
+    return int(lib().gso_fixed_shift(n, h))

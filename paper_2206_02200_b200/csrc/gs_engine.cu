@@ -1,0 +1,874 @@
+// gs_engine.cu — host orchestration of the GridShift engine and its C-ABI (gridshift_c.h).
+//
+// One gs_run clusters every frame of the input.  Phases:
+//   n-scale   K1 bounds -> K2 binning -> sort occupied cells -> K3 lex cell list
+//   m-scale   per iteration: K4 neighbour lists + dataflow sweep, K5 rehome + stable sort +
+//             ordered merge fold + index update + has_converged + root composition
+//   n-scale   K7 label propagation, centroids out
+// Frames are independent: they share one launch sequence, and a frame that has
+// terminated is frozen (its cells are neither swept nor rehomed) while others keep iterating.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gridshift_c.h"
+#include "gs_kernels.cuh"
+
+namespace {
+
+constexpr int64_t kMaxDenseCells = int64_t(1) << 28;  // dense grid cap (u32 keys, <= ~10 GB)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+int64_t ipow3(int d) {
+  int64_t k = 1;
+  for (int i = 0; i < d; ++i) k *= 3;
+  return k;
+}
+
+unsigned blocks_for(int64_t n, int threads, int64_t cap = 1 << 20) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+struct gs_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  uint32_t epoch = 0;
+
+  // dense cell grid (clean invariant between runs: cnt = 0, qs = 0, idx = -1)
+  DevBuf cnt, qs, idx, lab;
+  int64_t dense_cap = 0;
+  int qs_dim = 0;
+  // per point
+  DevBuf pts, slot, labels;
+  // per cell (double-buffered state)
+  DevBuf occ, occ_sorted, ckey[2], ccnt[2], S[2], S1, nbl, nbn, nbe, den, flag, nkey, vals,
+      skey, sval, head, sid, segstart, parent, root, initkey;
+  int64_t cell_cap = 0, nbl_cap = 0;
+  // per frame
+  DevBuf fdone, fchanged, fadj, fm, fdisp, ffirst;
+  int64_t frame_cap = 0;
+  // misc
+  DevBuf counters, errflag, bpart, cub_tmp, dbg;
+  // last run (host side)
+  GsBox box{};
+  int64_t nframes = 0;
+  int cur = 0;  // which ckey/ccnt/S buffer holds the final cells
+  int64_t k_total = 0;
+  std::vector<int32_t> h_ffirst;
+  std::vector<int64_t> h_k;
+  std::vector<int32_t> h_iters, h_conv, h_done;
+  std::vector<std::vector<int64_t>> hist_m;
+  std::vector<std::vector<double>> hist_d;
+  bool have_run = false;
+  gs_stats stats{};
+  cudaEvent_t ev[12] = {};
+};
+
+namespace {
+
+#define GS_CK(call)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+      return (e_ == cudaErrorMemoryAllocation) ? GS_E_OOM : GS_E_CUDA;               \
+    }                                                                                \
+  } while (0)
+
+#define GS_TRY(expr)             \
+  do {                           \
+    gs_status s_ = (expr);       \
+    if (s_ != GS_OK) return s_;  \
+  } while (0)
+
+gs_status fail(gs_ctx* ctx, gs_status s, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return s;
+}
+
+gs_status grow(gs_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes <= b.bytes) return GS_OK;
+  b.release();
+  size_t want = std::max<size_t>(bytes, 256);
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    cudaGetLastError();
+    return fail(ctx, GS_E_OOM, "cudaMalloc(" + std::to_string(want) + ") failed");
+  }
+  b.bytes = want;
+  return GS_OK;
+}
+
+gs_status check_launch(gs_ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, GS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  ctx->stats.kernel_launches++;
+  return GS_OK;
+}
+
+#define GS_LAUNCHED(name) GS_TRY(check_launch(ctx, name))
+
+gs_status check_lib(gs_ctx* ctx, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, GS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  ctx->stats.lib_calls++;
+  return GS_OK;
+}
+
+gs_status validate(const gs_input* in, const gs_config* cfg) {
+  if (!in || !cfg) return GS_E_INVALID_PARAMETER;
+  if (!(cfg->h > 0.0) || !std::isfinite(cfg->h)) return GS_E_INVALID_BANDWIDTH;
+  if (in->n < 1 || in->batch < 1) return in->n < 1 ? GS_E_EMPTY_INPUT : GS_E_INVALID_PARAMETER;
+  if (in->d < 1 || in->d > GS_MAX_DIM) return GS_E_INVALID_PARAMETER;
+  if (in->dtype != GS_F32 && in->dtype != GS_F64) return GS_E_INVALID_PARAMETER;
+  if (cfg->max_iter < 1) return GS_E_INVALID_PARAMETER;
+  if (!in->points) return GS_E_INVALID_PARAMETER;
+  if (in->n * in->batch > (int64_t(1) << 40)) return GS_E_INVALID_PARAMETER;
+  return GS_OK;
+}
+
+// Dense grid: grow to hold `cells` cells of dimension d; fresh memory gets the clean state.
+gs_status ensure_dense(gs_ctx* ctx, int64_t cells, int d) {
+  if (cells <= ctx->dense_cap && d <= ctx->qs_dim) return GS_OK;
+  int64_t cap = std::max<int64_t>(cells, ctx->dense_cap);
+  int qd = std::max(d, ctx->qs_dim);
+  ctx->cnt.release();
+  ctx->qs.release();
+  ctx->idx.release();
+  ctx->lab.release();
+  ctx->dense_cap = 0;
+  GS_TRY(grow(ctx, ctx->cnt, sizeof(uint32_t) * cap));
+  GS_TRY(grow(ctx, ctx->qs, sizeof(unsigned long long) * cap * qd));
+  GS_TRY(grow(ctx, ctx->idx, sizeof(int32_t) * cap));
+  GS_TRY(grow(ctx, ctx->lab, sizeof(int32_t) * cap));
+  GS_CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(uint32_t) * cap, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->qs.p, 0, sizeof(unsigned long long) * cap * qd, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->idx.p, 0xff, sizeof(int32_t) * cap, ctx->stream));
+  ctx->dense_cap = cap;
+  ctx->qs_dim = qd;
+  return GS_OK;
+}
+
+gs_status ensure_cells(gs_ctx* ctx, int64_t m, int d) {
+  if (m <= ctx->cell_cap) return GS_OK;
+  int64_t c = std::max<int64_t>(m, 1024);
+  for (DevBuf* b : {&ctx->occ, &ctx->occ_sorted, &ctx->ckey[0], &ctx->ckey[1], &ctx->ccnt[0],
+                    &ctx->ccnt[1], &ctx->nkey, &ctx->vals, &ctx->skey, &ctx->sval})
+    GS_TRY(grow(ctx, *b, sizeof(uint32_t) * c));
+  for (DevBuf* b : {&ctx->nbn, &ctx->nbe, &ctx->head, &ctx->sid, &ctx->segstart, &ctx->parent,
+                    &ctx->root, &ctx->initkey})
+    GS_TRY(grow(ctx, *b, sizeof(int32_t) * c));
+  GS_TRY(grow(ctx, ctx->den, sizeof(unsigned long long) * c));
+  for (DevBuf* b : {&ctx->S[0], &ctx->S[1], &ctx->S1})
+    GS_TRY(grow(ctx, *b, sizeof(double) * c * GS_MAX_DIM));
+  if (ctx->flag.bytes < sizeof(uint32_t) * c) {
+    GS_TRY(grow(ctx, ctx->flag, sizeof(uint32_t) * c));
+    GS_CK(cudaMemsetAsync(ctx->flag.p, 0, ctx->flag.bytes, ctx->stream));
+  }
+  // CUB temporaries for the largest sort/scan on c items
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, (int)c, 0, 32,
+                                  ctx->stream);
+  cub::DeviceScan::InclusiveSum(nullptr, t2, (int32_t*)nullptr, (int32_t*)nullptr, (int)c,
+                                ctx->stream);
+  size_t t3 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)c, 0,
+                                 32, ctx->stream);
+  GS_TRY(grow(ctx, ctx->cub_tmp, std::max({t1, t2, t3})));
+  ctx->cell_cap = c;
+  return GS_OK;
+}
+
+gs_status ensure_frames(gs_ctx* ctx, int64_t nf) {
+  if (nf <= ctx->frame_cap) return GS_OK;
+  for (DevBuf* b : {&ctx->fdone, &ctx->fchanged, &ctx->fadj, &ctx->fm, &ctx->ffirst})
+    GS_TRY(grow(ctx, *b, sizeof(int32_t) * nf));
+  GS_TRY(grow(ctx, ctx->fdisp, sizeof(unsigned long long) * nf));
+  ctx->frame_cap = nf;
+  return GS_OK;
+}
+
+int bits_for(int64_t v) {  // bits needed to represent values < v
+  int b = 1;
+  while (b < 32 && (int64_t(1) << b) < v) ++b;
+  return b;
+}
+
+// Box from per-dim data min/max (host).  floor(min/h) <= floor(x/h) <= floor(max/h) for every
+// x by monotonicity of IEEE division and floor.
+gs_status make_box(gs_ctx* ctx, int d, double h, int64_t n, int64_t nframes, const double* mn,
+                   const double* mx, GsBox* b) {
+  std::memset(b, 0, sizeof(*b));
+  b->d = d;
+  b->h = h;
+  b->inv_h = 1.0 / h;
+  b->F = gs_fixed_shift(n, h);
+  b->scale = std::ldexp(1.0, b->F);
+  b->inv_scale = std::ldexp(1.0, -b->F);
+  b->n = n;
+  b->nframes = nframes;
+  double vol = 1.0;
+  for (int c = 0; c < d; ++c) {
+    double lo = std::floor(mn[c] / h), hi = std::floor(mx[c] / h);
+    if (!(std::fabs(lo) < 4e15) || !(std::fabs(hi) < 4e15))
+      return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+    b->kmin[c] = (int64_t)lo - GS_APRON;
+    b->ext[c] = (int64_t)hi - (int64_t)lo + 1 + 2 * GS_APRON;
+    vol *= (double)b->ext[c];
+  }
+  if (vol * (double)nframes > (double)kMaxDenseCells)
+    return fail(ctx, GS_E_KEY_RANGE,
+                "key box of " + std::to_string((long long)(vol * nframes)) +
+                    " cells exceeds the dense cell grid (2^28)");
+  int64_t s = 1;
+  for (int c = d - 1; c >= 0; --c) {
+    b->stride[c] = s;
+    s *= b->ext[c];
+  }
+  b->vol_frame = s;
+  b->vol_total = s * nframes;
+  return GS_OK;
+}
+
+// Box for an injected cell state (test hook): covers the keys and floor(centroid/h).
+gs_status make_box_from_cells(gs_ctx* ctx, int d, double h, int64_t m, const int64_t* keys,
+                              const double* cent, GsBox* b) {
+  std::vector<double> mn(d, INFINITY), mx(d, -INFINITY);
+  for (int64_t i = 0; i < m; ++i)
+    for (int c = 0; c < d; ++c) {
+      double kh = (double)keys[i * d + c] * h;  // any x with floor(x/h) == key
+      double lo = std::min(cent[i * d + c], kh), hi = std::max(cent[i * d + c], kh);
+      mn[c] = std::min(mn[c], lo);
+      mx[c] = std::max(mx[c], hi);
+    }
+  GS_TRY(make_box(ctx, d, h, 1 << 20, 1, mn.data(), mx.data(), b));
+  for (int64_t i = 0; i < m; ++i)
+    for (int c = 0; c < d; ++c) {
+      int64_t rel = keys[i * d + c] - b->kmin[c];
+      if (rel < GS_APRON || rel >= b->ext[c] - GS_APRON) {  // widen: keys define the box
+        int64_t lo = std::min<int64_t>(keys[i * d + c], b->kmin[c] + GS_APRON);
+        int64_t hi = std::max<int64_t>(keys[i * d + c], b->kmin[c] + b->ext[c] - GS_APRON - 1);
+        b->kmin[c] = lo - GS_APRON;
+        b->ext[c] = hi - lo + 1 + 2 * GS_APRON;
+      }
+    }
+  int64_t s = 1;
+  for (int c = d - 1; c >= 0; --c) {
+    b->stride[c] = s;
+    s *= b->ext[c];
+  }
+  b->vol_frame = s;
+  b->vol_total = s;
+  if (s > kMaxDenseCells) return fail(ctx, GS_E_KEY_RANGE, "injected key box too large");
+  return GS_OK;
+}
+
+template <int D>
+gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t ntot, bool bounds,
+                            const GsBox* box, unsigned nblk) {
+  if (bounds) {
+    if (dtype == GS_F32)
+      gs::k_bounds<D, float><<<nblk, 256, 0, ctx->stream>>>(
+          (const float*)pts, ntot, ctx->bpart.as<double>(),
+          ctx->bpart.as<double>() + (size_t)nblk * D, ctx->errflag.as<int>());
+    else
+      gs::k_bounds<D, double><<<nblk, 256, 0, ctx->stream>>>(
+          (const double*)pts, ntot, ctx->bpart.as<double>(),
+          ctx->bpart.as<double>() + (size_t)nblk * D, ctx->errflag.as<int>());
+    GS_LAUNCHED("k_bounds");
+  } else {
+    if (dtype == GS_F32)
+      gs::k_bin<D, float><<<nblk, 256, 0, ctx->stream>>>(
+          (const float*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
+          ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
+    else
+      gs::k_bin<D, double><<<nblk, 256, 0, ctx->stream>>>(
+          (const double*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
+          ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
+    GS_LAUNCHED("k_bin");
+  }
+  return GS_OK;
+}
+
+gs_status dispatch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int d, int64_t ntot,
+                              bool bounds, const GsBox* box, unsigned nblk) {
+  switch (d) {
+#define GS_CASE(D) \
+  case D:          \
+    return launch_bounds_bin<D>(ctx, pts, dtype, ntot, bounds, box, nblk);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+    GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
+#undef GS_CASE
+  }
+  return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
+}
+
+gs_status read_err(gs_ctx* ctx, int* out) {
+  GS_CK(cudaMemcpyAsync(out, ctx->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  return GS_OK;
+}
+
+// n-scale phase: bounds, binning, lex cell list.  On return ctx->box is set, cells are in
+// ckey[0]/ccnt[0]/S[0], *m0_out is the number of initial cells.
+gs_status build_cells(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t n, int64_t nf,
+                      double h, int64_t* m0_out) {
+  const int64_t ntot = n * nf;
+  const unsigned nblk = blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8);
+  GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
+  GS_TRY(grow(ctx, ctx->errflag, sizeof(int) * 4));
+  GS_TRY(grow(ctx, ctx->counters, sizeof(unsigned int) * 16));
+  GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, sizeof(int) * 4, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned int) * 16, ctx->stream));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nullptr, nblk));
+  std::vector<double> part((size_t)nblk * d * 2);
+  GS_CK(cudaMemcpyAsync(part.data(), ctx->bpart.p, sizeof(double) * part.size(),
+                        cudaMemcpyDeviceToHost, ctx->stream));
+  int err = 0;
+  GS_TRY(read_err(ctx, &err));
+  if (err & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+  std::vector<double> mn(d, INFINITY), mx(d, -INFINITY);
+  for (unsigned b = 0; b < nblk; ++b)
+    for (int c = 0; c < d; ++c) {
+      mn[c] = std::min(mn[c], part[(size_t)b * d + c]);
+      mx[c] = std::max(mx[c], part[(size_t)nblk * d + (size_t)b * d + c]);
+    }
+  GS_TRY(make_box(ctx, d, h, n, nf, mn.data(), mx.data(), &ctx->box));
+  GS_TRY(ensure_dense(ctx, ctx->box.vol_total, d));
+  const int64_t mcap = std::min<int64_t>(ntot, ctx->box.vol_total);
+  GS_TRY(ensure_cells(ctx, mcap, d));
+  GS_TRY(grow(ctx, ctx->slot, sizeof(uint32_t) * ntot));
+  GS_CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, &ctx->box, nblk));
+  GS_CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  unsigned int m0 = 0;
+  GS_CK(cudaMemcpyAsync(&m0, ctx->counters.p, sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  GS_TRY(read_err(ctx, &err));
+  if (err & 2) return fail(ctx, GS_E_INTERNAL_INVARIANT, "point outside the computed key box");
+  const int kb = bits_for(ctx->box.vol_total);
+  size_t tb = ctx->cub_tmp.bytes;
+  GS_CK(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tb, ctx->occ.as<uint32_t>(),
+                                       ctx->occ_sorted.as<uint32_t>(), (int)m0, 0, kb,
+                                       ctx->stream));
+  GS_TRY(check_lib(ctx, "cub_sort_occ"));
+  gs::k_make_cells<<<blocks_for(m0, 256), 256, 0, ctx->stream>>>(
+      (int)m0, ctx->box, ctx->occ_sorted.as<uint32_t>(), ctx->cnt.as<uint32_t>(),
+      ctx->qs.as<unsigned long long>(), ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(),
+      ctx->S[0].as<double>(), ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(),
+      ctx->initkey.as<uint32_t>());
+  GS_LAUNCHED("k_make_cells");
+  *m0_out = m0;
+  return GS_OK;
+}
+
+// One iterate_once over all frames (frozen frames excluded).  Cells in buffer `cur`; the new
+// cells land in buffer 1-cur.  Per-frame changed/adjacency/m/disp land in the f* arrays.
+gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
+  const GsBox& b = ctx->box;
+  const int d = b.d;
+  const int K = (int)ipow3(d);
+  const int cur = ctx->cur, nxt = 1 - cur;
+  const int64_t nf = b.nframes;
+  if ((int64_t)K * m > ctx->nbl_cap) {
+    GS_TRY(grow(ctx, ctx->nbl, sizeof(int32_t) * (size_t)K * m));
+    ctx->nbl_cap = (int64_t)K * m;
+  }
+  GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->counters.as<unsigned int>() + 1, 0, sizeof(unsigned int),
+                        ctx->stream));
+  const unsigned mb = blocks_for(m, 256);
+  gs::k_nbr<<<mb, 256, 0, ctx->stream>>>((int)m, b, K, ctx->ckey[cur].as<uint32_t>(),
+                                         ctx->ccnt[cur].as<uint32_t>(), ctx->idx.as<int32_t>(),
+                                         ctx->fdone.as<int32_t>(), ctx->nbl.as<int32_t>(),
+                                         ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
+                                         ctx->den.as<unsigned long long>(), ctx->fm.as<int32_t>());
+  GS_LAUNCHED("k_nbr");
+  const uint32_t epoch = ++ctx->epoch;
+  const unsigned sb = blocks_for((m + 31) / 32 * 32, 256, (int64_t)ctx->num_sms * 4);
+  gs::k_sweep<<<sb, 256, 0, ctx->stream>>>(
+      (int)m, d, K, ctx->ccnt[cur].as<uint32_t>(), ctx->S[cur].as<double>(), ctx->S1.as<double>(),
+      ctx->nbl.as<int32_t>(), ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
+      ctx->den.as<unsigned long long>(), ctx->flag.as<uint32_t>(), epoch,
+      ctx->counters.as<unsigned int>() + 1, ctx->errflag.as<int>());
+  GS_LAUNCHED("k_sweep");
+  gs::k_rehome<<<mb, 256, 0, ctx->stream>>>(
+      (int)m, b, ctx->ckey[cur].as<uint32_t>(), ctx->S[cur].as<double>(), ctx->S1.as<double>(),
+      ctx->fdone.as<int32_t>(), ctx->nkey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
+      ctx->fchanged.as<int32_t>(), ctx->fdisp.as<unsigned long long>(), ctx->errflag.as<int>());
+  GS_LAUNCHED("k_rehome");
+  const int kb = bits_for(b.vol_total);
+  size_t tb = ctx->cub_tmp.bytes;
+  GS_CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tb, ctx->nkey.as<uint32_t>(),
+                                        ctx->skey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
+                                        ctx->sval.as<uint32_t>(), (int)m, 0, kb, ctx->stream));
+  GS_TRY(check_lib(ctx, "cub_sort_pairs"));
+  gs::k_heads<<<mb, 256, 0, ctx->stream>>>((int)m, ctx->skey.as<uint32_t>(),
+                                           ctx->head.as<int32_t>());
+  GS_LAUNCHED("k_heads");
+  tb = ctx->cub_tmp.bytes;
+  GS_CK(cub::DeviceScan::InclusiveSum(ctx->cub_tmp.p, tb, ctx->head.as<int32_t>(),
+                                      ctx->sid.as<int32_t>(), (int)m, ctx->stream));
+  GS_TRY(check_lib(ctx, "cub_scan"));
+  gs::k_seg<<<mb, 256, 0, ctx->stream>>>((int)m, ctx->head.as<int32_t>(), ctx->sid.as<int32_t>(),
+                                         ctx->sval.as<uint32_t>(), ctx->parent.as<int32_t>(),
+                                         ctx->segstart.as<int32_t>());
+  GS_LAUNCHED("k_seg");
+  int32_t mnew = 0;
+  GS_CK(cudaMemcpyAsync(&mnew, ctx->sid.as<int32_t>() + (m - 1), sizeof(int32_t),
+                        cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  const unsigned nb = blocks_for(mnew, 256);
+  gs::k_fold<<<nb, 256, 0, ctx->stream>>>(
+      mnew, (int)m, d, ctx->segstart.as<int32_t>(), ctx->skey.as<uint32_t>(),
+      ctx->sval.as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(), ctx->S1.as<double>(),
+      ctx->ckey[nxt].as<uint32_t>(), ctx->ccnt[nxt].as<uint32_t>(), ctx->S[nxt].as<double>());
+  GS_LAUNCHED("k_fold");
+  gs::k_idx_clear<<<mb, 256, 0, ctx->stream>>>((int)m, ctx->ckey[cur].as<uint32_t>(),
+                                               ctx->idx.as<int32_t>());
+  GS_LAUNCHED("k_idx_clear");
+  gs::k_idx_set<<<nb, 256, 0, ctx->stream>>>(mnew, ctx->ckey[nxt].as<uint32_t>(),
+                                             ctx->idx.as<int32_t>());
+  GS_LAUNCHED("k_idx_set");
+  gs::k_adjacent<<<nb, 256, 0, ctx->stream>>>(mnew, b, K, ctx->ckey[nxt].as<uint32_t>(),
+                                              ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(),
+                                              ctx->fadj.as<int32_t>());
+  GS_LAUNCHED("k_adjacent");
+  ctx->cur = nxt;
+  *mnew_out = mnew;
+  return GS_OK;
+}
+
+gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
+  GS_TRY(validate(in, cfg));
+  if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
+  const int d = in->d;
+  const int64_t n = in->n, nf = in->batch, ntot = n * nf;
+  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
+  ctx->have_run = false;
+  ctx->stats = gs_stats{};
+  ctx->cur = 0;
+  GS_TRY(ensure_frames(ctx, nf));
+  const void* dpts = in->points;
+  cudaStream_t st = ctx->stream;
+  GS_CK(cudaEventRecord(ctx->ev[0], st));
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
+    dpts = ctx->pts.p;
+  }
+  GS_CK(cudaEventRecord(ctx->ev[1], st));
+  int64_t m0 = 0;
+  GS_TRY(build_cells(ctx, dpts, in->dtype, d, n, nf, cfg->h, &m0));
+  GS_CK(cudaEventRecord(ctx->ev[2], st));
+  const GsBox& b = ctx->box;
+  // ---- iteration phase
+  ctx->h_done.assign(nf, 0);
+  ctx->h_iters.assign(nf, 0);
+  ctx->h_conv.assign(nf, 0);
+  const bool rec = (cfg->flags & GS_RECORD_HISTORY) != 0;
+  ctx->hist_m.assign(rec ? nf : 0, {});
+  ctx->hist_d.assign(rec ? nf : 0, {});
+  GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
+  std::vector<int32_t> fch(nf), fadj(nf), fm(nf);
+  std::vector<unsigned long long> fdisp(nf);
+  int64_t m = m0, live = nf, swept = 0;
+  int iter = 0;
+  while (live > 0) {
+    int64_t mnew = 0;
+    GS_TRY(iterate(ctx, m, &mnew));
+    gs::k_compose<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->parent.as<int32_t>(),
+                                                        ctx->root.as<int32_t>());
+    GS_LAUNCHED("k_compose");
+    GS_CK(cudaMemcpyAsync(fch.data(), ctx->fchanged.p, sizeof(int32_t) * nf,
+                          cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(fadj.data(), ctx->fadj.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
+                          st));
+    GS_CK(cudaMemcpyAsync(fm.data(), ctx->fm.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(fdisp.data(), ctx->fdisp.p, sizeof(unsigned long long) * nf,
+                          cudaMemcpyDeviceToHost, st));
+    int err = 0;
+    GS_TRY(read_err(ctx, &err));
+    if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
+    if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
+  if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+    ++iter;
+    for (int64_t f = 0; f < nf; ++f) {
+      if (ctx->h_done[f]) continue;
+      swept += fm[f];
+      if (rec) {
+        double dsp;
+        std::memcpy(&dsp, &fdisp[f], sizeof(double));
+        ctx->hist_m[f].push_back(fm[f]);
+        ctx->hist_d[f].push_back(dsp);
+      }
+      ctx->h_iters[f] = iter;
+      const bool conv = !fadj[f] || !fch[f];
+      if (conv || iter >= cfg->max_iter) {
+        ctx->h_done[f] = 1;
+        ctx->h_conv[f] = conv ? 1 : 0;
+        --live;
+      }
+    }
+    m = mnew;
+    if (live > 0)
+      GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
+                            cudaMemcpyHostToDevice, st));
+  }
+  GS_CK(cudaEventRecord(ctx->ev[3], st));
+  // ---- labels
+  const int cur = ctx->cur;
+  gs::k_frame_first<<<blocks_for(m, 256), 256, 0, st>>>((int)m, b.vol_frame,
+                                                        ctx->ckey[cur].as<uint32_t>(),
+                                                        ctx->ffirst.as<int32_t>());
+  GS_LAUNCHED("k_frame_first");
+  gs::k_labtab<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, b.vol_frame,
+                                                    ctx->initkey.as<uint32_t>(),
+                                                    ctx->root.as<int32_t>(),
+                                                    ctx->ffirst.as<int32_t>(),
+                                                    ctx->lab.as<int32_t>());
+  GS_LAUNCHED("k_labtab");
+  int32_t* dlabels = out->labels;
+  const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
+  if (!dev_out) {
+    GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
+    dlabels = ctx->labels.as<int32_t>();
+  }
+  GS_CK(cudaEventRecord(ctx->ev[8], st));
+  gs::k_label<<<blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+      ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels);
+  GS_LAUNCHED("k_label");
+  GS_CK(cudaEventRecord(ctx->ev[9], st));
+  GS_CK(cudaEventRecord(ctx->ev[4], st));
+  if (!dev_out)
+    GS_CK(cudaMemcpyAsync(out->labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
+                          st));
+  GS_CK(cudaEventRecord(ctx->ev[5], st));
+  ctx->h_ffirst.assign(nf, 0);
+  GS_CK(cudaMemcpyAsync(ctx->h_ffirst.data(), ctx->ffirst.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  // restore the clean index invariant for the next run
+  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[cur].as<uint32_t>(),
+                                                      ctx->idx.as<int32_t>());
+  GS_CK(cudaGetLastError());
+  ctx->k_total = m;
+  ctx->h_k.assign(nf, 0);
+  for (int64_t f = 0; f < nf; ++f) {
+    const int64_t end = (f + 1 < nf) ? ctx->h_ffirst[f + 1] : m;
+    ctx->h_k[f] = end - ctx->h_ffirst[f];
+    out->k[f] = ctx->h_k[f];
+    out->iterations[f] = ctx->h_iters[f];
+    out->converged[f] = ctx->h_conv[f];
+  }
+  ctx->nframes = nf;
+  ctx->have_run = true;
+  float ms = 0;
+  gs_stats& s = ctx->stats;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  s.ms_h2d = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+  s.ms_bin = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  s.ms_iterate = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
+  s.ms_label = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
+  s.ms_d2h = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[4]);
+  s.ms_total = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+  s.ms_k_bin = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
+  s.ms_k_label = ms;
+  s.cells_swept = swept;
+  s.m0 = m0;
+  s.k_total = m;
+  s.max_iterations = iter;
+  s.fixed_shift = b.F;
+  s.dense_cells = b.vol_total;
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t gs_fixed_shift(int64_t n, double h) {
+  // mirrors oracle fixed_shift(): |sum| < 2^61 for any cell of <= n points, offsets in [~0, h]
+  int ln = 0;
+  while ((int64_t(1) << ln) < n) ++ln;
+  int eh = std::ilogb(h) + 1;
+  int F = 61 - ln - eh;
+  return std::max(-1000, std::min(1000, F));
+}
+
+const char* gs_status_string(gs_status s) {
+  switch (s) {
+    case GS_OK: return "ok";
+    case GS_E_INVALID_INPUT: return "invalid input";
+    case GS_E_INVALID_BANDWIDTH: return "invalid bandwidth";
+    case GS_E_EMPTY_INPUT: return "empty input";
+    case GS_E_INVALID_PARAMETER: return "invalid parameter";
+    case GS_E_INTERNAL_INVARIANT: return "internal invariant violated";
+    case GS_E_KEY_RANGE: return "key range exceeds the dense cell grid";
+    case GS_E_CUDA: return "CUDA error";
+    case GS_E_OOM: return "device out of memory";
+    case GS_E_NCCL: return "NCCL error";
+    case GS_E_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+gs_status gs_validate(const gs_input* in, const gs_config* cfg) { return validate(in, cfg); }
+
+gs_status gs_create(int device, void* cuda_stream, gs_ctx** out) {
+  if (!out) return GS_E_INVALID_PARAMETER;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) {
+    cudaGetLastError();
+    return GS_E_NO_DEVICE;
+  }
+  gs_ctx* ctx = new gs_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return GS_E_NO_DEVICE;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return GS_E_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return GS_OK;
+}
+
+void gs_destroy(gs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->cnt, &ctx->qs, &ctx->idx, &ctx->lab, &ctx->pts, &ctx->slot,
+                    &ctx->labels, &ctx->occ, &ctx->occ_sorted, &ctx->ckey[0], &ctx->ckey[1],
+                    &ctx->ccnt[0], &ctx->ccnt[1], &ctx->S[0], &ctx->S[1], &ctx->S1, &ctx->nbl,
+                    &ctx->nbn, &ctx->nbe, &ctx->den, &ctx->flag, &ctx->nkey, &ctx->vals,
+                    &ctx->skey, &ctx->sval, &ctx->head, &ctx->sid, &ctx->segstart, &ctx->parent,
+                    &ctx->root, &ctx->initkey, &ctx->fdone, &ctx->fchanged, &ctx->fadj,
+                    &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->counters, &ctx->errflag,
+                    &ctx->bpart, &ctx->cub_tmp, &ctx->dbg})
+    b->release();
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* gs_last_error(const gs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+gs_status gs_run(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
+  gs_status s = validate(in, cfg);
+  if (s != GS_OK) {
+    if (ctx) ctx->err = gs_status_string(s);
+    return s;
+  }
+  if (!ctx) return GS_E_INVALID_PARAMETER;
+  ctx->err.clear();
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GS_E_CUDA, "cudaSetDevice");
+  return run_impl(ctx, in, cfg, out);
+}
+
+gs_status gs_get_centroids(gs_ctx* ctx, int64_t frame, double* out, int64_t cap_k) {
+  if (!ctx || !out) return GS_E_INVALID_PARAMETER;
+  if (!ctx->have_run || frame < 0 || frame >= ctx->nframes)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "no such frame in the last run");
+  const int64_t k = ctx->h_k[frame];
+  if (cap_k < k) return fail(ctx, GS_E_INVALID_PARAMETER, "centroid buffer too small");
+  const int d = ctx->box.d;
+  GS_CK(cudaMemcpyAsync(out, ctx->S[ctx->cur].as<double>() + (size_t)ctx->h_ffirst[frame] * d,
+                        sizeof(double) * k * d, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  return GS_OK;
+}
+
+gs_status gs_get_history(gs_ctx* ctx, int64_t frame, int64_t* m_t, double* maxdisp_t,
+                         int32_t cap) {
+  if (!ctx) return GS_E_INVALID_PARAMETER;
+  if (!ctx->have_run || frame < 0 || frame >= (int64_t)ctx->hist_m.size())
+    return fail(ctx, GS_E_INVALID_PARAMETER, "no history for this frame (GS_RECORD_HISTORY?)");
+  const auto& hm = ctx->hist_m[frame];
+  const auto& hd = ctx->hist_d[frame];
+  for (int32_t t = 0; t < cap && t < (int32_t)hm.size(); ++t) {
+    if (m_t) m_t[t] = hm[t];
+    if (maxdisp_t) maxdisp_t[t] = hd[t];
+  }
+  return GS_OK;
+}
+
+gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out) {
+  if (!ctx || !out) return GS_E_INVALID_PARAMETER;
+  *out = ctx->stats;
+  return GS_OK;
+}
+
+gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_m,
+                         int64_t* m_out, int64_t* keys, int64_t* counts, double* centroids,
+                         int64_t* slot) {
+  gs_config cfg{h, 1, 0};
+  GS_TRY(validate(in, &cfg));
+  if (!ctx) return GS_E_INVALID_PARAMETER;
+  if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "debug build takes one frame");
+  cudaSetDevice(ctx->device);
+  const int d = in->d;
+  const int64_t n = in->n;
+  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
+  const void* dpts = in->points;
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice,
+                          ctx->stream));
+    dpts = ctx->pts.p;
+  }
+  int64_t m0 = 0;
+  GS_TRY(build_cells(ctx, dpts, in->dtype, d, n, 1, h, &m0));
+  *m_out = m0;
+  if (m0 > cap_m) return fail(ctx, GS_E_INVALID_PARAMETER, "cap_m too small");
+  std::vector<uint32_t> hk(m0), hc(m0);
+  GS_CK(cudaMemcpyAsync(hk.data(), ctx->ckey[0].p, 4 * m0, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(hc.data(), ctx->ccnt[0].p, 4 * m0, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(centroids, ctx->S[0].p, sizeof(double) * m0 * d, cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  GS_TRY(grow(ctx, ctx->dbg, sizeof(int64_t) * n));
+  gs::k_slot_rank<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
+      n, ctx->slot.as<uint32_t>(), ctx->idx.as<int32_t>(), ctx->dbg.as<int64_t>());
+  GS_CK(cudaGetLastError());
+  GS_CK(cudaMemcpyAsync(slot, ctx->dbg.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  gs::k_idx_clear<<<blocks_for(m0, 256), 256, 0, ctx->stream>>>(
+      (int)m0, ctx->ckey[0].as<uint32_t>(), ctx->idx.as<int32_t>());
+  GS_CK(cudaGetLastError());
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  const GsBox& b = ctx->box;
+  for (int64_t i = 0; i < m0; ++i) {
+    int64_t local = hk[i] % b.vol_frame;
+    for (int c = 0; c < d; ++c) keys[i * d + c] = (local / b.stride[c]) % b.ext[c] + b.kmin[c];
+    counts[i] = hc[i];
+  }
+  return GS_OK;
+}
+
+gs_status gs_debug_iterate_once(gs_ctx* ctx, int32_t d, double h, int64_t m, const int64_t* keys,
+                                const int64_t* counts, const double* centroids, int64_t* m_out,
+                                int64_t* keys_out, int64_t* counts_out, double* centroids_out,
+                                double* swept_out, int64_t* parent_out, int32_t* changed_out,
+                                int32_t* converged_out, double* maxdisp_out) {
+  if (!ctx) return GS_E_INVALID_PARAMETER;
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(ctx, GS_E_INVALID_BANDWIDTH, "h");
+  if (m < 1) return fail(ctx, GS_E_EMPTY_INPUT, "m");
+  if (d < 1 || d > GS_MAX_DIM) return fail(ctx, GS_E_INVALID_PARAMETER, "d");
+  cudaSetDevice(ctx->device);
+  GsBox b;
+  GS_TRY(make_box_from_cells(ctx, d, h, m, keys, centroids, &b));
+  ctx->box = b;
+  GS_TRY(ensure_dense(ctx, b.vol_total, d));
+  GS_TRY(ensure_cells(ctx, m, d));
+  GS_TRY(ensure_frames(ctx, 1));
+  GS_TRY(grow(ctx, ctx->errflag, sizeof(int) * 4));
+  GS_TRY(grow(ctx, ctx->counters, sizeof(unsigned int) * 16));
+  GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, sizeof(int) * 4, ctx->stream));
+  std::vector<uint32_t> hk(m), hc(m);
+  std::vector<int32_t> hidx(m);
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t L = 0;
+    for (int c = 0; c < d; ++c) L += (keys[i * d + c] - b.kmin[c]) * b.stride[c];
+    hk[i] = (uint32_t)L;
+    hc[i] = (uint32_t)counts[i];
+    if (i > 0 && hk[i] <= hk[i - 1])
+      return fail(ctx, GS_E_INVALID_INPUT, "injected keys must be strictly lex-sorted");
+  }
+  ctx->cur = 0;
+  GS_CK(cudaMemcpyAsync(ctx->ckey[0].p, hk.data(), 4 * m, cudaMemcpyHostToDevice, ctx->stream));
+  GS_CK(cudaMemcpyAsync(ctx->ccnt[0].p, hc.data(), 4 * m, cudaMemcpyHostToDevice, ctx->stream));
+  GS_CK(cudaMemcpyAsync(ctx->S[0].p, centroids, sizeof(double) * m * d, cudaMemcpyHostToDevice,
+                        ctx->stream));
+  GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t), ctx->stream));
+  gs::k_idx_set<<<blocks_for(m, 256), 256, 0, ctx->stream>>>((int)m, ctx->ckey[0].as<uint32_t>(),
+                                                             ctx->idx.as<int32_t>());
+  GS_CK(cudaGetLastError());
+  int64_t mnew = 0;
+  GS_TRY(iterate(ctx, m, &mnew));
+  int err = 0;
+  GS_TRY(read_err(ctx, &err));
+  if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
+  if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+  std::vector<uint32_t> nk(mnew), nc(mnew);
+  std::vector<int32_t> par(m);
+  int32_t fch = 0, fadj = 0;
+  unsigned long long fd = 0;
+  GS_CK(cudaMemcpyAsync(nk.data(), ctx->ckey[1].p, 4 * mnew, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(nc.data(), ctx->ccnt[1].p, 4 * mnew, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(centroids_out, ctx->S[1].p, sizeof(double) * mnew * d,
+                        cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(swept_out, ctx->S1.p, sizeof(double) * m * d, cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  GS_CK(cudaMemcpyAsync(par.data(), ctx->parent.p, 4 * m, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(&fch, ctx->fchanged.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(&fadj, ctx->fadj.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaMemcpyAsync(&fd, ctx->fdisp.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  gs::k_idx_clear<<<blocks_for(mnew, 256), 256, 0, ctx->stream>>>(
+      (int)mnew, ctx->ckey[1].as<uint32_t>(), ctx->idx.as<int32_t>());
+  GS_CK(cudaGetLastError());
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  *m_out = mnew;
+  for (int64_t g = 0; g < mnew; ++g) {
+    for (int c = 0; c < d; ++c) keys_out[g * d + c] = (nk[g] / b.stride[c]) % b.ext[c] + b.kmin[c];
+    counts_out[g] = nc[g];
+  }
+  for (int64_t i = 0; i < m; ++i) parent_out[i] = par[i];
+  *changed_out = fch;
+  *converged_out = fadj ? 0 : 1;
+  std::memcpy(maxdisp_out, &fd, sizeof(double));
+  ctx->have_run = false;
+  return GS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+"""Python mirror of the reference engine API over the C-ABI (include/gridshift_c.h).
+
+The reference's boundary is the C++ call ``gridshift::run(Dataset, EngineConfig) ->
+ClusterLabeling`` (types :107-114) with the exception
+taxonomy of /root/reference/proj/include/gridshift/errors.hpp.  This module keeps those names
+(``EngineConfig``, ``ClusterLabeling``, ``run``, ``InvalidBandwidthError`` ...) so the parity
+tests read like the reference's own, and routes every call to ``libgridshift_cuda.so``.  There
+is no CPU fallback: without the library or a device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libgridshift_cuda.so")
+
+# ----------------------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """gridshift::Error (errors.hpp:9-11)."""
+
+
+class InvalidInputError(Error):
+    """errors.hpp:14-16."""
+
+
+class InvalidBandwidthError(InvalidInputError):
+    """errors.hpp:18-20 (h <= 0)."""
+
+
+class EmptyInputError(InvalidInputError):
+    """errors.hpp:22-24 (n == 0)."""
+
+
+class InvalidParameterError(InvalidInputError):
+    """errors.hpp:26-28."""
+
+
+class InternalInvariantError(Error):
+    """errors.hpp:31-33."""
+
+
+GS_OK = 0
+_STATUS = {
+    1: InvalidInputError,
+    2: InvalidBandwidthError,
+    3: EmptyInputError,
+    4: InvalidParameterError,
+    5: InternalInvariantError,
+    6: InvalidParameterError,  # GS_E_KEY_RANGE
+    7: Error,  # GS_E_CUDA
+    8: Error,  # GS_E_OOM
+    9: Error,  # GS_E_NCCL
+    10: Error,  # GS_E_NO_DEVICE
+}
+STATUS_NAMES = {
+    0: "GS_OK", 1: "GS_E_INVALID_INPUT", 2: "GS_E_INVALID_BANDWIDTH", 3: "GS_E_EMPTY_INPUT",
+    4: "GS_E_INVALID_PARAMETER", 5: "GS_E_INTERNAL_INVARIANT", 6: "GS_E_KEY_RANGE",
+    7: "GS_E_CUDA", 8: "GS_E_OOM", 9: "GS_E_NCCL", 10: "GS_E_NO_DEVICE",
+}
+
+GS_F32, GS_F64 = 0, 1
+GS_RECORD_HISTORY, GS_DEVICE_OUTPUTS = 0x1, 0x2
+
+# every symbol include/gridshift_c.h declares (checked by tests/test_abi.py)
+EXPORTED = [
+    "gs_validate", "gs_create", "gs_destroy", "gs_run", "gs_get_centroids", "gs_get_history",
+    "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
+    "gs_debug_iterate_once", "gs_fixed_shift",
+]
+
+
+class GsInput(C.Structure):
+    _fields_ = [("points", C.c_void_p), ("n", C.c_int64), ("d", C.c_int32),
+                ("dtype", C.c_int32), ("batch", C.c_int64), ("on_device", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class GsConfig(C.Structure):
+    _fields_ = [("h", C.c_double), ("max_iter", C.c_int32), ("flags", C.c_uint32)]
+
+
+class GsResult(C.Structure):
+    _fields_ = [("labels", C.c_void_p), ("k", C.c_void_p), ("iterations", C.c_void_p),
+                ("converged", C.c_void_p)]
+
+
+class GsStats(C.Structure):
+    _fields_ = [("ms_total", C.c_double), ("ms_bin", C.c_double), ("ms_iterate", C.c_double),
+                ("ms_label", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
+                ("cells_swept", C.c_int64), ("m0", C.c_int64), ("k_total", C.c_int64),
+                ("kernel_launches", C.c_int64), ("max_iterations", C.c_int32),
+                ("fixed_shift", C.c_int32), ("dense_cells", C.c_int64),
+                ("ms_k_bin", C.c_double), ("ms_k_label", C.c_double), ("lib_calls", C.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libgridshift_cuda.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise Error(f"{path} missing: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    lib.gs_validate.argtypes = [C.POINTER(GsInput), C.POINTER(GsConfig)]
+    lib.gs_create.argtypes = [C.c_int, P, C.POINTER(P)]
+    lib.gs_destroy.argtypes = [P]
+    lib.gs_destroy.restype = None
+    lib.gs_run.argtypes = [P, C.POINTER(GsInput), C.POINTER(GsConfig), C.POINTER(GsResult)]
+    lib.gs_get_centroids.argtypes = [P, I64, P, I64]
+    lib.gs_get_history.argtypes = [P, I64, P, P, I32]
+    lib.gs_get_stats.argtypes = [P, C.POINTER(GsStats)]
+    lib.gs_last_error.argtypes = [P]
+    lib.gs_last_error.restype = C.c_char_p
+    lib.gs_status_string.argtypes = [C.c_int]
+    lib.gs_status_string.restype = C.c_char_p
+    lib.gs_debug_build.argtypes = [P, C.POINTER(GsInput), D, I64, P, P, P, P, P]
+    lib.gs_debug_iterate_once.argtypes = [P, I32, D, I64, P, P, P, P, P, P, P, P, P, P, P, P]
+    lib.gs_fixed_shift.argtypes = [I64, D]
+    lib.gs_fixed_shift.restype = I32
+    _lib = lib
+    return lib
+
+
+def _raise(status: int, detail: str = "") -> None:
+    if status == GS_OK:
+        return
+    exc = _STATUS.get(status, Error)
+    raise exc(f"{STATUS_NAMES.get(status, status)}: {detail}")
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ----------------------------------------------------------------------------- types
+@dataclass
+class EngineConfig:
+    """SPEC.md:111-114."""
+    h: float
+    max_iterations: int = 1000
+    record_history: bool = False
+
+
+@dataclass
+class ClusterLabeling:
+    """SPEC.md:107-110 (one frame)."""
+    labels: np.ndarray
+    centroids: np.ndarray
+    iterations: int
+    converged: bool
+    history: Optional[List[tuple]] = None
+
+
+@dataclass
+class BatchLabeling:
+    labels: np.ndarray          # [batch, n] int32
+    k: np.ndarray               # [batch] int64
+    iterations: np.ndarray      # [batch] int32
+    converged: np.ndarray       # [batch] int32
+    centroids: List[np.ndarray] = field(default_factory=list)
+    history: Optional[List[List[tuple]]] = None
+
+
+def validate(n: int, d: int, h: float, max_iter: int = 1000, batch: int = 1,
+             dtype: int = GS_F64) -> None:
+    """Host-only contract check through gs_validate (no device needed)."""
+    lib = load_library()
+    dummy = C.c_double(0.0)
+    inp = GsInput(C.addressof(dummy), n, d, dtype, batch, 0, 0)
+    cfg = GsConfig(h, max_iter, 0)
+    _raise(lib.gs_validate(C.byref(inp), C.byref(cfg)), "gs_validate")
+
+
+class Engine:
+    """A GridShift engine bound to one CUDA device (owns a gs_ctx)."""
+
+    def __init__(self, device: int = 0, stream: int = 0):
+        self._lib = load_library()
+        h = C.c_void_p()
+        _raise(self._lib.gs_create(device, C.c_void_p(stream or None), C.byref(h)), "gs_create")
+        self._ctx = h
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            self._lib.gs_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_error(self) -> str:
+        return self._lib.gs_last_error(self._ctx).decode()
+
+    def _check(self, status: int) -> None:
+        if status != GS_OK:
+            _raise(status, self.last_error())
+
+    # -- raw run over host numpy or device pointers --------------------------------------
+    def run_raw(self, points_ptr: int, n: int, d: int, dtype: int, batch: int, on_device: bool,
+                cfg: EngineConfig, labels_ptr: int, device_outputs: bool = False):
+        k = np.zeros(batch, np.int64)
+        it = np.zeros(batch, np.int32)
+        cv = np.zeros(batch, np.int32)
+        flags = (GS_RECORD_HISTORY if cfg.record_history else 0) | (
+            GS_DEVICE_OUTPUTS if device_outputs else 0)
+        inp = GsInput(points_ptr, n, d, dtype, batch, 1 if on_device else 0, 0)
+        c = GsConfig(cfg.h, cfg.max_iterations, flags)
+        res = GsResult(labels_ptr, _ptr(k), _ptr(it), _ptr(cv))
+        self._check(self._lib.gs_run(self._ctx, C.byref(inp), C.byref(c), C.byref(res)))
+        return k, it, cv
+
+    def run_batch(self, X: np.ndarray, cfg: EngineConfig, want_centroids: bool = True
+                  ) -> BatchLabeling:
+        """Independent frames X[batch, n, d] (float32 or float64, host memory)."""
+        X = np.ascontiguousarray(X)
+        if X.ndim == 2:
+            X = X[None]
+        if X.ndim != 3:
+            raise InvalidParameterError("X must be [n, d] or [batch, n, d]")
+        if X.dtype == np.float32:
+            dt = GS_F32
+        elif X.dtype == np.float64:
+            dt = GS_F64
+        else:
+            X = X.astype(np.float64)
+            dt = GS_F64
+        b, n, d = X.shape
+        labels = np.zeros((b, n), np.int32)
+        k, it, cv = self.run_raw(_ptr(X), n, d, dt, b, False, cfg, _ptr(labels))
+        out = BatchLabeling(labels, k, it, cv)
+        if want_centroids:
+            for f in range(b):
+                out.centroids.append(self.centroids(f, int(k[f]), d))
+        if cfg.record_history:
+            out.history = [self.history(f, int(it[f])) for f in range(b)]
+        return out
+
+    def run(self, X: np.ndarray, cfg: EngineConfig) -> ClusterLabeling:
+        """engine.run on one dataset X[n, d]."""
+        X = np.asarray(X)
+        if X.ndim != 2:
+            raise InvalidParameterError("X must be [n, d]")
+        r = self.run_batch(X[None], cfg)
+        return ClusterLabeling(r.labels[0], r.centroids[0], int(r.iterations[0]),
+                               bool(r.converged[0]), r.history[0] if r.history else None)
+
+    def centroids(self, frame: int, k: int, d: int) -> np.ndarray:
+        out = np.zeros((k, d), np.float64)
+        self._check(self._lib.gs_get_centroids(self._ctx, frame, _ptr(out), k))
+        return out
+
+    def history(self, frame: int, iters: int) -> List[tuple]:
+        m = np.zeros(max(iters, 1), np.int64)
+        dsp = np.zeros(max(iters, 1), np.float64)
+        self._check(self._lib.gs_get_history(self._ctx, frame, _ptr(m), _ptr(dsp), iters))
+        return [(int(m[t]), float(dsp[t])) for t in range(iters)]
+
+    def stats(self) -> dict:
+        s = GsStats()
+        self._check(self._lib.gs_get_stats(self._ctx, C.byref(s)))
+        return {name: getattr(s, name) for name, _ in GsStats._fields_}
+
+    # -- test hooks --------------------------------------------------------------------------
+    def debug_build(self, X: np.ndarray, h: float):
+        X = np.ascontiguousarray(X)
+        n, d = X.shape
+        dt = GS_F32 if X.dtype == np.float32 else GS_F64
+        if dt == GS_F64:
+            X = X.astype(np.float64)
+        cap = n
+        keys = np.zeros((cap, d), np.int64)
+        counts = np.zeros(cap, np.int64)
+        cent = np.zeros((cap, d), np.float64)
+        slot = np.zeros(n, np.int64)
+        m = C.c_int64()
+        inp = GsInput(_ptr(X), n, d, dt, 1, 0, 0)
+        self._check(self._lib.gs_debug_build(self._ctx, C.byref(inp), h, cap, C.byref(m),
+                                             _ptr(keys), _ptr(counts), _ptr(cent), _ptr(slot)))
+        m = m.value
+        return keys[:m], counts[:m], cent[:m], slot
+
+    def debug_iterate_once(self, keys: np.ndarray, counts: np.ndarray, cent: np.ndarray,
+                           h: float) -> dict:
+        keys = np.ascontiguousarray(keys, np.int64)
+        counts = np.ascontiguousarray(counts, np.int64)
+        cent = np.ascontiguousarray(cent, np.float64)
+        m, d = keys.shape
+        ko = np.zeros((m, d), np.int64)
+        co = np.zeros(m, np.int64)
+        so = np.zeros((m, d), np.float64)
+        sw = np.zeros((m, d), np.float64)
+        par = np.zeros(m, np.int64)
+        mo = C.c_int64()
+        ch = C.c_int32()
+        cv = C.c_int32()
+        md = C.c_double()
+        self._check(self._lib.gs_debug_iterate_once(
+            self._ctx, d, h, m, _ptr(keys), _ptr(counts), _ptr(cent), C.byref(mo), _ptr(ko),
+            _ptr(co), _ptr(so), _ptr(sw), _ptr(par), C.byref(ch), C.byref(cv), C.byref(md)))
+        mn = mo.value
+        return dict(keys=ko[:mn], counts=co[:mn], centroids=so[:mn], swept=sw, parent=par,
+                    changed=bool(ch.value), converged=bool(cv.value), maxdisp=md.value)
+
+
+_default_engine: Optional[Engine] = None
+
+
+def run(X, cfg: EngineConfig) -> ClusterLabeling:
+    """engine.run(X, cfg) on device 0."""
+    if not (cfg.h > 0) or not np.isfinite(cfg.h):
+        raise InvalidBandwidthError("h must be > 0")
+    X = np.asarray(X, dtype=np.float64 if np.asarray(X).dtype != np.float32 else np.float32)
+    if X.size == 0:
+        raise EmptyInputError("empty dataset")
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine(0)
+    return _default_engine.run(X, cfg)
+
+
+def fixed_shift(n: int, h: float) -> int:
+    return int(load_library().gs_fixed_shift(n, h))

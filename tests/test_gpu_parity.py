@@ -1,0 +1,169 @@
+"""GPU engine vs the CPU oracle on identical seeded inputs.
+
+Two oracles (oracle/gs_oracle.cpp):
+  * build mode "fixed" shares the engine's fixed-point binning definition; everything after
+    binning is the SPEC's sweep/merge/termination.  The GPU must match it BIT-EXACTLY:
+    keys, counts, centroids, parent structure, iterations, labels.
+  * build mode "spec" is the literal SPEC (incremental-mean binning).  The GPU must match it
+    within north_star's tolerances: centroids <= 1e-5 relative, labels >= 99.9 % after an
+    optimal permutation match.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2206_02200_b200 import configs as CF
+from paper_2206_02200_b200 import gridshift as G
+from tests.parity_util import matched_agreement, oracle_states
+
+pytestmark = pytest.mark.gpu
+
+CENTROID_RTOL = 1e-5      # north_star: centroids within 1e-5 relative
+LABEL_AGREEMENT = 0.999   # north_star: >= 99.9 % after optimal permutation match
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.int64)
+
+
+def assert_state_equal(gpu, ora, what=""):
+    assert np.array_equal(gpu[0], ora[0]), f"{what}: keys differ"
+    assert np.array_equal(gpu[1], ora[1]), f"{what}: counts differ"
+    assert np.array_equal(_bits(gpu[2]), _bits(ora[2])), f"{what}: centroids differ (bits)"
+
+
+def small_inputs():
+    """(name, X, h) small cases: configs at reduced size plus adversarial ones."""
+    out = []
+    out.append(("cfg1", CF.generate("cfg1")[0], 0.5))
+    out.append(("cfg2", CF.generate("cfg2")[0], 0.08))
+    out.append(("cfg3_small", CF.generate("cfg3", scale=0.05)[0], 0.06))
+    out.append(("cfg4_frame", CF.generate("cfg4", scale=0.25, frames=1)[0], 0.08))
+    out.append(("cfg5_small", CF.generate("cfg5", scale=1 / 256)[0], 1.0))
+    rng = np.random.default_rng(1)
+    # boundary points: exact multiples of h, negatives, duplicates
+    g = np.repeat(np.arange(-6, 7, dtype=np.float64) * 0.25, 3)
+    out.append(("boundaries", np.stack([g, g[::-1]], 1), 0.25))
+    out.append(("negative", rng.normal(-50.0, 3.0, size=(3000, 3)), 1.5))
+    out.append(("duplicates", np.repeat(rng.uniform(0, 1, size=(20, 2)), 50, 0), 0.1))
+    out.append(("d1", rng.normal(0, 1, size=(5000, 1)), 0.2))
+    out.append(("d4", rng.normal(0, 1, size=(4000, 4)), 0.6))
+    out.append(("d6", rng.normal(0, 1, size=(3000, 6)), 0.9))
+    out.append(("single", np.array([[1.0, 2.0, 3.0]]), 0.3))
+    return out
+
+
+@pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
+def test_build_bit_exact(engine, case):
+    name, X, h = case
+    g = engine.debug_build(X, h)
+    o = O.build_grid(X.astype(np.float64), h, O.BUILD_FIXED)
+    assert_state_equal(g[:3], o[:3], name)
+    assert np.array_equal(g[3], o[3]), "point -> cell rank differs"
+
+
+@pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
+def test_state_injection_bit_exact(engine, case):
+    """Feed the GPU the oracle's iteration-t state; iteration t+1 must be identical bitwise."""
+    name, X, h = case
+    states = oracle_states(X.astype(np.float64), h, steps=30)
+    for t, (keys, cnt, cen) in enumerate(states):
+        o = O.iterate_once(keys, cnt, cen, h)
+        g = engine.debug_iterate_once(keys, cnt, cen, h)
+        assert np.array_equal(_bits(g["swept"]), _bits(o["swept"])), f"{name} t={t}: sweep"
+        assert_state_equal((g["keys"], g["counts"], g["centroids"]),
+                           (o["keys"], o["counts"], o["centroids"]), f"{name} t={t}")
+        assert np.array_equal(g["parent"], o["parent"]), f"{name} t={t}: parent"
+        assert g["changed"] == o["changed"] and g["converged"] == o["converged"]
+        assert g["maxdisp"] == o["maxdisp"]
+
+
+def _check_run(engine, X, h, max_iter, name):
+    cfg = G.EngineConfig(h, max_iter, record_history=True)
+    g = engine.run(X, cfg)
+    ofx = O.run(X.astype(np.float64), h, max_iter, O.BUILD_FIXED)
+    # bit-exact against the fixed-point-build oracle
+    assert g.iterations == ofx["iterations"], name
+    assert g.converged == ofx["converged"]
+    assert np.array_equal(g.labels, ofx["labels"]), f"{name}: labels"
+    assert np.array_equal(_bits(g.centroids), _bits(ofx["centroids"])), f"{name}: centroids"
+    assert g.history == ofx["history"], f"{name}: history"
+    # tolerance parity against the literal SPEC oracle
+    osp = O.run(X.astype(np.float64), h, max_iter, O.BUILD_SPEC)
+    agree, match = matched_agreement(g.labels, osp["labels"])
+    assert agree >= LABEL_AGREEMENT, f"{name}: label agreement {agree}"
+    for a, b in match.items():
+        np.testing.assert_allclose(g.centroids[a], osp["centroids"][b], rtol=CENTROID_RTOL,
+                                   atol=CENTROID_RTOL * np.abs(X).max())
+    return g
+
+
+@pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
+def test_run_parity(engine, case):
+    name, X, h = case
+    _check_run(engine, X, h, 300, name)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_config_full_size(engine, name):
+    cfg = CF.CONFIGS[name]
+    X = CF.generate(name)[0]
+    _check_run(engine, X, cfg.h, cfg.max_iter, name)
+
+
+def test_batched_frames_heterogeneous(engine):
+    """Frames finish at different iterations; each must equal its own independent run."""
+    n = 4000
+    rng = np.random.default_rng(3)
+    frames = [
+        np.full((n, 3), 0.5, np.float32),                                   # one cell, 1 iter
+        CF.generate("cfg2", scale=n / 154401.0)[0][:n].astype(np.float32),  # image
+        rng.normal(0, 0.3, size=(n, 3)).astype(np.float32),                 # one blob
+        rng.uniform(0, 1, size=(n, 3)).astype(np.float32),                  # uniform cube
+    ]
+    frames[1] = np.resize(frames[1], (n, 3))
+    X = np.stack(frames)
+    h = 0.08
+    r = engine.run_batch(X, G.EngineConfig(h, 100, record_history=True))
+    for f in range(len(frames)):
+        o = O.run(X[f].astype(np.float64), h, 100, O.BUILD_FIXED)
+        assert r.k[f] == o["k"] and r.iterations[f] == o["iterations"], f
+        assert np.array_equal(r.labels[f], o["labels"]), f
+        assert np.array_equal(_bits(r.centroids[f]), _bits(o["centroids"])), f
+        assert r.history[f] == o["history"]
+
+
+def test_cfg4_frames_sampled(engine):
+    """cfg4 at full frame size, 16 consecutive frames batched; every frame vs the oracle."""
+    cfg = CF.CONFIGS["cfg4"]
+    X = CF.generate("cfg4", frames=16, frame0=100)
+    r = engine.run_batch(X, G.EngineConfig(cfg.h, cfg.max_iter))
+    for f in range(X.shape[0]):
+        o = O.run(X[f].astype(np.float64), cfg.h, cfg.max_iter, O.BUILD_FIXED)
+        assert r.k[f] == o["k"] and r.iterations[f] == o["iterations"]
+        assert np.array_equal(r.labels[f], o["labels"])
+        assert np.array_equal(_bits(r.centroids[f]), _bits(o["centroids"]))
+
+
+def test_determinism(engine):
+    X = CF.generate("cfg2")[0]
+    a = engine.run(X, G.EngineConfig(0.08, 100))
+    b = engine.run(X, G.EngineConfig(0.08, 100))
+    assert np.array_equal(a.labels, b.labels)
+    assert np.array_equal(_bits(a.centroids), _bits(b.centroids))
+
+
+def test_random_property_bit_exact(engine):
+    rng = np.random.default_rng(11)
+    for trial in range(25):
+        d = int(rng.integers(1, 6))
+        n = int(rng.integers(1, 3000))
+        X = rng.normal(size=(n, d)) * rng.uniform(0.1, 5) + rng.uniform(-20, 20)
+        if trial % 3 == 0:
+            X = X.astype(np.float32)
+        h = float(rng.uniform(0.05, 2.0))
+        g = engine.run(X, G.EngineConfig(h, 500))
+        o = O.run(np.asarray(X, np.float64), h, 500, O.BUILD_FIXED)
+        assert np.array_equal(g.labels, o["labels"]), trial
+        assert np.array_equal(_bits(g.centroids), _bits(o["centroids"])), trial
+        assert g.iterations == o["iterations"]
