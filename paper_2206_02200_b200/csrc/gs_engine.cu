@@ -523,7 +523,6 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     int err = 0;
     GS_TRY(read_err(ctx, &err));
     if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
-    if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
   if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
     ++iter;
     for (int64_t f = 0; f < nf; ++f) {
