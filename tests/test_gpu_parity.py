@@ -162,6 +162,12 @@ def test_random_property_bit_exact(engine):
         if trial % 3 == 0:
             X = X.astype(np.float32)
         h = float(rng.uniform(0.05, 2.0))
+        span = (X.max(0) - X.min(0)) / h + 5
+        if np.prod(span) > 2 ** 27:
+            # the dense cell grid covers boxes up to 2^28 cells; wider boxes are refused loudly
+            with pytest.raises(G.InvalidParameterError):
+                engine.run(X, G.EngineConfig(h, 500))
+            continue
         g = engine.run(X, G.EngineConfig(h, 500))
         o = O.run(np.asarray(X, np.float64), h, 500, O.BUILD_FIXED)
         assert np.array_equal(g.labels, o["labels"]), trial
