@@ -57,6 +57,7 @@ typedef struct {
 
 #define GS_RECORD_HISTORY 0x1u  /* keep per-iteration (m, max displacement)   */
 #define GS_DEVICE_OUTPUTS 0x2u  /* result.labels is a device pointer                          */
+#define GS_DEBUG_GLOBAL_PATH 0x80000000u /* test hook: iterate on the multi-CTA path only */
 
 /* EngineConfig. */
 typedef struct {

@@ -19,6 +19,7 @@
 
 #include "../../include/gridshift_c.h"
 #include "gs_kernels.cuh"
+#include "gs_resident.cuh"
 
 namespace {
 
@@ -70,7 +71,8 @@ struct gs_ctx {
       skey, sval, head, sid, segstart, parent, root, initkey;
   int64_t cell_cap = 0, nbl_cap = 0;
   // per frame
-  DevBuf fdone, fchanged, fadj, fm, fdisp, ffirst;
+  DevBuf fdone, fchanged, fadj, fm, fdisp, ffirst, fcount, ifirst, icount, fiters, fconv, fk,
+      hist;
   int64_t frame_cap = 0;
   // misc
   DevBuf counters, errflag, bpart, cub_tmp, dbg;
@@ -208,7 +210,8 @@ gs_status ensure_cells(gs_ctx* ctx, int64_t m, int d) {
 
 gs_status ensure_frames(gs_ctx* ctx, int64_t nf) {
   if (nf <= ctx->frame_cap) return GS_OK;
-  for (DevBuf* b : {&ctx->fdone, &ctx->fchanged, &ctx->fadj, &ctx->fm, &ctx->ffirst})
+  for (DevBuf* b : {&ctx->fdone, &ctx->fchanged, &ctx->fadj, &ctx->fm, &ctx->ffirst, &ctx->fcount,
+                    &ctx->ifirst, &ctx->icount, &ctx->fiters, &ctx->fconv, &ctx->fk})
     GS_TRY(grow(ctx, *b, sizeof(int32_t) * nf));
   GS_TRY(grow(ctx, ctx->fdisp, sizeof(unsigned long long) * nf));
   ctx->frame_cap = nf;
@@ -471,6 +474,57 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   return GS_OK;
 }
 
+// ---- K8 launch helpers
+constexpr size_t kResidentSmemBudget = 200 * 1024;
+
+size_t resident_smem_bytes(int d, int ms, int pool_cap) {
+  return (size_t)ms * gs::resident_bytes_per_cell(d) + (size_t)pool_cap * 2 + 64;
+}
+
+// Largest power-of-two cell capacity whose state + neighbour pool fit the smem budget.
+int resident_capacity(int d, int* pool_cap, size_t* smem) {
+  const int64_t K = ipow3(d);
+  const int kp = (int)std::min<int64_t>(K, 32);
+  for (int ms = 2048; ms >= 32; ms >>= 1) {
+    const size_t bytes = resident_smem_bytes(d, ms, ms * kp);
+    if (bytes <= kResidentSmemBudget) {
+      *pool_cap = ms * kp;
+      *smem = bytes;
+      return ms;
+    }
+  }
+  *pool_cap = 32 * kp;
+  *smem = resident_smem_bytes(d, 32, 32 * kp);
+  return 32;
+}
+
+template <int D>
+gs_status launch_resident_d(gs_ctx* ctx, unsigned grid, int threads, size_t smem,
+                            const gs::ResidentArgs& ra) {
+  static bool configured = false;
+  if (!configured) {
+    GS_CK(cudaFuncSetAttribute(gs::k_resident<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kResidentSmemBudget + 1024));
+    configured = true;
+  }
+  gs::k_resident<D><<<grid, threads, smem, ctx->stream>>>(ra);
+  GS_LAUNCHED("k_resident");
+  return GS_OK;
+}
+
+gs_status launch_resident(gs_ctx* ctx, int d, unsigned grid, int threads, size_t smem,
+                          const gs::ResidentArgs& ra) {
+  switch (d) {
+#define GS_CASE(D) \
+  case D:          \
+    return launch_resident_d<D>(ctx, grid, threads, smem, ra);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+    GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
+#undef GS_CASE
+  }
+  return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
+}
+
 gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
   GS_TRY(validate(in, cfg));
   if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
@@ -496,6 +550,9 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   GS_CK(cudaEventRecord(ctx->ev[2], st));
   const GsBox& b = ctx->box;
   // ---- iteration phase
+  // (a) global path (K4/K5 kernels, host-driven) while some live frame has more active cells
+  //     than one CTA's shared memory holds; (b) then the CTA-resident engine K8 runs every
+  //     remaining iteration of every frame on the device.
   ctx->h_done.assign(nf, 0);
   ctx->h_iters.assign(nf, 0);
   ctx->h_conv.assign(nf, 0);
@@ -503,27 +560,62 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ctx->hist_m.assign(rec ? nf : 0, {});
   ctx->hist_d.assign(rec ? nf : 0, {});
   GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
-  std::vector<int32_t> fch(nf), fadj(nf), fm(nf);
+  std::vector<int32_t> fch(nf), fadj(nf), fm(nf), fcnt(nf);
   std::vector<unsigned long long> fdisp(nf);
   int64_t m = m0, live = nf, swept = 0;
   int iter = 0;
-  while (live > 0) {
+  // initial per-frame cell ranges (root entries of frame f live in [ifirst_f, +icount_f))
+  gs::k_frame_ranges<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, b.vol_frame,
+                                                          ctx->ckey[0].as<uint32_t>(),
+                                                          ctx->ifirst.as<int32_t>(),
+                                                          ctx->icount.as<int32_t>());
+  GS_LAUNCHED("k_frame_ranges");
+  gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ifirst.as<int32_t>(),
+                                                          ctx->icount.as<int32_t>());
+  GS_LAUNCHED("k_frame_counts");
+  GS_CK(cudaMemcpyAsync(ctx->ffirst.p, ctx->ifirst.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->fcount.p, ctx->icount.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToDevice, st));
+  GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->icount.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
+                        st));
+  GS_CK(cudaStreamSynchronize(st));
+  int pool_cap = 0;
+  size_t rs_smem = 0;
+  const int ms_cap = resident_capacity(d, &pool_cap, &rs_smem);
+  auto max_live = [&]() {
+    int64_t mx = 0;
+    for (int64_t f = 0; f < nf; ++f)
+      if (!ctx->h_done[f]) mx = std::max<int64_t>(mx, fcnt[f]);
+    return mx;
+  };
+  const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
+  while (live > 0 && (force_global || max_live() > ms_cap)) {
     int64_t mnew = 0;
     GS_TRY(iterate(ctx, m, &mnew));
     gs::k_compose<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->parent.as<int32_t>(),
                                                         ctx->root.as<int32_t>());
     GS_LAUNCHED("k_compose");
+    gs::k_frame_ranges<<<blocks_for(mnew, 256), 256, 0, st>>>(
+        (int)mnew, b.vol_frame, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->ffirst.as<int32_t>(),
+        ctx->fcount.as<int32_t>());
+    GS_LAUNCHED("k_frame_ranges");
+    gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ffirst.as<int32_t>(),
+                                                            ctx->fcount.as<int32_t>());
+    GS_LAUNCHED("k_frame_counts");
     GS_CK(cudaMemcpyAsync(fch.data(), ctx->fchanged.p, sizeof(int32_t) * nf,
                           cudaMemcpyDeviceToHost, st));
     GS_CK(cudaMemcpyAsync(fadj.data(), ctx->fadj.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
                           st));
     GS_CK(cudaMemcpyAsync(fm.data(), ctx->fm.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->fcount.p, sizeof(int32_t) * nf,
+                          cudaMemcpyDeviceToHost, st));
     GS_CK(cudaMemcpyAsync(fdisp.data(), ctx->fdisp.p, sizeof(unsigned long long) * nf,
                           cudaMemcpyDeviceToHost, st));
     int err = 0;
     GS_TRY(read_err(ctx, &err));
     if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
-  if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+    if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
     ++iter;
     for (int64_t f = 0; f < nf; ++f) {
       if (ctx->h_done[f]) continue;
@@ -543,23 +635,59 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       }
     }
     m = mnew;
-    if (live > 0)
-      GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
-                            cudaMemcpyHostToDevice, st));
+    GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
+                          cudaMemcpyHostToDevice, st));
   }
+  // hand-off: K8 finishes every frame (frames already done are copied out unchanged)
+  std::vector<int32_t> g_iters = ctx->h_iters;
+  GS_CK(cudaMemcpyAsync(ctx->fiters.p, ctx->h_iters.data(), sizeof(int32_t) * nf,
+                        cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->fconv.p, ctx->h_conv.data(), sizeof(int32_t) * nf,
+                        cudaMemcpyHostToDevice, st));
+  GS_TRY(grow(ctx, ctx->hist, (sizeof(int64_t) + sizeof(double)) * nf * cfg->max_iter));
+  const int64_t ml = std::max<int64_t>(1, max_live());
+  int ms_run = 32;
+  while (ms_run < ml) ms_run <<= 1;
+  ms_run = std::min(ms_run, ms_cap);
+  const int threads = std::min(1024, std::max(128, ms_run));
+  const int fin = 1 - ctx->cur;
+  gs::ResidentArgs ra;
+  ra.box = b;
+  ra.ms = ms_run;
+  ra.pool_cap = (int)((int64_t)pool_cap * ms_run / ms_cap);
+  ra.max_iter = cfg->max_iter;
+  ra.record = 1;  // m_t feeds the cells x iterations counter even without GS_RECORD_HISTORY
+  ra.ckey = ctx->ckey[ctx->cur].as<uint32_t>();
+  ra.ccnt = ctx->ccnt[ctx->cur].as<uint32_t>();
+  ra.S = ctx->S[ctx->cur].as<double>();
+  ra.ffirst = ctx->ffirst.as<int32_t>();
+  ra.fcount = ctx->fcount.as<int32_t>();
+  ra.ifirst = ctx->ifirst.as<int32_t>();
+  ra.icount = ctx->icount.as<int32_t>();
+  ra.fdone = ctx->fdone.as<int32_t>();
+  ra.fiters = ctx->fiters.as<int32_t>();
+  ra.fconv = ctx->fconv.as<int32_t>();
+  ra.fk = ctx->fk.as<int32_t>();
+  ra.okey = ctx->ckey[fin].as<uint32_t>();
+  ra.ocnt = ctx->ccnt[fin].as<uint32_t>();
+  ra.oS = ctx->S[fin].as<double>();
+  ra.root = ctx->root.as<int32_t>();
+  ra.hist_m = ctx->hist.as<int64_t>();
+  ra.hist_d = (double*)(ctx->hist.as<int64_t>() + nf * cfg->max_iter);
+  ra.err = ctx->errflag.as<int>();
+  const size_t smem = resident_smem_bytes(d, ms_run, ra.pool_cap);
+  GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, smem, ra));
+  // the global index is not used after the hand-off: restore its clean invariant now
+  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[ctx->cur].as<uint32_t>(),
+                                                      ctx->idx.as<int32_t>());
+  GS_LAUNCHED("k_idx_clear");
+  ctx->cur = fin;
   GS_CK(cudaEventRecord(ctx->ev[3], st));
   // ---- labels
-  const int cur = ctx->cur;
-  gs::k_frame_first<<<blocks_for(m, 256), 256, 0, st>>>((int)m, b.vol_frame,
-                                                        ctx->ckey[cur].as<uint32_t>(),
-                                                        ctx->ffirst.as<int32_t>());
-  GS_LAUNCHED("k_frame_first");
-  gs::k_labtab<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, b.vol_frame,
-                                                    ctx->initkey.as<uint32_t>(),
-                                                    ctx->root.as<int32_t>(),
-                                                    ctx->ffirst.as<int32_t>(),
-                                                    ctx->lab.as<int32_t>());
-  GS_LAUNCHED("k_labtab");
+  gs::k_labtab_local<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->initkey.as<uint32_t>(),
+                                                          ctx->root.as<int32_t>(),
+                                                          ctx->lab.as<int32_t>());
+  GS_LAUNCHED("k_labtab_local");
   int32_t* dlabels = out->labels;
   const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
   if (!dev_out) {
@@ -577,22 +705,47 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
                           st));
   GS_CK(cudaEventRecord(ctx->ev[5], st));
   ctx->h_ffirst.assign(nf, 0);
+  std::vector<int32_t> hk(nf);
   GS_CK(cudaMemcpyAsync(ctx->h_ffirst.data(), ctx->ffirst.p, sizeof(int32_t) * nf,
                         cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaStreamSynchronize(st));
-  // restore the clean index invariant for the next run
-  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[cur].as<uint32_t>(),
-                                                      ctx->idx.as<int32_t>());
-  GS_CK(cudaGetLastError());
-  ctx->k_total = m;
+  GS_CK(cudaMemcpyAsync(hk.data(), ctx->fk.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(ctx->h_iters.data(), ctx->fiters.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(ctx->h_conv.data(), ctx->fconv.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> hm;
+  std::vector<double> hd;
+  {
+    hm.resize((size_t)nf * cfg->max_iter);
+    hd.resize((size_t)nf * cfg->max_iter);
+    GS_CK(cudaMemcpyAsync(hm.data(), ra.hist_m, sizeof(int64_t) * hm.size(),
+                          cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(hd.data(), ra.hist_d, sizeof(double) * hd.size(),
+                          cudaMemcpyDeviceToHost, st));
+  }
+  int err = 0;
+  GS_TRY(read_err(ctx, &err));
+  if (err & 16) return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
+  if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+  int64_t ktot = 0;
   ctx->h_k.assign(nf, 0);
   for (int64_t f = 0; f < nf; ++f) {
-    const int64_t end = (f + 1 < nf) ? ctx->h_ffirst[f + 1] : m;
-    ctx->h_k[f] = end - ctx->h_ffirst[f];
+    ctx->h_k[f] = hk[f];
+    ktot += hk[f];
     out->k[f] = ctx->h_k[f];
     out->iterations[f] = ctx->h_iters[f];
     out->converged[f] = ctx->h_conv[f];
+    for (int t = g_iters[f]; t < ctx->h_iters[f]; ++t) {
+      const int64_t mt = hm[(size_t)f * cfg->max_iter + t];
+      swept += mt;
+      if (rec) {
+        ctx->hist_m[f].push_back(mt);
+        ctx->hist_d[f].push_back(hd[(size_t)f * cfg->max_iter + t]);
+      }
+    }
   }
+  ctx->k_total = ktot;
+  m = ktot;
   ctx->nframes = nf;
   ctx->have_run = true;
   float ms = 0;
@@ -693,7 +846,8 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->nbn, &ctx->nbe, &ctx->den, &ctx->flag, &ctx->nkey, &ctx->vals,
                     &ctx->skey, &ctx->sval, &ctx->head, &ctx->sid, &ctx->segstart, &ctx->parent,
                     &ctx->root, &ctx->initkey, &ctx->fdone, &ctx->fchanged, &ctx->fadj,
-                    &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->counters, &ctx->errflag,
+                    &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->fcount, &ctx->ifirst, &ctx->icount,
+                    &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->hist, &ctx->counters, &ctx->errflag,
                     &ctx->bpart, &ctx->cub_tmp, &ctx->dbg})
     b->release();
   for (auto& e : ctx->ev)

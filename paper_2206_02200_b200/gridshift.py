@@ -65,6 +65,7 @@ STATUS_NAMES = {
 
 GS_F32, GS_F64 = 0, 1
 GS_RECORD_HISTORY, GS_DEVICE_OUTPUTS = 0x1, 0x2
+GS_DEBUG_GLOBAL_PATH = 0x80000000
 
 # every symbol include/gridshift_c.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -148,6 +149,7 @@ class EngineConfig:
     h: float
     max_iterations: int = 1000
     record_history: bool = False
+    debug_flags: int = 0          # test hooks (GS_DEBUG_GLOBAL_PATH)
 
 
 @dataclass
@@ -214,7 +216,7 @@ class Engine:
         it = np.zeros(batch, np.int32)
         cv = np.zeros(batch, np.int32)
         flags = (GS_RECORD_HISTORY if cfg.record_history else 0) | (
-            GS_DEVICE_OUTPUTS if device_outputs else 0)
+            GS_DEVICE_OUTPUTS if device_outputs else 0) | cfg.debug_flags
         inp = GsInput(points_ptr, n, d, dtype, batch, 1 if on_device else 0, 0)
         c = GsConfig(cfg.h, cfg.max_iterations, flags)
         res = GsResult(labels_ptr, _ptr(k), _ptr(it), _ptr(cv))

@@ -78,8 +78,8 @@ def test_state_injection_bit_exact(engine, case):
         assert g["maxdisp"] == o["maxdisp"]
 
 
-def _check_run(engine, X, h, max_iter, name):
-    cfg = G.EngineConfig(h, max_iter, record_history=True)
+def _check_run(engine, X, h, max_iter, name, flags=0):
+    cfg = G.EngineConfig(h, max_iter, record_history=True, debug_flags=flags)
     g = engine.run(X, cfg)
     ofx = O.run(X.astype(np.float64), h, max_iter, O.BUILD_FIXED)
     # bit-exact against the fixed-point-build oracle
@@ -100,8 +100,16 @@ def _check_run(engine, X, h, max_iter, name):
 
 @pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
 def test_run_parity(engine, case):
+    """Default schedule: CTA-resident engine (K8), global path first when a frame is large."""
     name, X, h = case
     _check_run(engine, X, h, 300, name)
+
+
+@pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
+def test_run_parity_global_path(engine, case):
+    """Every iteration on the multi-CTA global path (K4/K5 kernels)."""
+    name, X, h = case
+    _check_run(engine, X, h, 300, name, flags=G.GS_DEBUG_GLOBAL_PATH)
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
@@ -162,8 +170,9 @@ def test_random_property_bit_exact(engine):
         if trial % 3 == 0:
             X = X.astype(np.float32)
         h = float(rng.uniform(0.05, 2.0))
-        span = (X.max(0) - X.min(0)) / h + 5
-        if np.prod(span) > 2 ** 27:
+        Xd = np.asarray(X, np.float64)
+        ext = np.floor(Xd.max(0) / h) - np.floor(Xd.min(0) / h) + 5   # engine's box + apron
+        if np.prod(ext) > 2 ** 28:
             # the dense cell grid covers boxes up to 2^28 cells; wider boxes are refused loudly
             with pytest.raises(G.InvalidParameterError):
                 engine.run(X, G.EngineConfig(h, 500))
