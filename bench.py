@@ -281,6 +281,7 @@ def main():
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
                 "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},
         "gpu_launches": launches, "lib_calls": lib_calls,
+        "sweep_modes": s0.get("sweep_modes"), "resident_cycles": s0.get("resident_cycles"),
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -117,6 +117,9 @@ typedef struct {
   double ms_k_bin;       /* the binning kernel K2 alone                                     */
   double ms_k_label;     /* the label kernel K7 alone                                       */
   int64_t lib_calls;     /* library (CUB) device calls, not counted in kernel_launches      */
+  int64_t sweep_modes[3];/* K8 iterations by sweep mode: fast records / slot lists / inline */
+  int64_t resident_cycles[8]; /* K8 SM cycles per phase (census, sweep, rehome, sort, merge,
+                                 hash+converged, -, load), summed over frames */
 } gs_stats;
 gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out);
 

@@ -75,7 +75,7 @@ struct gs_ctx {
       hist;
   int64_t frame_cap = 0;
   // misc
-  DevBuf counters, errflag, bpart, cub_tmp, dbg;
+  DevBuf counters, errflag, bpart, cub_tmp, dbg, modes;
   // last run (host side)
   GsBox box{};
   int64_t nframes = 0;
@@ -307,17 +307,29 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
           ctx->bpart.as<double>() + (size_t)nblk * D, ctx->errflag.as<int>());
     GS_LAUNCHED("k_bounds");
   } else {
+    // privatised binning: one 1024-thread CTA per SM at most, >= 4096 points per CTA
+    constexpr int TBL = gs::bin_table_entries<D>();
+    const size_t smem = (size_t)TBL * (8 * D + 8);
+    static bool configured = false;
+    if (!configured) {
+      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, double>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    const unsigned grid = blocks_for(ntot, 4096, ctx->num_sms);
     if (dtype == GS_F32)
-      gs::k_bin<D, float><<<nblk, 256, 0, ctx->stream>>>(
+      gs::k_bin_priv<D, float><<<grid, 1024, smem, ctx->stream>>>(
           (const float*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
           ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
           ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
     else
-      gs::k_bin<D, double><<<nblk, 256, 0, ctx->stream>>>(
+      gs::k_bin_priv<D, double><<<grid, 1024, smem, ctx->stream>>>(
           (const double*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
           ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
           ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
-    GS_LAUNCHED("k_bin");
+    GS_LAUNCHED("k_bin_priv");
   }
   return GS_OK;
 }
@@ -475,27 +487,16 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
 }
 
 // ---- K8 launch helpers
-constexpr size_t kResidentSmemBudget = 200 * 1024;
+constexpr size_t kResidentSmemBudget = 224 * 1024;  // of 227 KB per CTA (static smem < 1 KB)
+constexpr size_t kResidentStateMax = 140 * 1024;    // cell state may take at most this much
 
-size_t resident_smem_bytes(int d, int ms, int pool_cap) {
-  return (size_t)ms * gs::resident_bytes_per_cell(d) + (size_t)pool_cap * 2 + 64;
-}
-
-// Largest power-of-two cell capacity whose state + neighbour pool fit the smem budget.
-int resident_capacity(int d, int* pool_cap, size_t* smem) {
-  const int64_t K = ipow3(d);
-  const int kp = (int)std::min<int64_t>(K, 32);
-  for (int ms = 2048; ms >= 32; ms >>= 1) {
-    const size_t bytes = resident_smem_bytes(d, ms, ms * kp);
-    if (bytes <= kResidentSmemBudget) {
-      *pool_cap = ms * kp;
-      *smem = bytes;
-      return ms;
-    }
-  }
-  *pool_cap = 32 * kp;
-  *smem = resident_smem_bytes(d, 32, 32 * kp);
-  return 32;
+// Largest power-of-two cell capacity whose per-cell state fits kResidentStateMax; the rest of
+// the budget holds the neighbour records (gs_resident.cuh falls back to slower sweep modes
+// when a frame's records do not fit).
+int resident_capacity(int d) {
+  int ms = 4096;
+  while (ms > 32 && (size_t)ms * gs::resident_bytes_per_cell(d) > kResidentStateMax) ms >>= 1;
+  return ms;
 }
 
 template <int D>
@@ -580,9 +581,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->icount.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
                         st));
   GS_CK(cudaStreamSynchronize(st));
-  int pool_cap = 0;
-  size_t rs_smem = 0;
-  const int ms_cap = resident_capacity(d, &pool_cap, &rs_smem);
+  const int ms_cap = resident_capacity(d);
   auto max_live = [&]() {
     int64_t mx = 0;
     for (int64_t f = 0; f < nf; ++f)
@@ -650,11 +649,23 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   while (ms_run < ml) ms_run <<= 1;
   ms_run = std::min(ms_run, ms_cap);
   const int threads = std::min(1024, std::max(128, ms_run));
+  // several frames per SM when there are more frames than SMs (one wave for cfg4)
+  const int64_t per_sm = std::min<int64_t>(4, std::max<int64_t>(1, (nf + ctx->num_sms - 1) / ctx->num_sms));
+  const size_t budget = kResidentSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
+  const size_t state = (size_t)ms_run * gs::resident_bytes_per_cell(d);
+  // dense int16 key->slot table of the frame box in smem when it is small (cfg1/2/4 frames:
+  // a few thousand cells); otherwise K8 indexes through the global dense grid
+  const size_t sidx = (b.vol_frame * 2 <= 48 * 1024) ? ((size_t)b.vol_frame * 2 + 15) & ~size_t(15) : 0;
+  const size_t pool_bytes = budget > state + sidx + 1024 ? budget - state - sidx : 1024;
+  // K8 owns the global index from here on (it re-keys it per frame and leaves it clean)
+  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[ctx->cur].as<uint32_t>(),
+                                                      ctx->idx.as<int32_t>());
+  GS_LAUNCHED("k_idx_clear");
   const int fin = 1 - ctx->cur;
   gs::ResidentArgs ra;
   ra.box = b;
   ra.ms = ms_run;
-  ra.pool_cap = (int)((int64_t)pool_cap * ms_run / ms_cap);
+  ra.pool_bytes = (int)(pool_bytes & ~size_t(15));
   ra.max_iter = cfg->max_iter;
   ra.record = 1;  // m_t feeds the cells x iterations counter even without GS_RECORD_HISTORY
   ra.ckey = ctx->ckey[ctx->cur].as<uint32_t>();
@@ -675,12 +686,14 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ra.hist_m = ctx->hist.as<int64_t>();
   ra.hist_d = (double*)(ctx->hist.as<int64_t>() + nf * cfg->max_iter);
   ra.err = ctx->errflag.as<int>();
-  const size_t smem = resident_smem_bytes(d, ms_run, ra.pool_cap);
+  GS_TRY(grow(ctx, ctx->modes, sizeof(int64_t) * 12));
+  GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
+  ra.mode_count = ctx->modes.as<int64_t>();
+  ra.prof = (long long*)(ctx->modes.as<int64_t>() + 4);
+  ra.gidx = ctx->idx.as<int32_t>();
+  ra.sidx_bytes = (int)sidx;
+  const size_t smem = state + sidx + ra.pool_bytes;
   GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, smem, ra));
-  // the global index is not used after the hand-off: restore its clean invariant now
-  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[ctx->cur].as<uint32_t>(),
-                                                      ctx->idx.as<int32_t>());
-  GS_LAUNCHED("k_idx_clear");
   ctx->cur = fin;
   GS_CK(cudaEventRecord(ctx->ev[3], st));
   // ---- labels
@@ -723,6 +736,8 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     GS_CK(cudaMemcpyAsync(hd.data(), ra.hist_d, sizeof(double) * hd.size(),
                           cudaMemcpyDeviceToHost, st));
   }
+  int64_t h_modes[12] = {0};
+  GS_CK(cudaMemcpyAsync(h_modes, ctx->modes.p, sizeof(int64_t) * 12, cudaMemcpyDeviceToHost, st));
   int err = 0;
   GS_TRY(read_err(ctx, &err));
   if (err & 16) return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
@@ -769,7 +784,10 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   s.cells_swept = swept;
   s.m0 = m0;
   s.k_total = m;
-  s.max_iterations = iter;
+  s.max_iterations = 0;
+  for (int64_t f = 0; f < nf; ++f) s.max_iterations = std::max(s.max_iterations, ctx->h_iters[f]);
+  for (int k = 0; k < 3; ++k) s.sweep_modes[k] = h_modes[k];
+  for (int k = 0; k < 8; ++k) s.resident_cycles[k] = h_modes[4 + k];
   s.fixed_shift = b.F;
   s.dense_cells = b.vol_total;
   return GS_OK;
@@ -848,7 +866,7 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->root, &ctx->initkey, &ctx->fdone, &ctx->fchanged, &ctx->fadj,
                     &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->fcount, &ctx->ifirst, &ctx->icount,
                     &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->hist, &ctx->counters, &ctx->errflag,
-                    &ctx->bpart, &ctx->cub_tmp, &ctx->dbg})
+                    &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes})
     b->release();
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);

@@ -104,6 +104,93 @@ __global__ void __launch_bounds__(256) k_bin(const T* __restrict__ pts, int64_t 
   }
 }
 
+// K2 with shared-memory privatisation.  Hot cells take tens of thousands of points (cfg2:
+// 16K in one cell, cfg5: 415K), so per-point global atomics serialise at one L2 slice.  Each
+// CTA bins a contiguous range of points into a shared-memory open-addressing table of cell
+// accumulators (count + D int64 fixed-point sums); a point whose probe run finds no room falls
+// back to global atomics.  The table is flushed once per CTA.  int64 sums are associative, so
+// the result is bit-identical to k_bin for any schedule.
+template <int D>
+__host__ __device__ constexpr int bin_table_entries() {
+  return D <= 3 ? 4096 : (D <= 5 ? 2048 : 1024);
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, int64_t ntot,
+                                                   GsBox b, uint32_t* __restrict__ cnt,
+                                                   unsigned long long* __restrict__ qs,
+                                                   uint32_t* __restrict__ slot,
+                                                   uint32_t* __restrict__ occ, unsigned int* m0,
+                                                   int* err) {
+  constexpr int TBL = bin_table_entries<D>();
+  constexpr uint32_t EMPTY = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long* ts = (unsigned long long*)smem;      // TBL * D sums
+  uint32_t* tk = (uint32_t*)(ts + (size_t)TBL * D);        // TBL keys
+  uint32_t* tc = tk + TBL;                                 // TBL counts
+  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
+    tk[j] = EMPTY;
+    tc[j] = 0u;
+#pragma unroll
+    for (int c = 0; c < D; ++c) ts[j * D + c] = 0ull;
+  }
+  __syncthreads();
+  const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = (int64_t)blockIdx.x * per;
+  const int64_t p1 = min(ntot, p0 + per);
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    const int64_t f = p / b.n;
+    int64_t L = f * b.vol_frame;
+    long long q[D];
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double x = (double)pts[p * D + c];
+      const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
+      const int64_t rel = k - b.kmin[c];
+      bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
+      L += rel * b.stride[c];
+      q[c] = gs_fixq(x, k, b.h, b.scale);
+    }
+    if (bad) {
+      atomicOr(err, 2);
+      continue;
+    }
+    const uint32_t key = (uint32_t)L;
+    uint32_t h = (key * 2654435761u) & (TBL - 1);
+    int hit = -1;
+#pragma unroll 1
+    for (int probe = 0; probe < 16; ++probe) {
+      uint32_t k = tk[h];
+      if (k == EMPTY) k = atomicCAS(&tk[h], EMPTY, key);
+      if (k == EMPTY || k == key) {
+        hit = (int)h;
+        break;
+      }
+      h = (h + 1) & (TBL - 1);
+    }
+    if (hit >= 0) {
+      atomicAdd(&tc[hit], 1u);
+#pragma unroll
+      for (int c = 0; c < D; ++c) atomicAdd(&ts[hit * D + c], (unsigned long long)q[c]);
+    } else {
+      if (atomicAdd(&cnt[L], 1u) == 0u) occ[atomicAdd(m0, 1u)] = key;
+#pragma unroll
+      for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], (unsigned long long)q[c]);
+    }
+    slot[p] = key;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
+    const uint32_t key = tk[j];
+    if (key == EMPTY) continue;
+    const int64_t L = key;
+    if (atomicAdd(&cnt[L], tc[j]) == 0u) occ[atomicAdd(m0, 1u)] = key;
+#pragma unroll
+    for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], ts[j * D + c]);
+  }
+}
+
 // ---------------------------------------------------------------- K3: cells
 // Lex-ordered cell list from the sorted occupied list; restores the clean-grid invariant
 // (cnt = 0, qs = 0) for the cells it consumes.

@@ -3,7 +3,7 @@
 // One thread block owns one frame (frames are independent runs) and executes
 // the whole engine loop of SPEC.md:135-143 for it with the cell state in shared memory:
 //   hash index of the active keys (smem open addressing)
-//   -> neighbour lists in lexicographic v order
+//   -> neighbour records in lexicographic v order
 //   -> Eq. (5) sweep with exact sequential semantics: per-cell dataflow on smem ready-flags
 //      (a cell waits only for its lex-earlier active neighbours; SPEC.md:120(b,c))
 //   -> rehome floor(S/h), changed / max displacement (SPEC.md:120(d,e), :108)
@@ -11,6 +11,14 @@
 //   -> root composition for the member sets (Eq. 4), has_converged
 // with no global synchronisation and no host round trip per iteration.  Every fp64
 // expression is the same _rn sequence as the global-path kernels and the CPU oracle.
+//
+// Sweep critical path.  The DAG depth of one sweep (31-184 on the configs) multiplies the
+// latency of ONE cell update, so that latency is what this kernel minimises: before the
+// sweep, every cell gets a record {slot, C'} per lex-earlier neighbour and the products
+// C'*S_old of itself and its lex-later neighbours (they do not depend on the sweep).  While
+// waiting, a cell folds each earlier neighbour's term in as soon as its flag is released
+// (still in lex order); after the last one only the precomputed tail of adds and the
+// division remain.
 #pragma once
 
 #include <cstdint>
@@ -21,8 +29,8 @@ namespace gs {
 
 struct ResidentArgs {
   GsBox box;
-  int ms;        // shared-memory cell capacity (power of two)
-  int pool_cap;  // neighbour-pool capacity (u16 entries)
+  int ms;          // shared-memory cell capacity (power of two)
+  int pool_bytes;  // shared-memory bytes for neighbour records
   int max_iter;
   int record;
   const uint32_t* ckey;  // current cells (global, frame-major, lex order within a frame)
@@ -43,28 +51,62 @@ struct ResidentArgs {
   int64_t* hist_m;
   double* hist_d;
   int* err;
+  int64_t* mode_count;  // [3]: iterations run in fast / list / inline sweep mode (diagnostic)
+  long long* prof;      // [8] per-phase SM cycles summed over frames (diagnostic), or null
+  // cell index (key -> slot): a dense int16 table over the frame's key box in shared memory
+  // when it fits (sidx_bytes > 0), else the engine's global dense grid (int32, clean = -1)
+  int32_t* gidx;
+  int sidx_bytes;
 };
 
-// shared-memory bytes per cell (excluding the neighbour pool) for dimension D
+// shared-memory bytes per cell (excluding the index and neighbour-record pool)
 __host__ __device__ constexpr int resident_bytes_per_cell(int D) {
   return 16 * D /*S0,S1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 4 /*flag*/ +
-         16 /*nbn, nbe, nboff, par*/ + 4 /*tmp*/ + 16 /*hash: 2 slots x (key, val)*/;
+         20 /*nbn, nbe, eoff, loff, par*/ + 4 /*tmp*/;
 }
 
-__device__ __forceinline__ uint32_t rs_hash(uint32_t k, int bits) {
-  return (k * 2654435761u) >> (32 - bits);
-}
-
-__device__ __forceinline__ int rs_lookup(const uint32_t* htk, const int32_t* htv, int bits,
-                                         uint32_t k) {
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t h = rs_hash(k, bits);
-  for (;;) {
-    const uint32_t kk = htk[h];
-    if (kk == k) return htv[h];
-    if (kk == 0xffffffffu) return -1;
-    h = (h + 1) & mask;
+// Register odometer over the 3^D neighbour offsets in lexicographic v order (dim 0 most
+// significant); D is a compile-time constant so v[] stays in registers.
+template <int D>
+struct OdoD {
+  int8_t v[D];
+  int64_t off;
+  __device__ __forceinline__ void init(const GsBox& b) {
+    off = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      v[c] = -1;
+      off -= b.stride[c];
+    }
   }
+  __device__ __forceinline__ void next(const GsBox& b) {
+#pragma unroll
+    for (int c = D - 1; c >= 0; --c) {
+      if (v[c] < 1) {
+        ++v[c];
+        off += b.stride[c];
+        return;
+      }
+      v[c] = -1;
+      off -= 2 * b.stride[c];
+    }
+  }
+};
+
+__device__ __forceinline__ uint32_t rs_ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void rs_st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
 }
 
 // Exclusive scan of a[0..n) in shared memory (in place); returns the total.  All threads.
@@ -123,7 +165,8 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     for (int i = tid; i < m; i += T) {  // finished in the global path: copy out
       a.okey[first + i] = a.ckey[first + i];
       a.ocnt[first + i] = a.ccnt[first + i];
-      for (int c = 0; c < D; ++c) a.oS[(int64_t)(first + i) * D + c] = a.S[(int64_t)(first + i) * D + c];
+      for (int c = 0; c < D; ++c)
+        a.oS[(int64_t)(first + i) * D + c] = a.S[(int64_t)(first + i) * D + c];
     }
     if (tid == 0) a.fk[f] = m;
     return;
@@ -144,12 +187,12 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
   uint32_t* flag = (uint32_t*)p;    p += 4 * MS;
   int* nbn = (int*)p;               p += 4 * MS;
   int* nbe = (int*)p;               p += 4 * MS;
-  int* nboff = (int*)p;             p += 4 * MS;
+  int* eoff = (int*)p;              p += 4 * MS;
+  int* loff = (int*)p;              p += 4 * MS;
   int* par = (int*)p;               p += 4 * MS;
   int* tmp = (int*)p;               p += 4 * MS;
-  uint32_t* htk = (uint32_t*)p;     p += 4 * 2 * MS;
-  int32_t* htv = (int32_t*)p;       p += 4 * 2 * MS;
-  uint16_t* pool = (uint16_t*)p;
+  int16_t* sidx = (int16_t*)p;      p += a.sidx_bytes;
+  unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
   volatile uint32_t* vflag = flag;
@@ -171,70 +214,95 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     return k;
   }();
 
-  auto build_hash = [&](int mm, int& bits) {
-    bits = 1;
-    while ((1 << bits) < 2 * mm) ++bits;
-    const int hs = 1 << bits;
-    for (int j = tid; j < hs; j += T) htk[j] = 0xffffffffu;
-    __syncthreads();
-    const uint32_t mask = (uint32_t)hs - 1u;
-    for (int i = tid; i < mm; i += T) {
-      uint32_t h = rs_hash(key[i], bits);
-      for (;;) {
-        const uint32_t prev = atomicCAS(&htk[h], 0xffffffffu, key[i]);
-        if (prev == 0xffffffffu) {
-          htv[h] = i;
-          break;
-        }
-        h = (h + 1) & mask;
-      }
-    }
-    __syncthreads();
+  // dense cell index of this frame: smem int16 table or the global grid (L2-resident)
+  const bool sdense = a.sidx_bytes > 0;
+  int32_t* gidx = a.gidx + fbase;
+  auto idx_get = [&](int64_t L) -> int { return sdense ? (int)sidx[L] : gidx[L]; };
+  auto idx_put = [&](int64_t L, int v) {
+    if (sdense)
+      sidx[L] = (int16_t)v;
+    else
+      gidx[L] = v;
   };
-
-  int bits;
+  if (sdense)
+    for (int j = tid; j < (int)(a.sidx_bytes >> 1); j += T) sidx[j] = -1;
   __syncthreads();
-  build_hash(m, bits);
+  for (int i = tid; i < m; i += T) idx_put(key[i], i);
+  __syncthreads();
 
   bool done = false;
+  long long t_prev = clock64();
+  auto lap = [&](int ph) {
+    if (a.prof && tid == 0) {
+      const long long t = clock64();
+      atomicAdd((unsigned long long*)&a.prof[ph], (unsigned long long)(t - t_prev));
+      t_prev = t;
+    }
+  };
+  lap(7);
   while (!done) {
     const uint32_t epoch = (uint32_t)iters + 1u;
-    // ---- (1) neighbour lists: active 1-neighbourhood in lex v order, #earlier, ΣC'
+    // ---- (1) neighbourhood census: #active neighbours, #lex-earlier ones
     for (int i = tid; i < m; i += T) {
-      GsNbrOdometer od;
+      OdoD<D> od;
       od.init(b);
-      int n = 0;
+      int n = 0, e = 0;
+      const int64_t Li = key[i];
+#pragma unroll 9
       for (int t = 0; t < K; ++t) {
-        n += rs_lookup(htk, htv, bits, (uint32_t)((int64_t)key[i] + od.off)) >= 0;
+        const int j = idx_get(Li + od.off);
+        n += (j >= 0);
+        e += (j >= 0) & (j < i);
         od.next(b);
       }
       nbn[i] = n;
+      nbe[i] = e;
+      eoff[i] = e;
+      loff[i] = n - e;
       tmp[i] = n;
     }
     __syncthreads();
-    const int total = rs_scan(tmp, m, wtmp);
-    const bool pooled = total <= a.pool_cap;
+    const int n_early = rs_scan(eoff, m, wtmp);
+    const int n_late = rs_scan(loff, m, wtmp);
+    const int n_all = rs_scan(tmp, m, wtmp);
+    // fast: {slot, C'} per earlier neighbour + C'*S_old for self and later neighbours
+    const int fast_bytes = 8 * n_early + 8 * D * n_late;
+    const int mode = fast_bytes <= a.pool_bytes ? 0 : (2 * n_all <= a.pool_bytes ? 1 : 2);
+    uint64_t* erec = (uint64_t*)pool;
+    double* lprod = (double*)(pool + 8 * n_early);
+    uint16_t* lst = (uint16_t*)pool;
     for (int i = tid; i < m; i += T) {
-      nboff[i] = tmp[i];
-      GsNbrOdometer od;
+      OdoD<D> od;
       od.init(b);
-      int e = 0, n = 0;
+      int ne = 0, nl = 0, nn = 0;
       uint32_t s = 0;
+      const int64_t Li = key[i];
       for (int t = 0; t < K; ++t) {
-        const int j = rs_lookup(htk, htv, bits, (uint32_t)((int64_t)key[i] + od.off));
-        if (j >= 0) {
-          if (pooled) pool[tmp[i] + n] = (uint16_t)j;
-          ++n;
-          e += (j < i);
-          s += cnt[j];
-        }
+        const int j = idx_get(Li + od.off);
         od.next(b);
+        if (j < 0) continue;
+        const uint32_t w = cnt[j];
+        s += w;
+        if (mode == 0) {
+          if (j < i) {
+            erec[eoff[i] + ne++] = ((uint64_t)w << 32) | (uint32_t)j;
+          } else {
+            double* dst = lprod + (int64_t)(loff[i] + nl++) * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c) dst[c] = __dmul_rn((double)w, S0[j * D + c]);
+          }
+        } else if (mode == 1) {
+          lst[tmp[i] + nn++] = (uint16_t)j;
+        }
       }
-      nbe[i] = e;
       den[i] = s;
     }
-    if (tid == 0) s_dmax = 0ull;
+    if (tid == 0) {
+      s_dmax = 0ull;
+      if (a.mode_count) atomicAdd((unsigned long long*)&a.mode_count[mode], 1ull);
+    }
     __syncthreads();
+    lap(0);
 
     // ---- (2) the sweep: dataflow over the static DAG of this iteration
     for (int base = 0; base < m; base += T) {
@@ -246,23 +314,52 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
         e = nbe[i];
         if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
           for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
-          __threadfence_block();
-          vflag[i] = epoch;
+          rs_st_release(&flag[i], epoch);
           pending = false;
         }
       }
-      if (pooled) {
-        const uint16_t* lst = pool + (pending ? nboff[i] : 0);
+      double num[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) num[c] = 0.0;
+      if (mode == 0) {
+        const uint64_t* er = erec + (pending ? eoff[i] : 0);
+        const double* lp = lprod + (int64_t)(pending ? loff[i] : 0) * D;
+        const int nl = n - e;
         while (__any_sync(0xffffffffu, pending)) {
           if (pending) {
-            while (t_ok < e && vflag[lst[t_ok]] == epoch) ++t_ok;
-            if (t_ok == e) {
-              __threadfence_block();
-              double num[D];
+            // fold earlier neighbours' NEW centroids in lex order as their flags release
+            while (t_ok < e) {
+              const uint64_t r = er[t_ok];
+              const uint32_t j = (uint32_t)r;
+              if (rs_ld_acquire(&flag[j]) != epoch) break;
+              const double w = (double)(uint32_t)(r >> 32);
 #pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = 0.0;
+              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, S1[j * D + c]));
+              ++t_ok;
+            }
+            if (t_ok == e) {
+              // self + later neighbours: precomputed C'*S_old products, in lex order
+#pragma unroll 4
+              for (int t = 0; t < nl; ++t) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], lp[t * D + c]);
+              }
+              const double dd = (double)den[i];
+#pragma unroll
+              for (int c = 0; c < D; ++c) S1[i * D + c] = __ddiv_rn(num[c], dd);
+              rs_st_release(&flag[i], epoch);
+              pending = false;
+            }
+          }
+        }
+      } else if (mode == 1) {
+        const uint16_t* ls = lst + (pending ? tmp[i] : 0);
+        while (__any_sync(0xffffffffu, pending)) {
+          if (pending) {
+            while (t_ok < e && rs_ld_acquire(&flag[ls[t_ok]]) == epoch) ++t_ok;
+            if (t_ok == e) {
               for (int t = 0; t < n; ++t) {
-                const int j = lst[t];
+                const int j = ls[t];
                 const double w = (double)cnt[j];
                 const double* src = (t < e) ? S1 : S0;
 #pragma unroll
@@ -271,22 +368,19 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
               const double dd = (double)den[i];
 #pragma unroll
               for (int c = 0; c < D; ++c) S1[i * D + c] = __ddiv_rn(num[c], dd);
-              __threadfence_block();
-              vflag[i] = epoch;
+              rs_st_release(&flag[i], epoch);
               pending = false;
             }
           }
         }
       } else if (pending) {
-        // pool overflow (very dense high-d neighbourhoods): look neighbours up again, waiting
-        // on each earlier one in turn (independent thread scheduling keeps lanes progressing)
-        double num[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) num[c] = 0.0;
-        GsNbrOdometer od;
+        // records do not fit (very dense high-d neighbourhoods): look neighbours up again,
+        // waiting on each earlier one in turn (independent thread scheduling keeps lanes going)
+        OdoD<D> od;
         od.init(b);
+        const int64_t Li = key[i];
         for (int t = 0; t < K; ++t) {
-          const int j = rs_lookup(htk, htv, bits, (uint32_t)((int64_t)key[i] + od.off));
+          const int j = idx_get(Li + od.off);
           od.next(b);
           if (j < 0) continue;
           if (j < i) {
@@ -308,6 +402,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     }
     __syncthreads();
 
+    lap(1);
     // ---- (3) rehome, changed, displacement
     int P = 1;
     while (P < m) P <<= 1;
@@ -319,17 +414,19 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
       }
       int64_t Ln = 0;
       double acc = 0.0;
+      bool bad_i = false;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
         const double s1 = S1[i * D + c], s0 = S0[i * D + c];
         const int64_t rel = gs_grid_coord(s1, b.h, b.inv_h) - b.kmin[c];
-        bad |= (rel < 1) | (rel > b.ext[c] - 2);
+        bad_i |= (rel < 1) | (rel > b.ext[c] - 2);
         Ln += rel * b.stride[c];
         ch |= __double_as_longlong(s1) != __double_as_longlong(s0);
         const double t = __dsub_rn(s1, s0);
         acc = __dadd_rn(acc, __dmul_rn(t, t));
       }
-      if (bad) Ln = key[i];
+      if (bad_i) Ln = key[i];
+      bad |= bad_i;
       ch |= (Ln != (int64_t)key[i]);
       atomicMax(&s_dmax, (unsigned long long)__double_as_longlong(__dsqrt_rn(acc)));
       sk[i] = ((uint64_t)(uint32_t)Ln << 32) | (uint32_t)i;
@@ -337,6 +434,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     if (bad) atomicOr(a.err, 4);
     const int changed = __syncthreads_or(ch);
     const double dmax = __longlong_as_double((long long)s_dmax);
+    lap(2);
 
     // ---- (4) bitonic sort of (new key, old rank): members of a merge group end up
     //          adjacent and in visit order
@@ -356,6 +454,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
       }
     }
 
+    lap(3);
     // ---- (5) segments -> new cells; parent map
     for (int j = tid; j < m; j += T)
       tmp[j] = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32)) ? 1 : 0;
@@ -365,13 +464,13 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
       const bool head = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32));
       const int g = tmp[j] + (head ? 1 : 0) - 1;
       par[(uint32_t)sk[j]] = g;
-      if (head) nboff[g] = j;  // segment start (nboff is free after the sweep)
+      if (head) eoff[g] = j;  // segment start (eoff is free after the sweep)
     }
     __syncthreads();
     // merge_into folded in visit order (Eq. 3, pin P4)
     for (int g = tid; g < mnew; g += T) {
-      const int start = nboff[g];
-      const int end = (g + 1 < mnew) ? nboff[g + 1] : m;
+      const int start = eoff[g];
+      const int end = (g + 1 < mnew) ? eoff[g + 1] : m;
       const uint32_t i0 = (uint32_t)sk[start];
       double s[D];
 #pragma unroll
@@ -393,6 +492,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     }
     // member union (Eq. 4) as root composition
     for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.root[c] = par[a.root[c]];
+    for (int i = tid; i < m; i += T) idx_put(key[i], -1);  // retire the old keys
     __syncthreads();
     {
       uint32_t* t1 = key;
@@ -404,15 +504,18 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     }
     const int m_before = m;
     m = mnew;
-    build_hash(m, bits);
+    lap(4);
+    for (int i = tid; i < m; i += T) idx_put(key[i], i);
+    __syncthreads();
 
     // ---- (6) has_converged on the new state
     bool adj = false;
     for (int i = tid; i < m && !adj; i += T) {
-      GsNbrOdometer od;
+      OdoD<D> od;
       od.init(b);
+      const int64_t Li = key[i];
       for (int t = 0; t < K; ++t) {
-        if (od.off != 0 && rs_lookup(htk, htv, bits, (uint32_t)((int64_t)key[i] + od.off)) >= 0) {
+        if (od.off != 0 && idx_get(Li + od.off) >= 0) {
           adj = true;
           break;
         }
@@ -424,6 +527,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
       a.hist_m[(int64_t)f * a.max_iter + iters] = m_before;
       a.hist_d[(int64_t)f * a.max_iter + iters] = dmax;
     }
+    lap(5);
     ++iters;
     conv = (!any_adj || !changed) ? 1 : 0;
     done = conv || iters >= a.max_iter;
@@ -433,6 +537,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     a.okey[first + i] = (uint32_t)((int64_t)key[i] + fbase);
     a.ocnt[first + i] = cnt[i];
     for (int c = 0; c < D; ++c) a.oS[(int64_t)(first + i) * D + c] = S0[i * D + c];
+    if (!sdense) gidx[key[i]] = -1;  // clean-grid invariant for the next run
   }
   if (tid == 0) {
     a.fk[f] = m;

@@ -96,7 +96,8 @@ class GsStats(C.Structure):
                 ("cells_swept", C.c_int64), ("m0", C.c_int64), ("k_total", C.c_int64),
                 ("kernel_launches", C.c_int64), ("max_iterations", C.c_int32),
                 ("fixed_shift", C.c_int32), ("dense_cells", C.c_int64),
-                ("ms_k_bin", C.c_double), ("ms_k_label", C.c_double), ("lib_calls", C.c_int64)]
+                ("ms_k_bin", C.c_double), ("ms_k_label", C.c_double), ("lib_calls", C.c_int64),
+                ("sweep_modes", C.c_int64 * 3), ("resident_cycles", C.c_int64 * 8)]
 
 
 _lib = None
@@ -272,7 +273,10 @@ class Engine:
     def stats(self) -> dict:
         s = GsStats()
         self._check(self._lib.gs_get_stats(self._ctx, C.byref(s)))
-        return {name: getattr(s, name) for name, _ in GsStats._fields_}
+        out = {name: getattr(s, name) for name, _ in GsStats._fields_}
+        out["sweep_modes"] = list(out["sweep_modes"])
+        out["resident_cycles"] = list(out["resident_cycles"])
+        return out
 
     # -- test hooks --------------------------------------------------------------------------
     def debug_build(self, X: np.ndarray, h: float):
