@@ -138,25 +138,55 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
   const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
   const int64_t p0 = (int64_t)blockIdx.x * per;
   const int64_t p1 = min(ntot, p0 + per);
-  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-    const int64_t f = p / b.n;
-    int64_t L = f * b.vol_frame;
+  const unsigned lane = threadIdx.x & 31;
+  // warp-uniform trip count so every lane takes part in the warp aggregation
+  for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
+    const int64_t p = pb + threadIdx.x;
+    const bool valid = p < p1;
+    int64_t L = 0;
     long long q[D];
     bool bad = false;
+    if (valid) {
+      L = (p / b.n) * b.vol_frame;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const double x = (double)pts[p * D + c];
-      const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
-      const int64_t rel = k - b.kmin[c];
-      bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
-      L += rel * b.stride[c];
-      q[c] = gs_fixq(x, k, b.h, b.scale);
+      for (int c = 0; c < D; ++c) {
+        const double x = (double)pts[p * D + c];
+        const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
+        const int64_t rel = k - b.kmin[c];
+        bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
+        L += rel * b.stride[c];
+        q[c] = gs_fixq(x, k, b.h, b.scale);
+      }
+      if (bad) atomicOr(err, 2);
+      else slot[p] = (uint32_t)L;
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) q[c] = 0;
     }
-    if (bad) {
-      atomicOr(err, 2);
-      continue;
+    const uint32_t key = (valid && !bad) ? (uint32_t)L : EMPTY;
+    // ---- warp aggregation: lanes binning into the same cell (pixel-ordered images put
+    // most of a warp into 1-4 cells) reduce to their group leader before any atomic
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int gsize = __popc(peers);
+    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)gsize);
+    uint32_t my_cnt = 1;
+    if (maxg > 1) {
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      for (int s = 1; s < maxg; s <<= 1) {
+        // partner = the group member s ranks above; __fns counts set bits from `lane` upward
+        const unsigned partner = __fns(peers, lane, s + 1);
+        const bool take = ((rank & (2 * s - 1)) == 0) && partner < 32u;
+        const int src = take ? (int)partner : (int)lane;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const long long v = __shfl_sync(0xffffffffu, q[c], src);
+          if (take) q[c] += v;
+        }
+      }
+      my_cnt = (uint32_t)gsize;
+      if (rank != 0) continue;  // only the group leader carries the group's sums
     }
-    const uint32_t key = (uint32_t)L;
+    if (key == EMPTY) continue;
     uint32_t h = (key * 2654435761u) & (TBL - 1);
     int hit = -1;
 #pragma unroll 1
@@ -170,15 +200,14 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
       h = (h + 1) & (TBL - 1);
     }
     if (hit >= 0) {
-      atomicAdd(&tc[hit], 1u);
+      atomicAdd(&tc[hit], my_cnt);
 #pragma unroll
       for (int c = 0; c < D; ++c) atomicAdd(&ts[hit * D + c], (unsigned long long)q[c]);
     } else {
-      if (atomicAdd(&cnt[L], 1u) == 0u) occ[atomicAdd(m0, 1u)] = key;
+      if (atomicAdd(&cnt[L], my_cnt) == 0u) occ[atomicAdd(m0, 1u)] = key;
 #pragma unroll
       for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], (unsigned long long)q[c]);
     }
-    slot[p] = key;
   }
   __syncthreads();
   for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
