@@ -493,6 +493,17 @@ constexpr size_t kResidentStateMax = 140 * 1024;    // cell state may take at mo
 // Largest power-of-two cell capacity whose per-cell state fits kResidentStateMax; the rest of
 // the budget holds the neighbour records (gs_resident.cuh falls back to slower sweep modes
 // when a frame's records do not fit).
+int resident_offs_bytes_host(int d) {
+  switch (d) {
+#define GS_CASE(D) \
+  case D:          \
+    return gs::resident_offs_bytes(D);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+#undef GS_CASE
+  }
+  return 0;
+}
+
 int resident_capacity(int d) {
   int ms = 4096;
   while (ms > 32 && (size_t)ms * gs::resident_bytes_per_cell(d) > kResidentStateMax) ms >>= 1;
@@ -656,7 +667,9 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   // dense int16 key->slot table of the frame box in smem when it is small (cfg1/2/4 frames:
   // a few thousand cells); otherwise K8 indexes through the global dense grid
   const size_t sidx = (b.vol_frame * 2 <= 48 * 1024) ? ((size_t)b.vol_frame * 2 + 15) & ~size_t(15) : 0;
-  const size_t pool_bytes = budget > state + sidx + 1024 ? budget - state - sidx : 1024;
+  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d);
+  const size_t fixed = state + sidx + offs_bytes;
+  const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
   // K8 owns the global index from here on (it re-keys it per frame and leaves it clean)
   gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[ctx->cur].as<uint32_t>(),
                                                       ctx->idx.as<int32_t>());
@@ -692,7 +705,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ra.prof = (long long*)(ctx->modes.as<int64_t>() + 4);
   ra.gidx = ctx->idx.as<int32_t>();
   ra.sidx_bytes = (int)sidx;
-  const size_t smem = state + sidx + ra.pool_bytes;
+  const size_t smem = fixed + ra.pool_bytes;
   GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, smem, ra));
   ctx->cur = fin;
   GS_CK(cudaEventRecord(ctx->ev[3], st));

@@ -61,8 +61,27 @@ struct ResidentArgs {
 
 // shared-memory bytes per cell (excluding the index and neighbour-record pool)
 __host__ __device__ constexpr int resident_bytes_per_cell(int D) {
-  return 16 * D /*S0,S1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 4 /*flag*/ +
-         20 /*nbn, nbe, eoff, loff, par*/ + 4 /*tmp*/;
+  return 16 * D /*S0,S1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 8 /*1/den*/ +
+         4 /*flag*/ + 20 /*nbn, nbe, eoff, loff, par*/ + 4 /*tmp*/;
+}
+
+// shared-memory bytes of the neighbour-offset table (int32 per offset) for dimension D
+__host__ __device__ constexpr int resident_offs_bytes(int D) {
+  return D <= 6 ? (((D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 : 729) *
+                    4 + 15) & ~15)
+                : 0;
+}
+
+// RN(a / b) from y = RN(1/b) (precomputed off the critical path): q0 = RN(a*y); the residual
+// a - b*q0 is exact in one FMA; RN(q0 + r*y) is the correctly rounded quotient (Markstein's
+// theorem; b is a positive integer count here).  Outside the exponent range where the theorem's
+// no-underflow/no-overflow premises hold, fall back to the IEEE division.
+__device__ __forceinline__ double rs_div(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double fa = fabs(a);
+  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return __ddiv_rn(a, b);
+  const double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, y, q0);
 }
 
 // Register odometer over the 3^D neighbour offsets in lexicographic v order (dim 0 most
@@ -178,6 +197,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
   unsigned char* p = smem;
   double* S0 = (double*)p;          p += sizeof(double) * MS * D;
   double* S1 = (double*)p;          p += sizeof(double) * MS * D;
+  double* rden = (double*)p;        p += sizeof(double) * MS;
   uint64_t* sk = (uint64_t*)p;      p += sizeof(uint64_t) * MS;
   uint32_t* keyA = (uint32_t*)p;    p += 4 * MS;
   uint32_t* keyB = (uint32_t*)p;    p += 4 * MS;
@@ -192,6 +212,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
   int* par = (int*)p;               p += 4 * MS;
   int* tmp = (int*)p;               p += 4 * MS;
   int16_t* sidx = (int16_t*)p;      p += a.sidx_bytes;
+  int* offs = (int*)p;              p += resident_offs_bytes(D);
   unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
@@ -208,11 +229,33 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     for (int c = 0; c < D; ++c) S0[i * D + c] = a.S[(int64_t)(first + i) * D + c];
     flag[i] = 0u;
   }
-  const int K = [] {
-    int k = 1;
-    for (int c = 0; c < D; ++c) k *= 3;
-    return k;
-  }();
+  constexpr int K = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 :
+                    D == 6 ? 729 : D == 7 ? 2187 : D == 8 ? 6561 : D == 9 ? 19683 :
+                    D == 10 ? 59049 : D == 11 ? 177147 : 531441;
+  constexpr bool kTable = resident_offs_bytes(D) > 0;
+  if (kTable && tid == 0) {  // lexicographic neighbour offsets, linear in the frame box
+    OdoD<D> od;
+    od.init(b);
+    for (int t = 0; t < K; ++t) {
+      offs[t] = (int)od.off;
+      od.next(b);
+    }
+  }
+  // the offset of neighbour t: table lookup (D <= 6) or a register odometer (D > 6)
+  struct NbrIt {
+    OdoD<D> od;
+    const int* tbl;
+    __device__ __forceinline__ int64_t at(int t) const { return kTable ? (int64_t)tbl[t] : od.off; }
+    __device__ __forceinline__ void step(const GsBox& bb) {
+      if (!kTable) od.next(bb);
+    }
+  };
+  auto nbr_begin = [&]() {
+    NbrIt it;
+    it.tbl = offs;
+    if (!kTable) it.od.init(b);
+    return it;
+  };
 
   // dense cell index of this frame: smem int16 table or the global grid (L2-resident)
   const bool sdense = a.sidx_bytes > 0;
@@ -244,16 +287,15 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     const uint32_t epoch = (uint32_t)iters + 1u;
     // ---- (1) neighbourhood census: #active neighbours, #lex-earlier ones
     for (int i = tid; i < m; i += T) {
-      OdoD<D> od;
-      od.init(b);
+      NbrIt it = nbr_begin();
       int n = 0, e = 0;
       const int64_t Li = key[i];
-#pragma unroll 9
+#pragma unroll 27
       for (int t = 0; t < K; ++t) {
-        const int j = idx_get(Li + od.off);
+        const int j = idx_get(Li + it.at(t));
         n += (j >= 0);
         e += (j >= 0) & (j < i);
-        od.next(b);
+        it.step(b);
       }
       nbn[i] = n;
       nbe[i] = e;
@@ -272,14 +314,13 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     double* lprod = (double*)(pool + 8 * n_early);
     uint16_t* lst = (uint16_t*)pool;
     for (int i = tid; i < m; i += T) {
-      OdoD<D> od;
-      od.init(b);
+      NbrIt it = nbr_begin();
       int ne = 0, nl = 0, nn = 0;
       uint32_t s = 0;
       const int64_t Li = key[i];
       for (int t = 0; t < K; ++t) {
-        const int j = idx_get(Li + od.off);
-        od.next(b);
+        const int j = idx_get(Li + it.at(t));
+        it.step(b);
         if (j < 0) continue;
         const uint32_t w = cnt[j];
         s += w;
@@ -296,6 +337,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
         }
       }
       den[i] = s;
+      rden[i] = __drcp_rn((double)s);  // for rs_div on the sweep's critical path
     }
     if (tid == 0) {
       s_dmax = 0ull;
@@ -346,7 +388,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
               }
               const double dd = (double)den[i];
 #pragma unroll
-              for (int c = 0; c < D; ++c) S1[i * D + c] = __ddiv_rn(num[c], dd);
+              for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
               rs_st_release(&flag[i], epoch);
               pending = false;
             }
@@ -367,7 +409,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
               }
               const double dd = (double)den[i];
 #pragma unroll
-              for (int c = 0; c < D; ++c) S1[i * D + c] = __ddiv_rn(num[c], dd);
+              for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
               rs_st_release(&flag[i], epoch);
               pending = false;
             }
@@ -376,12 +418,11 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
       } else if (pending) {
         // records do not fit (very dense high-d neighbourhoods): look neighbours up again,
         // waiting on each earlier one in turn (independent thread scheduling keeps lanes going)
-        OdoD<D> od;
-        od.init(b);
+        NbrIt it = nbr_begin();
         const int64_t Li = key[i];
         for (int t = 0; t < K; ++t) {
-          const int j = idx_get(Li + od.off);
-          od.next(b);
+          const int j = idx_get(Li + it.at(t));
+          it.step(b);
           if (j < 0) continue;
           if (j < i) {
             while (vflag[j] != epoch) {
@@ -395,7 +436,7 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
         }
         const double dd = (double)den[i];
 #pragma unroll
-        for (int c = 0; c < D; ++c) S1[i * D + c] = __ddiv_rn(num[c], dd);
+        for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
         __threadfence_block();
         vflag[i] = epoch;
       }
@@ -511,16 +552,15 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     // ---- (6) has_converged on the new state
     bool adj = false;
     for (int i = tid; i < m && !adj; i += T) {
-      OdoD<D> od;
-      od.init(b);
+      NbrIt it = nbr_begin();
       const int64_t Li = key[i];
+      int hits = 0;
+#pragma unroll 27
       for (int t = 0; t < K; ++t) {
-        if (od.off != 0 && idx_get(Li + od.off) >= 0) {
-          adj = true;
-          break;
-        }
-        od.next(b);
+        hits += (t != (K - 1) / 2) && idx_get(Li + it.at(t)) >= 0;
+        it.step(b);
       }
+      adj = hits > 0;
     }
     const int any_adj = __syncthreads_or(adj);
     if (tid == 0 && a.record) {
