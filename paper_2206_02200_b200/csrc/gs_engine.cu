@@ -75,7 +75,25 @@ struct gs_ctx {
       hist;
   int64_t frame_cap = 0;
   // misc
-  DevBuf counters, errflag, bpart, cub_tmp, dbg, modes;
+  DevBuf counters, errflag, bpart, cub_tmp, dbg, modes, tiles, dbox;
+  // pinned readback area (one async D2H per result array, one sync per run)
+  void* pin = nullptr;
+  size_t pin_bytes = 0;
+  // shape cache: a run whose frames all went straight to K8 lets later runs of the same
+  // shape launch K8 optimistically (no host round trip between binning and labels)
+  struct ShapeKey {
+    int64_t n = 0, nf = 0;
+    int d = 0, dtype = 0;
+    double h = 0;
+    int max_iter = 0;
+    bool operator==(const ShapeKey& o) const {
+      return n == o.n && nf == o.nf && d == o.d && dtype == o.dtype && h == o.h &&
+             max_iter == o.max_iter;
+    }
+  } shape;
+  int shape_ms = 0;
+  GsBox shape_box{};
+  int64_t shape_vol_frame = 0;
   // last run (host side)
   GsBox box{};
   int64_t nframes = 0;
@@ -295,7 +313,7 @@ gs_status make_box_from_cells(gs_ctx* ctx, int d, double h, int64_t m, const int
 
 template <int D>
 gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t ntot, bool bounds,
-                            const GsBox* box, unsigned nblk) {
+                            unsigned nblk) {
   if (bounds) {
     if (dtype == GS_F32)
       gs::k_bounds<D, float><<<nblk, 256, 0, ctx->stream>>>(
@@ -321,25 +339,23 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
     const unsigned grid = blocks_for(ntot, 4096, ctx->num_sms);
     if (dtype == GS_F32)
       gs::k_bin_priv<D, float><<<grid, 1024, smem, ctx->stream>>>(
-          (const float*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
-          ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
+          (const float*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
     else
       gs::k_bin_priv<D, double><<<grid, 1024, smem, ctx->stream>>>(
-          (const double*)pts, ntot, *box, ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->occ.as<uint32_t>(),
-          ctx->counters.as<unsigned int>(), ctx->errflag.as<int>());
+          (const double*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
     GS_LAUNCHED("k_bin_priv");
   }
   return GS_OK;
 }
 
 gs_status dispatch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int d, int64_t ntot,
-                              bool bounds, const GsBox* box, unsigned nblk) {
+                              bool bounds, unsigned nblk) {
   switch (d) {
 #define GS_CASE(D) \
   case D:          \
-    return launch_bounds_bin<D>(ctx, pts, dtype, ntot, bounds, box, nblk);
+    return launch_bounds_bin<D>(ctx, pts, dtype, ntot, bounds, nblk);
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
     GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
 #undef GS_CASE
@@ -353,56 +369,63 @@ gs_status read_err(gs_ctx* ctx, int* out) {
   return GS_OK;
 }
 
-// n-scale phase: bounds, binning, lex cell list.  On return ctx->box is set, cells are in
-// ckey[0]/ccnt[0]/S[0], *m0_out is the number of initial cells.
-gs_status build_cells(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t n, int64_t nf,
-                      double h, int64_t* m0_out) {
+// device scratch layout
+//   errflag (int[8]): [0] error bits, [2..3] int64 cells needed when bit 32 is set
+//   counters (unsigned[16]): [0] m0, [1] global-sweep ticket, [2] largest frame (cells),
+//                            [4] K8 deferred
+constexpr int64_t kDefaultDenseCells = int64_t(1) << 22;
+
+// n-scale phase with no host round trip: bounds -> device box -> privatised binning ->
+// compaction by scan (cells come out lexicographically sorted) -> per-frame cell ranges.
+// Errors (non-finite input, key box beyond the grid) surface in errflag at the next sync.
+gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t n, int64_t nf,
+                        double h) {
+  cudaStream_t st = ctx->stream;
   const int64_t ntot = n * nf;
   const unsigned nblk = blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8);
   GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
-  GS_TRY(grow(ctx, ctx->errflag, sizeof(int) * 4));
-  GS_TRY(grow(ctx, ctx->counters, sizeof(unsigned int) * 16));
-  GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, sizeof(int) * 4, ctx->stream));
-  GS_CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned int) * 16, ctx->stream));
-  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nullptr, nblk));
-  std::vector<double> part((size_t)nblk * d * 2);
-  GS_CK(cudaMemcpyAsync(part.data(), ctx->bpart.p, sizeof(double) * part.size(),
-                        cudaMemcpyDeviceToHost, ctx->stream));
-  int err = 0;
-  GS_TRY(read_err(ctx, &err));
-  if (err & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
-  std::vector<double> mn(d, INFINITY), mx(d, -INFINITY);
-  for (unsigned b = 0; b < nblk; ++b)
-    for (int c = 0; c < d; ++c) {
-      mn[c] = std::min(mn[c], part[(size_t)b * d + c]);
-      mx[c] = std::max(mx[c], part[(size_t)nblk * d + (size_t)b * d + c]);
-    }
-  GS_TRY(make_box(ctx, d, h, n, nf, mn.data(), mx.data(), &ctx->box));
-  GS_TRY(ensure_dense(ctx, ctx->box.vol_total, d));
-  const int64_t mcap = std::min<int64_t>(ntot, ctx->box.vol_total);
-  GS_TRY(ensure_cells(ctx, mcap, d));
+  GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
+  GS_TRY(ensure_dense(ctx, std::max<int64_t>(ctx->dense_cap, kDefaultDenseCells), d));
+  GS_TRY(ensure_cells(ctx, std::min<int64_t>(ntot, ctx->dense_cap), d));
+  GS_TRY(ensure_frames(ctx, nf));
   GS_TRY(grow(ctx, ctx->slot, sizeof(uint32_t) * ntot));
-  GS_CK(cudaEventRecord(ctx->ev[6], ctx->stream));
-  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, &ctx->box, nblk));
-  GS_CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-  unsigned int m0 = 0;
-  GS_CK(cudaMemcpyAsync(&m0, ctx->counters.p, sizeof(unsigned int), cudaMemcpyDeviceToHost,
-                        ctx->stream));
-  GS_TRY(read_err(ctx, &err));
-  if (err & 2) return fail(ctx, GS_E_INTERNAL_INVARIANT, "point outside the computed key box");
-  const int kb = bits_for(ctx->box.vol_total);
-  size_t tb = ctx->cub_tmp.bytes;
-  GS_CK(cub::DeviceRadixSort::SortKeys(ctx->cub_tmp.p, tb, ctx->occ.as<uint32_t>(),
-                                       ctx->occ_sorted.as<uint32_t>(), (int)m0, 0, kb,
-                                       ctx->stream));
-  GS_TRY(check_lib(ctx, "cub_sort_occ"));
-  gs::k_make_cells<<<blocks_for(m0, 256), 256, 0, ctx->stream>>>(
-      (int)m0, ctx->box, ctx->occ_sorted.as<uint32_t>(), ctx->cnt.as<uint32_t>(),
-      ctx->qs.as<unsigned long long>(), ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(),
-      ctx->S[0].as<double>(), ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(),
-      ctx->initkey.as<uint32_t>());
-  GS_LAUNCHED("k_make_cells");
-  *m0_out = m0;
+  const int64_t ntiles = ctx->dense_cap / gs::kOccTile + 1;
+  GS_TRY(grow(ctx, ctx->tiles, sizeof(int) * ntiles));
+  GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, 32, st));
+  GS_CK(cudaMemsetAsync(ctx->counters.p, 0, 64, st));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk));
+  gs::k_box<<<1, 32, 0, st>>>(ctx->bpart.as<double>(), (int)nblk, d, h, gs_fixed_shift(n, h), n,
+                              nf, ctx->dense_cap, ctx->dbox.as<GsBox>(), ctx->errflag.as<int>(),
+                              (long long*)(ctx->errflag.as<int>() + 2));
+  GS_LAUNCHED("k_box");
+  GS_CK(cudaEventRecord(ctx->ev[6], st));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk));
+  GS_CK(cudaEventRecord(ctx->ev[7], st));
+  const GsBox* pb = ctx->dbox.as<GsBox>();
+  int* err = ctx->errflag.as<int>();
+  unsigned* cnt32 = ctx->counters.as<unsigned>();
+  const unsigned tg = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 4);
+  gs::k_occ_count<<<tg, 256, 0, st>>>(pb, ctx->cnt.as<uint32_t>(), ctx->tiles.as<int>(), err);
+  GS_LAUNCHED("k_occ_count");
+  gs::k_occ_scan<<<1, 1024, 0, st>>>(pb, ctx->tiles.as<int>(), cnt32, err);
+  GS_LAUNCHED("k_occ_scan");
+  gs::k_occ_compact<<<tg, 256, 0, st>>>(
+      pb, ctx->tiles.as<int>(), ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+      ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(), ctx->S[0].as<double>(),
+      ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(), err);
+  GS_LAUNCHED("k_occ_compact");
+  const unsigned cg = blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
+                                 (int64_t)ctx->num_sms * 4);
+  gs::k_frame_ranges_dev<<<cg, 256, 0, st>>>(cnt32, pb, ctx->ckey[0].as<uint32_t>(),
+                                             ctx->ifirst.as<int32_t>(), ctx->icount.as<int32_t>());
+  GS_LAUNCHED("k_frame_ranges_dev");
+  gs::k_frame_counts_dev<<<blocks_for(nf, 256, 1024), 256, 0, st>>>(
+      nf, ctx->ifirst.as<int32_t>(), ctx->icount.as<int32_t>(), (int*)(cnt32 + 2));
+  GS_LAUNCHED("k_frame_counts_dev");
+  GS_CK(cudaMemcpyAsync(ctx->ffirst.p, ctx->ifirst.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->fcount.p, ctx->icount.p, sizeof(int32_t) * nf,
+                        cudaMemcpyDeviceToDevice, st));
   return GS_OK;
 }
 
@@ -537,146 +560,75 @@ gs_status launch_resident(gs_ctx* ctx, int d, unsigned grid, int threads, size_t
   return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
 }
 
-gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
-  GS_TRY(validate(in, cfg));
-  if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
-    return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
-  const int d = in->d;
-  const int64_t n = in->n, nf = in->batch, ntot = n * nf;
-  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
-  ctx->have_run = false;
-  ctx->stats = gs_stats{};
-  ctx->cur = 0;
-  GS_TRY(ensure_frames(ctx, nf));
-  const void* dpts = in->points;
+// Readback area in pinned host memory (one async D2H per array, one sync per run).
+struct Readback {
+  int* err;          // 8 ints
+  unsigned* ctr;     // 16
+  int32_t* ffirst;   // nf
+  int32_t* fk;
+  int32_t* fiters;
+  int32_t* fconv;
+  int64_t* modes;    // 12
+  int64_t* hm;       // nf * max_iter
+  double* hd;        // nf * max_iter
+};
+
+gs_status map_readback(gs_ctx* ctx, int64_t nf, int max_iter, Readback* rb) {
+  const size_t need = 32 + 64 + 4 * 4 * (size_t)nf + 96 + 16 * (size_t)nf * max_iter + 64;
+  if (need > ctx->pin_bytes) {
+    if (ctx->pin) cudaFreeHost(ctx->pin);
+    ctx->pin = nullptr;
+    ctx->pin_bytes = 0;
+    GS_CK(cudaMallocHost(&ctx->pin, need));
+    ctx->pin_bytes = need;
+  }
+  char* p = (char*)ctx->pin;
+  rb->err = (int*)p;          p += 32;
+  rb->ctr = (unsigned*)p;     p += 64;
+  rb->modes = (int64_t*)p;    p += 96;
+  rb->hm = (int64_t*)p;       p += 8 * (size_t)nf * max_iter;
+  rb->hd = (double*)p;        p += 8 * (size_t)nf * max_iter;
+  rb->ffirst = (int32_t*)p;   p += 4 * (size_t)nf;
+  rb->fk = (int32_t*)p;       p += 4 * (size_t)nf;
+  rb->fiters = (int32_t*)p;   p += 4 * (size_t)nf;
+  rb->fconv = (int32_t*)p;
+  return GS_OK;
+}
+
+// K8 over every frame, then labels; results copied to the pinned readback area; one sync.
+// deferrable: the launch is optimistic (smem sized from the shape cache) and K8 may refuse.
+gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t ntot, int d,
+                      int ms_run, bool deferrable, int64_t m_host, int32_t* user_labels,
+                      bool dev_out, bool rec, const Readback& rb) {
   cudaStream_t st = ctx->stream;
-  GS_CK(cudaEventRecord(ctx->ev[0], st));
-  if (!in->on_device) {
-    GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
-    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
-    dpts = ctx->pts.p;
-  }
-  GS_CK(cudaEventRecord(ctx->ev[1], st));
-  int64_t m0 = 0;
-  GS_TRY(build_cells(ctx, dpts, in->dtype, d, n, nf, cfg->h, &m0));
-  GS_CK(cudaEventRecord(ctx->ev[2], st));
-  const GsBox& b = ctx->box;
-  // ---- iteration phase
-  // (a) global path (K4/K5 kernels, host-driven) while some live frame has more active cells
-  //     than one CTA's shared memory holds; (b) then the CTA-resident engine K8 runs every
-  //     remaining iteration of every frame on the device.
-  ctx->h_done.assign(nf, 0);
-  ctx->h_iters.assign(nf, 0);
-  ctx->h_conv.assign(nf, 0);
-  const bool rec = (cfg->flags & GS_RECORD_HISTORY) != 0;
-  ctx->hist_m.assign(rec ? nf : 0, {});
-  ctx->hist_d.assign(rec ? nf : 0, {});
-  GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
-  std::vector<int32_t> fch(nf), fadj(nf), fm(nf), fcnt(nf);
-  std::vector<unsigned long long> fdisp(nf);
-  int64_t m = m0, live = nf, swept = 0;
-  int iter = 0;
-  // initial per-frame cell ranges (root entries of frame f live in [ifirst_f, +icount_f))
-  gs::k_frame_ranges<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, b.vol_frame,
-                                                          ctx->ckey[0].as<uint32_t>(),
-                                                          ctx->ifirst.as<int32_t>(),
-                                                          ctx->icount.as<int32_t>());
-  GS_LAUNCHED("k_frame_ranges");
-  gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ifirst.as<int32_t>(),
-                                                          ctx->icount.as<int32_t>());
-  GS_LAUNCHED("k_frame_counts");
-  GS_CK(cudaMemcpyAsync(ctx->ffirst.p, ctx->ifirst.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToDevice, st));
-  GS_CK(cudaMemcpyAsync(ctx->fcount.p, ctx->icount.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToDevice, st));
-  GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->icount.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
-                        st));
-  GS_CK(cudaStreamSynchronize(st));
   const int ms_cap = resident_capacity(d);
-  auto max_live = [&]() {
-    int64_t mx = 0;
-    for (int64_t f = 0; f < nf; ++f)
-      if (!ctx->h_done[f]) mx = std::max<int64_t>(mx, fcnt[f]);
-    return mx;
-  };
-  const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
-  while (live > 0 && (force_global || max_live() > ms_cap)) {
-    int64_t mnew = 0;
-    GS_TRY(iterate(ctx, m, &mnew));
-    gs::k_compose<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->parent.as<int32_t>(),
-                                                        ctx->root.as<int32_t>());
-    GS_LAUNCHED("k_compose");
-    gs::k_frame_ranges<<<blocks_for(mnew, 256), 256, 0, st>>>(
-        (int)mnew, b.vol_frame, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->ffirst.as<int32_t>(),
-        ctx->fcount.as<int32_t>());
-    GS_LAUNCHED("k_frame_ranges");
-    gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ffirst.as<int32_t>(),
-                                                            ctx->fcount.as<int32_t>());
-    GS_LAUNCHED("k_frame_counts");
-    GS_CK(cudaMemcpyAsync(fch.data(), ctx->fchanged.p, sizeof(int32_t) * nf,
-                          cudaMemcpyDeviceToHost, st));
-    GS_CK(cudaMemcpyAsync(fadj.data(), ctx->fadj.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
-                          st));
-    GS_CK(cudaMemcpyAsync(fm.data(), ctx->fm.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
-    GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->fcount.p, sizeof(int32_t) * nf,
-                          cudaMemcpyDeviceToHost, st));
-    GS_CK(cudaMemcpyAsync(fdisp.data(), ctx->fdisp.p, sizeof(unsigned long long) * nf,
-                          cudaMemcpyDeviceToHost, st));
-    int err = 0;
-    GS_TRY(read_err(ctx, &err));
-    if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
-    if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
-    ++iter;
-    for (int64_t f = 0; f < nf; ++f) {
-      if (ctx->h_done[f]) continue;
-      swept += fm[f];
-      if (rec) {
-        double dsp;
-        std::memcpy(&dsp, &fdisp[f], sizeof(double));
-        ctx->hist_m[f].push_back(fm[f]);
-        ctx->hist_d[f].push_back(dsp);
-      }
-      ctx->h_iters[f] = iter;
-      const bool conv = !fadj[f] || !fch[f];
-      if (conv || iter >= cfg->max_iter) {
-        ctx->h_done[f] = 1;
-        ctx->h_conv[f] = conv ? 1 : 0;
-        --live;
-      }
-    }
-    m = mnew;
-    GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
-                          cudaMemcpyHostToDevice, st));
-  }
-  // hand-off: K8 finishes every frame (frames already done are copied out unchanged)
-  std::vector<int32_t> g_iters = ctx->h_iters;
-  GS_CK(cudaMemcpyAsync(ctx->fiters.p, ctx->h_iters.data(), sizeof(int32_t) * nf,
-                        cudaMemcpyHostToDevice, st));
-  GS_CK(cudaMemcpyAsync(ctx->fconv.p, ctx->h_conv.data(), sizeof(int32_t) * nf,
-                        cudaMemcpyHostToDevice, st));
-  GS_TRY(grow(ctx, ctx->hist, (sizeof(int64_t) + sizeof(double)) * nf * cfg->max_iter));
-  const int64_t ml = std::max<int64_t>(1, max_live());
-  int ms_run = 32;
-  while (ms_run < ml) ms_run <<= 1;
-  ms_run = std::min(ms_run, ms_cap);
-  const int threads = std::min(1024, std::max(128, ms_run));
-  // several frames per SM when there are more frames than SMs (one wave for cfg4)
+  ms_run = std::min(std::max(ms_run, 32), ms_cap);
+  const int threads = std::min(512, std::max(128, ms_run));
   const int64_t per_sm = std::min<int64_t>(4, std::max<int64_t>(1, (nf + ctx->num_sms - 1) / ctx->num_sms));
   const size_t budget = kResidentSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
   const size_t state = (size_t)ms_run * gs::resident_bytes_per_cell(d);
-  // dense int16 key->slot table of the frame box in smem when it is small (cfg1/2/4 frames:
-  // a few thousand cells); otherwise K8 indexes through the global dense grid
-  const size_t sidx = (b.vol_frame * 2 <= 48 * 1024) ? ((size_t)b.vol_frame * 2 + 15) & ~size_t(15) : 0;
+  // the box's frame volume is host-known only on the synchronous path; the optimistic path
+  // uses the cached choice
+  const int64_t vf = deferrable ? ctx->shape_vol_frame : ctx->box.vol_frame;
+  const size_t sidx = (vf * 2 <= 48 * 1024) ? ((size_t)vf * 2 + 15) & ~size_t(15) : 0;
   const size_t offs_bytes = (size_t)resident_offs_bytes_host(d);
   const size_t fixed = state + sidx + offs_bytes;
   const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
+  unsigned* cnt32 = ctx->counters.as<unsigned>();
   // K8 owns the global index from here on (it re-keys it per frame and leaves it clean)
-  gs::k_idx_clear<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[ctx->cur].as<uint32_t>(),
-                                                      ctx->idx.as<int32_t>());
-  GS_LAUNCHED("k_idx_clear");
+  if (m_host < 0) {
+    gs::k_idx_put_dev<<<blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
+                                   (int64_t)ctx->num_sms * 4), 256, 0, st>>>(
+        cnt32, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->idx.as<int32_t>(), 0);
+    GS_LAUNCHED("k_idx_put_dev");
+  } else {
+    gs::k_idx_clear<<<blocks_for(m_host, 256), 256, 0, st>>>(
+        (int)m_host, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->idx.as<int32_t>());
+    GS_LAUNCHED("k_idx_clear");
+  }
   const int fin = 1 - ctx->cur;
   gs::ResidentArgs ra;
-  ra.box = b;
+  ra.box = deferrable ? ctx->shape_box : ctx->box;
   ra.ms = ms_run;
   ra.pool_bytes = (int)(pool_bytes & ~size_t(15));
   ra.max_iter = cfg->max_iter;
@@ -699,23 +651,21 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ra.hist_m = ctx->hist.as<int64_t>();
   ra.hist_d = (double*)(ctx->hist.as<int64_t>() + nf * cfg->max_iter);
   ra.err = ctx->errflag.as<int>();
-  GS_TRY(grow(ctx, ctx->modes, sizeof(int64_t) * 12));
-  GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
   ra.mode_count = ctx->modes.as<int64_t>();
   ra.prof = (long long*)(ctx->modes.as<int64_t>() + 4);
   ra.gidx = ctx->idx.as<int32_t>();
   ra.sidx_bytes = (int)sidx;
-  const size_t smem = fixed + ra.pool_bytes;
-  GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, smem, ra));
-  ctx->cur = fin;
+  ra.fmax = deferrable ? (const int*)(cnt32 + 2) : nullptr;
+  ra.deferred = (int*)(cnt32 + 4);
+  GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
+  GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, fixed + ra.pool_bytes, ra));
   GS_CK(cudaEventRecord(ctx->ev[3], st));
-  // ---- labels
-  gs::k_labtab_local<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->initkey.as<uint32_t>(),
-                                                          ctx->root.as<int32_t>(),
-                                                          ctx->lab.as<int32_t>());
-  GS_LAUNCHED("k_labtab_local");
-  int32_t* dlabels = out->labels;
-  const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
+  // ---- labels: lab[initial cell] = final frame-local id, then label[p] = lab[slot[p]]
+  gs::k_labtab_dev<<<blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
+                                (int64_t)ctx->num_sms * 4), 256, 0, st>>>(
+      cnt32, ctx->initkey.as<uint32_t>(), ctx->root.as<int32_t>(), ctx->lab.as<int32_t>());
+  GS_LAUNCHED("k_labtab_dev");
+  int32_t* dlabels = user_labels;
   if (!dev_out) {
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
@@ -727,53 +677,223 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   GS_CK(cudaEventRecord(ctx->ev[9], st));
   GS_CK(cudaEventRecord(ctx->ev[4], st));
   if (!dev_out)
-    GS_CK(cudaMemcpyAsync(out->labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
+    GS_CK(cudaMemcpyAsync(user_labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
                           st));
   GS_CK(cudaEventRecord(ctx->ev[5], st));
-  ctx->h_ffirst.assign(nf, 0);
-  std::vector<int32_t> hk(nf);
-  GS_CK(cudaMemcpyAsync(ctx->h_ffirst.data(), ctx->ffirst.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(hk.data(), ctx->fk.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(ctx->h_iters.data(), ctx->fiters.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(ctx->h_conv.data(), ctx->fconv.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToHost, st));
-  std::vector<int64_t> hm;
-  std::vector<double> hd;
-  {
-    hm.resize((size_t)nf * cfg->max_iter);
-    hd.resize((size_t)nf * cfg->max_iter);
-    GS_CK(cudaMemcpyAsync(hm.data(), ra.hist_m, sizeof(int64_t) * hm.size(),
-                          cudaMemcpyDeviceToHost, st));
-    GS_CK(cudaMemcpyAsync(hd.data(), ra.hist_d, sizeof(double) * hd.size(),
-                          cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.err, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.modes, ctx->modes.p, 96, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.ffirst, ctx->ffirst.p, 4 * nf, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.fk, ctx->fk.p, 4 * nf, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.fiters, ctx->fiters.p, 4 * nf, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.fconv, ctx->fconv.p, 4 * nf, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(rb.hm, ra.hist_m, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
+  if (rec)
+    GS_CK(cudaMemcpyAsync(rb.hd, ra.hist_d, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
+gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
+  GS_TRY(validate(in, cfg));
+  if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
+  const int d = in->d;
+  const int64_t n = in->n, nf = in->batch, ntot = n * nf;
+  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
+  const bool rec = (cfg->flags & GS_RECORD_HISTORY) != 0;
+  const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
+  const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
+  ctx->have_run = false;
+  ctx->stats = gs_stats{};
+  ctx->cur = 0;
+  cudaStream_t st = ctx->stream;
+  GS_TRY(grow(ctx, ctx->errflag, 32));
+  GS_TRY(grow(ctx, ctx->counters, 64));
+  GS_TRY(ensure_frames(ctx, nf));
+  GS_TRY(grow(ctx, ctx->hist, (sizeof(int64_t) + sizeof(double)) * nf * cfg->max_iter));
+  GS_TRY(grow(ctx, ctx->modes, sizeof(int64_t) * 12));
+  Readback rb;
+  GS_TRY(map_readback(ctx, nf, cfg->max_iter, &rb));
+  const void* dpts = in->points;
+  GS_CK(cudaEventRecord(ctx->ev[0], st));
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
+    dpts = ctx->pts.p;
   }
-  int64_t h_modes[12] = {0};
-  GS_CK(cudaMemcpyAsync(h_modes, ctx->modes.p, sizeof(int64_t) * 12, cudaMemcpyDeviceToHost, st));
-  int err = 0;
-  GS_TRY(read_err(ctx, &err));
-  if (err & 16) return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
-  if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
-  int64_t ktot = 0;
+  GS_CK(cudaEventRecord(ctx->ev[1], st));
+  const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
+  bool optimistic = !force_global && ctx->shape_ms > 0 && key == ctx->shape;
+  std::vector<int32_t> g_iters(nf, 0);
+  int64_t swept = 0;
+  for (int attempt = 0;; ++attempt) {
+    if (attempt > 3) return fail(ctx, GS_E_INTERNAL_INVARIANT, "could not size the cell grid");
+    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h));
+    GS_CK(cudaEventRecord(ctx->ev[2], st));
+    GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fiters.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fconv.p, 0, sizeof(int32_t) * nf, st));
+    bool deferred = false;
+    if (optimistic) {
+      GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, -1, out->labels, dev_out,
+                         rec, rb));
+      if (rb.err[0] & 32) {  // key box beyond the grid: grow and redo the run
+        GS_TRY(ensure_dense(ctx, *(long long*)(rb.err + 2), d));
+        continue;
+      }
+      if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+      if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+      if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+      deferred = rb.ctr[4] != 0;
+      if (!deferred) break;
+      optimistic = false;
+      ctx->shape_ms = 0;
+    }
+    // ---- synchronous path: the host sees the initial cells and drives the global path
+    int hdr[8];
+    unsigned ctr[16];
+    GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaStreamSynchronize(st));
+    if (hdr[0] & 32) {
+      GS_TRY(ensure_dense(ctx, *(long long*)(hdr + 2), d));
+      continue;
+    }
+    if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    if (hdr[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+    const int64_t m0 = ctr[0];
+    const GsBox& b = ctx->box;
+    if (deferred) {  // the optimistic tail cleared the index: put the initial cells back
+      gs::k_idx_set<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->ckey[0].as<uint32_t>(),
+                                                         ctx->idx.as<int32_t>());
+      GS_LAUNCHED("k_idx_set");
+      GS_CK(cudaMemsetAsync(ctx->counters.as<unsigned>() + 4, 0, 4, st));
+    }
+    // (a) global path (K4/K5 kernels, host-driven) while some live frame has more active
+    //     cells than one CTA's shared memory holds; (b) then K8 runs every remaining
+    //     iteration of every frame on the device.
+    ctx->h_done.assign(nf, 0);
+    ctx->h_iters.assign(nf, 0);
+    ctx->h_conv.assign(nf, 0);
+    ctx->hist_m.assign(rec ? nf : 0, {});
+    ctx->hist_d.assign(rec ? nf : 0, {});
+    std::vector<int32_t> fch(nf), fadj(nf), fm(nf), fcnt(nf);
+    std::vector<unsigned long long> fdisp(nf);
+    GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->icount.p, sizeof(int32_t) * nf,
+                          cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaStreamSynchronize(st));
+    int64_t m = m0, live = nf;
+    int iter = 0;
+    const int ms_cap = resident_capacity(d);
+    auto max_live = [&]() {
+      int64_t mx = 0;
+      for (int64_t f = 0; f < nf; ++f)
+        if (!ctx->h_done[f]) mx = std::max<int64_t>(mx, fcnt[f]);
+      return mx;
+    };
+    while (live > 0 && (force_global || max_live() > ms_cap)) {
+      int64_t mnew = 0;
+      GS_TRY(iterate(ctx, m, &mnew));
+      gs::k_compose<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->parent.as<int32_t>(),
+                                                          ctx->root.as<int32_t>());
+      GS_LAUNCHED("k_compose");
+      gs::k_frame_ranges<<<blocks_for(mnew, 256), 256, 0, st>>>(
+          (int)mnew, b.vol_frame, ctx->ckey[ctx->cur].as<uint32_t>(),
+          ctx->ffirst.as<int32_t>(), ctx->fcount.as<int32_t>());
+      GS_LAUNCHED("k_frame_ranges");
+      gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ffirst.as<int32_t>(),
+                                                              ctx->fcount.as<int32_t>());
+      GS_LAUNCHED("k_frame_counts");
+      GS_CK(cudaMemcpyAsync(fch.data(), ctx->fchanged.p, sizeof(int32_t) * nf,
+                            cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaMemcpyAsync(fadj.data(), ctx->fadj.p, sizeof(int32_t) * nf,
+                            cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaMemcpyAsync(fm.data(), ctx->fm.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
+                            st));
+      GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->fcount.p, sizeof(int32_t) * nf,
+                            cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaMemcpyAsync(fdisp.data(), ctx->fdisp.p, sizeof(unsigned long long) * nf,
+                            cudaMemcpyDeviceToHost, st));
+      int err = 0;
+      GS_TRY(read_err(ctx, &err));
+      if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
+      if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+      ++iter;
+      for (int64_t f = 0; f < nf; ++f) {
+        if (ctx->h_done[f]) continue;
+        swept += fm[f];
+        if (rec) {
+          double dsp;
+          std::memcpy(&dsp, &fdisp[f], sizeof(double));
+          ctx->hist_m[f].push_back(fm[f]);
+          ctx->hist_d[f].push_back(dsp);
+        }
+        ctx->h_iters[f] = iter;
+        const bool conv = !fadj[f] || !fch[f];
+        if (conv || iter >= cfg->max_iter) {
+          ctx->h_done[f] = 1;
+          ctx->h_conv[f] = conv ? 1 : 0;
+          --live;
+        }
+      }
+      m = mnew;
+      GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
+                            cudaMemcpyHostToDevice, st));
+    }
+    g_iters = ctx->h_iters;
+    GS_CK(cudaMemcpyAsync(ctx->fiters.p, ctx->h_iters.data(), sizeof(int32_t) * nf,
+                          cudaMemcpyHostToDevice, st));
+    GS_CK(cudaMemcpyAsync(ctx->fconv.p, ctx->h_conv.data(), sizeof(int32_t) * nf,
+                          cudaMemcpyHostToDevice, st));
+    const int64_t ml = std::max<int64_t>(1, max_live());
+    int ms_run = 32;
+    while (ms_run < ml) ms_run <<= 1;
+    ms_run = std::min(ms_run, ms_cap);
+    if (iter == 0 && !force_global) {  // K8 straight from binning: later runs go optimistic
+      ctx->shape = key;
+      ctx->shape_ms = std::min(ms_cap, 2 * ms_run);  // headroom for data-dependent m0
+      ctx->shape_box = b;
+      ctx->shape_vol_frame = b.vol_frame;
+    }
+    GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, m, out->labels, dev_out, rec, rb));
+    if (rb.err[0] & 16)
+      return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
+    if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+    break;
+  }
+  ctx->cur = 1 - ctx->cur;
+  // ---- results
+  if (!ctx->hist_m.size() && rec) {
+    ctx->hist_m.assign(nf, {});
+    ctx->hist_d.assign(nf, {});
+  }
+  if (ctx->hist_m.size() != (size_t)(rec ? nf : 0)) {
+    ctx->hist_m.assign(rec ? nf : 0, {});
+    ctx->hist_d.assign(rec ? nf : 0, {});
+  }
+  ctx->h_ffirst.assign(rb.ffirst, rb.ffirst + nf);
   ctx->h_k.assign(nf, 0);
+  ctx->h_iters.assign(rb.fiters, rb.fiters + nf);
+  ctx->h_conv.assign(rb.fconv, rb.fconv + nf);
+  int64_t ktot = 0;
   for (int64_t f = 0; f < nf; ++f) {
-    ctx->h_k[f] = hk[f];
-    ktot += hk[f];
-    out->k[f] = ctx->h_k[f];
-    out->iterations[f] = ctx->h_iters[f];
-    out->converged[f] = ctx->h_conv[f];
-    for (int t = g_iters[f]; t < ctx->h_iters[f]; ++t) {
-      const int64_t mt = hm[(size_t)f * cfg->max_iter + t];
+    ctx->h_k[f] = rb.fk[f];
+    ktot += rb.fk[f];
+    out->k[f] = rb.fk[f];
+    out->iterations[f] = rb.fiters[f];
+    out->converged[f] = rb.fconv[f];
+    for (int t = g_iters[f]; t < rb.fiters[f]; ++t) {
+      const int64_t mt = rb.hm[(size_t)f * cfg->max_iter + t];
       swept += mt;
       if (rec) {
         ctx->hist_m[f].push_back(mt);
-        ctx->hist_d[f].push_back(hd[(size_t)f * cfg->max_iter + t]);
+        ctx->hist_d[f].push_back(rb.hd[(size_t)f * cfg->max_iter + t]);
       }
     }
   }
   ctx->k_total = ktot;
-  m = ktot;
   ctx->nframes = nf;
   ctx->have_run = true;
   float ms = 0;
@@ -795,16 +915,17 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
   s.ms_k_label = ms;
   s.cells_swept = swept;
-  s.m0 = m0;
-  s.k_total = m;
+  s.m0 = rb.ctr[0];
+  s.k_total = ktot;
   s.max_iterations = 0;
   for (int64_t f = 0; f < nf; ++f) s.max_iterations = std::max(s.max_iterations, ctx->h_iters[f]);
-  for (int k = 0; k < 3; ++k) s.sweep_modes[k] = h_modes[k];
-  for (int k = 0; k < 8; ++k) s.resident_cycles[k] = h_modes[4 + k];
-  s.fixed_shift = b.F;
-  s.dense_cells = b.vol_total;
+  for (int k = 0; k < 3; ++k) s.sweep_modes[k] = rb.modes[k];
+  for (int k = 0; k < 8; ++k) s.resident_cycles[k] = rb.modes[4 + k];
+  s.fixed_shift = gs_fixed_shift(n, cfg->h);
+  s.dense_cells = ctx->box.vol_total;
   return GS_OK;
 }
+
 
 }  // namespace
 
@@ -879,8 +1000,10 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->root, &ctx->initkey, &ctx->fdone, &ctx->fchanged, &ctx->fadj,
                     &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->fcount, &ctx->ifirst, &ctx->icount,
                     &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->hist, &ctx->counters, &ctx->errflag,
-                    &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes})
+                    &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes, &ctx->tiles,
+                    &ctx->dbox})
     b->release();
+  if (ctx->pin) cudaFreeHost(ctx->pin);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -952,8 +1075,27 @@ gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_
                           ctx->stream));
     dpts = ctx->pts.p;
   }
+  GS_TRY(grow(ctx, ctx->errflag, 32));
+  GS_TRY(grow(ctx, ctx->counters, 64));
   int64_t m0 = 0;
-  GS_TRY(build_cells(ctx, dpts, in->dtype, d, n, 1, h, &m0));
+  for (int attempt = 0;; ++attempt) {
+    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, 1, h));
+    int hdr[8];
+    unsigned ctr[16];
+    GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaMemcpyAsync(ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    GS_CK(cudaStreamSynchronize(ctx->stream));
+    if ((hdr[0] & 32) && attempt < 3) {
+      GS_TRY(ensure_dense(ctx, *(long long*)(hdr + 2), d));
+      continue;
+    }
+    if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    if (hdr[0] & (32 | 64)) return fail(ctx, GS_E_KEY_RANGE, "key box too large");
+    m0 = ctr[0];
+    break;
+  }
   *m_out = m0;
   if (m0 > cap_m) return fail(ctx, GS_E_INVALID_PARAMETER, "cap_m too small");
   std::vector<uint32_t> hk(m0), hc(m0);

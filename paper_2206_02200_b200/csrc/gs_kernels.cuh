@@ -117,13 +117,15 @@ __host__ __device__ constexpr int bin_table_entries() {
 
 template <int D, typename T>
 __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, int64_t ntot,
-                                                   GsBox b, uint32_t* __restrict__ cnt,
+                                                   const GsBox* __restrict__ pb,
+                                                   uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
-                                                   uint32_t* __restrict__ slot,
-                                                   uint32_t* __restrict__ occ, unsigned int* m0,
-                                                   int* err) {
+                                                   uint32_t* __restrict__ slot, int* err) {
   constexpr int TBL = bin_table_entries<D>();
   constexpr uint32_t EMPTY = 0xffffffffu;
+  if (*err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
+  __shared__ GsBox b;
+  if (threadIdx.x == 0) b = *pb;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* ts = (unsigned long long*)smem;      // TBL * D sums
   uint32_t* tk = (uint32_t*)(ts + (size_t)TBL * D);        // TBL keys
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
 #pragma unroll
       for (int c = 0; c < D; ++c) atomicAdd(&ts[hit * D + c], (unsigned long long)q[c]);
     } else {
-      if (atomicAdd(&cnt[L], my_cnt) == 0u) occ[atomicAdd(m0, 1u)] = key;
+      atomicAdd(&cnt[L], my_cnt);
 #pragma unroll
       for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], (unsigned long long)q[c]);
     }
@@ -214,9 +216,201 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
     const uint32_t key = tk[j];
     if (key == EMPTY) continue;
     const int64_t L = key;
-    if (atomicAdd(&cnt[L], tc[j]) == 0u) occ[atomicAdd(m0, 1u)] = key;
+    atomicAdd(&cnt[L], tc[j]);
 #pragma unroll
     for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], ts[j * D + c]);
+  }
+}
+
+// ---------------------------------------------------------------- K1b: box on the device
+// Reduces k_bounds' per-block partials and writes the dense-grid geometry, so no host round
+// trip sits between the bounds pass and binning.  err bit 1: non-finite input (from
+// k_bounds); bit 32: key box larger than the allocated grid (*need = cells required).
+__global__ void k_box(const double* __restrict__ bpart, int nblk, int d, double h, int F,
+                      int64_t n, int64_t nframes, int64_t cap_cells, GsBox* __restrict__ out,
+                      int* err, long long* need) {
+  __shared__ double mn[GS_DMAX], mx[GS_DMAX];
+  const int c = threadIdx.x;
+  if (c < d) {
+    double a = INFINITY, z = -INFINITY;
+    for (int k = 0; k < nblk; ++k) {
+      a = fmin(a, bpart[k * d + c]);
+      z = fmax(z, bpart[(int64_t)nblk * d + k * d + c]);
+    }
+    mn[c] = a;
+    mx[c] = z;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  GsBox b;
+  b.d = d;
+  b.F = F;
+  b.h = h;
+  b.inv_h = __drcp_rn(h);
+  b.scale = ldexp(1.0, F);
+  b.inv_scale = ldexp(1.0, -F);
+  b.n = n;
+  b.nframes = nframes;
+  double vol = 1.0;
+  bool bad = (*err & 1) != 0;
+  for (int k = 0; k < GS_DMAX; ++k) b.kmin[k] = 0, b.ext[k] = 1, b.stride[k] = 0;
+  for (int k = 0; k < d && !bad; ++k) {
+    const double lo = floor(__ddiv_rn(mn[k], h)), hi = floor(__ddiv_rn(mx[k], h));
+    if (!(fabs(lo) < 4e15) || !(fabs(hi) < 4e15)) {
+      bad = true;
+      break;
+    }
+    b.kmin[k] = (int64_t)lo - GS_APRON;
+    b.ext[k] = (int64_t)hi - (int64_t)lo + 1 + 2 * GS_APRON;
+    vol *= (double)b.ext[k];
+  }
+  int64_t s = 1;
+  for (int k = d - 1; k >= 0; --k) {
+    b.stride[k] = s;
+    s *= b.ext[k];
+  }
+  b.vol_frame = s;
+  b.vol_total = s * nframes;
+  if (!bad && vol * (double)nframes > (double)cap_cells) {
+    atomicOr(err, 32);
+    *need = (vol * (double)nframes < 9e18) ? (long long)(vol * (double)nframes) : (1ll << 62);
+  }
+  if (bad && !(*err & 1)) atomicOr(err, 64);  // key magnitude beyond the int64 key range
+  *out = b;
+}
+
+// ---------------------------------------------------------------- K3: compaction by scan
+// The dense grid is in lexicographic order, so scanning its occupancy yields the cell list
+// already sorted: no occupied list, no sort, no host round trip for m0.
+constexpr int kOccTile = 2048;  // cells per tile: 256 threads x 8
+
+__device__ __forceinline__ int block_excl_scan_256(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < 8 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < 8) sh[lane] = t;
+  }
+  __syncthreads();
+  const int excl = x - v + (w > 0 ? sh[w - 1] : 0);
+  *total = sh[7];
+  __syncthreads();
+  return excl;
+}
+
+__global__ void __launch_bounds__(256) k_occ_count(const GsBox* __restrict__ pb,
+                                                   const uint32_t* __restrict__ cnt,
+                                                   int* __restrict__ tile_cnt,
+                                                   const int* __restrict__ err) {
+  if (*err & (1 | 32 | 64)) return;
+  __shared__ int sh[8];
+  const int64_t V = pb->vol_total;
+  const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * 8;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += (base + k < V) && cnt[base + k] != 0u;
+    int total;
+    block_excl_scan_256(c, sh, &total);
+    if (threadIdx.x == 0) tile_cnt[t] = total;
+  }
+}
+
+// single block: tile counts -> exclusive tile offsets (in place); m0 = total
+__global__ void __launch_bounds__(1024) k_occ_scan(const GsBox* __restrict__ pb,
+                                                   int* __restrict__ tile, unsigned int* m0,
+                                                   const int* __restrict__ err) {
+  if (*err & (1 | 32 | 64)) return;
+  __shared__ int sh[32];
+  const int64_t V = pb->vol_total;
+  const int ntiles = (int)((V + kOccTile - 1) / kOccTile);
+  const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int chunk = (ntiles + T - 1) / T;
+  const int beg = min(ntiles, tid * chunk), end = min(ntiles, beg + chunk);
+  int local = 0;
+  for (int j = beg; j < end; ++j) local += tile[j];
+  int x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < (T >> 5) ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) t += y;
+    }
+    sh[lane] = t;
+  }
+  __syncthreads();
+  int run = x - local + (w > 0 ? sh[w - 1] : 0);
+  for (int j = beg; j < end; ++j) {
+    const int v = tile[j];
+    tile[j] = run;
+    run += v;
+  }
+  if (tid == 0) *m0 = (unsigned)sh[(T >> 5) - 1];
+}
+
+// per tile: occupied cells -> lex-ordered cell list; centroids from the fixed-point sums;
+// restores the clean-grid invariant (cnt = qs = 0) for what it consumes.
+__global__ void __launch_bounds__(256) k_occ_compact(
+    const GsBox* __restrict__ pb, const int* __restrict__ tile_off, uint32_t* __restrict__ cnt,
+    unsigned long long* __restrict__ qs, uint32_t* __restrict__ ckey,
+    uint32_t* __restrict__ ccnt, double* __restrict__ S, int32_t* __restrict__ idx,
+    int32_t* __restrict__ root, uint32_t* __restrict__ initkey, const int* __restrict__ err) {
+  if (*err & (1 | 32 | 64)) return;
+  __shared__ int sh[8];
+  __shared__ GsBox b;
+  if (threadIdx.x == 0) b = *pb;
+  __syncthreads();
+  const int64_t V = b.vol_total;
+  const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * 8;
+    uint32_t c8[8];
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c8[k] = (base + k < V) ? cnt[base + k] : 0u;
+      c += c8[k] != 0u;
+    }
+    int total;
+    int pos = tile_off[t] + block_excl_scan_256(c, sh, &total);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (c8[k] == 0u) continue;
+      const int64_t L = base + k;
+      for (int q = 0; q < b.d; ++q) {
+        const long long s = (long long)qs[L * b.d + q];
+        S[(int64_t)pos * b.d + q] = gs_fix_centroid(gs_key_of(b, L, q), s, c8[k], b.h, b.inv_scale);
+        qs[L * b.d + q] = 0ull;
+      }
+      cnt[L] = 0u;
+      ckey[pos] = (uint32_t)L;
+      ccnt[pos] = c8[k];
+      idx[L] = pos;
+      root[pos] = pos;
+      initkey[pos] = (uint32_t)L;
+      ++pos;
+    }
   }
 }
 

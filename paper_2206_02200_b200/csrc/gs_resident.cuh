@@ -57,6 +57,10 @@ struct ResidentArgs {
   // when it fits (sidx_bytes > 0), else the engine's global dense grid (int32, clean = -1)
   int32_t* gidx;
   int sidx_bytes;
+  // optimistic launch: if the largest frame (*fmax) exceeds ms, every CTA leaves the state
+  // untouched and raises *deferred; the host then takes the global path first
+  const int* fmax;
+  int* deferred;
 };
 
 // shared-memory bytes per cell (excluding the index and neighbour-record pool)
@@ -167,10 +171,14 @@ __device__ int rs_scan(int* a, int n, int* wtmp) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
+__global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   const GsBox& b = a.box;
   const int f = blockIdx.x;
   const int tid = threadIdx.x, T = blockDim.x;
+  if (a.fmax && *a.fmax > a.ms) {
+    if (f == 0 && tid == 0) *a.deferred = 1;
+    return;
+  }
   const int first = a.ffirst[f];
   int m = a.fcount[f];
   const int ifirst = a.ifirst[f], icnt = a.icount[f];
@@ -346,102 +354,132 @@ __global__ void __launch_bounds__(1024) k_resident(ResidentArgs a) {
     __syncthreads();
     lap(0);
 
-    // ---- (2) the sweep: dataflow over the static DAG of this iteration
-    for (int base = 0; base < m; base += T) {
-      const int i = base + tid;
-      bool pending = i < m;
-      int n = 0, e = 0, t_ok = 0;
-      if (pending) {
-        n = nbn[i];
-        e = nbe[i];
-        if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
-          for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
-          rs_st_release(&flag[i], epoch);
-          pending = false;
-        }
+    // ---- (2) the sweep.  The DAG of one sweep is static, so (a) every cell's level = longest
+    // path over lex-earlier active neighbours is found by an integer relaxation, (b) cells are
+    // bucketed by level, and (c) levels run in order separated by barriers: when a cell is
+    // updated all its earlier neighbours are final, so the update is a straight-line sum in lex
+    // order with no polling.  Same operands, same order: bit-identical to the serial sweep.
+    auto early_nb = [&](int i, int t) -> int {
+      return mode == 0 ? (int)(uint32_t)erec[eoff[i] + t] : (int)lst[tmp[i] + t];
+    };
+    auto update_cell = [&](int i) {
+      const int n = nbn[i], e = nbe[i];
+      if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
+#pragma unroll
+        for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
+        return;
       }
       double num[D];
 #pragma unroll
       for (int c = 0; c < D; ++c) num[c] = 0.0;
       if (mode == 0) {
-        const uint64_t* er = erec + (pending ? eoff[i] : 0);
-        const double* lp = lprod + (int64_t)(pending ? loff[i] : 0) * D;
+        const uint64_t* er = erec + eoff[i];
+        for (int t = 0; t < e; ++t) {  // earlier neighbours: NEW centroids, lex order
+          const uint64_t r = er[t];
+          const uint32_t j = (uint32_t)r;
+          const double w = (double)(uint32_t)(r >> 32);
+#pragma unroll
+          for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, S1[j * D + c]));
+        }
+        const double* lp = lprod + (int64_t)loff[i] * D;
         const int nl = n - e;
-        while (__any_sync(0xffffffffu, pending)) {
-          if (pending) {
-            // fold earlier neighbours' NEW centroids in lex order as their flags release
-            while (t_ok < e) {
-              const uint64_t r = er[t_ok];
-              const uint32_t j = (uint32_t)r;
-              if (rs_ld_acquire(&flag[j]) != epoch) break;
-              const double w = (double)(uint32_t)(r >> 32);
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, S1[j * D + c]));
-              ++t_ok;
-            }
-            if (t_ok == e) {
-              // self + later neighbours: precomputed C'*S_old products, in lex order
 #pragma unroll 4
-              for (int t = 0; t < nl; ++t) {
+        for (int t = 0; t < nl; ++t) {  // itself + later neighbours: C'*S_old, lex order
 #pragma unroll
-                for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], lp[t * D + c]);
-              }
-              const double dd = (double)den[i];
-#pragma unroll
-              for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
-              rs_st_release(&flag[i], epoch);
-              pending = false;
-            }
-          }
+          for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], lp[t * D + c]);
         }
-      } else if (mode == 1) {
-        const uint16_t* ls = lst + (pending ? tmp[i] : 0);
-        while (__any_sync(0xffffffffu, pending)) {
-          if (pending) {
-            while (t_ok < e && rs_ld_acquire(&flag[ls[t_ok]]) == epoch) ++t_ok;
-            if (t_ok == e) {
-              for (int t = 0; t < n; ++t) {
-                const int j = ls[t];
-                const double w = (double)cnt[j];
-                const double* src = (t < e) ? S1 : S0;
-#pragma unroll
-                for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, src[j * D + c]));
-              }
-              const double dd = (double)den[i];
-#pragma unroll
-              for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
-              rs_st_release(&flag[i], epoch);
-              pending = false;
-            }
-          }
-        }
-      } else if (pending) {
-        // records do not fit (very dense high-d neighbourhoods): look neighbours up again,
-        // waiting on each earlier one in turn (independent thread scheduling keeps lanes going)
-        NbrIt it = nbr_begin();
-        const int64_t Li = key[i];
-        for (int t = 0; t < K; ++t) {
-          const int j = idx_get(Li + it.at(t));
-          it.step(b);
-          if (j < 0) continue;
-          if (j < i) {
-            while (vflag[j] != epoch) {
-            }
-            __threadfence_block();
-          }
+      } else {
+        const uint16_t* ls = lst + tmp[i];
+        for (int t = 0; t < n; ++t) {
+          const int j = ls[t];
           const double w = (double)cnt[j];
-          const double* src = (j < i) ? S1 : S0;
+          const double* src = (t < e) ? S1 : S0;
 #pragma unroll
           for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, src[j * D + c]));
         }
-        const double dd = (double)den[i];
+      }
+      const double dd = (double)den[i];
 #pragma unroll
-        for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
+      for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
+    };
+    if (mode != 2) {
+      // (a) levels (flag[] holds them; monotone relaxation, converges in depth+1 rounds)
+      volatile uint32_t* lvl = flag;
+      for (int i = tid; i < m; i += T) flag[i] = 0u;
+      __syncthreads();
+      for (;;) {
+        bool ch = false;
+        for (int i = tid; i < m; i += T) {
+          const int e = nbe[i];
+          uint32_t mx = 0u;
+          for (int t = 0; t < e; ++t) mx = max(mx, lvl[early_nb(i, t)] + 1u);
+          if (mx > lvl[i]) {
+            lvl[i] = mx;
+            ch = true;
+          }
+        }
+        if (!__syncthreads_or(ch)) break;
+      }
+      // (b) bucket by level: counts -> offsets -> order (reusing sk as int scratch)
+      int* lcnt = (int*)sk;        // [MS] level counts, then offsets
+      int* order = (int*)sk + MS;  // [MS] cells in level order
+      __shared__ unsigned s_maxl;
+      if (tid == 0) s_maxl = 0u;
+      for (int j = tid; j < m; j += T) lcnt[j] = 0;
+      __syncthreads();
+      for (int i = tid; i < m; i += T) {
+        atomicAdd(&lcnt[flag[i]], 1);
+        atomicMax(&s_maxl, flag[i]);
+      }
+      __syncthreads();
+      const int nlev = (int)s_maxl + 1;
+      rs_scan(lcnt, nlev, wtmp);
+      for (int i = tid; i < m; i += T) order[atomicAdd(&lcnt[flag[i]], 1)] = i;
+      __syncthreads();
+      // lcnt[l] now holds the END of level l; level l spans [l ? lcnt[l-1] : 0, lcnt[l])
+      // (c) level-synchronous update
+      for (int l = 0; l < nlev; ++l) {
+        const int beg = l ? lcnt[l - 1] : 0, end = lcnt[l];
+        for (int k = beg + tid; k < end; k += T) update_cell(order[k]);
+        __syncthreads();
+      }
+    } else {
+      // records do not fit (very dense high-d neighbourhoods): dataflow with lookups, waiting
+      // on each earlier neighbour in turn (independent thread scheduling keeps lanes going)
+      for (int i = tid; i < m; i += T) {
+        double num[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) num[c] = 0.0;
+        const int n = nbn[i];
+        if (n <= 1) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
+        } else {
+          NbrIt it = nbr_begin();
+          const int64_t Li = key[i];
+          for (int t = 0; t < K; ++t) {
+            const int j = idx_get(Li + it.at(t));
+            it.step(b);
+            if (j < 0) continue;
+            if (j < i) {
+              while (vflag[j] != epoch) {
+              }
+              __threadfence_block();
+            }
+            const double w = (double)cnt[j];
+            const double* src = (j < i) ? S1 : S0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, src[j * D + c]));
+          }
+          const double dd = (double)den[i];
+#pragma unroll
+          for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
+        }
         __threadfence_block();
         vflag[i] = epoch;
       }
+      __syncthreads();
     }
-    __syncthreads();
 
     lap(1);
     // ---- (3) rehome, changed, displacement
@@ -608,6 +646,42 @@ __global__ void k_labtab_local(int m0, const uint32_t* __restrict__ initkey,
                                const int32_t* __restrict__ root, int32_t* __restrict__ lab) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m0) lab[initkey[i]] = root[i];
+}
+
+// ---- variants whose cell count lives on the device (no host round trip): grid-stride
+__global__ void k_frame_ranges_dev(const unsigned* __restrict__ pm, const GsBox* __restrict__ pb,
+                                   const uint32_t* __restrict__ key, int32_t* __restrict__ first,
+                                   int32_t* __restrict__ end) {
+  const int m = (int)*pm;
+  const int64_t vf = pb->vol_frame;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < m; g += gridDim.x * blockDim.x) {
+    const int64_t f = key[g] / vf;
+    if (g == 0 || (int64_t)(key[g - 1] / vf) != f) first[f] = g;
+    if (g == m - 1 || (int64_t)(key[g + 1] / vf) != f) end[f] = g + 1;
+  }
+}
+
+__global__ void k_frame_counts_dev(int64_t nf, const int32_t* __restrict__ first,
+                                   int32_t* __restrict__ count, int* __restrict__ fmax) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    count[f] -= first[f];
+    atomicMax(fmax, count[f]);
+  }
+}
+
+__global__ void k_labtab_dev(const unsigned* __restrict__ pm, const uint32_t* __restrict__ initkey,
+                             const int32_t* __restrict__ root, int32_t* __restrict__ lab) {
+  const int m0 = (int)*pm;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m0; i += gridDim.x * blockDim.x)
+    lab[initkey[i]] = root[i];
+}
+
+__global__ void k_idx_put_dev(const unsigned* __restrict__ pm, const uint32_t* __restrict__ key,
+                              int32_t* __restrict__ idx, int set) {
+  const int m = (int)*pm;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    idx[key[i]] = set ? i : -1;
 }
 
 }  // namespace gs
