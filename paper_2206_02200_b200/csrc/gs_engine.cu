@@ -375,6 +375,15 @@ gs_status read_err(gs_ctx* ctx, int* out) {
 //                            [4] K8 deferred
 constexpr int64_t kDefaultDenseCells = int64_t(1) << 22;
 
+// The device found a key box larger than the allocated grid: grow to it, or refuse loudly
+// when it exceeds the dense-grid cap (no silent approximation).
+gs_status grow_dense_for(gs_ctx* ctx, long long need, int d) {
+  if (need <= 0 || need > kMaxDenseCells)
+    return fail(ctx, GS_E_KEY_RANGE,
+                "key box of " + std::to_string(need) + " cells exceeds the dense cell grid (2^28)");
+  return ensure_dense(ctx, (int64_t)need, d);
+}
+
 // n-scale phase with no host round trip: bounds -> device box -> privatised binning ->
 // compaction by scan (cells come out lexicographically sorted) -> per-frame cell ranges.
 // Errors (non-finite input, key box beyond the grid) surface in errflag at the next sync.
@@ -394,7 +403,7 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, 32, st));
   GS_CK(cudaMemsetAsync(ctx->counters.p, 0, 64, st));
   GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk));
-  gs::k_box<<<1, 32, 0, st>>>(ctx->bpart.as<double>(), (int)nblk, d, h, gs_fixed_shift(n, h), n,
+  gs::k_box<<<1, 384, 0, st>>>(ctx->bpart.as<double>(), (int)nblk, d, h, gs_fixed_shift(n, h), n,
                               nf, ctx->dense_cap, ctx->dbox.as<GsBox>(), ctx->errflag.as<int>(),
                               (long long*)(ctx->errflag.as<int>() + 2));
   GS_LAUNCHED("k_box");
@@ -603,7 +612,9 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   cudaStream_t st = ctx->stream;
   const int ms_cap = resident_capacity(d);
   ms_run = std::min(std::max(ms_run, 32), ms_cap);
-  const int threads = std::min(512, std::max(128, ms_run));
+  // the sweep itself uses 128 threads (named barrier); the parallel phases loop over cells, so
+  // 256 threads keep block barriers cheap up to ~1K cells
+  const int threads = ms_run <= 128 ? 128 : 256;
   const int64_t per_sm = std::min<int64_t>(4, std::max<int64_t>(1, (nf + ctx->num_sms - 1) / ctx->num_sms));
   const size_t budget = kResidentSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
   const size_t state = (size_t)ms_run * gs::resident_bytes_per_cell(d);
@@ -739,7 +750,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, -1, out->labels, dev_out,
                          rec, rb));
       if (rb.err[0] & 32) {  // key box beyond the grid: grow and redo the run
-        GS_TRY(ensure_dense(ctx, *(long long*)(rb.err + 2), d));
+        GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
         continue;
       }
       if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
@@ -758,7 +769,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost, st));
     GS_CK(cudaStreamSynchronize(st));
     if (hdr[0] & 32) {
-      GS_TRY(ensure_dense(ctx, *(long long*)(hdr + 2), d));
+      GS_TRY(grow_dense_for(ctx, *(long long*)(hdr + 2), d));
       continue;
     }
     if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
@@ -1088,7 +1099,7 @@ gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_
                           ctx->stream));
     GS_CK(cudaStreamSynchronize(ctx->stream));
     if ((hdr[0] & 32) && attempt < 3) {
-      GS_TRY(ensure_dense(ctx, *(long long*)(hdr + 2), d));
+      GS_TRY(grow_dense_for(ctx, *(long long*)(hdr + 2), d));
       continue;
     }
     if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");

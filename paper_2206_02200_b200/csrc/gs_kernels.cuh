@@ -230,15 +230,22 @@ __global__ void k_box(const double* __restrict__ bpart, int nblk, int d, double 
                       int64_t n, int64_t nframes, int64_t cap_cells, GsBox* __restrict__ out,
                       int* err, long long* need) {
   __shared__ double mn[GS_DMAX], mx[GS_DMAX];
-  const int c = threadIdx.x;
-  if (c < d) {
+  // 32 lanes per dimension, strided over the partials, then a shuffle reduction
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = w; c < d; c += blockDim.x >> 5) {
     double a = INFINITY, z = -INFINITY;
-    for (int k = 0; k < nblk; ++k) {
+    for (int k = lane; k < nblk; k += 32) {
       a = fmin(a, bpart[k * d + c]);
       z = fmax(z, bpart[(int64_t)nblk * d + k * d + c]);
     }
-    mn[c] = a;
-    mx[c] = z;
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(kFull, a, o));
+      z = fmax(z, __shfl_xor_sync(kFull, z, o));
+    }
+    if (lane == 0) {
+      mn[c] = a;
+      mx[c] = z;
+    }
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -282,7 +289,8 @@ __global__ void k_box(const double* __restrict__ bpart, int nblk, int d, double 
 // ---------------------------------------------------------------- K3: compaction by scan
 // The dense grid is in lexicographic order, so scanning its occupancy yields the cell list
 // already sorted: no occupied list, no sort, no host round trip for m0.
-constexpr int kOccTile = 2048;  // cells per tile: 256 threads x 8
+constexpr int kOccPer = 2;                // cells per thread
+constexpr int kOccTile = 256 * kOccPer;   // cells per tile (256 threads)
 
 __device__ __forceinline__ int block_excl_scan_256(int v, int* sh, int* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -319,10 +327,10 @@ __global__ void __launch_bounds__(256) k_occ_count(const GsBox* __restrict__ pb,
   const int64_t V = pb->vol_total;
   const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * 8;
+    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * kOccPer;
     int c = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c += (base + k < V) && cnt[base + k] != 0u;
+    for (int k = 0; k < kOccPer; ++k) c += (base + k < V) && cnt[base + k] != 0u;
     int total;
     block_excl_scan_256(c, sh, &total);
     if (threadIdx.x == 0) tile_cnt[t] = total;
@@ -384,18 +392,18 @@ __global__ void __launch_bounds__(256) k_occ_compact(
   const int64_t V = b.vol_total;
   const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * 8;
-    uint32_t c8[8];
+    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * kOccPer;
+    uint32_t c8[kOccPer];
     int c = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kOccPer; ++k) {
       c8[k] = (base + k < V) ? cnt[base + k] : 0u;
       c += c8[k] != 0u;
     }
     int total;
     int pos = tile_off[t] + block_excl_scan_256(c, sh, &total);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kOccPer; ++k) {
       if (c8[k] == 0u) continue;
       const int64_t L = base + k;
       for (int q = 0; q < b.d; ++q) {

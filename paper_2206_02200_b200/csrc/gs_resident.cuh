@@ -132,6 +132,21 @@ __device__ __forceinline__ void rs_st_release(uint32_t* p, uint32_t v) {
                : "memory");
 }
 
+// named barrier over the first n threads (n a multiple of 32), and its OR-reduction form
+__device__ __forceinline__ void rs_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ int rs_bar_or(int id, int n, int pred) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.s32 p, %3, 0;\n bar.red.or.pred q, %1, %2, p;\n"
+      " selp.s32 %0, 1, 0, q;\n}"
+      : "=r"(r)
+      : "r"(id), "r"(n), "r"(pred)
+      : "memory");
+  return r;
+}
+
 // Exclusive scan of a[0..n) in shared memory (in place); returns the total.  All threads.
 __device__ int rs_scan(int* a, int n, int* wtmp) {
   const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -224,6 +239,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
+  __shared__ unsigned s_maxl;
   volatile uint32_t* vflag = flag;
 
   uint32_t* key = keyA;
@@ -362,6 +378,10 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     auto early_nb = [&](int i, int t) -> int {
       return mode == 0 ? (int)(uint32_t)erec[eoff[i] + t] : (int)lst[tmp[i] + t];
     };
+    // One cell update with every dependency final.  Term loads are issued in predicated
+    // chunks ahead of the arithmetic (the adds still run in lex order, one at a time), so the
+    // critical path is ~2 smem round trips plus the chain of adds, not a load per add.
+    constexpr int CH = D <= 3 ? 8 : 4;
     auto update_cell = [&](int i) {
       const int n = nbn[i], e = nbe[i];
       if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
@@ -374,28 +394,61 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       for (int c = 0; c < D; ++c) num[c] = 0.0;
       if (mode == 0) {
         const uint64_t* er = erec + eoff[i];
-        for (int t = 0; t < e; ++t) {  // earlier neighbours: NEW centroids, lex order
-          const uint64_t r = er[t];
-          const uint32_t j = (uint32_t)r;
-          const double w = (double)(uint32_t)(r >> 32);
+        for (int t0 = 0; t0 < e; t0 += CH) {  // earlier neighbours: NEW centroids
+          uint64_t r[CH];
+          double v[CH][D];
 #pragma unroll
-          for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, S1[j * D + c]));
+          for (int u = 0; u < CH; ++u) r[u] = (t0 + u < e) ? er[t0 + u] : 0ull;
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const uint32_t j = (uint32_t)r[u];
+#pragma unroll
+            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < e) ? S1[j * D + c] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            if (t0 + u < e) {
+              const double w = (double)(uint32_t)(r[u] >> 32);
+#pragma unroll
+              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, v[u][c]));
+            }
+          }
         }
         const double* lp = lprod + (int64_t)loff[i] * D;
         const int nl = n - e;
-#pragma unroll 4
-        for (int t = 0; t < nl; ++t) {  // itself + later neighbours: C'*S_old, lex order
+        for (int t0 = 0; t0 < nl; t0 += CH) {  // itself + later neighbours: C'*S_old
+          double v[CH][D];
 #pragma unroll
-          for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], lp[t * D + c]);
+          for (int u = 0; u < CH; ++u)
+#pragma unroll
+            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < nl) ? lp[(t0 + u) * D + c] : 0.0;
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (t0 + u < nl) {
+#pragma unroll
+              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
+            }
         }
       } else {
         const uint16_t* ls = lst + tmp[i];
-        for (int t = 0; t < n; ++t) {
-          const int j = ls[t];
-          const double w = (double)cnt[j];
-          const double* src = (t < e) ? S1 : S0;
+        for (int t0 = 0; t0 < n; t0 += CH) {
+          int jj[CH];
+          double v[CH][D], w[CH];
 #pragma unroll
-          for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, src[j * D + c]));
+          for (int u = 0; u < CH; ++u) jj[u] = (t0 + u < n) ? (int)ls[t0 + u] : 0;
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const double* src = (t0 + u < e) ? S1 : S0;
+            w[u] = (double)cnt[jj[u]];
+#pragma unroll
+            for (int c = 0; c < D; ++c) v[u][c] = src[jj[u] * D + c];
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (t0 + u < n) {
+#pragma unroll
+              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w[u], v[u][c]));
+            }
         }
       }
       const double dd = (double)den[i];
@@ -403,46 +456,72 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
     };
     if (mode != 2) {
-      // (a) levels (flag[] holds them; monotone relaxation, converges in depth+1 rounds)
-      volatile uint32_t* lvl = flag;
-      for (int i = tid; i < m; i += T) flag[i] = 0u;
-      __syncthreads();
-      for (;;) {
-        bool ch = false;
-        for (int i = tid; i < m; i += T) {
-          const int e = nbe[i];
-          uint32_t mx = 0u;
-          for (int t = 0; t < e; ++t) mx = max(mx, lvl[early_nb(i, t)] + 1u);
-          if (mx > lvl[i]) {
-            lvl[i] = mx;
-            ch = true;
+      // the sweep runs on the first SW threads with a named barrier (fewer warps to sync);
+      // the others wait at the block barrier after it
+      const int SW = min(T, 128);
+      if (tid < SW) {
+        // (a) levels (flag[] holds them; monotone relaxation, converges in depth+1 rounds)
+        volatile uint32_t* lvl = flag;
+        for (int i = tid; i < m; i += SW) flag[i] = 0u;
+        rs_bar(1, SW);
+        for (;;) {
+          int ch = 0;
+          for (int i = tid; i < m; i += SW) {
+            const int e = nbe[i];
+            uint32_t mx = 0u;
+            for (int t0 = 0; t0 < e; t0 += CH) {
+              int jj[CH];
+#pragma unroll
+              for (int u = 0; u < CH; ++u) jj[u] = (t0 + u < e) ? early_nb(i, t0 + u) : -1;
+#pragma unroll
+              for (int u = 0; u < CH; ++u)
+                if (jj[u] >= 0) mx = max(mx, lvl[jj[u]] + 1u);
+            }
+            if (mx > lvl[i]) {
+              lvl[i] = mx;
+              ch = 1;
+            }
+          }
+          if (!rs_bar_or(1, SW, ch)) break;
+        }
+        // (b) bucket by level: counts -> offsets -> order (reusing sk as int scratch)
+        int* lcnt = (int*)sk;        // [MS] level counts, then ends
+        int* order = (int*)sk + MS;  // [MS] cells in level order
+        for (int j = tid; j < m; j += SW) lcnt[j] = 0;
+        if (tid == 0) s_maxl = 0u;
+        rs_bar(1, SW);
+        for (int i = tid; i < m; i += SW) {
+          atomicAdd(&lcnt[flag[i]], 1);
+          atomicMax(&s_maxl, flag[i]);
+        }
+        rs_bar(1, SW);
+        const int nlev = (int)s_maxl + 1;
+        if (tid < 32) {  // one warp scans the level counts into ends
+          int run = 0;
+          for (int base = 0; base < nlev; base += 32) {
+            const int l = base + tid;
+            int x = l < nlev ? lcnt[l] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, x, o);
+              if (tid >= o) x += y;
+            }
+            if (l < nlev) lcnt[l] = run + x - (lcnt[l]);  // exclusive start
+            run += __shfl_sync(0xffffffffu, x, 31);
           }
         }
-        if (!__syncthreads_or(ch)) break;
-      }
-      // (b) bucket by level: counts -> offsets -> order (reusing sk as int scratch)
-      int* lcnt = (int*)sk;        // [MS] level counts, then offsets
-      int* order = (int*)sk + MS;  // [MS] cells in level order
-      __shared__ unsigned s_maxl;
-      if (tid == 0) s_maxl = 0u;
-      for (int j = tid; j < m; j += T) lcnt[j] = 0;
-      __syncthreads();
-      for (int i = tid; i < m; i += T) {
-        atomicAdd(&lcnt[flag[i]], 1);
-        atomicMax(&s_maxl, flag[i]);
+        rs_bar(1, SW);
+        for (int i = tid; i < m; i += SW) order[atomicAdd(&lcnt[flag[i]], 1)] = i;
+        rs_bar(1, SW);
+        // lcnt[l] now holds the END of level l; level l spans [l ? lcnt[l-1] : 0, lcnt[l])
+        // (c) level-synchronous update
+        for (int l = 0; l < nlev; ++l) {
+          const int beg = l ? lcnt[l - 1] : 0, end = lcnt[l];
+          for (int k = beg + tid; k < end; k += SW) update_cell(order[k]);
+          rs_bar(1, SW);
+        }
       }
       __syncthreads();
-      const int nlev = (int)s_maxl + 1;
-      rs_scan(lcnt, nlev, wtmp);
-      for (int i = tid; i < m; i += T) order[atomicAdd(&lcnt[flag[i]], 1)] = i;
-      __syncthreads();
-      // lcnt[l] now holds the END of level l; level l spans [l ? lcnt[l-1] : 0, lcnt[l])
-      // (c) level-synchronous update
-      for (int l = 0; l < nlev; ++l) {
-        const int beg = l ? lcnt[l - 1] : 0, end = lcnt[l];
-        for (int k = beg + tid; k < end; k += T) update_cell(order[k]);
-        __syncthreads();
-      }
     } else {
       // records do not fit (very dense high-d neighbourhoods): dataflow with lookups, waiting
       // on each earlier neighbour in turn (independent thread scheduling keeps lanes going)
