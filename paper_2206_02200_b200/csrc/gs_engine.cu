@@ -19,6 +19,7 @@
 
 #include "../../include/gridshift_c.h"
 #include "gs_kernels.cuh"
+#include "gs_global.cuh"
 #include "gs_resident.cuh"
 
 namespace {
@@ -68,7 +69,8 @@ struct gs_ctx {
   DevBuf pts, slot, labels;
   // per cell (double-buffered state)
   DevBuf occ, occ_sorted, ckey[2], ccnt[2], S[2], S1, nbl, nbn, nbe, den, flag, nkey, vals,
-      skey, sval, head, sid, segstart, parent, root, initkey;
+      skey, sval, head, sid, segstart, parent, root, initkey, erec, lprod, rden, lvl, lsucc,
+      order;
   int64_t cell_cap = 0, nbl_cap = 0;
   // per frame
   DevBuf fdone, fchanged, fadj, fm, fdisp, ffirst, fcount, ifirst, icount, fiters, fconv, fk,
@@ -438,6 +440,40 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   return GS_OK;
 }
 
+template <int D>
+gs_status launch_sweep_levels_d(gs_ctx* ctx, int64_t m, const int32_t* eoff,
+                                const int32_t* loff) {
+  // pending counts + queue in smem when they fit (8 bytes per cell), else in global scratch
+  const int smem_cells = (int)std::min<int64_t>(m, 200 * 1024 / 8);
+  const size_t smem = (size_t)smem_cells * 8;
+  static bool configured = false;
+  if (!configured) {
+    GS_CK(cudaFuncSetAttribute(gs::k_sweep_kahn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024 + 1024));
+    configured = true;
+  }
+  gs::k_sweep_kahn<D><<<1, 1024, smem, ctx->stream>>>(
+      (int)m, smem_cells, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(), eoff, loff,
+      ctx->erec.as<unsigned long long>(), ctx->lprod.as<double>(), ctx->lsucc.as<int32_t>(),
+      ctx->den.as<uint32_t>(), ctx->rden.as<double>(), ctx->S[ctx->cur].as<double>(),
+      ctx->S1.as<double>(), ctx->lvl.as<int>(), ctx->order.as<int>());
+  GS_LAUNCHED("k_sweep_kahn");
+  return GS_OK;
+}
+
+gs_status launch_sweep_levels(gs_ctx* ctx, int d, int64_t m, const int32_t* eoff,
+                              const int32_t* loff) {
+  switch (d) {
+#define GS_CASE(D) \
+  case D:          \
+    return launch_sweep_levels_d<D>(ctx, m, eoff, loff);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+    GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
+#undef GS_CASE
+  }
+  return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
+}
+
 // One iterate_once over all frames (frozen frames excluded).  Cells in buffer `cur`; the new
 // cells land in buffer 1-cur.  Per-frame changed/adjacency/m/disp land in the f* arrays.
 gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
@@ -446,38 +482,56 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   const int K = (int)ipow3(d);
   const int cur = ctx->cur, nxt = 1 - cur;
   const int64_t nf = b.nframes;
-  if ((int64_t)K * m > ctx->nbl_cap) {
-    GS_TRY(grow(ctx, ctx->nbl, sizeof(int32_t) * (size_t)K * m));
-    ctx->nbl_cap = (int64_t)K * m;
-  }
-  GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, ctx->stream));
-  GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, ctx->stream));
-  GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, ctx->stream));
-  GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, ctx->stream));
-  GS_CK(cudaMemsetAsync(ctx->counters.as<unsigned int>() + 1, 0, sizeof(unsigned int),
-                        ctx->stream));
+  cudaStream_t st = ctx->stream;
+  GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, st));
+  GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, st));
+  GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, st));
+  GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, st));
   const unsigned mb = blocks_for(m, 256);
-  gs::k_nbr<<<mb, 256, 0, ctx->stream>>>((int)m, b, K, ctx->ckey[cur].as<uint32_t>(),
-                                         ctx->ccnt[cur].as<uint32_t>(), ctx->idx.as<int32_t>(),
-                                         ctx->fdone.as<int32_t>(), ctx->nbl.as<int32_t>(),
-                                         ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
-                                         ctx->den.as<unsigned long long>(), ctx->fm.as<int32_t>());
-  GS_LAUNCHED("k_nbr");
-  const uint32_t epoch = ++ctx->epoch;
-  const unsigned sb = blocks_for((m + 31) / 32 * 32, 256, (int64_t)ctx->num_sms * 4);
-  gs::k_sweep<<<sb, 256, 0, ctx->stream>>>(
-      (int)m, d, K, ctx->ccnt[cur].as<uint32_t>(), ctx->S[cur].as<double>(), ctx->S1.as<double>(),
-      ctx->nbl.as<int32_t>(), ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
-      ctx->den.as<unsigned long long>(), ctx->flag.as<uint32_t>(), epoch,
-      ctx->counters.as<unsigned int>() + 1, ctx->errflag.as<int>());
-  GS_LAUNCHED("k_sweep");
+  // (1) neighbour census -> scanned record offsets -> records (all SMs)
+  gs::k_nbr_count<<<mb, 256, 0, st>>>((int)m, b, K, ctx->ckey[cur].as<uint32_t>(),
+                                      ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(),
+                                      ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
+                                      ctx->head.as<int32_t>(), ctx->sid.as<int32_t>(),
+                                      ctx->fm.as<int32_t>());
+  GS_LAUNCHED("k_nbr_count");
+  int32_t* eoff = ctx->segstart.as<int32_t>();
+  int32_t* loff = ctx->parent.as<int32_t>();  // parent is rewritten by k_seg later
+  size_t tb = ctx->cub_tmp.bytes;
+  GS_CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tb, ctx->head.as<int32_t>(), eoff, (int)m, st));
+  GS_TRY(check_lib(ctx, "cub_scan_e"));
+  tb = ctx->cub_tmp.bytes;
+  GS_CK(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tb, ctx->sid.as<int32_t>(), loff, (int)m, st));
+  GS_TRY(check_lib(ctx, "cub_scan_l"));
+  int32_t tails[4];
+  GS_CK(cudaMemcpyAsync(&tails[0], eoff + (m - 1), 4, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(&tails[1], ctx->head.as<int32_t>() + (m - 1), 4, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(&tails[2], loff + (m - 1), 4, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(&tails[3], ctx->sid.as<int32_t>() + (m - 1), 4, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  const int64_t n_early = (int64_t)tails[0] + tails[1], n_late = (int64_t)tails[2] + tails[3];
+  GS_TRY(grow(ctx, ctx->erec, 8 * std::max<int64_t>(1, n_early)));
+  GS_TRY(grow(ctx, ctx->lprod, 8 * d * std::max<int64_t>(1, n_late)));
+  GS_TRY(grow(ctx, ctx->rden, 8 * m));
+  GS_TRY(grow(ctx, ctx->lvl, 4 * (m + 1)));
+  GS_TRY(grow(ctx, ctx->lsucc, 4 * std::max<int64_t>(1, n_late)));
+  GS_TRY(grow(ctx, ctx->order, 4 * m));
+  gs::k_nbr_fill<<<mb, 256, 0, st>>>((int)m, b, K, ctx->ckey[cur].as<uint32_t>(),
+                                     ctx->ccnt[cur].as<uint32_t>(), ctx->S[cur].as<double>(),
+                                     ctx->idx.as<int32_t>(), ctx->nbn.as<int32_t>(), eoff, loff,
+                                     ctx->erec.as<unsigned long long>(), ctx->lprod.as<double>(),
+                                     ctx->lsucc.as<int32_t>(), ctx->den.as<uint32_t>(),
+                                     ctx->rden.as<double>());
+  GS_LAUNCHED("k_nbr_fill");
+  // (2) the sweep: one CTA, DAG levels, level-synchronous exact Eq. (5)
+  GS_TRY(launch_sweep_levels(ctx, d, m, eoff, loff));
   gs::k_rehome<<<mb, 256, 0, ctx->stream>>>(
       (int)m, b, ctx->ckey[cur].as<uint32_t>(), ctx->S[cur].as<double>(), ctx->S1.as<double>(),
       ctx->fdone.as<int32_t>(), ctx->nkey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
       ctx->fchanged.as<int32_t>(), ctx->fdisp.as<unsigned long long>(), ctx->errflag.as<int>());
   GS_LAUNCHED("k_rehome");
   const int kb = bits_for(b.vol_total);
-  size_t tb = ctx->cub_tmp.bytes;
+  tb = ctx->cub_tmp.bytes;
   GS_CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tb, ctx->nkey.as<uint32_t>(),
                                         ctx->skey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
                                         ctx->sval.as<uint32_t>(), (int)m, 0, kb, ctx->stream));
@@ -1012,7 +1066,8 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->fm, &ctx->fdisp, &ctx->ffirst, &ctx->fcount, &ctx->ifirst, &ctx->icount,
                     &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->hist, &ctx->counters, &ctx->errflag,
                     &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes, &ctx->tiles,
-                    &ctx->dbox})
+                    &ctx->dbox, &ctx->erec, &ctx->lprod, &ctx->rden, &ctx->lvl,
+                    &ctx->lsucc, &ctx->order})
     b->release();
   if (ctx->pin) cudaFreeHost(ctx->pin);
   for (auto& e : ctx->ev)

@@ -332,10 +332,12 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     const int n_late = rs_scan(loff, m, wtmp);
     const int n_all = rs_scan(tmp, m, wtmp);
     // fast: {slot, C'} per earlier neighbour + C'*S_old for self and later neighbours
-    const int fast_bytes = 8 * n_early + 8 * D * n_late;
+    // fast mode also keeps the slot of every later neighbour: the sweep's successor lists
+    const int fast_bytes = 8 * n_early + 8 * D * n_late + 2 * n_late;
     const int mode = fast_bytes <= a.pool_bytes ? 0 : (2 * n_all <= a.pool_bytes ? 1 : 2);
     uint64_t* erec = (uint64_t*)pool;
     double* lprod = (double*)(pool + 8 * n_early);
+    uint16_t* lsucc = (uint16_t*)(pool + 8 * n_early + 8 * D * n_late);
     uint16_t* lst = (uint16_t*)pool;
     for (int i = tid; i < m; i += T) {
       NbrIt it = nbr_begin();
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
           if (j < i) {
             erec[eoff[i] + ne++] = ((uint64_t)w << 32) | (uint32_t)j;
           } else {
+            lsucc[loff[i] + nl] = (uint16_t)j;
             double* dst = lprod + (int64_t)(loff[i] + nl++) * D;
 #pragma unroll
             for (int c = 0; c < D; ++c) dst[c] = __dmul_rn((double)w, S0[j * D + c]);
@@ -460,65 +463,37 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       // the others wait at the block barrier after it
       const int SW = min(T, 128);
       if (tid < SW) {
-        // (a) levels (flag[] holds them; monotone relaxation, converges in depth+1 rounds)
-        volatile uint32_t* lvl = flag;
-        for (int i = tid; i < m; i += SW) flag[i] = 0u;
-        rs_bar(1, SW);
-        for (;;) {
-          int ch = 0;
-          for (int i = tid; i < m; i += SW) {
-            const int e = nbe[i];
-            uint32_t mx = 0u;
-            for (int t0 = 0; t0 < e; t0 += CH) {
-              int jj[CH];
-#pragma unroll
-              for (int u = 0; u < CH; ++u) jj[u] = (t0 + u < e) ? early_nb(i, t0 + u) : -1;
-#pragma unroll
-              for (int u = 0; u < CH; ++u)
-                if (jj[u] >= 0) mx = max(mx, lvl[jj[u]] + 1u);
-            }
-            if (mx > lvl[i]) {
-              lvl[i] = mx;
-              ch = 1;
-            }
-          }
-          if (!rs_bar_or(1, SW, ch)) break;
-        }
-        // (b) bucket by level: counts -> offsets -> order (reusing sk as int scratch)
-        int* lcnt = (int*)sk;        // [MS] level counts, then ends
-        int* order = (int*)sk + MS;  // [MS] cells in level order
-        for (int j = tid; j < m; j += SW) lcnt[j] = 0;
-        if (tid == 0) s_maxl = 0u;
+        // Kahn frontier over the sweep DAG: a cell joins the queue when its last lex-earlier
+        // neighbour has been updated; each level is updated in parallel (all its operands are
+        // final), then releases its lex-later neighbours.  flag[] = pending earlier neighbours,
+        // sk[] (as int) = the queue.
+        int* pend = (int*)flag;
+        int* queue = (int*)sk;
+        if (tid == 0) s_maxl = 0u;  // queue tail
         rs_bar(1, SW);
         for (int i = tid; i < m; i += SW) {
-          atomicAdd(&lcnt[flag[i]], 1);
-          atomicMax(&s_maxl, flag[i]);
+          pend[i] = nbe[i];
+          if (nbe[i] == 0) queue[atomicAdd(&s_maxl, 1u)] = i;
         }
-        rs_bar(1, SW);
-        const int nlev = (int)s_maxl + 1;
-        if (tid < 32) {  // one warp scans the level counts into ends
-          int run = 0;
-          for (int base = 0; base < nlev; base += 32) {
-            const int l = base + tid;
-            int x = l < nlev ? lcnt[l] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, x, o);
-              if (tid >= o) x += y;
+        auto succ_of = [&](int i, int t) -> int {  // t-th lex-later neighbour (self excluded)
+          return mode == 0 ? (int)lsucc[loff[i] + 1 + t] : (int)lst[tmp[i] + nbe[i] + 1 + t];
+        };
+        int qhead = 0;
+        for (;;) {
+          rs_bar(1, SW);  // the previous level's appends are complete
+          const int lev_end = (int)*(volatile unsigned*)&s_maxl;
+          rs_bar(1, SW);  // everyone holds lev_end before new appends
+          if (qhead >= lev_end) break;
+          for (int k = qhead + tid; k < lev_end; k += SW) {
+            const int i = queue[k];
+            update_cell(i);
+            const int ns = nbn[i] - nbe[i] - 1;  // lex-later active neighbours
+            for (int t = 0; t < ns; ++t) {
+              const int j = succ_of(i, t);
+              if (atomicSub(&pend[j], 1) == 1) queue[atomicAdd(&s_maxl, 1u)] = j;
             }
-            if (l < nlev) lcnt[l] = run + x - (lcnt[l]);  // exclusive start
-            run += __shfl_sync(0xffffffffu, x, 31);
           }
-        }
-        rs_bar(1, SW);
-        for (int i = tid; i < m; i += SW) order[atomicAdd(&lcnt[flag[i]], 1)] = i;
-        rs_bar(1, SW);
-        // lcnt[l] now holds the END of level l; level l spans [l ? lcnt[l-1] : 0, lcnt[l])
-        // (c) level-synchronous update
-        for (int l = 0; l < nlev; ++l) {
-          const int beg = l ? lcnt[l - 1] : 0, end = lcnt[l];
-          for (int k = beg + tid; k < end; k += SW) update_cell(order[k]);
-          rs_bar(1, SW);
+          qhead = lev_end;
         }
       }
       __syncthreads();
