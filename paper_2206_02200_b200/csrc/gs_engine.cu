@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -444,20 +445,34 @@ template <int D>
 gs_status launch_sweep_levels_d(gs_ctx* ctx, int64_t m, const int32_t* eoff,
                                 const int32_t* loff) {
   // pending counts + queue in smem when they fit (8 bytes per cell), else in global scratch
-  const int smem_cells = (int)std::min<int64_t>(m, 200 * 1024 / 8);
-  const size_t smem = (size_t)smem_cells * 8;
+  constexpr size_t kBudget = 220 * 1024;
+  const size_t stage = (size_t)1024 * D * 8;
+  const int smem_cells = (int)std::min<int64_t>(m, (int64_t)((kBudget - stage) / 8));
+  if (getenv("GS_DEBUG_KAHN")) {
+    GS_TRY(grow(ctx, ctx->dbg, 64));
+    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 32, ctx->stream));
+  }
+  const size_t smem = stage + (size_t)smem_cells * 8;
   static bool configured = false;
   if (!configured) {
     GS_CK(cudaFuncSetAttribute(gs::k_sweep_kahn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               200 * 1024 + 1024));
+                               (int)kBudget));
     configured = true;
   }
   gs::k_sweep_kahn<D><<<1, 1024, smem, ctx->stream>>>(
       (int)m, smem_cells, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(), eoff, loff,
       ctx->erec.as<unsigned long long>(), ctx->lprod.as<double>(), ctx->lsucc.as<int32_t>(),
       ctx->den.as<uint32_t>(), ctx->rden.as<double>(), ctx->S[ctx->cur].as<double>(),
-      ctx->S1.as<double>(), ctx->lvl.as<int>(), ctx->order.as<int>());
+      ctx->S1.as<double>(), ctx->lvl.as<int>(), ctx->order.as<int>(),
+      getenv("GS_DEBUG_KAHN") ? (long long*)ctx->dbg.p : nullptr);
   GS_LAUNCHED("k_sweep_kahn");
+  if (getenv("GS_DEBUG_KAHN")) {
+    long long h[4];
+    GS_CK(cudaMemcpyAsync(h, ctx->dbg.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaStreamSynchronize(ctx->stream));
+    fprintf(stderr, "kahn m=%lld levels=%lld cells=%lld thread0_cycles=%lld\n", (long long)m, h[0], h[1], h[2]);
+    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 32, ctx->stream));
+  }
   return GS_OK;
 }
 
@@ -676,7 +691,7 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   // uses the cached choice
   const int64_t vf = deferrable ? ctx->shape_vol_frame : ctx->box.vol_frame;
   const size_t sidx = (vf * 2 <= 48 * 1024) ? ((size_t)vf * 2 + 15) & ~size_t(15) : 0;
-  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d);
+  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)256 * d * 8;  // + stage
   const size_t fixed = state + sidx + offs_bytes;
   const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
   unsigned* cnt32 = ctx->counters.as<unsigned>();

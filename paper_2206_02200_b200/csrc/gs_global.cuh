@@ -7,8 +7,8 @@
 //                                        products and slots of itself and its lex-later ones,
 //                                        ΣC' and RN(1/ΣC')
 //   k_sweep_kahn (one CTA)               Kahn frontier over the sweep DAG: each level is
-//                                        updated with every operand final, then releases its
-//                                        lex-later neighbours
+//                                        updated with every operand final (a lane group per
+//                                        cell), then releases its lex-later neighbours
 // Operands and order of the fp64 adds are exactly the serial sweep's (pins P2/P3).
 #pragma once
 
@@ -93,8 +93,15 @@ __device__ __forceinline__ double gl_div(double a, double b, double y) {
   return __fma_rn(r, y, q0);
 }
 
+// Lanes per cell in the cooperative update.
+template <int D>
+__host__ __device__ constexpr int sweep_group() {
+  return D <= 3 ? 16 : 32;
+}
+
 // One CTA.  pend/queue live in dynamic shared memory when 8*m bytes fit (smem_cells >= m),
-// else in the global scratch arrays.
+// else in the global scratch arrays.  Dynamic smem layout: [stage: blockDim*D doubles]
+// [pend: smem_cells ints][queue: smem_cells ints].
 template <int D>
 __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
     int m, int smem_cells, const int32_t* __restrict__ nbn, const int32_t* __restrict__ nbe,
@@ -102,13 +109,19 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
     const unsigned long long* __restrict__ erec, const double* __restrict__ lprod,
     const int32_t* __restrict__ lsucc, const uint32_t* __restrict__ den,
     const double* __restrict__ rden, const double* __restrict__ S0, double* S1, int* pend_g,
-    int* queue_g) {
-  extern __shared__ int sq[];
+    int* queue_g, long long* dbg) {
+  extern __shared__ __align__(16) unsigned char dsm[];
   const int tid = threadIdx.x, T = blockDim.x;
-  constexpr int CH = D <= 3 ? 8 : 4;
+  constexpr int G = sweep_group<D>();
+  double* stage = (double*)dsm;
+  int* sq = (int*)(stage + (size_t)T * D);
   const bool in_smem = m <= smem_cells;
-  volatile int* pend = in_smem ? sq : pend_g;
+  int* pend = in_smem ? sq : pend_g;
   volatile int* queue = in_smem ? sq + smem_cells : queue_g;
+  const int grp = tid / G, g = tid % G, ngroups = T / G;
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+  double* stg = stage + (size_t)grp * G * D;
   __shared__ unsigned tail;
   if (tid == 0) tail = 0u;
   __syncthreads();
@@ -122,62 +135,52 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
     const int lev_end = (int)*(volatile unsigned*)&tail;
     __syncthreads();  // everyone holds lev_end before new appends
     if (qhead >= lev_end) break;
-    for (int k = qhead + tid; k < lev_end; k += T) {
+    if (dbg && tid == 0) {
+      atomicAdd((unsigned long long*)&dbg[0], 1ull);
+      atomicAdd((unsigned long long*)&dbg[1], (unsigned long long)(lev_end - qhead));
+    }
+    const long long tl0 = clock64();
+    for (int k = qhead + grp; k < lev_end; k += ngroups) {
       const int i = queue[k];
       const int n = nbn[i], e = nbe[i];
       if (n <= 1) {  // isolated or frozen: centroid kept bit-for-bit (pin P3)
-#pragma unroll
-        for (int c = 0; c < D; ++c) S1[(int64_t)i * D + c] = S0[(int64_t)i * D + c];
+        if (g < D) S1[(int64_t)i * D + g] = S0[(int64_t)i * D + g];
       } else {
-        double num[D];
+        double num = 0.0;  // lane g < D accumulates coordinate g
+        for (int t0 = 0; t0 < n; t0 += G) {
+          const int t = t0 + g;
+          if (t < n) {
+            if (t < e) {  // earlier neighbour: its NEW centroid
+              const unsigned long long r = erec[eoff[i] + t];
+              const int64_t j = (uint32_t)r;
+              const double w = (double)(uint32_t)(r >> 32);
 #pragma unroll
-        for (int c = 0; c < D; ++c) num[c] = 0.0;
-        const unsigned long long* er = erec + eoff[i];
-        for (int t0 = 0; t0 < e; t0 += CH) {  // earlier neighbours: NEW centroids
-          unsigned long long r[CH];
-          double v[CH][D];
+              for (int c = 0; c < D; ++c) stg[g * D + c] = __dmul_rn(w, __ldcg(&S1[j * D + c]));
+            } else {  // itself / later neighbour: precomputed C'*S_old
+              const double* lp = lprod + (int64_t)(loff[i] + (t - e)) * D;
 #pragma unroll
-          for (int u = 0; u < CH; ++u) r[u] = (t0 + u < e) ? er[t0 + u] : 0ull;
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const int64_t j = (uint32_t)r[u];
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < e) ? __ldcg(&S1[j * D + c]) : 0.0;
+              for (int c = 0; c < D; ++c) stg[g * D + c] = lp[c];
+            }
           }
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (t0 + u < e) {
-              const double w = (double)(uint32_t)(r[u] >> 32);
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, v[u][c]));
-            }
+          __syncwarp(gmask);
+          if (g < D) {
+            const int len = min(G, n - t0);
+#pragma unroll 4
+            for (int u = 0; u < len; ++u) num = __dadd_rn(num, stg[u * D + g]);
+          }
+          __syncwarp(gmask);
         }
-        const double* lp = lprod + (int64_t)loff[i] * D;
-        const int nl = n - e;
-        for (int t0 = 0; t0 < nl; t0 += CH) {  // itself + later neighbours: C'*S_old
-          double v[CH][D];
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < nl) ? lp[(t0 + u) * D + c] : 0.0;
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (t0 + u < nl) {
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
-            }
-        }
-        const double dd = (double)den[i], y = rden[i];
-#pragma unroll
-        for (int c = 0; c < D; ++c) S1[(int64_t)i * D + c] = gl_div(num[c], dd, y);
+        if (g < D) S1[(int64_t)i * D + g] = gl_div(num, (double)den[i], rden[i]);
       }
-      // release the lex-later neighbours (self is the first late record)
+      // release the lex-later neighbours (self is the first late record), in parallel
       const int l0 = loff[i] + 1, ns = n - e - 1;
-      for (int t = 0; t < ns; ++t) {
+      for (int t = g; t < ns; t += G) {
         const int j = lsucc[l0 + t];
-        if (atomicSub((int*)&pend[j], 1) == 1) queue[atomicAdd(&tail, 1u)] = j;
+        if (atomicSub(&pend[j], 1) == 1) queue[atomicAdd(&tail, 1u)] = j;
       }
     }
+    if (dbg && tid == 0)
+      atomicAdd((unsigned long long*)&dbg[2], (unsigned long long)(clock64() - tl0));
     qhead = lev_end;
   }
 }

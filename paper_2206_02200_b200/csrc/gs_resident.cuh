@@ -76,6 +76,9 @@ __host__ __device__ constexpr int resident_offs_bytes(int D) {
                 : 0;
 }
 
+// shared-memory bytes of the sweep's per-group term staging (K8 runs at most 256 threads)
+__host__ __device__ constexpr int resident_stage_bytes(int D) { return 256 * D * 8; }
+
 // RN(a / b) from y = RN(1/b) (precomputed off the critical path): q0 = RN(a*y); the residual
 // a - b*q0 is exact in one FMA; RN(q0 + r*y) is the correctly rounded quotient (Markstein's
 // theorem; b is a positive integer count here).  Outside the exponent range where the theorem's
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   int* tmp = (int*)p;               p += 4 * MS;
   int16_t* sidx = (int16_t*)p;      p += a.sidx_bytes;
   int* offs = (int*)p;              p += resident_offs_bytes(D);
+  double* stage = (double*)p;       p += resident_stage_bytes(D);
   unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
@@ -381,88 +385,58 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     auto early_nb = [&](int i, int t) -> int {
       return mode == 0 ? (int)(uint32_t)erec[eoff[i] + t] : (int)lst[tmp[i] + t];
     };
-    // One cell update with every dependency final.  Term loads are issued in predicated
-    // chunks ahead of the arithmetic (the adds still run in lex order, one at a time), so the
-    // critical path is ~2 smem round trips plus the chain of adds, not a load per add.
-    constexpr int CH = D <= 3 ? 8 : 4;
-    auto update_cell = [&](int i) {
+    // Group-cooperative cell update: G lanes own one cell.  Lanes load and multiply the
+    // cell's terms in parallel into a per-group staging buffer; lane c < D then adds them in
+    // lex order (the only serial part: one add per term), divides, and the group releases the
+    // cell's lex-later neighbours in parallel.  Operands and order of the adds are the serial
+    // sweep's, so the result is bit-identical.
+    constexpr int G = D <= 3 ? 8 : (D <= 6 ? 16 : 32);
+    const int grp = tid / G, g = tid % G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+    double* stg = stage + grp * G * D;
+    auto coop_update = [&](int i) {
       const int n = nbn[i], e = nbe[i];
       if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
-#pragma unroll
-        for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
+        if (g < D) S1[i * D + g] = S0[i * D + g];
         return;
       }
-      double num[D];
+      double num = 0.0;  // lane g < D accumulates coordinate g
+      for (int t0 = 0; t0 < n; t0 += G) {
+        const int t = t0 + g;
+        if (t < n) {
+          if (mode == 0) {
+            if (t < e) {  // earlier neighbour: its NEW centroid
+              const uint64_t r = erec[eoff[i] + t];
+              const uint32_t j = (uint32_t)r;
+              const double w = (double)(uint32_t)(r >> 32);
 #pragma unroll
-      for (int c = 0; c < D; ++c) num[c] = 0.0;
-      if (mode == 0) {
-        const uint64_t* er = erec + eoff[i];
-        for (int t0 = 0; t0 < e; t0 += CH) {  // earlier neighbours: NEW centroids
-          uint64_t r[CH];
-          double v[CH][D];
+              for (int c = 0; c < D; ++c) stg[g * D + c] = __dmul_rn(w, S1[j * D + c]);
+            } else {  // itself / later neighbour: precomputed C'*S_old
+              const double* lp = lprod + (int64_t)(loff[i] + (t - e)) * D;
 #pragma unroll
-          for (int u = 0; u < CH; ++u) r[u] = (t0 + u < e) ? er[t0 + u] : 0ull;
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const uint32_t j = (uint32_t)r[u];
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < e) ? S1[j * D + c] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            if (t0 + u < e) {
-              const double w = (double)(uint32_t)(r[u] >> 32);
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, v[u][c]));
+              for (int c = 0; c < D; ++c) stg[g * D + c] = lp[c];
             }
+          } else {
+            const int j = lst[tmp[i] + t];
+            const double w = (double)cnt[j];
+            const double* src = (t < e) ? S1 : S0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) stg[g * D + c] = __dmul_rn(w, src[j * D + c]);
           }
         }
-        const double* lp = lprod + (int64_t)loff[i] * D;
-        const int nl = n - e;
-        for (int t0 = 0; t0 < nl; t0 += CH) {  // itself + later neighbours: C'*S_old
-          double v[CH][D];
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = (t0 + u < nl) ? lp[(t0 + u) * D + c] : 0.0;
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (t0 + u < nl) {
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
-            }
+        __syncwarp(gmask);
+        if (g < D) {
+          const int len = min(G, n - t0);
+#pragma unroll 4
+          for (int u = 0; u < len; ++u) num = __dadd_rn(num, stg[u * D + g]);
         }
-      } else {
-        const uint16_t* ls = lst + tmp[i];
-        for (int t0 = 0; t0 < n; t0 += CH) {
-          int jj[CH];
-          double v[CH][D], w[CH];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) jj[u] = (t0 + u < n) ? (int)ls[t0 + u] : 0;
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const double* src = (t0 + u < e) ? S1 : S0;
-            w[u] = (double)cnt[jj[u]];
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = src[jj[u] * D + c];
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (t0 + u < n) {
-#pragma unroll
-              for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w[u], v[u][c]));
-            }
-        }
+        __syncwarp(gmask);
       }
-      const double dd = (double)den[i];
-#pragma unroll
-      for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
+      if (g < D) S1[i * D + g] = rs_div(num, (double)den[i], rden[i]);
     };
     if (mode != 2) {
-      // the sweep runs on the first SW threads with a named barrier (fewer warps to sync);
-      // the others wait at the block barrier after it
-      const int SW = min(T, 128);
-      if (tid < SW) {
+      const int SW = T;
+      {
         // Kahn frontier over the sweep DAG: a cell joins the queue when its last lex-earlier
         // neighbour has been updated; each level is updated in parallel (all its operands are
         // final), then releases its lex-later neighbours.  flag[] = pending earlier neighbours,
@@ -478,17 +452,18 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         auto succ_of = [&](int i, int t) -> int {  // t-th lex-later neighbour (self excluded)
           return mode == 0 ? (int)lsucc[loff[i] + 1 + t] : (int)lst[tmp[i] + nbe[i] + 1 + t];
         };
+        const int ngroups = SW / G;
         int qhead = 0;
         for (;;) {
           rs_bar(1, SW);  // the previous level's appends are complete
           const int lev_end = (int)*(volatile unsigned*)&s_maxl;
           rs_bar(1, SW);  // everyone holds lev_end before new appends
           if (qhead >= lev_end) break;
-          for (int k = qhead + tid; k < lev_end; k += SW) {
+          for (int k = qhead + grp; k < lev_end; k += ngroups) {
             const int i = queue[k];
-            update_cell(i);
+            coop_update(i);
             const int ns = nbn[i] - nbe[i] - 1;  // lex-later active neighbours
-            for (int t = 0; t < ns; ++t) {
+            for (int t = g; t < ns; t += G) {
               const int j = succ_of(i, t);
               if (atomicSub(&pend[j], 1) == 1) queue[atomicAdd(&s_maxl, 1u)] = j;
             }
