@@ -97,6 +97,21 @@ struct gs_ctx {
   int shape_ms = 0;
   GsBox shape_box{};
   int64_t shape_vol_frame = 0;
+  // CUDA graph of the optimistic run for one (shape, caller buffers) combination
+  struct GraphKey {
+    ShapeKey shape;
+    const void* points = nullptr;
+    const void* labels = nullptr;
+    uint32_t flags = 0;
+    int on_device = 0;
+    bool operator==(const GraphKey& o) const {
+      return shape == o.shape && points == o.points && labels == o.labels && flags == o.flags &&
+             on_device == o.on_device;
+    }
+  } gkey;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  bool use_graphs = true;
   // last run (host side)
   GsBox box{};
   int64_t nframes = 0;
@@ -770,8 +785,18 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   GS_CK(cudaMemcpyAsync(rb.hm, ra.hist_m, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
   if (rec)
     GS_CK(cudaMemcpyAsync(rb.hd, ra.hist_d, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaStreamSynchronize(st));
-  return GS_OK;
+  return GS_OK;  // the caller synchronises (or captures this sequence into a graph)
+}
+
+// Host memory the graph may copy from/to without staging: pinned or device-visible.
+bool graph_safe(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+         at.type == cudaMemoryTypeManaged;
 }
 
 gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
@@ -795,41 +820,75 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   GS_TRY(grow(ctx, ctx->modes, sizeof(int64_t) * 12));
   Readback rb;
   GS_TRY(map_readback(ctx, nf, cfg->max_iter, &rb));
-  const void* dpts = in->points;
-  GS_CK(cudaEventRecord(ctx->ev[0], st));
-  if (!in->on_device) {
-    GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
-    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
-    dpts = ctx->pts.p;
-  }
-  GS_CK(cudaEventRecord(ctx->ev[1], st));
-  const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
-  bool optimistic = !force_global && ctx->shape_ms > 0 && key == ctx->shape;
-  std::vector<int32_t> g_iters(nf, 0);
-  int64_t swept = 0;
-  for (int attempt = 0;; ++attempt) {
-    if (attempt > 3) return fail(ctx, GS_E_INTERNAL_INVARIANT, "could not size the cell grid");
+  ctx->hist_m.assign(rec ? nf : 0, {});
+  ctx->hist_d.assign(rec ? nf : 0, {});
+  if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
+  const void* dpts = in->on_device ? in->points : ctx->pts.p;
+  auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
+    GS_CK(cudaEventRecord(ctx->ev[0], st));
+    if (!in->on_device)
+      GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
+    GS_CK(cudaEventRecord(ctx->ev[1], st));
     GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h));
     GS_CK(cudaEventRecord(ctx->ev[2], st));
     GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
     GS_CK(cudaMemsetAsync(ctx->fiters.p, 0, sizeof(int32_t) * nf, st));
     GS_CK(cudaMemsetAsync(ctx->fconv.p, 0, sizeof(int32_t) * nf, st));
-    bool deferred = false;
-    if (optimistic) {
-      GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, -1, out->labels, dev_out,
-                         rec, rb));
-      if (rb.err[0] & 32) {  // key box beyond the grid: grow and redo the run
-        GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
-        continue;
+    return GS_OK;
+  };
+  const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
+  std::vector<int32_t> g_iters(nf, 0);
+  int64_t swept = 0;
+  if (!force_global && ctx->shape_ms > 0 && key == ctx->shape) {
+    // ---- optimistic path: the whole run with no host round trip, replayed from a CUDA graph
+    //      when the caller's buffers allow it (pinned or device memory)
+    const bool graphed = ctx->use_graphs && (in->on_device || graph_safe(in->points)) &&
+                         (dev_out || graph_safe(out->labels));
+    auto enqueue_all = [&]() -> gs_status {
+      GS_TRY(enqueue_front());
+      return launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, -1, out->labels, dev_out,
+                         rec, rb);
+    };
+    if (graphed) {
+      const gs_ctx::GraphKey gk{key, in->points, out->labels, cfg->flags, in->on_device};
+      if (!(ctx->gexec && ctx->gkey == gk)) {
+        if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+        const int64_t l0 = ctx->stats.kernel_launches;
+        GS_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        const gs_status s = enqueue_all();
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (s != GS_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          return s;
+        }
+        GS_CK(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        GS_CK(ie);
+        ctx->gkey = gk;
+        ctx->graph_launches = ctx->stats.kernel_launches - l0;
       }
-      if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
-      if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
-      if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
-      deferred = rb.ctr[4] != 0;
-      if (!deferred) break;
-      optimistic = false;
-      ctx->shape_ms = 0;
+      GS_CK(cudaGraphLaunch(ctx->gexec, st));
+      ctx->stats.kernel_launches = ctx->graph_launches;
+    } else {
+      GS_TRY(enqueue_all());
     }
+    GS_CK(cudaStreamSynchronize(st));
+    if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+    if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+    if ((rb.err[0] & 32) || rb.ctr[4] != 0) {  // grid too small / a frame too big: redo it
+      ctx->shape_ms = 0;                        // synchronously below
+      if (rb.err[0] & 32) GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
+    } else {
+      goto results;
+    }
+  }
+  for (int attempt = 0;; ++attempt) {
+    if (attempt > 3) return fail(ctx, GS_E_INTERNAL_INVARIANT, "could not size the cell grid");
+    GS_TRY(enqueue_front());
     // ---- synchronous path: the host sees the initial cells and drives the global path
     int hdr[8];
     unsigned ctr[16];
@@ -845,12 +904,6 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     if (hdr[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
     const int64_t m0 = ctr[0];
     const GsBox& b = ctx->box;
-    if (deferred) {  // the optimistic tail cleared the index: put the initial cells back
-      gs::k_idx_set<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->ckey[0].as<uint32_t>(),
-                                                         ctx->idx.as<int32_t>());
-      GS_LAUNCHED("k_idx_set");
-      GS_CK(cudaMemsetAsync(ctx->counters.as<unsigned>() + 4, 0, 4, st));
-    }
     // (a) global path (K4/K5 kernels, host-driven) while some live frame has more active
     //     cells than one CTA's shared memory holds; (b) then K8 runs every remaining
     //     iteration of every frame on the device.
@@ -938,17 +991,15 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       ctx->shape_vol_frame = b.vol_frame;
     }
     GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, m, out->labels, dev_out, rec, rb));
+    GS_CK(cudaStreamSynchronize(st));
     if (rb.err[0] & 16)
       return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
     break;
   }
-  ctx->cur = 1 - ctx->cur;
+results:
+  ctx->cur = 1 - ctx->cur;  // K8 wrote the final cells to the other buffer
   // ---- results
-  if (!ctx->hist_m.size() && rec) {
-    ctx->hist_m.assign(nf, {});
-    ctx->hist_d.assign(nf, {});
-  }
   if (ctx->hist_m.size() != (size_t)(rec ? nf : 0)) {
     ctx->hist_m.assign(rec ? nf : 0, {});
     ctx->hist_d.assign(rec ? nf : 0, {});
@@ -1085,6 +1136,7 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->lsucc, &ctx->order})
     b->release();
   if (ctx->pin) cudaFreeHost(ctx->pin);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
