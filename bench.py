@@ -186,7 +186,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(device=dev)  # the engine and the timing events share it
     eng = G.Engine(local, stream.cuda_stream)
 
     cfg, X = workload_input(args.workload, rank)
@@ -214,7 +214,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         for s in range(steps):
-            flush.zero_()
+            with torch.cuda.stream(stream):
+                flush.zero_()
             ev[s][0].record(stream)
             step(device_resident)
             ev[s][1].record(stream)

@@ -163,6 +163,17 @@ gs_status grow(gs_ctx* ctx, DevBuf& b, size_t bytes) {
   return GS_OK;
 }
 
+// Phase events; recorded as external event nodes while the stream is being captured so the
+// graph replay records them too (elapsed times keep working on the graph path).
+gs_status rec_event(gs_ctx* ctx, int i) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  GS_CK(cudaStreamIsCapturing(ctx->stream, &cs));
+  GS_CK(cudaEventRecordWithFlags(ctx->ev[i], ctx->stream,
+                                 cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                     : cudaEventRecordDefault));
+  return GS_OK;
+}
+
 gs_status check_launch(gs_ctx* ctx, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, GS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -425,9 +436,9 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
                               nf, ctx->dense_cap, ctx->dbox.as<GsBox>(), ctx->errflag.as<int>(),
                               (long long*)(ctx->errflag.as<int>() + 2));
   GS_LAUNCHED("k_box");
-  GS_CK(cudaEventRecord(ctx->ev[6], st));
+  GS_TRY(rec_event(ctx, 6));
   GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk));
-  GS_CK(cudaEventRecord(ctx->ev[7], st));
+  GS_TRY(rec_event(ctx, 7));
   const GsBox* pb = ctx->dbox.as<GsBox>();
   int* err = ctx->errflag.as<int>();
   unsigned* cnt32 = ctx->counters.as<unsigned>();
@@ -754,7 +765,7 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   ra.deferred = (int*)(cnt32 + 4);
   GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
   GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, fixed + ra.pool_bytes, ra));
-  GS_CK(cudaEventRecord(ctx->ev[3], st));
+  GS_TRY(rec_event(ctx, 3));
   // ---- labels: lab[initial cell] = final frame-local id, then label[p] = lab[slot[p]]
   gs::k_labtab_dev<<<blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
                                 (int64_t)ctx->num_sms * 4), 256, 0, st>>>(
@@ -765,16 +776,16 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
   }
-  GS_CK(cudaEventRecord(ctx->ev[8], st));
+  GS_TRY(rec_event(ctx, 8));
   gs::k_label<<<blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
       ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels);
   GS_LAUNCHED("k_label");
-  GS_CK(cudaEventRecord(ctx->ev[9], st));
-  GS_CK(cudaEventRecord(ctx->ev[4], st));
+  GS_TRY(rec_event(ctx, 9));
+  GS_TRY(rec_event(ctx, 4));
   if (!dev_out)
     GS_CK(cudaMemcpyAsync(user_labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
                           st));
-  GS_CK(cudaEventRecord(ctx->ev[5], st));
+  GS_TRY(rec_event(ctx, 5));
   GS_CK(cudaMemcpyAsync(rb.err, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
   GS_CK(cudaMemcpyAsync(rb.ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
   GS_CK(cudaMemcpyAsync(rb.modes, ctx->modes.p, 96, cudaMemcpyDeviceToHost, st));
@@ -812,6 +823,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ctx->have_run = false;
   ctx->stats = gs_stats{};
   ctx->cur = 0;
+  cudaGetLastError();  // a stale error from an unrelated earlier call must not fail this run
   cudaStream_t st = ctx->stream;
   GS_TRY(grow(ctx, ctx->errflag, 32));
   GS_TRY(grow(ctx, ctx->counters, 64));
@@ -825,12 +837,12 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
   const void* dpts = in->on_device ? in->points : ctx->pts.p;
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
-    GS_CK(cudaEventRecord(ctx->ev[0], st));
+    GS_TRY(rec_event(ctx, 0));
     if (!in->on_device)
       GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
-    GS_CK(cudaEventRecord(ctx->ev[1], st));
+    GS_TRY(rec_event(ctx, 1));
     GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h));
-    GS_CK(cudaEventRecord(ctx->ev[2], st));
+    GS_TRY(rec_event(ctx, 2));
     GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
     GS_CK(cudaMemsetAsync(ctx->fiters.p, 0, sizeof(int32_t) * nf, st));
     GS_CK(cudaMemsetAsync(ctx->fconv.p, 0, sizeof(int32_t) * nf, st));
@@ -1045,6 +1057,7 @@ results:
   s.ms_k_bin = ms;
   cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
   s.ms_k_label = ms;
+  cudaGetLastError();  // timing is best-effort diagnostics
   s.cells_swept = swept;
   s.m0 = rb.ctr[0];
   s.k_total = ktot;

@@ -182,3 +182,29 @@ def test_random_property_bit_exact(engine):
         assert np.array_equal(g.labels, o["labels"]), trial
         assert np.array_equal(_bits(g.centroids), _bits(o["centroids"])), trial
         assert g.iterations == o["iterations"]
+
+
+def test_graph_replay_pinned_buffers():
+    """Repeated runs of one shape with pinned host buffers take the optimistic path replayed
+    from a CUDA graph; every replay must still equal the oracle bit for bit."""
+    import torch
+    X = CF.generate("cfg2")[0]
+    Xp = torch.from_numpy(X).pin_memory()
+    lab = torch.empty(X.shape[0], dtype=torch.int32).pin_memory()
+    o = O.run(X.astype(np.float64), 0.08, 100, O.BUILD_FIXED)
+    eng = G.Engine(0)
+    for rep in range(4):
+        k, it, cv = eng.run_raw(Xp.data_ptr(), X.shape[0], 3, G.GS_F32, 1, False,
+                                G.EngineConfig(0.08, 100), lab.data_ptr())
+        assert int(k[0]) == o["k"] and int(it[0]) == o["iterations"], rep
+        assert np.array_equal(lab.numpy(), o["labels"]), rep
+        cen = eng.centroids(0, int(k[0]), 3)
+        assert np.array_equal(_bits(cen), _bits(o["centroids"])), rep
+    # device-resident input and outputs (the bench's `value` configuration)
+    Xd = Xp.cuda()
+    labd = torch.empty(X.shape[0], dtype=torch.int32, device="cuda")
+    for rep in range(3):
+        eng.run_raw(Xd.data_ptr(), X.shape[0], 3, G.GS_F32, 1, True, G.EngineConfig(0.08, 100),
+                    labd.data_ptr(), device_outputs=True)
+        assert np.array_equal(labd.cpu().numpy(), o["labels"]), rep
+    eng.close()
