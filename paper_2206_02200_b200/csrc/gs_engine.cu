@@ -709,7 +709,9 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   ms_run = std::min(std::max(ms_run, 32), ms_cap);
   // the sweep itself uses 128 threads (named barrier); the parallel phases loop over cells, so
   // 256 threads keep block barriers cheap up to ~1K cells
-  const int threads = ms_run <= 128 ? 128 : 256;
+  // the sweep runs one warp per cell, so a level of up to T/32 cells completes in one round;
+  // fewer threads when frames share an SM
+  const int threads = nf > ctx->num_sms ? 256 : 512;
   const int64_t per_sm = std::min<int64_t>(4, std::max<int64_t>(1, (nf + ctx->num_sms - 1) / ctx->num_sms));
   const size_t budget = kResidentSmemBudget / per_sm - (per_sm > 1 ? 1024 : 0);
   const size_t state = (size_t)ms_run * gs::resident_bytes_per_cell(d);
@@ -717,7 +719,7 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   // uses the cached choice
   const int64_t vf = deferrable ? ctx->shape_vol_frame : ctx->box.vol_frame;
   const size_t sidx = (vf * 2 <= 48 * 1024) ? ((size_t)vf * 2 + 15) & ~size_t(15) : 0;
-  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)256 * d * 8;  // + stage
+  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)512 * d * 8;  // + stage
   const size_t fixed = state + sidx + offs_bytes;
   const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
   unsigned* cnt32 = ctx->counters.as<unsigned>();
@@ -758,9 +760,16 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   ra.hist_d = (double*)(ctx->hist.as<int64_t>() + nf * cfg->max_iter);
   ra.err = ctx->errflag.as<int>();
   ra.mode_count = ctx->modes.as<int64_t>();
-  ra.prof = (long long*)(ctx->modes.as<int64_t>() + 4);
+  // per-phase cycle counters cost a global atomic per phase: opt-in diagnostics only
+  ra.prof = getenv("GS_PROF") ? (long long*)(ctx->modes.as<int64_t>() + 4) : nullptr;
   ra.gidx = ctx->idx.as<int32_t>();
   ra.sidx_bytes = (int)sidx;
+  ra.trace = nullptr;
+  if (getenv("GS_TRACE_LEVELS")) {
+    GS_TRY(grow(ctx, ctx->dbg, 8 * 8 * 512));
+    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * 8 * 512, st));
+    ra.trace = (long long*)ctx->dbg.p;
+  }
   ra.fmax = deferrable ? (const int*)(cnt32 + 2) : nullptr;
   ra.deferred = (int*)(cnt32 + 4);
   GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
@@ -1004,6 +1013,14 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     }
     GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, m, out->labels, dev_out, rec, rb));
     GS_CK(cudaStreamSynchronize(st));
+    if (getenv("GS_TRACE_LEVELS")) {
+      std::vector<long long> tr(8 * 512);
+      cudaMemcpy(tr.data(), ctx->dbg.p, 8 * 8 * 512, cudaMemcpyDeviceToHost);
+      for (int l = 0; l < 512 && (tr[8 * l + 1] || tr[8 * l]); ++l)
+        fprintf(stderr, "level %3d bar %5lld upd %5lld rel %5lld width %3lld n %3lld e %3lld stage %5lld chain %5lld\n", l,
+                tr[8 * l], tr[8 * l + 1], tr[8 * l + 2], tr[8 * l + 3], tr[8 * l + 4], tr[8 * l + 5],
+                tr[8 * l + 6], tr[8 * l + 7]);
+    }
     if (rb.err[0] & 16)
       return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");

@@ -96,7 +96,7 @@ __device__ __forceinline__ double gl_div(double a, double b, double y) {
 // Lanes per cell in the cooperative update.
 template <int D>
 __host__ __device__ constexpr int sweep_group() {
-  return D <= 3 ? 16 : 32;
+  return 32;  // one warp per cell: no intra-warp serialisation between cells
 }
 
 // One CTA.  pend/queue live in dynamic shared memory when 8*m bytes fit (smem_cells >= m),

@@ -61,6 +61,7 @@ struct ResidentArgs {
   // untouched and raises *deferred; the host then takes the global path first
   const int* fmax;
   int* deferred;
+  long long* trace;  // optional per-level timeline of frame 0's first iteration (diagnostic)
 };
 
 // shared-memory bytes per cell (excluding the index and neighbour-record pool)
@@ -77,7 +78,7 @@ __host__ __device__ constexpr int resident_offs_bytes(int D) {
 }
 
 // shared-memory bytes of the sweep's per-group term staging (K8 runs at most 256 threads)
-__host__ __device__ constexpr int resident_stage_bytes(int D) { return 256 * D * 8; }
+__host__ __device__ constexpr int resident_stage_bytes(int D) { return 512 * D * 8; }
 
 // RN(a / b) from y = RN(1/b) (precomputed off the critical path): q0 = RN(a*y); the residual
 // a - b*q0 is exact in one FMA; RN(q0 + r*y) is the correctly rounded quotient (Markstein's
@@ -390,49 +391,61 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     // lex order (the only serial part: one add per term), divides, and the group releases the
     // cell's lex-later neighbours in parallel.  Operands and order of the adds are the serial
     // sweep's, so the result is bit-identical.
-    constexpr int G = D <= 3 ? 8 : (D <= 6 ? 16 : 32);
+    // one warp per cell: cells never share a warp, so no cell waits behind another's
+    // divergent path (measured: 4 cells per warp serialised to ~2-4K cycles per update)
+    constexpr int G = 32;
     const int grp = tid / G, g = tid % G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
-    double* stg = stage + grp * G * D;
-    auto coop_update = [&](int i) {
-      const int n = nbn[i], e = nbe[i];
+    const unsigned gmask = 0xffffffffu;
+    double* stg = stage + grp * G * D;  // coordinate-major: stg[c * G + lane]
+    long long ctr[3] = {0, 0, 0};
+    bool ctr_on = false;
+    auto coop_update = [&](int i, int n, int e) {
       if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
         if (g < D) S1[i * D + g] = S0[i * D + g];
         return;
       }
       double num = 0.0;  // lane g < D accumulates coordinate g
+      const int eo = mode == 0 ? eoff[i] : tmp[i], lo = loff[i];
       for (int t0 = 0; t0 < n; t0 += G) {
         const int t = t0 + g;
+        // one code path for every term: weight * value.  A later term reads its precomputed
+        // C'*S_old with weight 1.0 (exact), an earlier one its neighbour's NEW centroid.
+        const double* base;
+        int64_t off;
+        double w;
+        if (mode == 0) {
+          const uint64_t r = (t < e) ? erec[eo + t] : 0ull;
+          base = (t < e) ? S1 : lprod;
+          off = (t < e) ? (int64_t)(uint32_t)r * D : (int64_t)(lo + (t - e)) * D;
+          w = (t < e) ? (double)(uint32_t)(r >> 32) : 1.0;
+        } else {
+          const int j = (t < n) ? (int)lst[eo + t] : 0;
+          base = (t < e) ? S1 : S0;
+          off = (int64_t)j * D;
+          w = (double)cnt[j];
+        }
         if (t < n) {
-          if (mode == 0) {
-            if (t < e) {  // earlier neighbour: its NEW centroid
-              const uint64_t r = erec[eoff[i] + t];
-              const uint32_t j = (uint32_t)r;
-              const double w = (double)(uint32_t)(r >> 32);
 #pragma unroll
-              for (int c = 0; c < D; ++c) stg[g * D + c] = __dmul_rn(w, S1[j * D + c]);
-            } else {  // itself / later neighbour: precomputed C'*S_old
-              const double* lp = lprod + (int64_t)(loff[i] + (t - e)) * D;
+          for (int c = 0; c < D; ++c) stg[c * G + g] = __dmul_rn(w, base[off + c]);
+        }
+        __syncwarp(gmask);
+        if (ctr_on) ctr[0] = clock64();
+        if (g < D) {
+          const int len = min(G, n - t0);
+          for (int u0 = 0; u0 < len; u0 += 8) {  // 8 independent loads, then 8 adds in order
+            double v[8];
 #pragma unroll
-              for (int c = 0; c < D; ++c) stg[g * D + c] = lp[c];
-            }
-          } else {
-            const int j = lst[tmp[i] + t];
-            const double w = (double)cnt[j];
-            const double* src = (t < e) ? S1 : S0;
+            for (int u = 0; u < 8; ++u) v[u] = stg[g * G + u0 + u];
 #pragma unroll
-            for (int c = 0; c < D; ++c) stg[g * D + c] = __dmul_rn(w, src[j * D + c]);
+            for (int u = 0; u < 8; ++u)
+              if (u0 + u < len) num = __dadd_rn(num, v[u]);  // lex order, one add at a time
           }
         }
         __syncwarp(gmask);
-        if (g < D) {
-          const int len = min(G, n - t0);
-#pragma unroll 4
-          for (int u = 0; u < len; ++u) num = __dadd_rn(num, stg[u * D + g]);
-        }
-        __syncwarp(gmask);
+        if (ctr_on) ctr[1] = clock64();
       }
       if (g < D) S1[i * D + g] = rs_div(num, (double)den[i], rden[i]);
+      if (ctr_on) ctr[2] = clock64();
     };
     if (mode != 2) {
       const int SW = T;
@@ -453,20 +466,47 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
           return mode == 0 ? (int)lsucc[loff[i] + 1 + t] : (int)lst[tmp[i] + nbe[i] + 1 + t];
         };
         const int ngroups = SW / G;
-        int qhead = 0;
+        int qhead = 0, qtrace = 0;
         for (;;) {
+          long long tt0 = 0, tt1 = 0, tt2 = 0, tt3 = 0;
+          const bool trace = a.trace && f == 0 && tid == 0 && iters == 0;
+          if (trace) tt0 = clock64();
           rs_bar(1, SW);  // the previous level's appends are complete
           const int lev_end = (int)*(volatile unsigned*)&s_maxl;
           rs_bar(1, SW);  // everyone holds lev_end before new appends
           if (qhead >= lev_end) break;
+          if (trace) tt1 = clock64();
           for (int k = qhead + grp; k < lev_end; k += ngroups) {
             const int i = queue[k];
-            coop_update(i);
-            const int ns = nbn[i] - nbe[i] - 1;  // lex-later active neighbours
-            for (int t = g; t < ns; t += G) {
+            const int n = nbn[i], e = nbe[i];
+            const int ns = n - e - 1;  // lex-later active neighbours
+            // release the successors first: they run only after the level barrier, so the
+            // atomics' latency overlaps the update below
+            const int j0 = g < ns ? succ_of(i, g) : -1;
+            const int p0 = j0 >= 0 ? atomicSub(&pend[j0], 1) : 0;
+            ctr_on = trace && k == qhead;
+            if (ctr_on) tt1 = clock64();
+            coop_update(i, n, e);
+            ctr_on = false;
+            if (trace && k == qhead) tt2 = clock64();
+            if (j0 >= 0 && p0 == 1) queue[atomicAdd(&s_maxl, 1u)] = j0;
+            for (int t = g + G; t < ns; t += G) {
               const int j = succ_of(i, t);
               if (atomicSub(&pend[j], 1) == 1) queue[atomicAdd(&s_maxl, 1u)] = j;
             }
+            if (trace && k == qhead) tt3 = clock64();
+          }
+          if (trace) {
+            long long* tr = a.trace + 8 * min(qtrace, 511);
+            tr[0] = tt1 - tt0;           // barriers + tail read
+            tr[1] = tt2 - tt1;           // first cell's update
+            tr[2] = tt3 - tt2;           // its successor release
+            tr[3] = lev_end - qhead;     // level width
+            tr[4] = nbn[queue[qhead]];   // its neighbour count
+            tr[5] = nbe[queue[qhead]];
+            tr[6] = ctr[0] - tt1;        // staging (loads, products, smem stores)
+            tr[7] = ctr[1] - ctr[0];     // the ordered add chain
+            ++qtrace;
           }
           qhead = lev_end;
         }
