@@ -719,7 +719,7 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   // uses the cached choice
   const int64_t vf = deferrable ? ctx->shape_vol_frame : ctx->box.vol_frame;
   const size_t sidx = (vf * 2 <= 48 * 1024) ? ((size_t)vf * 2 + 15) & ~size_t(15) : 0;
-  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)512 * d * 8;  // + stage
+  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)16 * d * 34 * 8;  // + stage
   const size_t fixed = state + sidx + offs_bytes;
   const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
   unsigned* cnt32 = ctx->counters.as<unsigned>();

@@ -78,7 +78,8 @@ __host__ __device__ constexpr int resident_offs_bytes(int D) {
 }
 
 // shared-memory bytes of the sweep's per-group term staging (K8 runs at most 256 threads)
-__host__ __device__ constexpr int resident_stage_bytes(int D) { return 512 * D * 8; }
+// (16 warps x D rows x 34 doubles: one padded staging row per coordinate per warp)
+__host__ __device__ constexpr int resident_stage_bytes(int D) { return 16 * D * 34 * 8; }
 
 // RN(a / b) from y = RN(1/b) (precomputed off the critical path): q0 = RN(a*y); the residual
 // a - b*q0 is exact in one FMA; RN(q0 + r*y) is the correctly rounded quotient (Markstein's
@@ -396,7 +397,8 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     constexpr int G = 32;
     const int grp = tid / G, g = tid % G;
     const unsigned gmask = 0xffffffffu;
-    double* stg = stage + grp * G * D;  // coordinate-major: stg[c * G + lane]
+    constexpr int GP = G + 2;  // staging row pitch: rows of different coordinates in distinct banks
+    double* stg = stage + grp * GP * D;  // coordinate-major: stg[c * GP + lane]
     long long ctr[3] = {0, 0, 0};
     bool ctr_on = false;
     auto coop_update = [&](int i, int n, int e) {
@@ -410,35 +412,45 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         const int t = t0 + g;
         // one code path for every term: weight * value.  A later term reads its precomputed
         // C'*S_old with weight 1.0 (exact), an earlier one its neighbour's NEW centroid.
-        const double* base;
-        int64_t off;
-        double w;
+        // lanes past the last term stage 0*S0[0] = +-0: adding +-0.0 is an exact identity and
+        // the running sum is never -0.0, so zero padding leaves every bit of the result unchanged
+        const double* base = S0;
+        int64_t off = 0;
+        double w = 0.0;
         if (mode == 0) {
           const uint64_t r = (t < e) ? erec[eo + t] : 0ull;
-          base = (t < e) ? S1 : lprod;
-          off = (t < e) ? (int64_t)(uint32_t)r * D : (int64_t)(lo + (t - e)) * D;
-          w = (t < e) ? (double)(uint32_t)(r >> 32) : 1.0;
-        } else {
-          const int j = (t < n) ? (int)lst[eo + t] : 0;
+          if (t < e) {
+            base = S1;
+            off = (int64_t)(uint32_t)r * D;
+            w = (double)(uint32_t)(r >> 32);
+          } else if (t < n) {
+            base = lprod;
+            off = (int64_t)(lo + (t - e)) * D;
+            w = 1.0;
+          }
+        } else if (t < n) {
+          const int j = (int)lst[eo + t];
           base = (t < e) ? S1 : S0;
           off = (int64_t)j * D;
           w = (double)cnt[j];
         }
-        if (t < n) {
 #pragma unroll
-          for (int c = 0; c < D; ++c) stg[c * G + g] = __dmul_rn(w, base[off + c]);
-        }
+        for (int c = 0; c < D; ++c) stg[c * GP + g] = __dmul_rn(w, base[off + c]);
         __syncwarp(gmask);
         if (ctr_on) ctr[0] = clock64();
         if (g < D) {
           const int len = min(G, n - t0);
-          for (int u0 = 0; u0 < len; u0 += 8) {  // 8 independent loads, then 8 adds in order
-            double v[8];
+          const double2* row = (const double2*)(stg + g * GP);
+          for (int u0 = 0; u0 < len; u0 += 16) {  // 16 values as 8 LDS.128, then 16 adds
+            double2 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = stg[g * G + u0 + u];
+            for (int q = 0; q < 8; ++q) v[q] = row[(u0 >> 1) + q];
+            asm volatile("" ::: "memory");  // keep every load ahead of the add chain
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (u0 + u < len) num = __dadd_rn(num, v[u]);  // lex order, one add at a time
+            for (int q = 0; q < 8; ++q) {  // lex order, one add at a time
+              num = __dadd_rn(num, v[q].x);
+              num = __dadd_rn(num, v[q].y);
+            }
           }
         }
         __syncwarp(gmask);
