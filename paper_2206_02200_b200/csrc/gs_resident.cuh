@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
   __shared__ unsigned s_maxl;
+  __shared__ int s_dummy;
   volatile uint32_t* vflag = flag;
 
   uint32_t* key = keyA;
@@ -384,140 +385,155 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     // bucketed by level, and (c) levels run in order separated by barriers: when a cell is
     // updated all its earlier neighbours are final, so the update is a straight-line sum in lex
     // order with no polling.  Same operands, same order: bit-identical to the serial sweep.
-    auto early_nb = [&](int i, int t) -> int {
-      return mode == 0 ? (int)(uint32_t)erec[eoff[i] + t] : (int)lst[tmp[i] + t];
-    };
-    // Group-cooperative cell update: G lanes own one cell.  Lanes load and multiply the
-    // cell's terms in parallel into a per-group staging buffer; lane c < D then adds them in
-    // lex order (the only serial part: one add per term), divides, and the group releases the
-    // cell's lex-later neighbours in parallel.  Operands and order of the adds are the serial
-    // sweep's, so the result is bit-identical.
-    // one warp per cell: cells never share a warp, so no cell waits behind another's
-    // divergent path (measured: 4 cells per warp serialised to ~2-4K cycles per update)
-    constexpr int G = 32;
-    const int grp = tid / G, g = tid % G;
-    const unsigned gmask = 0xffffffffu;
-    constexpr int GP = G + 2;  // staging row pitch: rows of different coordinates in distinct banks
-    double* stg = stage + grp * GP * D;  // coordinate-major: stg[c * GP + lane]
-    long long ctr[3] = {0, 0, 0};
-    bool ctr_on = false;
-    auto coop_update = [&](int i, int n, int e) {
+    // ---- (2) the sweep: ONE warp, one lane per cell, Kahn frontier over the sweep's DAG.
+    // A cell enters the frontier when its last lex-earlier active neighbour has been updated;
+    // a frontier (one DAG level) is updated lane-parallel with every operand final, then
+    // releases its lex-later neighbours.  No block barrier is involved (only __syncwarp: the
+    // measured multi-warp version spent ~2K cycles per level in barriers and warp divergence).
+    // Each lane sums its cell's terms in lex order over exactly the serial sweep's operands;
+    // padding terms are 0*0 = +0, and adding +0.0 is an exact identity (the running sum is
+    // never -0.0), so the result is bit-identical.
+    constexpr int CH = D <= 3 ? 4 : 2;  // terms loaded ahead of their adds
+    // Branch-free: every load is unconditional (indices clamped into the cell's own range) and
+    // padding terms get weight 0, so loads never wait behind per-term branches.
+    auto lane_update = [&](int i, int n, int e) {
       if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
-        if (g < D) S1[i * D + g] = S0[i * D + g];
+#pragma unroll
+        for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
         return;
       }
-      double num = 0.0;  // lane g < D accumulates coordinate g
-      const int eo = mode == 0 ? eoff[i] : tmp[i], lo = loff[i];
-      for (int t0 = 0; t0 < n; t0 += G) {
-        const int t = t0 + g;
-        // one code path for every term: weight * value.  A later term reads its precomputed
-        // C'*S_old with weight 1.0 (exact), an earlier one its neighbour's NEW centroid.
-        // lanes past the last term stage 0*S0[0] = +-0: adding +-0.0 is an exact identity and
-        // the running sum is never -0.0, so zero padding leaves every bit of the result unchanged
-        const double* base = S0;
-        int64_t off = 0;
-        double w = 0.0;
-        if (mode == 0) {
-          const uint64_t r = (t < e) ? erec[eo + t] : 0ull;
-          if (t < e) {
-            base = S1;
-            off = (int64_t)(uint32_t)r * D;
-            w = (double)(uint32_t)(r >> 32);
-          } else if (t < n) {
-            base = lprod;
-            off = (int64_t)(lo + (t - e)) * D;
-            w = 1.0;
+      double num[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) num[c] = 0.0;
+      if (mode == 0) {
+        const uint64_t* er = erec + eoff[i];
+        for (int t0 = 0; t0 < e; t0 += CH) {  // earlier neighbours: NEW centroids
+          uint64_t r[CH];
+          double v[CH][D];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) r[u] = er[min(t0 + u, e - 1)];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const uint32_t j = (uint32_t)r[u];
+#pragma unroll
+            for (int c = 0; c < D; ++c) v[u][c] = S1[j * D + c];
           }
-        } else if (t < n) {
-          const int j = (int)lst[eo + t];
-          base = (t < e) ? S1 : S0;
-          off = (int64_t)j * D;
-          w = (double)cnt[j];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const double w = (t0 + u < e) ? (double)(uint32_t)(r[u] >> 32) : 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, v[u][c]));
+          }
         }
+        const double* lp = lprod + (int64_t)loff[i] * D;
+        const int nl = n - e;  // >= 1: the cell itself
+        for (int t0 = 0; t0 < nl; t0 += CH) {  // itself + later neighbours: C'*S_old
+          double v[CH][D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) stg[c * GP + g] = __dmul_rn(w, base[off + c]);
-        __syncwarp(gmask);
-        if (ctr_on) ctr[0] = clock64();
-        if (g < D) {
-          const int len = min(G, n - t0);
-          const double2* row = (const double2*)(stg + g * GP);
-          for (int u0 = 0; u0 < len; u0 += 16) {  // 16 values as 8 LDS.128, then 16 adds
-            double2 v[8];
+          for (int u = 0; u < CH; ++u) {
+            const int q = min(t0 + u, nl - 1);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = row[(u0 >> 1) + q];
-            asm volatile("" ::: "memory");  // keep every load ahead of the add chain
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {  // lex order, one add at a time
-              num = __dadd_rn(num, v[q].x);
-              num = __dadd_rn(num, v[q].y);
+            for (int c = 0; c < D; ++c) {
+              const double x = lp[q * D + c];
+              v[u][c] = (t0 + u < nl) ? x : 0.0;
             }
           }
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+#pragma unroll
+            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
         }
-        __syncwarp(gmask);
-        if (ctr_on) ctr[1] = clock64();
+      } else {
+        const uint16_t* ls = lst + tmp[i];
+        for (int t0 = 0; t0 < n; t0 += CH) {
+          int jj[CH];
+          double v[CH][D], w[CH];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) jj[u] = (int)ls[min(t0 + u, n - 1)];
+#pragma unroll
+          for (int u = 0; u < CH; ++u) {
+            const double* src = (t0 + u < e) ? S1 : S0;
+            const double cw = (double)cnt[jj[u]];
+            w[u] = (t0 + u < n) ? cw : 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) v[u][c] = src[jj[u] * D + c];
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+#pragma unroll
+            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w[u], v[u][c]));
+        }
       }
-      if (g < D) S1[i * D + g] = rs_div(num, (double)den[i], rden[i]);
-      if (ctr_on) ctr[2] = clock64();
+      const double dd = (double)den[i];
+#pragma unroll
+      for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
     };
     if (mode != 2) {
-      const int SW = T;
-      {
-        // Kahn frontier over the sweep DAG: a cell joins the queue when its last lex-earlier
-        // neighbour has been updated; each level is updated in parallel (all its operands are
-        // final), then releases its lex-later neighbours.  flag[] = pending earlier neighbours,
-        // sk[] (as int) = the queue.
-        int* pend = (int*)flag;
-        int* queue = (int*)sk;
-        if (tid == 0) s_maxl = 0u;  // queue tail
-        rs_bar(1, SW);
-        for (int i = tid; i < m; i += SW) {
-          pend[i] = nbe[i];
-          if (nbe[i] == 0) queue[atomicAdd(&s_maxl, 1u)] = i;
+      if (tid < 32) {
+        const int lane = tid;
+        const unsigned lt = (1u << lane) - 1u;
+        int* pend = (int*)flag;  // lex-earlier active neighbours not yet updated
+        int* queue = (int*)sk;   // frontier after frontier
+        int qtail = 0;
+        for (int base = 0; base < m; base += 32) {
+          const int i = base + lane;
+          const bool ready = i < m && nbe[i] == 0;
+          if (i < m) pend[i] = nbe[i];
+          const unsigned mk = __ballot_sync(0xffffffffu, ready);
+          if (ready) queue[qtail + __popc(mk & lt)] = i;
+          qtail += __popc(mk);
         }
-        auto succ_of = [&](int i, int t) -> int {  // t-th lex-later neighbour (self excluded)
-          return mode == 0 ? (int)lsucc[loff[i] + 1 + t] : (int)lst[tmp[i] + nbe[i] + 1 + t];
-        };
-        const int ngroups = SW / G;
+        __syncwarp();
+        constexpr int RB = 8;  // successor releases issued together
         int qhead = 0, qtrace = 0;
-        for (;;) {
-          long long tt0 = 0, tt1 = 0, tt2 = 0, tt3 = 0;
-          const bool trace = a.trace && f == 0 && tid == 0 && iters == 0;
+        while (qhead < qtail) {
+          const int lev_end = qtail;
+          long long tt0 = 0, tt1 = 0;
+          const bool trace = a.trace && f == 0 && lane == 0 && iters == 0;
           if (trace) tt0 = clock64();
-          rs_bar(1, SW);  // the previous level's appends are complete
-          const int lev_end = (int)*(volatile unsigned*)&s_maxl;
-          rs_bar(1, SW);  // everyone holds lev_end before new appends
-          if (qhead >= lev_end) break;
-          if (trace) tt1 = clock64();
-          for (int k = qhead + grp; k < lev_end; k += ngroups) {
-            const int i = queue[k];
-            const int n = nbn[i], e = nbe[i];
-            const int ns = n - e - 1;  // lex-later active neighbours
-            // release the successors first: they run only after the level barrier, so the
-            // atomics' latency overlaps the update below
-            const int j0 = g < ns ? succ_of(i, g) : -1;
-            const int p0 = j0 >= 0 ? atomicSub(&pend[j0], 1) : 0;
-            ctr_on = trace && k == qhead;
-            if (ctr_on) tt1 = clock64();
-            coop_update(i, n, e);
-            ctr_on = false;
-            if (trace && k == qhead) tt2 = clock64();
-            if (j0 >= 0 && p0 == 1) queue[atomicAdd(&s_maxl, 1u)] = j0;
-            for (int t = g + G; t < ns; t += G) {
-              const int j = succ_of(i, t);
-              if (atomicSub(&pend[j], 1) == 1) queue[atomicAdd(&s_maxl, 1u)] = j;
+          for (int base = qhead; base < lev_end; base += 32) {
+            const int k = base + lane;
+            const bool act = k < lev_end;
+            const int i = act ? queue[k] : 0;
+            const int n = act ? nbn[i] : 0, e = act ? nbe[i] : 0;
+            if (act) lane_update(i, n, e);
+            if (trace && base == qhead) tt1 = clock64();
+            // release the lex-later neighbours; each batch's atomics are independent
+            const int ns = act ? n - e - 1 : 0;
+            const uint16_t* sl = mode == 0 ? lsucc + loff[i] + 1 : lst + tmp[i] + e + 1;
+            const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)max(ns, 0));
+            for (int t0 = 0; t0 < mx; t0 += RB) {
+              int jj[RB], old[RB];
+#pragma unroll
+              for (int u = 0; u < RB; ++u) {  // unconditional load (address kept in smem)
+                const int q = t0 + u < ns ? t0 + u : 0;
+                const int j = (int)sl[q];
+                jj[u] = (t0 + u < ns) ? j : -1;
+              }
+#pragma unroll
+              for (int u = 0; u < RB; ++u) {  // unconditional atomics: idle lanes add 0 to a dummy
+                int* tgt = jj[u] >= 0 ? &pend[jj[u]] : &s_dummy;
+                old[u] = atomicAdd(tgt, jj[u] >= 0 ? -1 : 0);
+              }
+#pragma unroll
+              for (int u = 0; u < RB; ++u) {
+                const bool rdy = jj[u] >= 0 && old[u] == 1;
+                const unsigned mk = __ballot_sync(0xffffffffu, rdy);
+                if (rdy) queue[qtail + __popc(mk & lt)] = jj[u];
+                qtail += __popc(mk);
+              }
             }
-            if (trace && k == qhead) tt3 = clock64();
           }
+          __syncwarp();  // this level's centroids are visible to the next level's lanes
           if (trace) {
             long long* tr = a.trace + 8 * min(qtrace, 511);
-            tr[0] = tt1 - tt0;           // barriers + tail read
-            tr[1] = tt2 - tt1;           // first cell's update
-            tr[2] = tt3 - tt2;           // its successor release
-            tr[3] = lev_end - qhead;     // level width
-            tr[4] = nbn[queue[qhead]];   // its neighbour count
+            tr[0] = 0;
+            tr[1] = tt1 - tt0;                 // the level's (first pass) updates
+            tr[2] = clock64() - tt1;           // releases
+            tr[3] = lev_end - qhead;           // level width
+            tr[4] = nbn[queue[qhead]];
             tr[5] = nbe[queue[qhead]];
-            tr[6] = ctr[0] - tt1;        // staging (loads, products, smem stores)
-            tr[7] = ctr[1] - ctr[0];     // the ordered add chain
+            tr[6] = tr[7] = 0;
             ++qtrace;
           }
           qhead = lev_end;
