@@ -30,12 +30,19 @@ constexpr int64_t kMaxDenseCells = int64_t(1) << 28;  // dense grid cap (u32 key
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool owned = true;  // false: a view into another allocation (the control block)
   template <typename T>
   T* as() const { return static_cast<T*>(p); }
   void release() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     bytes = 0;
+  }
+  void view(void* q, size_t n) {
+    release();
+    p = q;
+    bytes = n;
+    owned = false;
   }
 };
 
@@ -78,7 +85,14 @@ struct gs_ctx {
       hist;
   int64_t frame_cap = 0;
   // misc
-  DevBuf counters, errflag, bpart, cub_tmp, dbg, modes, tiles, dbox;
+  DevBuf counters, errflag, bpart, cub_tmp, dbg, modes, tiles, dbox, epoch_dev;
+  // control block: one allocation, one memset and one readback copy per run
+  //   [errflag 32 B][counters 64 B][modes 96 B][fswept i64 x nf][fdone][fiters][fconv][fk][fout]
+  //   (zeroed up to fk; read back whole)
+  DevBuf ctl, fswept, fout;
+  int64_t ctl_nf = 0;
+  // bumped whenever a device buffer is (re)allocated: a cached graph holds raw pointers
+  uint64_t alloc_gen = 0;
   // pinned readback area (one async D2H per result array, one sync per run)
   void* pin = nullptr;
   size_t pin_bytes = 0;
@@ -104,9 +118,10 @@ struct gs_ctx {
     const void* labels = nullptr;
     uint32_t flags = 0;
     int on_device = 0;
+    uint64_t gen = 0;
     bool operator==(const GraphKey& o) const {
       return shape == o.shape && points == o.points && labels == o.labels && flags == o.flags &&
-             on_device == o.on_device;
+             on_device == o.on_device && gen == o.gen;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
@@ -160,6 +175,8 @@ gs_status grow(gs_ctx* ctx, DevBuf& b, size_t bytes) {
     return fail(ctx, GS_E_OOM, "cudaMalloc(" + std::to_string(want) + ") failed");
   }
   b.bytes = want;
+  b.owned = true;
+  ++ctx->alloc_gen;
   return GS_OK;
 }
 
@@ -255,11 +272,40 @@ gs_status ensure_cells(gs_ctx* ctx, int64_t m, int d) {
   return GS_OK;
 }
 
+// control-block geometry for nf frames
+constexpr size_t kCtlHeader = 192;
+size_t ctl_zero_bytes(int64_t nf) { return kCtlHeader + 8 * (size_t)nf + 12 * (size_t)nf; }
+size_t ctl_bytes(int64_t nf) { return kCtlHeader + 8 * (size_t)nf + 20 * (size_t)nf; }
+
+gs_status ensure_ctl(gs_ctx* ctx, int64_t nf) {
+  if (nf <= ctx->ctl_nf && ctx->ctl.p) return GS_OK;
+  for (DevBuf* b : {&ctx->errflag, &ctx->counters, &ctx->modes, &ctx->fswept, &ctx->fdone,
+                    &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->fout})
+    b->release();
+  ctx->ctl.release();
+  GS_TRY(grow(ctx, ctx->ctl, ctl_bytes(nf)));
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_bytes(nf), ctx->stream));
+  char* p = ctx->ctl.as<char>();
+  ctx->errflag.view(p, 32);
+  ctx->counters.view(p + 32, 64);
+  ctx->modes.view(p + 96, 96);
+  p += kCtlHeader;
+  ctx->fswept.view(p, 8 * nf);  p += 8 * nf;
+  ctx->fdone.view(p, 4 * nf);   p += 4 * nf;
+  ctx->fiters.view(p, 4 * nf);  p += 4 * nf;
+  ctx->fconv.view(p, 4 * nf);   p += 4 * nf;
+  ctx->fk.view(p, 4 * nf);      p += 4 * nf;
+  ctx->fout.view(p, 4 * nf);
+  ctx->ctl_nf = nf;
+  return GS_OK;
+}
+
 gs_status ensure_frames(gs_ctx* ctx, int64_t nf) {
+  GS_TRY(ensure_ctl(ctx, nf));
   if (nf <= ctx->frame_cap) return GS_OK;
-  for (DevBuf* b : {&ctx->fdone, &ctx->fchanged, &ctx->fadj, &ctx->fm, &ctx->ffirst, &ctx->fcount,
-                    &ctx->ifirst, &ctx->icount, &ctx->fiters, &ctx->fconv, &ctx->fk})
+  for (DevBuf* b : {&ctx->fchanged, &ctx->fadj, &ctx->fm, &ctx->ffirst, &ctx->fcount})
     GS_TRY(grow(ctx, *b, sizeof(int32_t) * nf));
+  GS_TRY(grow(ctx, ctx->ifirst, sizeof(int32_t) * (nf + 1)));  // [nf] = m0
   GS_TRY(grow(ctx, ctx->fdisp, sizeof(unsigned long long) * nf));
   ctx->frame_cap = nf;
   return GS_OK;
@@ -342,17 +388,22 @@ gs_status make_box_from_cells(gs_ctx* ctx, int d, double h, int64_t m, const int
 
 template <int D>
 gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t ntot, bool bounds,
-                            unsigned nblk) {
+                            unsigned nblk, double h = 0, int64_t n = 0, int64_t nf = 0) {
   if (bounds) {
+    unsigned* ctr = ctx->counters.as<unsigned>();
+    int* err = ctx->errflag.as<int>();
+    const int F = gs_fixed_shift(n, h);
     if (dtype == GS_F32)
-      gs::k_bounds<D, float><<<nblk, 256, 0, ctx->stream>>>(
-          (const float*)pts, ntot, ctx->bpart.as<double>(),
-          ctx->bpart.as<double>() + (size_t)nblk * D, ctx->errflag.as<int>());
+      gs::k_bounds_box<D, float><<<nblk, 256, 0, ctx->stream>>>(
+          (const float*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
+          ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
+          ctx->epoch_dev.as<unsigned>());
     else
-      gs::k_bounds<D, double><<<nblk, 256, 0, ctx->stream>>>(
-          (const double*)pts, ntot, ctx->bpart.as<double>(),
-          ctx->bpart.as<double>() + (size_t)nblk * D, ctx->errflag.as<int>());
-    GS_LAUNCHED("k_bounds");
+      gs::k_bounds_box<D, double><<<nblk, 256, 0, ctx->stream>>>(
+          (const double*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
+          ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
+          ctx->epoch_dev.as<unsigned>());
+    GS_LAUNCHED("k_bounds_box");
   } else {
     // privatised binning: one 1024-thread CTA per SM at most, >= 4096 points per CTA
     constexpr int TBL = gs::bin_table_entries<D>();
@@ -380,11 +431,12 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
 }
 
 gs_status dispatch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int d, int64_t ntot,
-                              bool bounds, unsigned nblk) {
+                              bool bounds, unsigned nblk, double h = 0, int64_t n = 0,
+                              int64_t nf = 0) {
   switch (d) {
 #define GS_CASE(D) \
   case D:          \
-    return launch_bounds_bin<D>(ctx, pts, dtype, ntot, bounds, nblk);
+    return launch_bounds_bin<D>(ctx, pts, dtype, ntot, bounds, nblk, h, n, nf);
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
     GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
 #undef GS_CASE
@@ -413,14 +465,15 @@ gs_status grow_dense_for(gs_ctx* ctx, long long need, int d) {
   return ensure_dense(ctx, (int64_t)need, d);
 }
 
-// n-scale phase with no host round trip: bounds -> device box -> privatised binning ->
-// compaction by scan (cells come out lexicographically sorted) -> per-frame cell ranges.
-// Errors (non-finite input, key box beyond the grid) surface in errflag at the next sync.
+// n-scale phase with no host round trip: control block cleared -> bounds + device box ->
+// privatised binning -> single-pass compaction (cells come out lexicographically sorted, with
+// per-frame first indices).  Errors (non-finite input, key box beyond the grid) surface in
+// errflag at the next sync.  vol_hint sizes the compaction grid (any value is correct).
 gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t n, int64_t nf,
-                        double h) {
+                        double h, int64_t vol_hint = 0) {
   cudaStream_t st = ctx->stream;
   const int64_t ntot = n * nf;
-  const unsigned nblk = blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8);
+  const unsigned nblk = blocks_for(ntot, 256 * 4, (int64_t)ctx->num_sms * 2);
   GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
   GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
   GS_TRY(ensure_dense(ctx, std::max<int64_t>(ctx->dense_cap, kDefaultDenseCells), d));
@@ -428,42 +481,29 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   GS_TRY(ensure_frames(ctx, nf));
   GS_TRY(grow(ctx, ctx->slot, sizeof(uint32_t) * ntot));
   const int64_t ntiles = ctx->dense_cap / gs::kOccTile + 1;
-  GS_TRY(grow(ctx, ctx->tiles, sizeof(int) * ntiles));
-  GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, 32, st));
-  GS_CK(cudaMemsetAsync(ctx->counters.p, 0, 64, st));
-  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk));
-  gs::k_box<<<1, 384, 0, st>>>(ctx->bpart.as<double>(), (int)nblk, d, h, gs_fixed_shift(n, h), n,
-                              nf, ctx->dense_cap, ctx->dbox.as<GsBox>(), ctx->errflag.as<int>(),
-                              (long long*)(ctx->errflag.as<int>() + 2));
-  GS_LAUNCHED("k_box");
+  if (ctx->tiles.bytes < sizeof(unsigned long long) * ntiles) {  // epoch-tagged: cleared once
+    GS_TRY(grow(ctx, ctx->tiles, sizeof(unsigned long long) * ntiles));
+    GS_CK(cudaMemsetAsync(ctx->tiles.p, 0, ctx->tiles.bytes, st));
+  }
+  if (!ctx->epoch_dev.p) {
+    GS_TRY(grow(ctx, ctx->epoch_dev, 16));
+    GS_CK(cudaMemsetAsync(ctx->epoch_dev.p, 0, 16, st));
+  }
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
   GS_TRY(rec_event(ctx, 6));
   GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk));
   GS_TRY(rec_event(ctx, 7));
-  const GsBox* pb = ctx->dbox.as<GsBox>();
-  int* err = ctx->errflag.as<int>();
   unsigned* cnt32 = ctx->counters.as<unsigned>();
-  const unsigned tg = (unsigned)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 4);
-  gs::k_occ_count<<<tg, 256, 0, st>>>(pb, ctx->cnt.as<uint32_t>(), ctx->tiles.as<int>(), err);
-  GS_LAUNCHED("k_occ_count");
-  gs::k_occ_scan<<<1, 1024, 0, st>>>(pb, ctx->tiles.as<int>(), cnt32, err);
-  GS_LAUNCHED("k_occ_scan");
-  gs::k_occ_compact<<<tg, 256, 0, st>>>(
-      pb, ctx->tiles.as<int>(), ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+  const int64_t vt = vol_hint > 0 ? std::min(vol_hint, ctx->dense_cap) : ctx->dense_cap;
+  const unsigned tg = (unsigned)std::min<int64_t>(vt / gs::kOccTile + 1, (int64_t)ctx->num_sms * 4);
+  gs::k_occ<<<tg, 256, 0, st>>>(
+      ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>(), ctx->tiles.as<unsigned long long>(),
+      cnt32 + 5, cnt32, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
       ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(), ctx->S[0].as<double>(),
-      ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(), err);
-  GS_LAUNCHED("k_occ_compact");
-  const unsigned cg = blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
-                                 (int64_t)ctx->num_sms * 4);
-  gs::k_frame_ranges_dev<<<cg, 256, 0, st>>>(cnt32, pb, ctx->ckey[0].as<uint32_t>(),
-                                             ctx->ifirst.as<int32_t>(), ctx->icount.as<int32_t>());
-  GS_LAUNCHED("k_frame_ranges_dev");
-  gs::k_frame_counts_dev<<<blocks_for(nf, 256, 1024), 256, 0, st>>>(
-      nf, ctx->ifirst.as<int32_t>(), ctx->icount.as<int32_t>(), (int*)(cnt32 + 2));
-  GS_LAUNCHED("k_frame_counts_dev");
-  GS_CK(cudaMemcpyAsync(ctx->ffirst.p, ctx->ifirst.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToDevice, st));
-  GS_CK(cudaMemcpyAsync(ctx->fcount.p, ctx->icount.p, sizeof(int32_t) * nf,
-                        cudaMemcpyDeviceToDevice, st));
+      ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(),
+      ctx->ifirst.as<int32_t>(), ctx->errflag.as<int>());
+  GS_LAUNCHED("k_occ");
   return GS_OK;
 }
 
@@ -615,7 +655,7 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
 
 // ---- K8 launch helpers
 constexpr size_t kResidentSmemBudget = 224 * 1024;  // of 227 KB per CTA (static smem < 1 KB)
-constexpr size_t kResidentStateMax = 140 * 1024;    // cell state may take at most this much
+constexpr size_t kResidentStateMax = 160 * 1024;    // cell state may take at most this much
 
 // Largest power-of-two cell capacity whose per-cell state fits kResidentStateMax; the rest of
 // the budget holds the neighbour records (gs_resident.cuh falls back to slower sweep modes
@@ -664,45 +704,56 @@ gs_status launch_resident(gs_ctx* ctx, int d, unsigned grid, int threads, size_t
   return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
 }
 
-// Readback area in pinned host memory (one async D2H per array, one sync per run).
+// Readback area in pinned host memory: the control block's mirror (one D2H copy per run), then
+// the per-iteration history (copied only when recorded).
 struct Readback {
   int* err;          // 8 ints
   unsigned* ctr;     // 16
-  int32_t* ffirst;   // nf
-  int32_t* fk;
+  int64_t* modes;    // 12
+  int64_t* fswept;   // nf
+  int32_t* fdone;    // nf
   int32_t* fiters;
   int32_t* fconv;
-  int64_t* modes;    // 12
+  int32_t* fk;
+  int32_t* fout;
   int64_t* hm;       // nf * max_iter
   double* hd;        // nf * max_iter
 };
 
-gs_status map_readback(gs_ctx* ctx, int64_t nf, int max_iter, Readback* rb) {
-  const size_t need = 32 + 64 + 4 * 4 * (size_t)nf + 96 + 16 * (size_t)nf * max_iter + 64;
+gs_status map_readback(gs_ctx* ctx, int64_t nf_run, int max_iter, Readback* rb) {
+  const int64_t nf = ctx->ctl_nf;  // the control block's layout (>= this run's frames)
+  const size_t need = ctl_bytes(nf) + 16 * (size_t)nf_run * max_iter + 64;
   if (need > ctx->pin_bytes) {
     if (ctx->pin) cudaFreeHost(ctx->pin);
     ctx->pin = nullptr;
     ctx->pin_bytes = 0;
     GS_CK(cudaMallocHost(&ctx->pin, need));
     ctx->pin_bytes = need;
+    ++ctx->alloc_gen;
   }
   char* p = (char*)ctx->pin;
-  rb->err = (int*)p;          p += 32;
-  rb->ctr = (unsigned*)p;     p += 64;
-  rb->modes = (int64_t*)p;    p += 96;
-  rb->hm = (int64_t*)p;       p += 8 * (size_t)nf * max_iter;
-  rb->hd = (double*)p;        p += 8 * (size_t)nf * max_iter;
-  rb->ffirst = (int32_t*)p;   p += 4 * (size_t)nf;
-  rb->fk = (int32_t*)p;       p += 4 * (size_t)nf;
-  rb->fiters = (int32_t*)p;   p += 4 * (size_t)nf;
-  rb->fconv = (int32_t*)p;
+  rb->err = (int*)p;
+  rb->ctr = (unsigned*)(p + 32);
+  rb->modes = (int64_t*)(p + 96);
+  p += kCtlHeader;
+  rb->fswept = (int64_t*)p;  p += 8 * (size_t)nf;
+  rb->fdone = (int32_t*)p;   p += 4 * (size_t)nf;
+  rb->fiters = (int32_t*)p;  p += 4 * (size_t)nf;
+  rb->fconv = (int32_t*)p;   p += 4 * (size_t)nf;
+  rb->fk = (int32_t*)p;      p += 4 * (size_t)nf;
+  rb->fout = (int32_t*)p;    p += 4 * (size_t)nf;
+  p = (char*)ctx->pin + ((ctl_bytes(nf) + 15) & ~size_t(15));
+  rb->hm = (int64_t*)p;      p += 8 * (size_t)nf_run * max_iter;
+  rb->hd = (double*)p;
   return GS_OK;
 }
 
 // K8 over every frame, then labels; results copied to the pinned readback area; one sync.
 // deferrable: the launch is optimistic (smem sized from the shape cache) and K8 may refuse.
+bool graph_safe(const void* p);
+
 gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t ntot, int d,
-                      int ms_run, bool deferrable, int64_t m_host, int32_t* user_labels,
+                      int ms_run, bool deferrable, bool initial_ranges, int32_t* user_labels,
                       bool dev_out, bool rec, const Readback& rb) {
   cudaStream_t st = ctx->stream;
   const int ms_cap = resident_capacity(d);
@@ -719,39 +770,33 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   // uses the cached choice
   const int64_t vf = deferrable ? ctx->shape_vol_frame : ctx->box.vol_frame;
   const size_t sidx = (vf * 2 <= 48 * 1024) ? ((size_t)vf * 2 + 15) & ~size_t(15) : 0;
-  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + (size_t)16 * d * 34 * 8;  // + stage
+  const size_t offs_bytes = (size_t)resident_offs_bytes_host(d) + gs::resident_fixed_bytes(d);
   const size_t fixed = state + sidx + offs_bytes;
   const size_t pool_bytes = budget > fixed + 1024 ? budget - fixed : 1024;
   unsigned* cnt32 = ctx->counters.as<unsigned>();
-  // K8 owns the global index from here on (it re-keys it per frame and leaves it clean)
-  if (m_host < 0) {
-    gs::k_idx_put_dev<<<blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
-                                   (int64_t)ctx->num_sms * 4), 256, 0, st>>>(
-        cnt32, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->idx.as<int32_t>(), 0);
-    GS_LAUNCHED("k_idx_put_dev");
-  } else {
-    gs::k_idx_clear<<<blocks_for(m_host, 256), 256, 0, st>>>(
-        (int)m_host, ctx->ckey[ctx->cur].as<uint32_t>(), ctx->idx.as<int32_t>());
-    GS_LAUNCHED("k_idx_clear");
-  }
+  // K8 owns the global index from here on (it clears or re-keys each frame's entries and
+  // leaves the grid clean)
   const int fin = 1 - ctx->cur;
   gs::ResidentArgs ra;
-  ra.box = deferrable ? ctx->shape_box : ctx->box;
   ra.ms = ms_run;
   ra.pool_bytes = (int)(pool_bytes & ~size_t(15));
   ra.max_iter = cfg->max_iter;
-  ra.record = 1;  // m_t feeds the cells x iterations counter even without GS_RECORD_HISTORY
+  ra.record = rec ? 1 : 0;
   ra.ckey = ctx->ckey[ctx->cur].as<uint32_t>();
   ra.ccnt = ctx->ccnt[ctx->cur].as<uint32_t>();
   ra.S = ctx->S[ctx->cur].as<double>();
-  ra.ffirst = ctx->ffirst.as<int32_t>();
-  ra.fcount = ctx->fcount.as<int32_t>();
+  // current ranges: the initial ones (ffirst[f + 1] - ffirst[f]) unless the global path ran
+  ra.ffirst = initial_ranges ? ctx->ifirst.as<int32_t>() : ctx->ffirst.as<int32_t>();
+  ra.fcount = initial_ranges ? nullptr : ctx->fcount.as<int32_t>();
   ra.ifirst = ctx->ifirst.as<int32_t>();
-  ra.icount = ctx->icount.as<int32_t>();
+  ra.initkey = ctx->initkey.as<uint32_t>();
+  ra.lab = ctx->lab.as<int32_t>();
   ra.fdone = ctx->fdone.as<int32_t>();
   ra.fiters = ctx->fiters.as<int32_t>();
   ra.fconv = ctx->fconv.as<int32_t>();
   ra.fk = ctx->fk.as<int32_t>();
+  ra.fout = ctx->fout.as<int32_t>();
+  ra.fswept = ctx->fswept.as<int64_t>();
   ra.okey = ctx->ckey[fin].as<uint32_t>();
   ra.ocnt = ctx->ccnt[fin].as<uint32_t>();
   ra.oS = ctx->S[fin].as<double>();
@@ -770,41 +815,32 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
     GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * 8 * 512, st));
     ra.trace = (long long*)ctx->dbg.p;
   }
-  ra.fmax = deferrable ? (const int*)(cnt32 + 2) : nullptr;
+  ra.deferrable = deferrable ? 1 : 0;
   ra.deferred = (int*)(cnt32 + 4);
-  GS_CK(cudaMemsetAsync(ctx->modes.p, 0, sizeof(int64_t) * 12, st));
+  ra.pbox = ctx->dbox.as<GsBox>();
   GS_TRY(launch_resident(ctx, d, (unsigned)nf, threads, fixed + ra.pool_bytes, ra));
   GS_TRY(rec_event(ctx, 3));
-  // ---- labels: lab[initial cell] = final frame-local id, then label[p] = lab[slot[p]]
-  gs::k_labtab_dev<<<blocks_for(std::min<int64_t>(ntot, ctx->dense_cap), 256,
-                                (int64_t)ctx->num_sms * 4), 256, 0, st>>>(
-      cnt32, ctx->initkey.as<uint32_t>(), ctx->root.as<int32_t>(), ctx->lab.as<int32_t>());
-  GS_LAUNCHED("k_labtab_dev");
+  // ---- labels: K8 wrote lab[initial cell key] = final frame-local id; label[p] = lab[slot[p]]
+  //      (straight into pinned caller memory when it is graph-safe host memory)
   int32_t* dlabels = user_labels;
-  if (!dev_out) {
+  const bool direct = dev_out || graph_safe(user_labels);
+  if (!direct) {
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
   }
-  GS_TRY(rec_event(ctx, 8));
   gs::k_label<<<blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
       ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels);
   GS_LAUNCHED("k_label");
-  GS_TRY(rec_event(ctx, 9));
   GS_TRY(rec_event(ctx, 4));
-  if (!dev_out)
+  if (!direct)
     GS_CK(cudaMemcpyAsync(user_labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
                           st));
   GS_TRY(rec_event(ctx, 5));
-  GS_CK(cudaMemcpyAsync(rb.err, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.modes, ctx->modes.p, 96, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.ffirst, ctx->ffirst.p, 4 * nf, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.fk, ctx->fk.p, 4 * nf, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.fiters, ctx->fiters.p, 4 * nf, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.fconv, ctx->fconv.p, 4 * nf, cudaMemcpyDeviceToHost, st));
-  GS_CK(cudaMemcpyAsync(rb.hm, ra.hist_m, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
-  if (rec)
+  GS_CK(cudaMemcpyAsync(rb.err, ctx->ctl.p, ctl_bytes(ctx->ctl_nf), cudaMemcpyDeviceToHost, st));
+  if (rec) {
+    GS_CK(cudaMemcpyAsync(rb.hm, ra.hist_m, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
     GS_CK(cudaMemcpyAsync(rb.hd, ra.hist_d, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
+  }
   return GS_OK;  // the caller synchronises (or captures this sequence into a graph)
 }
 
@@ -845,16 +881,14 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ctx->hist_d.assign(rec ? nf : 0, {});
   if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
   const void* dpts = in->on_device ? in->points : ctx->pts.p;
+  int64_t vol_hint = 0;  // the cached shape's grid volume (sizes the compaction launch)
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
     GS_TRY(rec_event(ctx, 0));
     if (!in->on_device)
       GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
     GS_TRY(rec_event(ctx, 1));
-    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h));
+    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint));
     GS_TRY(rec_event(ctx, 2));
-    GS_CK(cudaMemsetAsync(ctx->fdone.p, 0, sizeof(int32_t) * nf, st));
-    GS_CK(cudaMemsetAsync(ctx->fiters.p, 0, sizeof(int32_t) * nf, st));
-    GS_CK(cudaMemsetAsync(ctx->fconv.p, 0, sizeof(int32_t) * nf, st));
     return GS_OK;
   };
   const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
@@ -865,13 +899,15 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     //      when the caller's buffers allow it (pinned or device memory)
     const bool graphed = ctx->use_graphs && (in->on_device || graph_safe(in->points)) &&
                          (dev_out || graph_safe(out->labels));
+    vol_hint = ctx->shape_vol_frame * nf;
     auto enqueue_all = [&]() -> gs_status {
       GS_TRY(enqueue_front());
-      return launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, -1, out->labels, dev_out,
+      return launch_tail(ctx, cfg, nf, ntot, d, ctx->shape_ms, true, true, out->labels, dev_out,
                          rec, rb);
     };
     if (graphed) {
-      const gs_ctx::GraphKey gk{key, in->points, out->labels, cfg->flags, in->on_device};
+      const gs_ctx::GraphKey gk{key, in->points, out->labels, cfg->flags, in->on_device,
+                                ctx->alloc_gen};
       if (!(ctx->gexec && ctx->gkey == gk)) {
         if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
         ctx->gexec = nullptr;
@@ -889,6 +925,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
         cudaGraphDestroy(graph);
         GS_CK(ie);
         ctx->gkey = gk;
+        ctx->gkey.gen = ctx->alloc_gen;  // buffers (re)allocated while capturing belong to it
         ctx->graph_launches = ctx->stats.kernel_launches - l0;
       }
       GS_CK(cudaGraphLaunch(ctx->gexec, st));
@@ -909,6 +946,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   }
   for (int attempt = 0;; ++attempt) {
     if (attempt > 3) return fail(ctx, GS_E_INTERNAL_INVARIANT, "could not size the cell grid");
+    vol_hint = 0;
     GS_TRY(enqueue_front());
     // ---- synchronous path: the host sees the initial cells and drives the global path
     int hdr[8];
@@ -935,9 +973,13 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     ctx->hist_d.assign(rec ? nf : 0, {});
     std::vector<int32_t> fch(nf), fadj(nf), fm(nf), fcnt(nf);
     std::vector<unsigned long long> fdisp(nf);
-    GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->icount.p, sizeof(int32_t) * nf,
-                          cudaMemcpyDeviceToHost, st));
-    GS_CK(cudaStreamSynchronize(st));
+    {
+      std::vector<int32_t> f0(nf + 1);
+      GS_CK(cudaMemcpyAsync(f0.data(), ctx->ifirst.p, sizeof(int32_t) * (nf + 1),
+                            cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaStreamSynchronize(st));
+      for (int64_t f = 0; f < nf; ++f) fcnt[f] = f0[f + 1] - f0[f];
+    }
     int64_t m = m0, live = nf;
     int iter = 0;
     const int ms_cap = resident_capacity(d);
@@ -1011,13 +1053,14 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       ctx->shape_box = b;
       ctx->shape_vol_frame = b.vol_frame;
     }
-    GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, m, out->labels, dev_out, rec, rb));
+    GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, iter == 0, out->labels, dev_out,
+                       rec, rb));
     GS_CK(cudaStreamSynchronize(st));
     if (getenv("GS_TRACE_LEVELS")) {
       std::vector<long long> tr(8 * 512);
       cudaMemcpy(tr.data(), ctx->dbg.p, 8 * 8 * 512, cudaMemcpyDeviceToHost);
       for (int l = 0; l < 512 && (tr[8 * l + 1] || tr[8 * l]); ++l)
-        fprintf(stderr, "level %3d bar %5lld upd %5lld rel %5lld width %3lld n %3lld e %3lld stage %5lld chain %5lld\n", l,
+        fprintf(stderr, "level %3d wait %5lld upd %5lld rel %5lld width %3lld n %3lld e %3lld stage %5lld chain %5lld\n", l,
                 tr[8 * l], tr[8 * l + 1], tr[8 * l + 2], tr[8 * l + 3], tr[8 * l + 4], tr[8 * l + 5],
                 tr[8 * l + 6], tr[8 * l + 7]);
     }
@@ -1033,7 +1076,7 @@ results:
     ctx->hist_m.assign(rec ? nf : 0, {});
     ctx->hist_d.assign(rec ? nf : 0, {});
   }
-  ctx->h_ffirst.assign(rb.ffirst, rb.ffirst + nf);
+  ctx->h_ffirst.assign(rb.fout, rb.fout + nf);
   ctx->h_k.assign(nf, 0);
   ctx->h_iters.assign(rb.fiters, rb.fiters + nf);
   ctx->h_conv.assign(rb.fconv, rb.fconv + nf);
@@ -1044,14 +1087,12 @@ results:
     out->k[f] = rb.fk[f];
     out->iterations[f] = rb.fiters[f];
     out->converged[f] = rb.fconv[f];
-    for (int t = g_iters[f]; t < rb.fiters[f]; ++t) {
-      const int64_t mt = rb.hm[(size_t)f * cfg->max_iter + t];
-      swept += mt;
-      if (rec) {
-        ctx->hist_m[f].push_back(mt);
+    swept += rb.fswept[f];
+    if (rec)
+      for (int t = g_iters[f]; t < rb.fiters[f]; ++t) {
+        ctx->hist_m[f].push_back(rb.hm[(size_t)f * cfg->max_iter + t]);
         ctx->hist_d[f].push_back(rb.hd[(size_t)f * cfg->max_iter + t]);
       }
-    }
   }
   ctx->k_total = ktot;
   ctx->nframes = nf;
@@ -1072,7 +1113,7 @@ results:
   s.ms_total = ms;
   cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
   s.ms_k_bin = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[8], ctx->ev[9]);
+  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
   s.ms_k_label = ms;
   cudaGetLastError();  // timing is best-effort diagnostics
   s.cells_swept = swept;

@@ -15,12 +15,19 @@ namespace gs {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// ---------------------------------------------------------------- K1: bounds
-// Per-block min/max of every coordinate; non-finite values set err bit 1.
+// ---------------------------------------------------------------- K1: bounds + box
+// Per-block min/max of every coordinate (non-finite values set err bit 1); the last block to
+// finish reduces the partials and writes the dense-grid geometry, so no host round trip and
+// no second launch sit between the bounds pass and binning.  err bit 32: key box larger than
+// the allocated grid (*need = cells required); bit 64: keys beyond the int64 key range.
+// *epoch is bumped once per run (it tags the compaction's look-back flags).
 template <int D, typename T>
-__global__ void __launch_bounds__(256) k_bounds(const T* __restrict__ pts, int64_t ntot,
-                                                double* __restrict__ bmin,
-                                                double* __restrict__ bmax, int* err) {
+__global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, int64_t ntot,
+                                                    double* __restrict__ bpart, double h, int F,
+                                                    int64_t n, int64_t nframes,
+                                                    int64_t cap_cells, GsBox* __restrict__ out,
+                                                    int* err, long long* need,
+                                                    unsigned* ticket, unsigned* epoch) {
   double mn[D], mx[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) {
@@ -40,6 +47,7 @@ __global__ void __launch_bounds__(256) k_bounds(const T* __restrict__ pts, int64
   }
   if (bad) atomicOr(err, 1);
   __shared__ double smn[8][D], smx[8][D];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int c = 0; c < D; ++c) {
@@ -54,6 +62,7 @@ __global__ void __launch_bounds__(256) k_bounds(const T* __restrict__ pts, int64
     }
   }
   __syncthreads();
+  const int nblk = gridDim.x;
   if (threadIdx.x < D) {
     int c = threadIdx.x;
     double a = INFINITY, b = -INFINITY;
@@ -61,9 +70,71 @@ __global__ void __launch_bounds__(256) k_bounds(const T* __restrict__ pts, int64
       a = fmin(a, smn[i][c]);
       b = fmax(b, smx[i][c]);
     }
-    bmin[blockIdx.x * D + c] = a;
-    bmax[blockIdx.x * D + c] = b;
+    bpart[blockIdx.x * D + c] = a;
+    bpart[(nblk + blockIdx.x) * D + c] = b;
   }
+  __threadfence();  // partials and error bits before the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (unsigned)nblk - 1u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last block: 32 lanes per dimension over the partials (L2 reads), shuffle reduction
+  __shared__ double bmn[D], bmx[D];
+  for (int c = w; c < D; c += blockDim.x >> 5) {
+    double a = INFINITY, z = -INFINITY;
+#pragma unroll 4
+    for (int k = lane; k < nblk; k += 32) {
+      a = fmin(a, __ldcg(&bpart[k * D + c]));
+      z = fmax(z, __ldcg(&bpart[(nblk + k) * D + c]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(kFull, a, o));
+      z = fmax(z, __shfl_xor_sync(kFull, z, o));
+    }
+    if (lane == 0) {
+      bmn[c] = a;
+      bmx[c] = z;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  GsBox b;
+  b.d = D;
+  b.F = F;
+  b.h = h;
+  b.inv_h = __drcp_rn(h);
+  b.scale = ldexp(1.0, F);
+  b.inv_scale = ldexp(1.0, -F);
+  b.n = n;
+  b.nframes = nframes;
+  double vol = 1.0;
+  bool badk = (atomicOr(err, 0) & 1) != 0;
+  for (int k = 0; k < GS_DMAX; ++k) b.kmin[k] = 0, b.ext[k] = 1, b.stride[k] = 0;
+  for (int k = 0; k < D && !badk; ++k) {
+    const double lo = floor(__ddiv_rn(bmn[k], h)), hi = floor(__ddiv_rn(bmx[k], h));
+    if (!(fabs(lo) < 4e15) || !(fabs(hi) < 4e15)) {
+      badk = true;
+      break;
+    }
+    b.kmin[k] = (int64_t)lo - GS_APRON;
+    b.ext[k] = (int64_t)hi - (int64_t)lo + 1 + 2 * GS_APRON;
+    vol *= (double)b.ext[k];
+  }
+  int64_t s = 1;
+  for (int k = D - 1; k >= 0; --k) {
+    b.stride[k] = s;
+    s *= b.ext[k];
+  }
+  b.vol_frame = s;
+  b.vol_total = s * nframes;
+  if (!badk && vol * (double)nframes > (double)cap_cells) {
+    atomicOr(err, 32);
+    *need = (vol * (double)nframes < 9e18) ? (long long)(vol * (double)nframes) : (1ll << 62);
+  }
+  if (badk && !(atomicOr(err, 0) & 1)) atomicOr(err, 64);  // keys beyond the int64 range
+  *out = b;
+  *epoch += 1u;
 }
 
 // ---------------------------------------------------------------- K2: binning
@@ -222,70 +293,6 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
   }
 }
 
-// ---------------------------------------------------------------- K1b: box on the device
-// Reduces k_bounds' per-block partials and writes the dense-grid geometry, so no host round
-// trip sits between the bounds pass and binning.  err bit 1: non-finite input (from
-// k_bounds); bit 32: key box larger than the allocated grid (*need = cells required).
-__global__ void k_box(const double* __restrict__ bpart, int nblk, int d, double h, int F,
-                      int64_t n, int64_t nframes, int64_t cap_cells, GsBox* __restrict__ out,
-                      int* err, long long* need) {
-  __shared__ double mn[GS_DMAX], mx[GS_DMAX];
-  // 32 lanes per dimension, strided over the partials, then a shuffle reduction
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int c = w; c < d; c += blockDim.x >> 5) {
-    double a = INFINITY, z = -INFINITY;
-    for (int k = lane; k < nblk; k += 32) {
-      a = fmin(a, bpart[k * d + c]);
-      z = fmax(z, bpart[(int64_t)nblk * d + k * d + c]);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      a = fmin(a, __shfl_xor_sync(kFull, a, o));
-      z = fmax(z, __shfl_xor_sync(kFull, z, o));
-    }
-    if (lane == 0) {
-      mn[c] = a;
-      mx[c] = z;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  GsBox b;
-  b.d = d;
-  b.F = F;
-  b.h = h;
-  b.inv_h = __drcp_rn(h);
-  b.scale = ldexp(1.0, F);
-  b.inv_scale = ldexp(1.0, -F);
-  b.n = n;
-  b.nframes = nframes;
-  double vol = 1.0;
-  bool bad = (*err & 1) != 0;
-  for (int k = 0; k < GS_DMAX; ++k) b.kmin[k] = 0, b.ext[k] = 1, b.stride[k] = 0;
-  for (int k = 0; k < d && !bad; ++k) {
-    const double lo = floor(__ddiv_rn(mn[k], h)), hi = floor(__ddiv_rn(mx[k], h));
-    if (!(fabs(lo) < 4e15) || !(fabs(hi) < 4e15)) {
-      bad = true;
-      break;
-    }
-    b.kmin[k] = (int64_t)lo - GS_APRON;
-    b.ext[k] = (int64_t)hi - (int64_t)lo + 1 + 2 * GS_APRON;
-    vol *= (double)b.ext[k];
-  }
-  int64_t s = 1;
-  for (int k = d - 1; k >= 0; --k) {
-    b.stride[k] = s;
-    s *= b.ext[k];
-  }
-  b.vol_frame = s;
-  b.vol_total = s * nframes;
-  if (!bad && vol * (double)nframes > (double)cap_cells) {
-    atomicOr(err, 32);
-    *need = (vol * (double)nframes < 9e18) ? (long long)(vol * (double)nframes) : (1ll << 62);
-  }
-  if (bad && !(*err & 1)) atomicOr(err, 64);  // key magnitude beyond the int64 key range
-  *out = b;
-}
-
 // ---------------------------------------------------------------- K3: compaction by scan
 // The dense grid is in lexicographic order, so scanning its occupancy yields the cell list
 // already sorted: no occupied list, no sort, no host round trip for m0.
@@ -318,80 +325,38 @@ __device__ __forceinline__ int block_excl_scan_256(int v, int* sh, int* total) {
   return excl;
 }
 
-__global__ void __launch_bounds__(256) k_occ_count(const GsBox* __restrict__ pb,
-                                                   const uint32_t* __restrict__ cnt,
-                                                   int* __restrict__ tile_cnt,
-                                                   const int* __restrict__ err) {
-  if (*err & (1 | 32 | 64)) return;
-  __shared__ int sh[8];
-  const int64_t V = pb->vol_total;
-  const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * kOccTile + (int64_t)threadIdx.x * kOccPer;
-    int c = 0;
-#pragma unroll
-    for (int k = 0; k < kOccPer; ++k) c += (base + k < V) && cnt[base + k] != 0u;
-    int total;
-    block_excl_scan_256(c, sh, &total);
-    if (threadIdx.x == 0) tile_cnt[t] = total;
-  }
+// Single pass (decoupled look-back): tiles are taken in ticket order; each publishes its
+// occupied-cell count, then sums its predecessors' counts (a warp reads 32 flags at a time)
+// until one that already carries its inclusive prefix.  Flags are tagged with the run epoch,
+// so the flag array is never cleared.  Per occupied cell: lex-ordered cell list, centroid from
+// the fixed-point sums, clean-grid restore (cnt = qs = 0), idx = slot; per frame: the first
+// cell index (ifirst[nframes] = m0).
+__device__ __forceinline__ unsigned long long occ_flag(unsigned epoch, unsigned st, unsigned v) {
+  return ((unsigned long long)epoch << 32) | ((unsigned long long)st << 30) | v;
 }
 
-// single block: tile counts -> exclusive tile offsets (in place); m0 = total
-__global__ void __launch_bounds__(1024) k_occ_scan(const GsBox* __restrict__ pb,
-                                                   int* __restrict__ tile, unsigned int* m0,
-                                                   const int* __restrict__ err) {
-  if (*err & (1 | 32 | 64)) return;
-  __shared__ int sh[32];
-  const int64_t V = pb->vol_total;
-  const int ntiles = (int)((V + kOccTile - 1) / kOccTile);
-  const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int chunk = (ntiles + T - 1) / T;
-  const int beg = min(ntiles, tid * chunk), end = min(ntiles, beg + chunk);
-  int local = 0;
-  for (int j = beg; j < end; ++j) local += tile[j];
-  int x = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sh[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < (T >> 5) ? sh[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, t, o);
-      if (lane >= o) t += y;
-    }
-    sh[lane] = t;
-  }
-  __syncthreads();
-  int run = x - local + (w > 0 ? sh[w - 1] : 0);
-  for (int j = beg; j < end; ++j) {
-    const int v = tile[j];
-    tile[j] = run;
-    run += v;
-  }
-  if (tid == 0) *m0 = (unsigned)sh[(T >> 5) - 1];
-}
-
-// per tile: occupied cells -> lex-ordered cell list; centroids from the fixed-point sums;
-// restores the clean-grid invariant (cnt = qs = 0) for what it consumes.
-__global__ void __launch_bounds__(256) k_occ_compact(
-    const GsBox* __restrict__ pb, const int* __restrict__ tile_off, uint32_t* __restrict__ cnt,
+__global__ void __launch_bounds__(256) k_occ(
+    const GsBox* __restrict__ pb, const unsigned* __restrict__ epoch_p,
+    unsigned long long* tflag, unsigned* ticket, unsigned* m0_out, uint32_t* __restrict__ cnt,
     unsigned long long* __restrict__ qs, uint32_t* __restrict__ ckey,
     uint32_t* __restrict__ ccnt, double* __restrict__ S, int32_t* __restrict__ idx,
-    int32_t* __restrict__ root, uint32_t* __restrict__ initkey, const int* __restrict__ err) {
+    int32_t* __restrict__ root, uint32_t* __restrict__ initkey, int32_t* __restrict__ ifirst,
+    const int* __restrict__ err) {
   if (*err & (1 | 32 | 64)) return;
   __shared__ int sh[8];
   __shared__ GsBox b;
+  __shared__ int s_tile, s_excl;
   if (threadIdx.x == 0) b = *pb;
+  const unsigned E = *epoch_p;
   __syncthreads();
-  const int64_t V = b.vol_total;
+  const int64_t V = b.vol_total, VF = b.vol_frame;
   const int64_t ntiles = (V + kOccTile - 1) / kOccTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    if (t >= ntiles) break;
     const int64_t base = t * kOccTile + (int64_t)threadIdx.x * kOccPer;
     uint32_t c8[kOccPer];
     int c = 0;
@@ -401,14 +366,62 @@ __global__ void __launch_bounds__(256) k_occ_compact(
       c += c8[k] != 0u;
     }
     int total;
-    int pos = tile_off[t] + block_excl_scan_256(c, sh, &total);
+    const int excl = block_excl_scan_256(c, sh, &total);
+    if (threadIdx.x < 32) {  // publish, then look back (warp-wide)
+      if (t == 0) {
+        if (lane == 0) {
+          atomicExch(&tflag[0], occ_flag(E, 2u, (unsigned)total));
+          s_excl = 0;
+        }
+      } else {
+        if (lane == 0) atomicExch(&tflag[t], occ_flag(E, 1u, (unsigned)total));
+        int prefix = 0;
+        int64_t hi = t - 1;  // flags [hi-31, hi] are examined per round
+        for (;;) {
+          const int64_t j = hi - lane;
+          unsigned long long fw = 0ull;
+          unsigned st = 3u;  // 3: beyond tile 0 (treated as an inclusive zero)
+          if (j >= 0) {
+            do {
+              fw = *(volatile unsigned long long*)&tflag[j];
+              st = ((unsigned)(fw >> 32) == E) ? (unsigned)(fw >> 30) & 3u : 0u;
+            } while (st == 0u);
+          }
+          // the nearest lane (lowest index = highest tile) holding an inclusive prefix
+          const unsigned incl = __ballot_sync(kFull, st >= 2u);
+          const int stop = incl ? __ffs(incl) - 1 : 32;
+          int v = (lane <= stop && st != 3u) ? (int)(fw & 0x3fffffffu) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+          prefix += v;
+          if (incl) break;
+          hi -= 32;
+        }
+        if (lane == 0) {
+          atomicExch(&tflag[t], occ_flag(E, 2u, (unsigned)(prefix + total)));
+          s_excl = prefix;
+        }
+      }
+    }
+    __syncthreads();
+    int pos = s_excl + excl;
+    if (t == ntiles - 1 && threadIdx.x == 0) {
+      *m0_out = (unsigned)(s_excl + total);
+      ifirst[b.nframes] = s_excl + total;
+    }
+    int64_t f = base / VF, r = base - f * VF;
 #pragma unroll
     for (int k = 0; k < kOccPer; ++k) {
-      if (c8[k] == 0u) continue;
       const int64_t L = base + k;
+      if (L < V && r == 0) ifirst[f] = pos;  // first cell index of frame f
+      if (++r == VF) {
+        r = 0;
+        ++f;
+      }
+      if (c8[k] == 0u) continue;
       for (int q = 0; q < b.d; ++q) {
-        const long long s = (long long)qs[L * b.d + q];
-        S[(int64_t)pos * b.d + q] = gs_fix_centroid(gs_key_of(b, L, q), s, c8[k], b.h, b.inv_scale);
+        const long long sq = (long long)qs[L * b.d + q];
+        S[(int64_t)pos * b.d + q] = gs_fix_centroid(gs_key_of(b, L, q), sq, c8[k], b.h, b.inv_scale);
         qs[L * b.d + q] = 0ull;
       }
       cnt[L] = 0u;
@@ -419,6 +432,7 @@ __global__ void __launch_bounds__(256) k_occ_compact(
       initkey[pos] = (uint32_t)L;
       ++pos;
     }
+    __syncthreads();  // s_tile / s_excl are rewritten by the next round
   }
 }
 

@@ -28,7 +28,7 @@
 namespace gs {
 
 struct ResidentArgs {
-  GsBox box;
+  const GsBox* pbox;  // the run's key box (device: the optimistic path never sees it on the host)
   int ms;          // shared-memory cell capacity (power of two)
   int pool_bytes;  // shared-memory bytes for neighbour records
   int max_iter;
@@ -36,14 +36,17 @@ struct ResidentArgs {
   const uint32_t* ckey;  // current cells (global, frame-major, lex order within a frame)
   const uint32_t* ccnt;
   const double* S;
-  const int32_t* ffirst;  // current cell range of each frame
-  const int32_t* fcount;
-  const int32_t* ifirst;  // initial cell range of each frame (root entries)
-  const int32_t* icount;
+  const int32_t* ffirst;  // first current cell of each frame
+  const int32_t* fcount;  // cells per frame, or null: ffirst[f + 1] - ffirst[f]
+  const int32_t* ifirst;  // initial cell range of each frame (root entries), nframes + 1
+  const uint32_t* initkey;  // initial cell -> its dense key (label table)
+  int32_t* lab;             // dense key of an initial cell -> frame-local final id
   int32_t* fdone;
   int32_t* fiters;
   int32_t* fconv;
   int32_t* fk;
+  int32_t* fout;    // first final cell of each frame (= ffirst[f])
+  int64_t* fswept;  // += active cells summed over this launch's iterations
   uint32_t* okey;  // final cells, written at the frame's current offset
   uint32_t* ocnt;
   double* oS;
@@ -57,17 +60,17 @@ struct ResidentArgs {
   // when it fits (sidx_bytes > 0), else the engine's global dense grid (int32, clean = -1)
   int32_t* gidx;
   int sidx_bytes;
-  // optimistic launch: if the largest frame (*fmax) exceeds ms, every CTA leaves the state
-  // untouched and raises *deferred; the host then takes the global path first
-  const int* fmax;
+  // optimistic launch: a frame with more than ms cells raises *deferred and its CTA leaves at
+  // once; the host then redoes the whole run on the synchronous path (global path first)
+  int deferrable;
   int* deferred;
   long long* trace;  // optional per-level timeline of frame 0's first iteration (diagnostic)
 };
 
 // shared-memory bytes per cell (excluding the index and neighbour-record pool)
 __host__ __device__ constexpr int resident_bytes_per_cell(int D) {
-  return 16 * D /*S0,S1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 8 /*1/den*/ +
-         4 /*flag*/ + 20 /*nbn, nbe, eoff, loff, par*/ + 4 /*tmp*/;
+  return 24 * D /*S0, Q = S1|P1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 8 /*1/den*/ +
+         4 /*flag*/ + 16 /*nbn, nbe, eoff, par*/ + 4 /*tmp*/;
 }
 
 // shared-memory bytes of the neighbour-offset table (int32 per offset) for dimension D
@@ -77,9 +80,8 @@ __host__ __device__ constexpr int resident_offs_bytes(int D) {
                 : 0;
 }
 
-// shared-memory bytes of the sweep's per-group term staging (K8 runs at most 256 threads)
-// (16 warps x D rows x 34 doubles: one padded staging row per coordinate per warp)
-__host__ __device__ constexpr int resident_stage_bytes(int D) { return 16 * D * 34 * 8; }
+// fixed shared-memory bytes besides the per-cell state: Q's zero row (+ one alignment row)
+__host__ __device__ constexpr int resident_fixed_bytes(int D) { return 16 * D; }
 
 // RN(a / b) from y = RN(1/b) (precomputed off the critical path): q0 = RN(a*y); the residual
 // a - b*q0 is exact in one FMA; RN(q0 + r*y) is the correctly rounded quotient (Markstein's
@@ -192,16 +194,22 @@ __device__ int rs_scan(int* a, int n, int* wtmp) {
 
 template <int D>
 __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
-  const GsBox& b = a.box;
+  __shared__ GsBox sbox;
   const int f = blockIdx.x;
   const int tid = threadIdx.x, T = blockDim.x;
-  if (a.fmax && *a.fmax > a.ms) {
-    if (f == 0 && tid == 0) *a.deferred = 1;
+  if (tid == 0) sbox = *a.pbox;
+  __syncthreads();
+  const GsBox& b = sbox;
+  // dense cell index of this frame: smem int16 table when the host reserved room for this
+  // box's frame volume, else the global grid (L2-resident)
+  const bool sdense = a.sidx_bytes >= 2 * b.vol_frame;
+  const int first = a.ffirst[f];
+  int m = a.fcount ? a.fcount[f] : a.ffirst[f + 1] - first;
+  if (a.deferrable && m > a.ms && !a.fdone[f]) {
+    if (tid == 0) atomicExch(a.deferred, 1);
     return;
   }
-  const int first = a.ffirst[f];
-  int m = a.fcount[f];
-  const int ifirst = a.ifirst[f], icnt = a.icount[f];
+  const int ifirst = a.ifirst[f], icnt = a.ifirst[f + 1] - ifirst;
   const int64_t fbase = (int64_t)f * b.vol_frame;
   int iters = a.fiters[f];
   int conv = a.fconv[f];
@@ -214,8 +222,13 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       a.ocnt[first + i] = a.ccnt[first + i];
       for (int c = 0; c < D; ++c)
         a.oS[(int64_t)(first + i) * D + c] = a.S[(int64_t)(first + i) * D + c];
+      a.gidx[a.ckey[first + i]] = -1;  // clean-grid invariant
     }
-    if (tid == 0) a.fk[f] = m;
+    for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.lab[a.initkey[c]] = a.root[c];
+    if (tid == 0) {
+      a.fk[f] = m;
+      a.fout[f] = first;
+    }
     return;
   }
 
@@ -224,7 +237,11 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   const int MS = a.ms;
   unsigned char* p = smem;
   double* S0 = (double*)p;          p += sizeof(double) * MS * D;
-  double* S1 = (double*)p;          p += sizeof(double) * MS * D;
+  // Q: rows [0, MS) the new centroids S1 (during the sweep: C'*S_old until a cell is updated),
+  // row MS zeros, rows [MS+1, 2MS+1) C'*S_new of updated cells
+  double* Q = (double*)p;           p += sizeof(double) * (2 * MS + 2) * D;
+  double* S1 = Q;
+  const int ZROW = MS, P1ROW = MS + 1;
   double* rden = (double*)p;        p += sizeof(double) * MS;
   uint64_t* sk = (uint64_t*)p;      p += sizeof(uint64_t) * MS;
   uint32_t* keyA = (uint32_t*)p;    p += 4 * MS;
@@ -236,17 +253,15 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   int* nbn = (int*)p;               p += 4 * MS;
   int* nbe = (int*)p;               p += 4 * MS;
   int* eoff = (int*)p;              p += 4 * MS;
-  int* loff = (int*)p;              p += 4 * MS;
   int* par = (int*)p;               p += 4 * MS;
   int* tmp = (int*)p;               p += 4 * MS;
   int16_t* sidx = (int16_t*)p;      p += a.sidx_bytes;
   int* offs = (int*)p;              p += resident_offs_bytes(D);
-  double* stage = (double*)p;       p += resident_stage_bytes(D);
   unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
-  __shared__ unsigned s_maxl;
-  __shared__ int s_dummy;
+  __shared__ int s_dummy[32];
+  int* levend = eoff;  // sweep: published frontier ends (+1), 0 = not yet
   volatile uint32_t* vflag = flag;
 
   uint32_t* key = keyA;
@@ -256,6 +271,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 
   for (int i = tid; i < m; i += T) {
     key[i] = (uint32_t)((int64_t)a.ckey[first + i] - fbase);
+    if (sdense) a.gidx[a.ckey[first + i]] = -1;  // the smem index takes over
     cnt[i] = a.ccnt[first + i];
     for (int c = 0; c < D; ++c) S0[i * D + c] = a.S[(int64_t)(first + i) * D + c];
     flag[i] = 0u;
@@ -289,7 +305,6 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   };
 
   // dense cell index of this frame: smem int16 table or the global grid (L2-resident)
-  const bool sdense = a.sidx_bytes > 0;
   int32_t* gidx = a.gidx + fbase;
   auto idx_get = [&](int64_t L) -> int { return sdense ? (int)sidx[L] : gidx[L]; };
   auto idx_put = [&](int64_t L, int v) {
@@ -299,12 +314,13 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       gidx[L] = v;
   };
   if (sdense)
-    for (int j = tid; j < (int)(a.sidx_bytes >> 1); j += T) sidx[j] = -1;
+    for (int j = tid; j < (int)b.vol_frame; j += T) sidx[j] = -1;
   __syncthreads();
   for (int i = tid; i < m; i += T) idx_put(key[i], i);
   __syncthreads();
 
   bool done = false;
+  int64_t swept = 0;
   long long t_prev = clock64();
   auto lap = [&](int ph) {
     if (a.prof && tid == 0) {
@@ -330,49 +346,40 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       }
       nbn[i] = n;
       nbe[i] = e;
-      eoff[i] = e;
-      loff[i] = n - e;
-      tmp[i] = n;
+      tmp[i] = (n + 3) & ~3;  // list length padded to whole 4-entry words
     }
     __syncthreads();
-    const int n_early = rs_scan(eoff, m, wtmp);
-    const int n_late = rs_scan(loff, m, wtmp);
     const int n_all = rs_scan(tmp, m, wtmp);
-    // fast: {slot, C'} per earlier neighbour + C'*S_old for self and later neighbours
-    // fast mode also keeps the slot of every later neighbour: the sweep's successor lists
-    const int fast_bytes = 8 * n_early + 8 * D * n_late + 2 * n_late;
-    const int mode = fast_bytes <= a.pool_bytes ? 0 : (2 * n_all <= a.pool_bytes ? 1 : 2);
-    uint64_t* erec = (uint64_t*)pool;
-    double* lprod = (double*)(pool + 8 * n_early);
-    uint16_t* lsucc = (uint16_t*)(pool + 8 * n_early + 8 * D * n_late);
+    // list mode: per cell the Q-row of every active neighbour in lex order (+ a slack word);
+    // inline mode when the lists do not fit (very dense high-d neighbourhoods)
+    const int mode = (2 * n_all + 8 <= a.pool_bytes) ? 1 : 2;
     uint16_t* lst = (uint16_t*)pool;
     for (int i = tid; i < m; i += T) {
       NbrIt it = nbr_begin();
-      int ne = 0, nl = 0, nn = 0;
+      int nn = 0;
       uint32_t s = 0;
       const int64_t Li = key[i];
+      uint16_t* li = lst + tmp[i];
       for (int t = 0; t < K; ++t) {
         const int j = idx_get(Li + it.at(t));
         it.step(b);
         if (j < 0) continue;
-        const uint32_t w = cnt[j];
-        s += w;
-        if (mode == 0) {
-          if (j < i) {
-            erec[eoff[i] + ne++] = ((uint64_t)w << 32) | (uint32_t)j;
-          } else {
-            lsucc[loff[i] + nl] = (uint16_t)j;
-            double* dst = lprod + (int64_t)(loff[i] + nl++) * D;
+        s += cnt[j];
+        if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+      }
+      if (mode == 1) {
+        for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
+        const double ci = (double)cnt[i];
 #pragma unroll
-            for (int c = 0; c < D; ++c) dst[c] = __dmul_rn((double)w, S0[j * D + c]);
-          }
-        } else if (mode == 1) {
-          lst[tmp[i] + nn++] = (uint16_t)j;
-        }
+        for (int c = 0; c < D; ++c)  // Q row i = C'*S_old until the cell is updated
+          Q[i * D + c] = nbn[i] <= 1 ? S0[i * D + c] : __dmul_rn(ci, S0[i * D + c]);
       }
       den[i] = s;
       rden[i] = __drcp_rn((double)s);  // for rs_div on the sweep's critical path
+      levend[i] = 0;
     }
+    if (tid < 4) lst[n_all + tid] = (uint16_t)ZROW;  // slack word read by the prefetch
+    for (int c = tid; c < D; c += T) Q[ZROW * D + c] = 0.0;
     if (tid == 0) {
       s_dmax = 0ull;
       if (a.mode_count) atomicAdd((unsigned long long*)&a.mode_count[mode], 1ull);
@@ -380,100 +387,21 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     __syncthreads();
     lap(0);
 
-    // ---- (2) the sweep.  The DAG of one sweep is static, so (a) every cell's level = longest
-    // path over lex-earlier active neighbours is found by an integer relaxation, (b) cells are
-    // bucketed by level, and (c) levels run in order separated by barriers: when a cell is
-    // updated all its earlier neighbours are final, so the update is a straight-line sum in lex
-    // order with no polling.  Same operands, same order: bit-identical to the serial sweep.
-    // ---- (2) the sweep: ONE warp, one lane per cell, Kahn frontier over the sweep's DAG.
-    // A cell enters the frontier when its last lex-earlier active neighbour has been updated;
-    // a frontier (one DAG level) is updated lane-parallel with every operand final, then
-    // releases its lex-later neighbours.  No block barrier is involved (only __syncwarp: the
-    // measured multi-warp version spent ~2K cycles per level in barriers and warp divergence).
-    // Each lane sums its cell's terms in lex order over exactly the serial sweep's operands;
-    // padding terms are 0*0 = +0, and adding +0.0 is an exact identity (the running sum is
-    // never -0.0), so the result is bit-identical.
-    constexpr int CH = D <= 3 ? 4 : 2;  // terms loaded ahead of their adds
-    // Branch-free: every load is unconditional (indices clamped into the cell's own range) and
-    // padding terms get weight 0, so loads never wait behind per-term branches.
-    auto lane_update = [&](int i, int n, int e) {
-      if (n <= 1) {  // no active neighbour but itself: centroid kept bit-for-bit (pin P3)
-#pragma unroll
-        for (int c = 0; c < D; ++c) S1[i * D + c] = S0[i * D + c];
-        return;
-      }
-      double num[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) num[c] = 0.0;
-      if (mode == 0) {
-        const uint64_t* er = erec + eoff[i];
-        for (int t0 = 0; t0 < e; t0 += CH) {  // earlier neighbours: NEW centroids
-          uint64_t r[CH];
-          double v[CH][D];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) r[u] = er[min(t0 + u, e - 1)];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const uint32_t j = (uint32_t)r[u];
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = S1[j * D + c];
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const double w = (t0 + u < e) ? (double)(uint32_t)(r[u] >> 32) : 0.0;
-#pragma unroll
-            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w, v[u][c]));
-          }
-        }
-        const double* lp = lprod + (int64_t)loff[i] * D;
-        const int nl = n - e;  // >= 1: the cell itself
-        for (int t0 = 0; t0 < nl; t0 += CH) {  // itself + later neighbours: C'*S_old
-          double v[CH][D];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const int q = min(t0 + u, nl - 1);
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const double x = lp[q * D + c];
-              v[u][c] = (t0 + u < nl) ? x : 0.0;
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-#pragma unroll
-            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
-        }
-      } else {
-        const uint16_t* ls = lst + tmp[i];
-        for (int t0 = 0; t0 < n; t0 += CH) {
-          int jj[CH];
-          double v[CH][D], w[CH];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) jj[u] = (int)ls[min(t0 + u, n - 1)];
-#pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const double* src = (t0 + u < e) ? S1 : S0;
-            const double cw = (double)cnt[jj[u]];
-            w[u] = (t0 + u < n) ? cw : 0.0;
-#pragma unroll
-            for (int c = 0; c < D; ++c) v[u][c] = src[jj[u] * D + c];
-          }
-#pragma unroll
-          for (int u = 0; u < CH; ++u)
-#pragma unroll
-            for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w[u], v[u][c]));
-        }
-      }
-      const double dd = (double)den[i];
-#pragma unroll
-      for (int c = 0; c < D; ++c) S1[i * D + c] = rs_div(num[c], dd, rden[i]);
-    };
-    if (mode != 2) {
-      if (tid < 32) {
-        const int lane = tid;
-        const unsigned lt = (1u << lane) - 1u;
-        int* pend = (int*)flag;  // lex-earlier active neighbours not yet updated
-        int* queue = (int*)sk;   // frontier after frontier
+    // ---- (2) the sweep: Kahn frontiers over the sweep's DAG (a cell waits for its lex-earlier
+    // active neighbours only).  The frontier schedule depends on the graph, not on the values,
+    // so warp 1 computes it (pending counts, successor release, one published level end per
+    // frontier) while warp 0 consumes it: one lane per cell, every operand of a frontier's cells
+    // final when the level end is published.  Each lane sums its cell's terms in lex order over
+    // exactly the serial sweep's operands, read as Q rows: C'*S_new of an earlier neighbour
+    // (P1, written by its updater), C'*S_old of itself / a later neighbour (P0, in place until
+    // that cell is updated -- all its readers precede it), +0.0 for padding (an exact identity:
+    // the running sum is never -0.0).  Bit-identical to the serial sweep.
+    if (mode == 1) {
+      const int warp = tid >> 5, lane = tid & 31;
+      const unsigned lt = (1u << lane) - 1u;
+      int* queue = (int*)sk;  // frontier after frontier
+      if (warp == 1) {
+        int* pend = (int*)flag;  // lex-earlier active neighbours not yet released
         int qtail = 0;
         for (int base = 0; base < m; base += 32) {
           const int i = base + lane;
@@ -483,36 +411,34 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
           if (ready) queue[qtail + __popc(mk & lt)] = i;
           qtail += __popc(mk);
         }
-        __syncwarp();
         constexpr int RB = 8;  // successor releases issued together
-        int qhead = 0, qtrace = 0;
+        int qhead = 0, lev = 0;
         while (qhead < qtail) {
           const int lev_end = qtail;
-          long long tt0 = 0, tt1 = 0;
-          const bool trace = a.trace && f == 0 && lane == 0 && iters == 0;
-          if (trace) tt0 = clock64();
+          __syncwarp();  // the frontier's queue entries are written
+          if (lane == 0) {
+            __threadfence_block();
+            rs_st_release((uint32_t*)&levend[lev], (uint32_t)lev_end + 1u);
+          }
+          ++lev;
           for (int base = qhead; base < lev_end; base += 32) {
             const int k = base + lane;
             const bool act = k < lev_end;
             const int i = act ? queue[k] : 0;
-            const int n = act ? nbn[i] : 0, e = act ? nbe[i] : 0;
-            if (act) lane_update(i, n, e);
-            if (trace && base == qhead) tt1 = clock64();
-            // release the lex-later neighbours; each batch's atomics are independent
-            const int ns = act ? n - e - 1 : 0;
-            const uint16_t* sl = mode == 0 ? lsucc + loff[i] + 1 : lst + tmp[i] + e + 1;
-            const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)max(ns, 0));
+            const int e = nbe[i];
+            const int ns = act ? nbn[i] - e - 1 : 0;
+            const uint16_t* sl = lst + tmp[i] + e + 1;  // later neighbours (rows == slots)
+            const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)ns);
             for (int t0 = 0; t0 < mx; t0 += RB) {
               int jj[RB], old[RB];
 #pragma unroll
-              for (int u = 0; u < RB; ++u) {  // unconditional load (address kept in smem)
-                const int q = t0 + u < ns ? t0 + u : 0;
-                const int j = (int)sl[q];
+              for (int u = 0; u < RB; ++u) {  // unconditional loads (slack keeps them in the pool)
+                const int j = (int)sl[t0 + u < ns ? t0 + u : 0];
                 jj[u] = (t0 + u < ns) ? j : -1;
               }
 #pragma unroll
-              for (int u = 0; u < RB; ++u) {  // unconditional atomics: idle lanes add 0 to a dummy
-                int* tgt = jj[u] >= 0 ? &pend[jj[u]] : &s_dummy;
+              for (int u = 0; u < RB; ++u) {  // idle lanes add 0 to their own dummy word
+                int* tgt = jj[u] >= 0 ? &pend[jj[u]] : &s_dummy[lane];
                 old[u] = atomicAdd(tgt, jj[u] >= 0 ? -1 : 0);
               }
 #pragma unroll
@@ -524,19 +450,81 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
               }
             }
           }
-          __syncwarp();  // this level's centroids are visible to the next level's lanes
+          qhead = lev_end;
+        }
+      } else if (warp == 0) {
+        const bool trace = a.trace && f == 0 && lane == 0 && iters == 0;
+        int qhead = 0, lev = 0;
+        while (qhead < m) {
+          long long tt0 = 0, tt1 = 0;
+          if (trace) tt0 = clock64();
+          int v;
+          while ((v = (int)rs_ld_acquire((const uint32_t*)&levend[lev])) == 0) {
+          }
+          if (trace) tt1 = clock64();
+          const int lev_end = v - 1;
+          for (int base = qhead; base < lev_end; base += 32) {
+            const int k = base + lane;
+            if (k < lev_end) {
+              const int i = queue[k];
+              if (nbn[i] > 1) {  // else: no active neighbour but itself, Q row i = S_old (P3)
+                const uint2* ls = (const uint2*)(lst + tmp[i]);
+                const int nch = (nbn[i] + 3) >> 2;
+                const double ci = (double)cnt[i], dd = (double)den[i], y = rden[i];
+                double num[D], va[4][D];
+#pragma unroll
+                for (int c = 0; c < D; ++c) num[c] = 0.0;
+                auto fetch = [&](double (&v)[4][D], uint2 w) {
+                  const uint32_t r[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) v[u][c] = Q[r[u] * D + c];
+                };
+                auto fold = [&](const double (&v)[4][D]) {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
+                };
+                if constexpr (D <= 4) {
+                  double vb[4][D];
+                  fetch(va, ls[0]);
+                  for (int ch = 0; ch < nch; ch += 2) {  // next word in flight during the adds
+                    fetch(vb, ls[ch + 1]);
+                    fold(va);
+                    if (ch + 1 >= nch) break;
+                    fetch(va, ls[ch + 2]);
+                    fold(vb);
+                  }
+                } else {  // wide rows: one word at a time (register budget)
+                  for (int ch = 0; ch < nch; ++ch) {
+                    fetch(va, ls[ch]);
+                    fold(va);
+                  }
+                }
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                  const double s1 = rs_div(num[c], dd, y);
+                  Q[(P1ROW + i) * D + c] = __dmul_rn(ci, s1);
+                  Q[i * D + c] = s1;
+                }
+              }
+            }
+          }
+          __syncwarp();  // this level's rows are visible to the next level's lanes
           if (trace) {
-            long long* tr = a.trace + 8 * min(qtrace, 511);
-            tr[0] = 0;
-            tr[1] = tt1 - tt0;                 // the level's (first pass) updates
-            tr[2] = clock64() - tt1;           // releases
-            tr[3] = lev_end - qhead;           // level width
+            long long* tr = a.trace + 8 * min(lev, 511);
+            tr[0] = tt1 - tt0;         // waiting for the schedule
+            tr[1] = clock64() - tt1;   // the level's updates
+            tr[2] = 0;
+            tr[3] = lev_end - qhead;   // level width
             tr[4] = nbn[queue[qhead]];
             tr[5] = nbe[queue[qhead]];
             tr[6] = tr[7] = 0;
-            ++qtrace;
           }
           qhead = lev_end;
+          ++lev;
         }
       }
       __syncthreads();
@@ -698,9 +686,12 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       adj = hits > 0;
     }
     const int any_adj = __syncthreads_or(adj);
-    if (tid == 0 && a.record) {
-      a.hist_m[(int64_t)f * a.max_iter + iters] = m_before;
-      a.hist_d[(int64_t)f * a.max_iter + iters] = dmax;
+    if (tid == 0) {
+      swept += m_before;
+      if (a.record) {
+        a.hist_m[(int64_t)f * a.max_iter + iters] = m_before;
+        a.hist_d[(int64_t)f * a.max_iter + iters] = dmax;
+      }
     }
     lap(5);
     ++iters;
@@ -714,11 +705,14 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     for (int c = 0; c < D; ++c) a.oS[(int64_t)(first + i) * D + c] = S0[i * D + c];
     if (!sdense) gidx[key[i]] = -1;  // clean-grid invariant for the next run
   }
+  for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.lab[a.initkey[c]] = a.root[c];
   if (tid == 0) {
     a.fk[f] = m;
     a.fiters[f] = iters;
     a.fconv[f] = conv;
     a.fdone[f] = 1;
+    a.fout[f] = first;
+    a.fswept[f] += swept;
   }
 }
 
@@ -743,42 +737,6 @@ __global__ void k_labtab_local(int m0, const uint32_t* __restrict__ initkey,
                                const int32_t* __restrict__ root, int32_t* __restrict__ lab) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m0) lab[initkey[i]] = root[i];
-}
-
-// ---- variants whose cell count lives on the device (no host round trip): grid-stride
-__global__ void k_frame_ranges_dev(const unsigned* __restrict__ pm, const GsBox* __restrict__ pb,
-                                   const uint32_t* __restrict__ key, int32_t* __restrict__ first,
-                                   int32_t* __restrict__ end) {
-  const int m = (int)*pm;
-  const int64_t vf = pb->vol_frame;
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < m; g += gridDim.x * blockDim.x) {
-    const int64_t f = key[g] / vf;
-    if (g == 0 || (int64_t)(key[g - 1] / vf) != f) first[f] = g;
-    if (g == m - 1 || (int64_t)(key[g + 1] / vf) != f) end[f] = g + 1;
-  }
-}
-
-__global__ void k_frame_counts_dev(int64_t nf, const int32_t* __restrict__ first,
-                                   int32_t* __restrict__ count, int* __restrict__ fmax) {
-  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    count[f] -= first[f];
-    atomicMax(fmax, count[f]);
-  }
-}
-
-__global__ void k_labtab_dev(const unsigned* __restrict__ pm, const uint32_t* __restrict__ initkey,
-                             const int32_t* __restrict__ root, int32_t* __restrict__ lab) {
-  const int m0 = (int)*pm;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m0; i += gridDim.x * blockDim.x)
-    lab[initkey[i]] = root[i];
-}
-
-__global__ void k_idx_put_dev(const unsigned* __restrict__ pm, const uint32_t* __restrict__ key,
-                              int32_t* __restrict__ idx, int set) {
-  const int m = (int)*pm;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-    idx[key[i]] = set ? i : -1;
 }
 
 }  // namespace gs

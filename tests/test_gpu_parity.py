@@ -208,3 +208,29 @@ def test_graph_replay_pinned_buffers():
                     labd.data_ptr(), device_outputs=True)
         assert np.array_equal(labd.cpu().numpy(), o["labels"]), rep
     eng.close()
+
+
+@pytest.mark.gpu
+def test_graph_replay_new_data_same_shape():
+    """The cached graph is keyed on the shape, not on the data: a replay over points with a
+    different key box (shifted, wider, narrower) and a different cell count must still equal
+    the oracle bit for bit (the box, the frame ranges and the index layout come from the
+    device, never from the capture)."""
+    import torch
+    base = CF.generate("cfg2", scale=0.2)[0].astype(np.float64)
+    rng = np.random.default_rng(7)
+    variants = [base, base * 0.5 + 0.25, base * 1.7 - 0.3, base + 3.0,
+                rng.random(base.shape) * 0.3, base]
+    eng = G.Engine(0)
+    Xp = torch.empty(base.shape, dtype=torch.float64).pin_memory()
+    lab = torch.empty(base.shape[0], dtype=torch.int32).pin_memory()
+    for rep, X in enumerate(variants):
+        Xp.copy_(torch.from_numpy(np.ascontiguousarray(X)))
+        o = O.run(X, 0.08, 100, O.BUILD_FIXED)
+        k, it, cv = eng.run_raw(Xp.data_ptr(), X.shape[0], 3, G.GS_F64, 1, False,
+                                G.EngineConfig(0.08, 100), lab.data_ptr())
+        assert int(k[0]) == o["k"] and int(it[0]) == o["iterations"], rep
+        assert np.array_equal(lab.numpy(), o["labels"]), rep
+        cen = eng.centroids(0, int(k[0]), 3)
+        assert np.array_equal(_bits(cen), _bits(o["centroids"])), rep
+    eng.close()
