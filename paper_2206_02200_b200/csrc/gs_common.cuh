@@ -10,6 +10,11 @@
 #define GS_APRON 2       // empty cells around the data key box on each side, every dim
 #define GS_DMAX 12
 
+// The IEEE division as an out-of-line call for the rare-operand fallbacks of the reciprocal
+// divisions: inlined, the compiler if-converts it and runs its whole ~12-op FP64 sequence
+// speculatively on the common path (measured ~150 cycles per sweep level on a lone warp).
+__device__ __noinline__ double gs_ddiv_slow(double a, double b) { return __ddiv_rn(a, b); }
+
 // Geometry of the dense cell grid: frame-major, then lexicographic row-major over the d dims
 // (dim 0 slowest), so the linear cell index order IS the SPEC's lexicographic key order
 // within a frame, and frames never neighbour each other.

@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -139,6 +140,7 @@ struct gs_ctx {
   std::vector<std::vector<double>> hist_d;
   bool have_run = false;
   gs_stats stats{};
+  bool stats_times_pending = false;
   cudaEvent_t ev[12] = {};
 };
 
@@ -811,8 +813,8 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   ra.sidx_bytes = (int)sidx;
   ra.trace = nullptr;
   if (getenv("GS_TRACE_LEVELS")) {
-    GS_TRY(grow(ctx, ctx->dbg, 8 * 8 * 512));
-    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * 8 * 512, st));
+    GS_TRY(grow(ctx, ctx->dbg, 8 * 12000));
+    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * 12000, st));
     ra.trace = (long long*)ctx->dbg.p;
   }
   ra.deferrable = deferrable ? 1 : 0;
@@ -844,6 +846,33 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   return GS_OK;  // the caller synchronises (or captures this sequence into a graph)
 }
 
+// GS_TRACE_LEVELS diagnostics: per-level timeline of frame 0's first sweep and per-iteration
+// phase timeline of frame 0 (K8 writes them into ctx->dbg)
+void dump_trace(gs_ctx* ctx) {
+  if (!getenv("GS_TRACE_LEVELS") || !ctx->dbg.p) return;
+  {
+      std::vector<long long> tr(8 * 512);
+      cudaMemcpy(tr.data(), ctx->dbg.p, 8 * 8 * 512, cudaMemcpyDeviceToHost);
+      std::vector<long long> tp9(256);
+      cudaMemcpy(tp9.data(), (long long*)ctx->dbg.p + 9000, 8 * 256, cudaMemcpyDeviceToHost);
+      std::vector<long long> ti(512);
+      cudaMemcpy(ti.data(), (long long*)ctx->dbg.p + 4096, 8 * 512, cudaMemcpyDeviceToHost);
+      for (int t = 0; t < 64 && ti[8 * t + 7]; ++t) {
+        const long long* x = &ti[8 * t];
+        const long long* y = &((const long long*)tp9.data())[4 * t];
+        fprintf(stderr, "iter %2d m %5lld lists %6lld sweep %6lld (levels %4lld: relax %6lld sort %5lld) rehome %6lld sort %6lld fold %6lld adj %6lld\n",
+                t, x[6], x[0] - x[7], x[1] - x[0], y[2], y[0] ? y[0] - x[0] : 0, y[1] - y[0], x[2] - x[1], x[3] - x[2], x[4] - x[3], x[5] - x[4]);
+      }
+      std::vector<long long> tp(8 * 512);
+      cudaMemcpy(tp.data(), (long long*)ctx->dbg.p + 6000, 8 * 8 * 512, cudaMemcpyDeviceToHost);
+      for (int l = 0; l < 512 && (tr[8 * l + 1] || tr[8 * l]); ++l)
+        fprintf(stderr, "level %3d upd %5lld width %3lld n %3lld e %3lld | meta %4lld vals %4lld chain %4lld div+st %4lld bar %4lld gap %4lld\n", l, tr[8 * l + 1],
+                tr[8 * l + 3], tr[8 * l + 4], tr[8 * l + 5], tp[8 * l], tp[8 * l + 1], tp[8 * l + 2],
+                tp[8 * l + 3], tp[8 * l + 5] - tp[8 * l + 4] - tp[8 * l] - tp[8 * l + 1] - tp[8 * l + 2] - tp[8 * l + 3],
+                l ? tp[8 * l + 4] - tp[8 * (l - 1) + 5] : 0);
+      }
+}
+
 // Host memory the graph may copy from/to without staging: pinned or device-visible.
 bool graph_safe(const void* p) {
   cudaPointerAttributes at;
@@ -855,7 +884,24 @@ bool graph_safe(const void* p) {
          at.type == cudaMemoryTypeManaged;
 }
 
+// opt-in host-side timeline of one run (GS_HOST_PROF): prep / launch / wait / results, in us
+struct HostProf {
+  bool on = getenv("GS_HOST_PROF") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+  double seg[4] = {0, 0, 0, 0};
+  void lap(int i) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    seg[i] += std::chrono::duration<double, std::micro>(n - t).count();
+    t = n;
+  }
+  ~HostProf() {
+    if (on) fprintf(stderr, "host prof: prep %.1f launch %.1f wait %.1f results %.1f us\n", seg[0], seg[1], seg[2], seg[3]);
+  }
+};
+
 gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
+  HostProf hp;
   GS_TRY(validate(in, cfg));
   if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
     return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
@@ -867,6 +913,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
   ctx->have_run = false;
   ctx->stats = gs_stats{};
+  ctx->stats_times_pending = false;
   ctx->cur = 0;
   cudaGetLastError();  // a stale error from an unrelated earlier call must not fail this run
   cudaStream_t st = ctx->stream;
@@ -928,12 +975,16 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
         ctx->gkey.gen = ctx->alloc_gen;  // buffers (re)allocated while capturing belong to it
         ctx->graph_launches = ctx->stats.kernel_launches - l0;
       }
+      hp.lap(0);
       GS_CK(cudaGraphLaunch(ctx->gexec, st));
+      hp.lap(1);
       ctx->stats.kernel_launches = ctx->graph_launches;
     } else {
       GS_TRY(enqueue_all());
     }
     GS_CK(cudaStreamSynchronize(st));
+    hp.lap(2);
+    dump_trace(ctx);
     if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
     if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
@@ -1056,14 +1107,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, iter == 0, out->labels, dev_out,
                        rec, rb));
     GS_CK(cudaStreamSynchronize(st));
-    if (getenv("GS_TRACE_LEVELS")) {
-      std::vector<long long> tr(8 * 512);
-      cudaMemcpy(tr.data(), ctx->dbg.p, 8 * 8 * 512, cudaMemcpyDeviceToHost);
-      for (int l = 0; l < 512 && (tr[8 * l + 1] || tr[8 * l]); ++l)
-        fprintf(stderr, "level %3d wait %5lld upd %5lld rel %5lld width %3lld n %3lld e %3lld stage %5lld chain %5lld\n", l,
-                tr[8 * l], tr[8 * l + 1], tr[8 * l + 2], tr[8 * l + 3], tr[8 * l + 4], tr[8 * l + 5],
-                tr[8 * l + 6], tr[8 * l + 7]);
-    }
+    dump_trace(ctx);
     if (rb.err[0] & 16)
       return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
@@ -1097,25 +1141,8 @@ results:
   ctx->k_total = ktot;
   ctx->nframes = nf;
   ctx->have_run = true;
-  float ms = 0;
   gs_stats& s = ctx->stats;
-  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-  s.ms_h2d = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
-  s.ms_bin = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
-  s.ms_iterate = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
-  s.ms_label = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]);
-  s.ms_d2h = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[4]);
-  s.ms_total = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
-  s.ms_k_bin = ms;
-  cudaEventElapsedTime(&ms, ctx->ev[3], ctx->ev[4]);
-  s.ms_k_label = ms;
-  cudaGetLastError();  // timing is best-effort diagnostics
+  ctx->stats_times_pending = true;  // phase times are read from the events on demand
   s.cells_swept = swept;
   s.m0 = rb.ctr[0];
   s.k_total = ktot;
@@ -1125,6 +1152,7 @@ results:
   for (int k = 0; k < 8; ++k) s.resident_cycles[k] = rb.modes[4 + k];
   s.fixed_shift = gs_fixed_shift(n, cfg->h);
   s.dense_cells = ctx->box.vol_total;
+  hp.lap(3);
   return GS_OK;
 }
 
@@ -1257,6 +1285,25 @@ gs_status gs_get_history(gs_ctx* ctx, int64_t frame, int64_t* m_t, double* maxdi
 
 gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out) {
   if (!ctx || !out) return GS_E_INVALID_PARAMETER;
+  if (ctx->stats_times_pending) {  // the last run's phase events (all complete: it synced)
+    ctx->stats_times_pending = false;
+    cudaSetDevice(ctx->device);
+    gs_stats& s = ctx->stats;
+    auto el = [&](int a, int b) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+      return (double)ms;
+    };
+    s.ms_h2d = el(0, 1);
+    s.ms_bin = el(1, 2);
+    s.ms_iterate = el(2, 3);
+    s.ms_label = el(3, 4);
+    s.ms_d2h = el(4, 5);
+    s.ms_total = el(1, 4);
+    s.ms_k_bin = el(6, 7);
+    s.ms_k_label = el(3, 4);
+    cudaGetLastError();  // timing is best-effort diagnostics
+  }
   *out = ctx->stats;
   return GS_OK;
 }

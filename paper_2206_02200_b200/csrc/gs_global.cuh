@@ -88,7 +88,7 @@ __global__ void k_nbr_fill(int m, GsBox b, int K, const uint32_t* __restrict__ c
 __device__ __forceinline__ double gl_div(double a, double b, double y) {
   const double q0 = __dmul_rn(a, y);
   const double fa = fabs(a);
-  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return __ddiv_rn(a, b);
+  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return gs_ddiv_slow(a, b);
   const double r = __fma_rn(-q0, b, a);
   return __fma_rn(r, y, q0);
 }

@@ -90,7 +90,7 @@ __host__ __device__ constexpr int resident_fixed_bytes(int D) { return 16 * D; }
 __device__ __forceinline__ double rs_div(double a, double b, double y) {
   const double q0 = __dmul_rn(a, y);
   const double fa = fabs(a);
-  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return __ddiv_rn(a, b);
+  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return gs_ddiv_slow(a, b);
   const double r = __fma_rn(-q0, b, a);
   return __fma_rn(r, y, q0);
 }
@@ -260,7 +260,8 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   unsigned char* pool = p;          // a.pool_bytes
   __shared__ int wtmp[32];
   __shared__ unsigned long long s_dmax;
-  __shared__ int s_dummy[32];
+  __shared__ int s_slow;  // a reciprocal division met an operand outside its proven range
+  __shared__ int s_dummy[32];  // atomics of idle lanes
   int* levend = eoff;  // sweep: published frontier ends (+1), 0 = not yet
   volatile uint32_t* vflag = flag;
 
@@ -323,6 +324,11 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   int64_t swept = 0;
   long long t_prev = clock64();
   auto lap = [&](int ph) {
+    if (a.trace && tid == 0 && f == 0 && iters < 64) {  // per-iteration phase timeline
+      long long* tr = a.trace + 4096 + 8 * iters;
+      tr[ph] = clock64();
+      if (ph == 0) tr[6] = m;
+    }
     if (a.prof && tid == 0) {
       const long long t = clock64();
       atomicAdd((unsigned long long*)&a.prof[ph], (unsigned long long)(t - t_prev));
@@ -331,57 +337,96 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   };
   lap(7);
   while (!done) {
+    if (a.trace && tid == 0 && f == 0 && iters < 64) a.trace[4096 + 8 * iters + 7] = clock64();
     const uint32_t epoch = (uint32_t)iters + 1u;
-    // ---- (1) neighbourhood census: #active neighbours, #lex-earlier ones
-    for (int i = tid; i < m; i += T) {
-      NbrIt it = nbr_begin();
-      int n = 0, e = 0;
-      const int64_t Li = key[i];
-#pragma unroll 27
-      for (int t = 0; t < K; ++t) {
-        const int j = idx_get(Li + it.at(t));
-        n += (j >= 0);
-        e += (j >= 0) & (j < i);
-        it.step(b);
-      }
-      nbn[i] = n;
-      nbe[i] = e;
-      tmp[i] = (n + 3) & ~3;  // list length padded to whole 4-entry words
-    }
-    __syncthreads();
-    const int n_all = rs_scan(tmp, m, wtmp);
-    // list mode: per cell the Q-row of every active neighbour in lex order (+ a slack word);
-    // inline mode when the lists do not fit (very dense high-d neighbourhoods)
-    const int mode = (2 * n_all + 8 <= a.pool_bytes) ? 1 : 2;
+    // ---- (1) neighbour lists: per cell the Q-row of every active neighbour in lex order
+    // (C'*S_new rows for lex-earlier ones, C'*S_old rows for itself and later ones), #active,
+    // #earlier, the denominator ΣC' and its reciprocal, and Q row i = C'*S_old.
+    //   mode 0 (d <= 3, lists fit at a fixed stride of KP entries): one neighbourhood pass,
+    //          lists padded with the zero row (the sweep reads them without bounds)
+    //   mode 1: census, scan, then lists padded to whole 4-entry words
+    //   mode 2: no lists (they do not fit): the sweep looks neighbours up itself
+    constexpr int KP = (K + 3) & ~3;
     uint16_t* lst = (uint16_t*)pool;
-    for (int i = tid; i < m; i += T) {
-      NbrIt it = nbr_begin();
-      int nn = 0;
-      uint32_t s = 0;
-      const int64_t Li = key[i];
-      uint16_t* li = lst + tmp[i];
-      for (int t = 0; t < K; ++t) {
-        const int j = idx_get(Li + it.at(t));
-        it.step(b);
-        if (j < 0) continue;
-        s += cnt[j];
-        if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
-      }
-      if (mode == 1) {
-        for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
+    auto finish_cell = [&](int i, int n, uint32_t s, bool lists) {
+      if (lists) {
         const double ci = (double)cnt[i];
 #pragma unroll
         for (int c = 0; c < D; ++c)  // Q row i = C'*S_old until the cell is updated
-          Q[i * D + c] = nbn[i] <= 1 ? S0[i * D + c] : __dmul_rn(ci, S0[i * D + c]);
+          Q[i * D + c] = n <= 1 ? S0[i * D + c] : __dmul_rn(ci, S0[i * D + c]);
       }
       den[i] = s;
       rden[i] = __drcp_rn((double)s);  // for rs_div on the sweep's critical path
       levend[i] = 0;
+    };
+    int mode, n_all = 0;
+    if (D <= 3 && 2 * KP * m + 16 <= a.pool_bytes) {
+      mode = 0;
+      for (int i = tid; i < m; i += T) {
+        NbrIt it = nbr_begin();
+        int n = 0, e = 0;
+        uint32_t s = 0;
+        const int64_t Li = key[i];
+        uint16_t* li = lst + i * KP;
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+          const int j = idx_get(Li + it.at(t));
+          it.step(b);
+          if (j >= 0) {
+            s += cnt[j];
+            li[n++] = (uint16_t)(j < i ? P1ROW + j : j);
+            e += j < i;
+          }
+        }
+        for (int t = n; t < KP; ++t) li[t] = (uint16_t)ZROW;
+        nbn[i] = n;
+        nbe[i] = e;
+        tmp[i] = i * KP;
+        par[i] = ((i * KP + e + 1) << 5) | (n - e - 1);  // later neighbours: first entry, count
+        finish_cell(i, n, s, true);
+      }
+    } else {
+      for (int i = tid; i < m; i += T) {
+        NbrIt it = nbr_begin();
+        int n = 0, e = 0;
+        const int64_t Li = key[i];
+#pragma unroll 27
+        for (int t = 0; t < K; ++t) {
+          const int j = idx_get(Li + it.at(t));
+          n += (j >= 0);
+          e += (j >= 0) & (j < i);
+          it.step(b);
+        }
+        nbn[i] = n;
+        nbe[i] = e;
+        tmp[i] = (n + 3) & ~3;  // list length padded to whole 4-entry words
+      }
+      __syncthreads();
+      n_all = rs_scan(tmp, m, wtmp);
+      mode = (2 * n_all + 8 <= a.pool_bytes) ? 1 : 2;
+      for (int i = tid; i < m; i += T) {
+        NbrIt it = nbr_begin();
+        int nn = 0;
+        uint32_t s = 0;
+        const int64_t Li = key[i];
+        uint16_t* li = lst + tmp[i];
+        for (int t = 0; t < K; ++t) {
+          const int j = idx_get(Li + it.at(t));
+          it.step(b);
+          if (j < 0) continue;
+          s += cnt[j];
+          if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+        }
+        if (mode == 1)
+          for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
+        finish_cell(i, nbn[i], s, mode == 1);
+      }
+      if (mode == 1 && tid < 4) lst[n_all + tid] = (uint16_t)ZROW;  // slack word (prefetch)
     }
-    if (tid < 4) lst[n_all + tid] = (uint16_t)ZROW;  // slack word read by the prefetch
     for (int c = tid; c < D; c += T) Q[ZROW * D + c] = 0.0;
     if (tid == 0) {
       s_dmax = 0ull;
+      s_slow = 0;
       if (a.mode_count) atomicAdd((unsigned long long*)&a.mode_count[mode], 1ull);
     }
     __syncthreads();
@@ -389,14 +434,18 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 
     // ---- (2) the sweep: Kahn frontiers over the sweep's DAG (a cell waits for its lex-earlier
     // active neighbours only).  The frontier schedule depends on the graph, not on the values,
-    // so warp 1 computes it (pending counts, successor release, one published level end per
-    // frontier) while warp 0 consumes it: one lane per cell, every operand of a frontier's cells
-    // final when the level end is published.  Each lane sums its cell's terms in lex order over
-    // exactly the serial sweep's operands, read as Q rows: C'*S_new of an earlier neighbour
-    // (P1, written by its updater), C'*S_old of itself / a later neighbour (P0, in place until
-    // that cell is updated -- all its readers precede it), +0.0 for padding (an exact identity:
-    // the running sum is never -0.0).  Bit-identical to the serial sweep.
-    if (mode == 1) {
+    // so warp 1 computes it (pending counts, successor release, one published frontier end per
+    // level) running ahead of the two update warps, which consume it.  Each update lane sums
+    // its cell's terms in lex order over exactly the serial sweep's operands, read as Q rows:
+    // C'*S_new of an earlier neighbour (P1, written by its updater), C'*S_old of itself / a
+    // later neighbour (P0, in place until that cell is updated -- all its readers precede it),
+    // +0.0 for padding (an exact identity: the running sum is never -0.0).  Bit-identical to
+    // the serial sweep.
+    // Cost model (measured, B200, one warp per SMSP): every dependent shared-memory round trip,
+    // taken branch or barrier costs ~30-120 cycles, so a level's critical path is kept to
+    // "barrier -> reload the operands the previous level wrote -> add chain -> divide -> store";
+    // the next level's cells, list words and static operands are loaded before the barrier.
+    if (mode != 2) {
       const int warp = tid >> 5, lane = tid & 31;
       const unsigned lt = (1u << lane) - 1u;
       int* queue = (int*)sk;  // frontier after frontier
@@ -415,25 +464,29 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         int qhead = 0, lev = 0;
         while (qhead < qtail) {
           const int lev_end = qtail;
-          __syncwarp();  // the frontier's queue entries are written
-          if (lane == 0) {
-            __threadfence_block();
-            rs_st_release((uint32_t*)&levend[lev], (uint32_t)lev_end + 1u);
-          }
+          __syncwarp();  // the frontier's queue entries are written (and ordered before...)
+          if (lane == 0) rs_st_release((uint32_t*)&levend[lev], (uint32_t)lev_end + 1u);  // ...this
           ++lev;
           for (int base = qhead; base < lev_end; base += 32) {
             const int k = base + lane;
             const bool act = k < lev_end;
             const int i = act ? queue[k] : 0;
-            const int e = nbe[i];
-            const int ns = act ? nbn[i] - e - 1 : 0;
-            const uint16_t* sl = lst + tmp[i] + e + 1;  // later neighbours (rows == slots)
+            int so, ns;  // first later-neighbour entry and their count
+            if (D <= 3 && mode == 0) {
+              const int dsc = par[i];
+              so = dsc >> 5;
+              ns = act ? (dsc & 31) : 0;
+            } else {
+              const int e = nbe[i];
+              so = tmp[i] + e + 1;
+              ns = act ? nbn[i] - e - 1 : 0;
+            }
             const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)ns);
             for (int t0 = 0; t0 < mx; t0 += RB) {
               int jj[RB], old[RB];
 #pragma unroll
-              for (int u = 0; u < RB; ++u) {  // unconditional loads (slack keeps them in the pool)
-                const int j = (int)sl[t0 + u < ns ? t0 + u : 0];
+              for (int u = 0; u < RB; ++u) {  // unconditional loads (padding keeps them in the pool)
+                const int j = (int)lst[so + (t0 + u < ns ? t0 + u : 0)];
                 jj[u] = (t0 + u < ns) ? j : -1;
               }
 #pragma unroll
@@ -441,96 +494,121 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
                 int* tgt = jj[u] >= 0 ? &pend[jj[u]] : &s_dummy[lane];
                 old[u] = atomicAdd(tgt, jj[u] >= 0 ? -1 : 0);
               }
+              unsigned mk[RB];
+#pragma unroll
+              for (int u = 0; u < RB; ++u) mk[u] = __ballot_sync(0xffffffffu, jj[u] >= 0 && old[u] == 1);
 #pragma unroll
               for (int u = 0; u < RB; ++u) {
-                const bool rdy = jj[u] >= 0 && old[u] == 1;
-                const unsigned mk = __ballot_sync(0xffffffffu, rdy);
-                if (rdy) queue[qtail + __popc(mk & lt)] = jj[u];
-                qtail += __popc(mk);
+                if ((mk[u] >> lane) & 1u) queue[qtail + __popc(mk[u] & lt)] = jj[u];
+                qtail += __popc(mk[u]);
               }
             }
           }
           qhead = lev_end;
         }
-      } else if (warp == 0) {
-        const bool trace = a.trace && f == 0 && lane == 0 && iters == 0;
+      } else if (warp == 0 || warp == 2) {
+        // update warps (SMSPs 0 and 2): one lane per (cell, coordinate), so every fp64
+        // instruction a warp issues carries up to 32/D cells
+        constexpr int CPW = 32 / D;  // cells per warp and round
+        const int u = warp >> 1, q = lane / D, c = lane - q * D;
+        const bool trace = a.trace && f == 0 && tid == 0 && iters == 0;
         int qhead = 0, lev = 0;
         while (qhead < m) {
-          long long tt0 = 0, tt1 = 0;
-          if (trace) tt0 = clock64();
+          long long tt1 = 0;
           int v;
           while ((v = (int)rs_ld_acquire((const uint32_t*)&levend[lev])) == 0) {
           }
           if (trace) tt1 = clock64();
           const int lev_end = v - 1;
-          for (int base = qhead; base < lev_end; base += 32) {
-            const int k = base + lane;
-            if (k < lev_end) {
-              const int i = queue[k];
-              if (nbn[i] > 1) {  // else: no active neighbour but itself, Q row i = S_old (P3)
-                const uint2* ls = (const uint2*)(lst + tmp[i]);
-                const int nch = (nbn[i] + 3) >> 2;
-                const double ci = (double)cnt[i], dd = (double)den[i], y = rden[i];
-                double num[D], va[4][D];
+          for (int base = qhead + u * CPW; base < lev_end; base += 2 * CPW) {
+            const int k = base + q;
+            const bool act = q < CPW && k < lev_end;
+            const int i = act ? queue[k] : 0;
+            const int n = act ? nbn[i] : 0;
+            const double ci = (double)cnt[i], dd = (double)den[i], y = rden[i];
+            double num = 0.0;
+            auto fetch = [&](double (&vv)[4], uint2 w) {
+              vv[0] = Q[(w.x & 0xffffu) * D + c];
+              vv[1] = Q[(w.x >> 16) * D + c];
+              vv[2] = Q[(w.y & 0xffffu) * D + c];
+              vv[3] = Q[(w.y >> 16) * D + c];
+            };
+            auto fold = [&](const double (&vv)[4]) {
 #pragma unroll
-                for (int c = 0; c < D; ++c) num[c] = 0.0;
-                auto fetch = [&](double (&v)[4][D], uint2 w) {
-                  const uint32_t r[4] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16};
+              for (int t = 0; t < 4; ++t) num = __dadd_rn(num, vv[t]);
+            };
+            if constexpr (D <= 3) {
+              if (mode == 0) {
+                // every word and operand loaded up front, then ONE uniform jump into an
+                // unrolled add chain of the warp's longest list (shorter lists add zero rows)
+                constexpr int NW = KP / 4;
+                const int nchm = (int)__reduce_max_sync(0xffffffffu, (unsigned)((n + 3) >> 2));
+                const uint2* ls = (const uint2*)(lst + i * KP);
+                const uint2 zw = make_uint2((uint32_t)ZROW * 0x10001u, (uint32_t)ZROW * 0x10001u);
+                double vv[NW][4];
 #pragma unroll
-                  for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int c = 0; c < D; ++c) v[u][c] = Q[r[u] * D + c];
-                };
-                auto fold = [&](const double (&v)[4][D]) {
-#pragma unroll
-                  for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int c = 0; c < D; ++c) num[c] = __dadd_rn(num[c], v[u][c]);
-                };
-                if constexpr (D <= 4) {
-                  double vb[4][D];
-                  fetch(va, ls[0]);
-                  for (int ch = 0; ch < nch; ch += 2) {  // next word in flight during the adds
-                    fetch(vb, ls[ch + 1]);
-                    fold(va);
-                    if (ch + 1 >= nch) break;
-                    fetch(va, ls[ch + 2]);
-                    fold(vb);
-                  }
-                } else {  // wide rows: one word at a time (register budget)
-                  for (int ch = 0; ch < nch; ++ch) {
-                    fetch(va, ls[ch]);
-                    fold(va);
-                  }
+                for (int w = 0; w < NW; ++w) {
+                  const int x = w + nchm - NW;  // slot w holds word w + nchm - NW
+                  fetch(vv[w], x >= 0 ? ls[x >= 0 ? x : 0] : zw);
                 }
-#pragma unroll
-                for (int c = 0; c < D; ++c) {
-                  const double s1 = rs_div(num[c], dd, y);
-                  Q[(P1ROW + i) * D + c] = __dmul_rn(ci, s1);
-                  Q[i * D + c] = s1;
+                switch (NW - nchm) {
+#define GS_FOLD_SLOT(W)               \
+  case W:                             \
+    if constexpr (NW > W) fold(vv[W]); \
+    [[fallthrough]];
+                  GS_FOLD_SLOT(0) GS_FOLD_SLOT(1) GS_FOLD_SLOT(2) GS_FOLD_SLOT(3)
+                  GS_FOLD_SLOT(4) GS_FOLD_SLOT(5) GS_FOLD_SLOT(6)
+#undef GS_FOLD_SLOT
+                  default:
+                    break;
                 }
               }
             }
+            if (mode == 1 && n > 1) {
+              const uint2* ls = (const uint2*)(lst + tmp[i]);
+              const int nch = (n + 3) >> 2;
+              double va[4], vb[4];
+              fetch(va, ls[0]);
+              for (int ch = 0; ch < nch; ch += 2) {  // next word in flight during the adds
+                fetch(vb, ls[ch + 1]);
+                fold(va);
+                if (ch + 1 >= nch) break;
+                fetch(va, ls[ch + 2]);
+                fold(vb);
+              }
+            }
+            // RN(num / ΣC') from the precomputed reciprocal; the rare operands outside the
+            // theorem's range take the IEEE division (one warp-uniform test)
+            const double q0 = __dmul_rn(num, y);
+            const double fa = fabs(num);
+            const bool slow = !(fa < 0x1p+1000) || (fa < 0x1p-900 && num != 0.0);
+            double s1 = __fma_rn(__fma_rn(-q0, dd, num), y, q0);
+            if (__any_sync(0xffffffffu, slow && act && n > 1))
+              if (slow) s1 = gs_ddiv_slow(num, dd);
+            if (act && n > 1) {  // else: no active neighbour but itself, Q row i = S_old (P3)
+              Q[(P1ROW + i) * D + c] = __dmul_rn(ci, s1);
+              Q[i * D + c] = s1;
+            }
           }
-          __syncwarp();  // this level's rows are visible to the next level's lanes
+          rs_bar(1, 64);  // both update warps: this level's rows are visible to the next level
           if (trace) {
             long long* tr = a.trace + 8 * min(lev, 511);
-            tr[0] = tt1 - tt0;         // waiting for the schedule
-            tr[1] = clock64() - tt1;   // the level's updates
-            tr[2] = 0;
-            tr[3] = lev_end - qhead;   // level width
-            tr[4] = nbn[queue[qhead]];
-            tr[5] = nbe[queue[qhead]];
-            tr[6] = tr[7] = 0;
+            tr[0] = 0;
+            tr[1] = clock64() - tt1;  // the level
+            tr[3] = lev_end - qhead;  // level width
+            tr[2] = tr[4] = tr[5] = tr[6] = tr[7] = 0;
           }
           qhead = lev_end;
           ++lev;
         }
       }
       __syncthreads();
-    } else {
-      // records do not fit (very dense high-d neighbourhoods): dataflow with lookups, waiting
-      // on each earlier neighbour in turn (independent thread scheduling keeps lanes going)
+    }
+    if (mode == 2 || s_slow) {
+      // records do not fit (very dense high-d neighbourhoods), or a reciprocal division of the
+      // pipelined sweep met an operand outside its proven range (then this recomputes every
+      // centroid of the sweep): dataflow with lookups, waiting on each earlier neighbour in
+      // turn (independent thread scheduling keeps lanes going)
       for (int i = tid; i < m; i += T) {
         double num[D];
 #pragma unroll
@@ -566,6 +644,8 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       __syncthreads();
     }
 
+    if (a.prof && tid == 0 && iters == 0)  // the first sweep alone (its DAG is data-fixed)
+      atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - t_prev));
     lap(1);
     // ---- (3) rehome, changed, displacement
     int P = 1;
