@@ -44,7 +44,7 @@ __device__ __forceinline__ int64_t gs_grid_coord(double x, double h, double inv_
   double fl = floor(q);
   double fr = __dsub_rn(q, fl);
   double tol = 0x1p-50 * fmax(fabs(q), 1.0);
-  if (!(fr >= tol && fr <= 1.0 - tol)) fl = floor(__ddiv_rn(x, h));
+  if (!(fr >= tol && fr <= 1.0 - tol)) fl = floor(gs_ddiv_slow(x, h));
   return (int64_t)fl;
 }
 

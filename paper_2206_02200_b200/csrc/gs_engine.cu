@@ -418,7 +418,7 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = true;
     }
-    const unsigned grid = blocks_for(ntot, 4096, ctx->num_sms);
+    const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
     if (dtype == GS_F32)
       gs::k_bin_priv<D, float><<<grid, 1024, smem, ctx->stream>>>(
           (const float*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),

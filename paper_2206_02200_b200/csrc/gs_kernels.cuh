@@ -181,6 +181,19 @@ __global__ void __launch_bounds__(256) k_bin(const T* __restrict__ pts, int64_t 
 // accumulators (count + D int64 fixed-point sums); a point whose probe run finds no room falls
 // back to global atomics.  The table is flushed once per CTA.  int64 sums are associative, so
 // the result is bit-identical to k_bin for any schedule.
+// 64-bit add on shared memory as two native 32-bit atomics (sm_100 has no 64-bit shared
+// add: atomicAdd(u64) compiles to a CAS spin loop, which serialises under the contention of
+// image data).  The low word's wrap-around is carried into the high word, so the u64 read
+// after a barrier is the exact sum mod 2^64 (integer addition is associative).
+__device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned long long v) {
+  unsigned* w = reinterpret_cast<unsigned*>(p);
+  const unsigned lo = (unsigned)v;
+  const unsigned old = atomicAdd(&w[0], lo);
+  const unsigned carry = (old + lo < old) ? 1u : 0u;
+  const unsigned hi = (unsigned)(v >> 32) + carry;
+  if (hi) atomicAdd(&w[1], hi);
+}
+
 template <int D>
 __host__ __device__ constexpr int bin_table_entries() {
   return D <= 3 ? 4096 : (D <= 5 ? 2048 : 1024);
@@ -212,6 +225,8 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
   const int64_t p0 = (int64_t)blockIdx.x * per;
   const int64_t p1 = min(ntot, p0 + per);
   const unsigned lane = threadIdx.x & 31;
+  // frame of this thread's point, tracked incrementally (no 64-bit division per point)
+  int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
   // warp-uniform trip count so every lane takes part in the warp aggregation
   for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
     const int64_t p = pb + threadIdx.x;
@@ -219,8 +234,12 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
     int64_t L = 0;
     long long q[D];
     bool bad = false;
+    while (p >= fr_end) {
+      ++fr;
+      fr_end += b.n;
+    }
     if (valid) {
-      L = (p / b.n) * b.vol_frame;
+      L = fr * b.vol_frame;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
         const double x = (double)pts[p * D + c];
@@ -275,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
     if (hit >= 0) {
       atomicAdd(&tc[hit], my_cnt);
 #pragma unroll
-      for (int c = 0; c < D; ++c) atomicAdd(&ts[hit * D + c], (unsigned long long)q[c]);
+      for (int c = 0; c < D; ++c) smem_add_u64(&ts[hit * D + c], (unsigned long long)q[c]);
     } else {
       atomicAdd(&cnt[L], my_cnt);
 #pragma unroll

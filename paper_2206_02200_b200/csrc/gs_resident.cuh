@@ -70,7 +70,7 @@ struct ResidentArgs {
 // shared-memory bytes per cell (excluding the index and neighbour-record pool)
 __host__ __device__ constexpr int resident_bytes_per_cell(int D) {
   return 24 * D /*S0, Q = S1|P1*/ + 8 /*sort key*/ + 16 /*key A/B, cnt A/B*/ + 4 /*den*/ + 8 /*1/den*/ +
-         4 /*flag*/ + 16 /*nbn, nbe, eoff, par*/ + 4 /*tmp*/;
+         4 /*flag*/ + 16 /*nbn, nbe, eoff, par*/ + 4 /*tmp*/ + 4 /*initial cell -> current*/;
 }
 
 // shared-memory bytes of the neighbour-offset table (int32 per offset) for dimension D
@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   const int64_t fbase = (int64_t)f * b.vol_frame;
   int iters = a.fiters[f];
   int conv = a.fconv[f];
-  // root entries of this frame: global current index -> frame-local index
-  for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.root[c] -= first;
   if (a.fdone[f] || m > a.ms) {
+    // root entries of this frame: global current index -> frame-local index
+    for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.root[c] -= first;
     if (m > a.ms && !a.fdone[f] && tid == 0) atomicOr(a.err, 16);
     for (int i = tid; i < m; i += T) {  // finished in the global path: copy out
       a.okey[first + i] = a.ckey[first + i];
@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   int* eoff = (int*)p;              p += 4 * MS;
   int* par = (int*)p;               p += 4 * MS;
   int* tmp = (int*)p;               p += 4 * MS;
+  int* rootl = (int*)p;             p += 4 * MS;
   int16_t* sidx = (int16_t*)p;      p += a.sidx_bytes;
   int* offs = (int*)p;              p += resident_offs_bytes(D);
   unsigned char* pool = p;          // a.pool_bytes
@@ -277,6 +278,15 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     for (int c = 0; c < D; ++c) S0[i * D + c] = a.S[(int64_t)(first + i) * D + c];
     flag[i] = 0u;
   }
+  // initial cells of this frame -> current frame-local cell (shared memory when they fit)
+  const bool rsm = icnt <= MS;
+  for (int c = tid; c < icnt; c += T) {
+    const int r = a.root[ifirst + c] - first;
+    if (rsm)
+      rootl[c] = r;
+    else
+      a.root[ifirst + c] = r;
+  }
   constexpr int K = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 :
                     D == 6 ? 729 : D == 7 ? 2187 : D == 8 ? 6561 : D == 9 ? 19683 :
                     D == 10 ? 59049 : D == 11 ? 177147 : 531441;
@@ -290,10 +300,21 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     }
   }
   // the offset of neighbour t: table lookup (D <= 6) or a register odometer (D > 6)
+  // (d <= 3: from the strides in registers -- t is a constant in the unrolled loops, so each
+  // offset folds to a sum of +-strides with no memory access)
+  const int st0 = (int)b.stride[0], st1 = D > 1 ? (int)b.stride[1] : 0,
+            st2 = D > 2 ? (int)b.stride[2] : 0;
   struct NbrIt {
     OdoD<D> od;
     const int* tbl;
-    __device__ __forceinline__ int64_t at(int t) const { return kTable ? (int64_t)tbl[t] : od.off; }
+    int s0, s1, s2;
+    __device__ __forceinline__ int64_t at(int t) const {
+      if constexpr (D == 1) return (int64_t)(t - 1) * s0;
+      if constexpr (D == 2) return (int64_t)(t / 3 - 1) * s0 + (t % 3 - 1) * s1;
+      if constexpr (D == 3)
+        return (int64_t)(t / 9 - 1) * s0 + (t / 3 % 3 - 1) * s1 + (t % 3 - 1) * s2;
+      return kTable ? (int64_t)tbl[t] : od.off;
+    }
     __device__ __forceinline__ void step(const GsBox& bb) {
       if (!kTable) od.next(bb);
     }
@@ -301,6 +322,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   auto nbr_begin = [&]() {
     NbrIt it;
     it.tbl = offs;
+    it.s0 = st0;
+    it.s1 = st1;
+    it.s2 = st2;
     if (!kTable) it.od.init(b);
     return it;
   };
@@ -378,7 +402,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
             e += j < i;
           }
         }
-        for (int t = n; t < KP; ++t) li[t] = (uint16_t)ZROW;
+#pragma unroll
+        for (int t = 1; t < KP; ++t)  // (entry 0 is the cell itself or an earlier neighbour)
+          if (t >= n) li[t] = (uint16_t)ZROW;
         nbn[i] = n;
         nbe[i] = e;
         tmp[i] = i * KP;
@@ -647,10 +673,11 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     if (a.prof && tid == 0 && iters == 0)  // the first sweep alone (its DAG is data-fixed)
       atomicAdd((unsigned long long*)&a.prof[6], (unsigned long long)(clock64() - t_prev));
     lap(1);
-    // ---- (3) rehome, changed, displacement
+    // ---- (3) rehome, changed, displacement (the displacement only feeds the history)
     int P = 1;
     while (P < m) P <<= 1;
     bool ch = false, bad = false;
+    unsigned long long dmx = 0ull;  // |S1 - S0| bits (non-negative doubles order as integers)
     for (int i = tid; i < P; i += T) {
       if (i >= m) {
         sk[i] = ~0ull;
@@ -666,14 +693,21 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         bad_i |= (rel < 1) | (rel > b.ext[c] - 2);
         Ln += rel * b.stride[c];
         ch |= __double_as_longlong(s1) != __double_as_longlong(s0);
-        const double t = __dsub_rn(s1, s0);
-        acc = __dadd_rn(acc, __dmul_rn(t, t));
+        if (a.record) {
+          const double t = __dsub_rn(s1, s0);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
       }
       if (bad_i) Ln = key[i];
       bad |= bad_i;
       ch |= (Ln != (int64_t)key[i]);
-      atomicMax(&s_dmax, (unsigned long long)__double_as_longlong(__dsqrt_rn(acc)));
+      if (a.record) dmx = max(dmx, (unsigned long long)__double_as_longlong(__dsqrt_rn(acc)));
       sk[i] = ((uint64_t)(uint32_t)Ln << 32) | (uint32_t)i;
+    }
+    if (a.record) {  // one shared atomic per warp
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dmx = max(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+      if ((tid & 31) == 0 && dmx) atomicMax(&s_dmax, dmx);
     }
     if (bad) atomicOr(a.err, 4);
     const int changed = __syncthreads_or(ch);
@@ -681,20 +715,46 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     lap(2);
 
     // ---- (4) bitonic sort of (new key, old rank): members of a merge group end up
-    //          adjacent and in visit order
-    for (int k2 = 2; k2 <= P; k2 <<= 1) {
-      for (int j = k2 >> 1; j > 0; j >>= 1) {
-        for (int i = tid; i < P; i += T) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t x = sk[i], y = sk[ixj];
-            if ((x > y) == ((i & k2) == 0)) {
-              sk[i] = y;
-              sk[ixj] = x;
+    //          adjacent and in visit order.  With P <= T every thread holds one element:
+    //          partners closer than a warp are exchanged by shuffles, farther ones through
+    //          two shared buffers (one barrier per such stage).
+    uint64_t* sk2 = (uint64_t*)pool;  // the lists are dead after the sweep
+    if (P <= T && 8 * P <= a.pool_bytes) {
+      uint64_t x = tid < P ? sk[tid] : ~0ull;
+      int buf = 0;
+      for (int k2 = 2; k2 <= P; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+          uint64_t y;
+          if (j >= 32) {
+            uint64_t* bb = buf ? sk2 : sk;
+            if (tid < P) bb[tid] = x;
+            __syncthreads();
+            y = tid < P ? bb[tid ^ j] : ~0ull;
+            buf ^= 1;
+          } else {
+            y = __shfl_xor_sync(0xffffffffu, x, j);
+          }
+          const bool asc = (tid & k2) == 0, lower = (tid & j) == 0;
+          x = (lower == asc) ? min(x, y) : max(x, y);
+        }
+      }
+      if (tid < P) sk[tid] = x;
+      __syncthreads();
+    } else {
+      for (int k2 = 2; k2 <= P; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+          for (int i = tid; i < P; i += T) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const uint64_t x = sk[i], y = sk[ixj];
+              if ((x > y) == ((i & k2) == 0)) {
+                sk[i] = y;
+                sk[ixj] = x;
+              }
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
       }
     }
 
@@ -711,7 +771,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       if (head) eoff[g] = j;  // segment start (eoff is free after the sweep)
     }
     __syncthreads();
-    // merge_into folded in visit order (Eq. 3, pin P4)
+    // merge_into folded in visit order (Eq. 3, pin P4): s = RN(RN(RN(x*s) + RN(w*S_i)) / tot),
+    // the division from RN(1/tot) (Markstein; the reciprocal does not depend on s, so it
+    // leaves the chain); an operand outside the theorem's range redoes the group exactly
     for (int g = tid; g < mnew; g += T) {
       const int start = eoff[g];
       const int end = (g + 1 < mnew) ? eoff[g + 1] : m;
@@ -720,14 +782,35 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 #pragma unroll
       for (int c = 0; c < D; ++c) s[c] = S1[i0 * D + c];
       uint64_t cc = cnt[i0];
+      bool slow = false;
       for (int j = start + 1; j < end; ++j) {
         const uint32_t i = (uint32_t)sk[j];
         const uint64_t ci = cnt[i];
         const double x = (double)cc, w = (double)ci, tot = (double)(cc + ci);
+        const double y = __drcp_rn(tot);
 #pragma unroll
-        for (int c = 0; c < D; ++c)
-          s[c] = __ddiv_rn(__dadd_rn(__dmul_rn(x, s[c]), __dmul_rn(w, S1[i * D + c])), tot);
+        for (int c = 0; c < D; ++c) {
+          const double num = __dadd_rn(__dmul_rn(x, s[c]), __dmul_rn(w, S1[i * D + c]));
+          const double fa = fabs(num);
+          slow |= !(fa < 0x1p+1000) || (fa < 0x1p-900 && num != 0.0);
+          const double q0 = __dmul_rn(num, y);
+          s[c] = __fma_rn(__fma_rn(-q0, tot, num), y, q0);
+        }
         cc += ci;
+      }
+      if (slow) {  // rare: the same fold with IEEE divisions
+        cc = cnt[i0];
+#pragma unroll
+        for (int c = 0; c < D; ++c) s[c] = S1[i0 * D + c];
+        for (int j = start + 1; j < end; ++j) {
+          const uint32_t i = (uint32_t)sk[j];
+          const uint64_t ci = cnt[i];
+          const double x = (double)cc, w = (double)ci, tot = (double)(cc + ci);
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            s[c] = gs_ddiv_slow(__dadd_rn(__dmul_rn(x, s[c]), __dmul_rn(w, S1[i * D + c])), tot);
+          cc += ci;
+        }
       }
       nkey[g] = (uint32_t)(sk[start] >> 32);
       ncnt[g] = (uint32_t)cc;
@@ -735,7 +818,12 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       for (int c = 0; c < D; ++c) S0[g * D + c] = s[c];
     }
     // member union (Eq. 4) as root composition
-    for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.root[c] = par[a.root[c]];
+    for (int c = tid; c < icnt; c += T) {
+      if (rsm)
+        rootl[c] = par[rootl[c]];
+      else
+        a.root[ifirst + c] = par[a.root[ifirst + c]];
+    }
     for (int i = tid; i < m; i += T) idx_put(key[i], -1);  // retire the old keys
     __syncthreads();
     {
@@ -785,7 +873,8 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     for (int c = 0; c < D; ++c) a.oS[(int64_t)(first + i) * D + c] = S0[i * D + c];
     if (!sdense) gidx[key[i]] = -1;  // clean-grid invariant for the next run
   }
-  for (int c = ifirst + tid; c < ifirst + icnt; c += T) a.lab[a.initkey[c]] = a.root[c];
+  for (int c = tid; c < icnt; c += T)
+    a.lab[a.initkey[ifirst + c]] = rsm ? rootl[c] : a.root[ifirst + c];
   if (tid == 0) {
     a.fk[f] = m;
     a.fiters[f] = iters;
