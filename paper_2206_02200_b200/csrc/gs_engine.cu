@@ -420,11 +420,11 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
     }
     const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
     if (dtype == GS_F32)
-      gs::k_bin_priv<D, float><<<grid, 1024, smem, ctx->stream>>>(
+      gs::k_bin_priv<D, float><<<grid, 768, smem, ctx->stream>>>(
           (const float*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
           ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
     else
-      gs::k_bin_priv<D, double><<<grid, 1024, smem, ctx->stream>>>(
+      gs::k_bin_priv<D, double><<<grid, 768, smem, ctx->stream>>>(
           (const double*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
           ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
     GS_LAUNCHED("k_bin_priv");

@@ -200,7 +200,7 @@ __host__ __device__ constexpr int bin_table_entries() {
 }
 
 template <int D, typename T>
-__global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, int64_t ntot,
+__global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, int64_t ntot,
                                                    const GsBox* __restrict__ pb,
                                                    uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
@@ -227,10 +227,20 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
   const unsigned lane = threadIdx.x & 31;
   // frame of this thread's point, tracked incrementally (no 64-bit division per point)
   int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
-  // warp-uniform trip count so every lane takes part in the warp aggregation
+  // warp-uniform trip count so every lane takes part in the warp aggregation; the next
+  // round's coordinates are loaded before this round is processed (twice the bytes in flight)
+  T xn[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * D + c] : T(0);
   for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
     const int64_t p = pb + threadIdx.x;
     const bool valid = p < p1;
+    T xc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xc[c] = xn[c];
+    const int64_t pn = p + blockDim.x;
+#pragma unroll
+    for (int c = 0; c < D; ++c) xn[c] = pn < p1 ? pts[pn * D + c] : T(0);
     int64_t L = 0;
     long long q[D];
     bool bad = false;
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
       L = fr * b.vol_frame;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double x = (double)pts[p * D + c];
+        const double x = (double)xc[c];
         const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
         const int64_t rel = k - b.kmin[c];
         bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
@@ -256,27 +266,34 @@ __global__ void __launch_bounds__(1024) k_bin_priv(const T* __restrict__ pts, in
       for (int c = 0; c < D; ++c) q[c] = 0;
     }
     const uint32_t key = (valid && !bad) ? (uint32_t)L : EMPTY;
-    // ---- warp aggregation: lanes binning into the same cell (pixel-ordered images put
-    // most of a warp into 1-4 cells) reduce to their group leader before any atomic
+    // ---- warp aggregation: lanes binning into the same cell (pixel-ordered images put most
+    // of a warp into 1-4 cells) reduce to their group leader before any atomic: per group,
+    // hardware reductions (REDUX) of the fixed-point sums in three 26/26/12-bit pieces (no
+    // piece sum of <= 32 lanes can overflow; the u64 recombination is exact mod 2^64).  Many
+    // small groups skip it: their atomics hardly contend.
     const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int gsize = __popc(peers);
-    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)gsize);
+    const bool leader = (peers & ((1u << lane) - 1u)) == 0u;
+    const unsigned leaders = __ballot_sync(0xffffffffu, leader);
     uint32_t my_cnt = 1;
-    if (maxg > 1) {
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      for (int s = 1; s < maxg; s <<= 1) {
-        // partner = the group member s ranks above; __fns counts set bits from `lane` upward
-        const unsigned partner = __fns(peers, lane, s + 1);
-        const bool take = ((rank & (2 * s - 1)) == 0) && partner < 32u;
-        const int src = take ? (int)partner : (int)lane;
+    if (__popc(leaders) <= 4) {
+      unsigned rem = leaders;
+      while (rem) {
+        const int ld = __ffs(rem) - 1;
+        rem &= rem - 1u;
+        const unsigned gm = __shfl_sync(0xffffffffu, peers, ld);
+        if ((gm >> lane) & 1u) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-          const long long v = __shfl_sync(0xffffffffu, q[c], src);
-          if (take) q[c] += v;
+          for (int c = 0; c < D; ++c) {
+            const unsigned long long u = (unsigned long long)q[c];
+            const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
+            const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
+            const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
+            q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
+          }
         }
       }
-      my_cnt = (uint32_t)gsize;
-      if (rank != 0) continue;  // only the group leader carries the group's sums
+      my_cnt = (uint32_t)__popc(peers);
+      if (!leader) continue;  // only the group leader carries the group's sums
     }
     if (key == EMPTY) continue;
     uint32_t h = (key * 2654435761u) & (TBL - 1);
