@@ -2,23 +2,19 @@
 //
 // One thread block owns one frame (frames are independent runs) and executes
 // the whole engine loop of SPEC.md:135-143 for it with the cell state in shared memory:
-//   hash index of the active keys (smem open addressing)
-//   -> neighbour records in lexicographic v order
-//   -> Eq. (5) sweep with exact sequential semantics: per-cell dataflow on smem ready-flags
-//      (a cell waits only for its lex-earlier active neighbours; SPEC.md:120(b,c))
+//   dense int16 key index over the frame's key box (or the global grid)
+//   -> neighbour lists in lexicographic v order, ΣC' and RN(1/ΣC')
+//   -> Eq. (5) sweep with exact sequential semantics as Kahn frontiers over the sweep's DAG
+//      (a cell waits only for its lex-earlier active neighbours; SPEC.md:120(b,c)): a schedule
+//      warp publishes frontier after frontier, two update warps consume them
 //   -> rehome floor(S/h), changed / max displacement (SPEC.md:120(d,e), :108)
 //   -> bitonic sort of (new key, old rank) and ordered Eq. (3) folds
 //   -> root composition for the member sets (Eq. 4), has_converged
 // with no global synchronisation and no host round trip per iteration.  Every fp64
 // expression is the same _rn sequence as the global-path kernels and the CPU oracle.
 //
-// Sweep critical path.  The DAG depth of one sweep (31-184 on the configs) multiplies the
-// latency of ONE cell update, so that latency is what this kernel minimises: before the
-// sweep, every cell gets a record {slot, C'} per lex-earlier neighbour and the products
-// C'*S_old of itself and its lex-later neighbours (they do not depend on the sweep).  While
-// waiting, a cell folds each earlier neighbour's term in as soon as its flag is released
-// (still in lex order); after the last one only the precomputed tail of adds and the
-// division remain.
+// The sweep's critical path is (DAG depth) x (one level's latency on a lone warp); DESIGN.md
+// §4 and profiles/r1_k8_sweep_level_probe.txt give the measured cost model it is built for.
 #pragma once
 
 #include <cstdint>
