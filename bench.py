@@ -86,6 +86,10 @@ class ClockSampler:
                 "samples": len(busy)}
 
 
+# K2 dram bytes (read + write) per launch, ncu --set full (profiles/r1_ncu_kernels.md)
+NCU_TRAFFIC = {"cfg2": 1_903_616, "cfg4": 961_585_408 + 305_048_320}
+
+
 def workload_input(name: str, rank: int):
     from paper_2206_02200_b200 import configs as CF
     cfg = CF.CONFIGS[name]
@@ -122,41 +126,47 @@ def cpu_baseline(name: str, X: np.ndarray, h: float, max_iter: int, budget_s: fl
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on all host threads, rank 0 only."""
+    """--impl reference: the CPU oracle (the reference's algorithm; the reference itself has no
+    code) on this arm's workload: the same frames, as independent runs spread over the host
+    threads -- one GridShift run is sequential, so a single frame uses one thread.
+    Rank 0 only.  Frames above 4M points are timed on a bounded prefix sample."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle import oracle as O
-    from paper_2206_02200_b200 import configs as CF
     cfg, X = workload_input(args.workload, 0)
-    threads = os.cpu_count() or 1
-    x0 = np.ascontiguousarray(X[0], np.float64)
-    n = x0.shape[0]
+    B, n = X.shape[0], X.shape[1]
+    cap = 4_000_000
+    frames = [np.ascontiguousarray(X[f][:cap], np.float64) for f in range(B)]
+    pts_step = sum(x.shape[0] for x in frames)
+    threads = max(1, min(os.cpu_count() or 1, B))
 
-    def one(_):
-        O.run(x0, cfg.h, cfg.max_iter, O.BUILD_SPEC)
+    def one(f):
+        O.run(frames[f], cfg.h, cfg.max_iter, O.BUILD_SPEC)
 
     from concurrent.futures import ThreadPoolExecutor
     pool = ThreadPoolExecutor(threads)
     step_times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        list(pool.map(one, range(threads)))
+        list(pool.map(one, range(B)))
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             step_times.append(dt)
     total = sum(step_times)
-    value = threads * n * args.steps / total
+    value = pts_step * args.steps / total
+    sample = (f"per step the workload's {B} frame(s) as independent oracle runs (SPEC-literal "
+              f"build) on {threads} thread(s)"
+              + (f", first {cap} points of each frame" if n > cap else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "n": n, "d": cfg.d, "h": cfg.h,
-                   "max_iter": cfg.max_iter, "batch": 1},
+                   "max_iter": cfg.max_iter, "batch": B},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
-                         "sample": f"per step {threads} concurrent independent oracle runs of "
-                                   f"one {args.workload} frame (SPEC-literal build)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -192,6 +202,14 @@ def main():
     eng = G.Engine(local, stream.cuda_stream)
 
     cfg, X = workload_input(args.workload, rank)
+    # cfg5 over several GPUs: ONE cloud split into contiguous point shards (dist.run_cloud:
+    # partial cells all-gathered, identical iteration on every rank, own points labelled)
+    shard_cloud = args.workload == "cfg5" and world > 1
+    n_global = X.shape[1]
+    if shard_cloud:
+        from paper_2206_02200_b200.dist import point_shard, run_cloud
+        p0, cnt_local = point_shard(n_global, world, rank)
+        X = np.ascontiguousarray(X[:, p0:p0 + cnt_local])
     B, n, d = X.shape
     dt = G.GS_F32 if X.dtype == np.float32 else G.GS_F64
     econf = G.EngineConfig(cfg.h, cfg.max_iter)
@@ -202,6 +220,9 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
     def step(device_resident: bool):
+        if shard_cloud:
+            run_cloud(eng, X_dev[0] if device_resident else X[0], cfg.h, cfg.max_iter)
+            return
         if device_resident:
             eng.run_raw(X_dev.data_ptr(), n, d, dt, B, True, econf, labels_dev.data_ptr(),
                         device_outputs=True)
@@ -243,7 +264,7 @@ def main():
         t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_dev, tot_e2e = t.tolist()
-    pts_all = world * B * n * args.steps
+    pts_all = (n_global if shard_cloud else world * B * n) * args.steps
     value = pts_all / (tot_dev / 1e3)
     e2e = pts_all / (tot_e2e / 1e3)
     # cells x iterations (Σ m_t) per second over the iteration phase
@@ -267,19 +288,25 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_dev / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if shard_cloud else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "desc": cfg.desc, "n": n, "d": d, "batch": B,
                    "h": cfg.h, "max_iter": cfg.max_iter, "input_dtype": "f32" if s_in == 4 else "f64",
                    "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": f"frames x{world} (independent images per rank)"},
+                   "parallelism": (f"one cloud in {world} point shards (partial cells "
+                                   f"all-gathered, replicated iteration)") if shard_cloud else
+                                  f"frames x{world} (independent images per rank)"},
         "cell_updates_per_s": cells / (it_ms / 1e3) if it_ms > 0 else None,
         "cells_swept_per_step": s0["cells_swept"], "m0": s0["m0"], "k": s0["k_total"],
         "iterations": s0["max_iterations"],
         "phase_ms": phase, "dominant_phase": dominant,
         "roofline": {"kernel": "k_bin (K2 binning)", "bound": "hbm", "achieved": kbin_gbs,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": kbin_gbs / peak, "traffic": None,
+                     "frac": kbin_gbs / peak,
+                     # dram read+write of one K2 launch from the committed ncu --set full
+                     # capture of this workload (profiles/r1_ncu_kernels.md), or null
+                     "traffic": NCU_TRAFFIC.get(args.workload) if not shard_cloud else None,
                      "algorithmic_bytes": kbin_bytes},
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
                 "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},

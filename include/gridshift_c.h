@@ -117,14 +117,38 @@ typedef struct {
   double ms_k_bin;       /* the binning kernel K2 alone                                     */
   double ms_k_label;     /* the label kernel K7 alone                                       */
   int64_t lib_calls;     /* library (CUB) device calls, not counted in kernel_launches      */
-  int64_t sweep_modes[3];/* K8 iterations by sweep mode: fast records / slot lists / inline */
-  int64_t resident_cycles[8]; /* K8 SM cycles per phase (census, sweep, rehome, sort, merge,
-                                 hash+converged, -, load), summed over frames */
+  int64_t sweep_modes[3];/* K8 iterations by sweep mode: fixed-stride lists / scanned lists /
+                            inline lookups */
+  int64_t resident_cycles[8]; /* K8 SM cycles per phase with GS_PROF set (lists, sweep, rehome,
+                                 sort, merge, converged, first sweep, load), summed over frames */
 } gs_stats;
 gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out);
 
 const char* gs_last_error(const gs_ctx* ctx); /* valid until the next call on ctx */
 const char* gs_status_string(gs_status s);
+
+/* ---- multi-GPU: one point cloud split over R ranks ----
+ * Each rank calls, on its own contiguous shard of the cloud (batch = 1):
+ *  1. gs_shard_keybounds: the shard's per-dim cell-key range floor(min/h) .. floor(max/h);
+ *     the caller all-reduces them (min of klo, max of khi) and the point counts (sum);
+ *  2. gs_shard_bin: bins the shard into partial cells of the global key box (dense linear
+ *     keys, counts and raw fixed-point sums -- integers, so partials merge exactly); the
+ *     caller all-gathers every rank's partial cells.  Returns GS_E_INVALID_PARAMETER with
+ *     *m_out = the needed count when cap is too small;
+ *  3. gs_shard_run: merges all partial cells (any order) into the global initial cells --
+ *     bit-identical to a single-GPU build_active_grid over the whole cloud -- runs the
+ *     iteration and labels this rank's shard.  Every rank computes the same clusters;
+ *     gs_get_centroids / gs_get_history then work as after gs_run.
+ * The calls must be made in order on the same ctx (the shard's point-to-cell map is kept from
+ * 2 to 3).  Replaces the whole-cloud engine.run of SPEC.md:135-143 for one dataset. */
+gs_status gs_shard_keybounds(gs_ctx* ctx, const gs_input* shard, double h, int64_t* klo,
+                             int64_t* khi);
+gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* shard, double h, int64_t n_global,
+                       const int64_t* klo, const int64_t* khi, int64_t cap, int64_t* m_out,
+                       uint32_t* keys, uint32_t* counts, int64_t* sums);
+gs_status gs_shard_run(gs_ctx* ctx, int64_t m_all, const uint32_t* keys, const uint32_t* counts,
+                       const int64_t* sums, int64_t n_shard, const gs_config* cfg,
+                       gs_result* out);
 
 /* ---- test hooks (parity harness; not needed by callers) ---- */
 

@@ -94,6 +94,15 @@ struct gs_ctx {
   int64_t ctl_nf = 0;
   // bumped whenever a device buffer is (re)allocated: a cached graph holds raw pointers
   uint64_t alloc_gen = 0;
+  // multi-GPU shard state (gs_shard_*): the global key box from gs_shard_bin, and for
+  // gs_shard_run the merged partial cells the run starts from instead of binning
+  bool shard_box = false;
+  bool shard_front = false;
+  int64_t shard_m = 0;
+  const uint32_t* shard_keys = nullptr;
+  const uint32_t* shard_counts = nullptr;
+  const int64_t* shard_sums = nullptr;
+  DevBuf xsum, pkeys, pcounts, psums;
   // pinned readback area (one async D2H per result array, one sync per run)
   void* pin = nullptr;
   size_t pin_bytes = 0;
@@ -884,6 +893,47 @@ bool graph_safe(const void* p) {
          at.type == cudaMemoryTypeManaged;
 }
 
+__global__ void k_epoch_bump(unsigned* e) { *e += 1u; }
+
+// The front of gs_shard_run: every rank's partial cells (host) -> the dense grid of the
+// global box -> compaction, leaving the same device state launch_nscale leaves after binning
+// the whole cloud (the shard's slot[] is still there from gs_shard_bin).
+gs_status launch_shard_front(gs_ctx* ctx, int d) {
+  cudaStream_t st = ctx->stream;
+  const int64_t m = ctx->shard_m;
+  GS_TRY(rec_event(ctx, 0));
+  GS_TRY(rec_event(ctx, 1));
+  GS_TRY(grow(ctx, ctx->pkeys, 4 * std::max<int64_t>(m, 1)));
+  GS_TRY(grow(ctx, ctx->pcounts, 4 * std::max<int64_t>(m, 1)));
+  GS_TRY(grow(ctx, ctx->psums, 8 * d * std::max<int64_t>(m, 1)));
+  GS_TRY(ensure_cells(ctx, std::min<int64_t>(m, ctx->box.vol_total), d));
+  GS_CK(cudaMemcpyAsync(ctx->pkeys.p, ctx->shard_keys, 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->pcounts.p, ctx->shard_counts, 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->psums.p, ctx->shard_sums, 8 * d * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_CK(cudaMemcpyAsync(ctx->dbox.p, &ctx->box, sizeof(GsBox), cudaMemcpyHostToDevice, st));
+  GS_TRY(rec_event(ctx, 6));
+  gs::k_scatter_partials<<<blocks_for(m, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+      m, d, ctx->pkeys.as<uint32_t>(), ctx->pcounts.as<uint32_t>(),
+      ctx->psums.as<long long>(), ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>());
+  GS_LAUNCHED("k_scatter_partials");
+  GS_TRY(rec_event(ctx, 7));
+  k_epoch_bump<<<1, 1, 0, st>>>(ctx->epoch_dev.as<unsigned>());
+  GS_LAUNCHED("k_epoch_bump");
+  unsigned* cnt32 = ctx->counters.as<unsigned>();
+  const unsigned tg = (unsigned)std::min<int64_t>(ctx->box.vol_total / gs::kOccTile + 1,
+                                                  (int64_t)ctx->num_sms * 4);
+  gs::k_occ<<<tg, 256, 0, st>>>(
+      ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>(), ctx->tiles.as<unsigned long long>(),
+      cnt32 + 5, cnt32, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+      ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(), ctx->S[0].as<double>(),
+      ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(),
+      ctx->ifirst.as<int32_t>(), ctx->errflag.as<int>());
+  GS_LAUNCHED("k_occ");
+  GS_TRY(rec_event(ctx, 2));
+  return GS_OK;
+}
+
 // opt-in host-side timeline of one run (GS_HOST_PROF): prep / launch / wait / results, in us
 struct HostProf {
   bool on = getenv("GS_HOST_PROF") != nullptr;
@@ -930,6 +980,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   const void* dpts = in->on_device ? in->points : ctx->pts.p;
   int64_t vol_hint = 0;  // the cached shape's grid volume (sizes the compaction launch)
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
+    if (ctx->shard_front) return launch_shard_front(ctx, d);
     GS_TRY(rec_event(ctx, 0));
     if (!in->on_device)
       GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
@@ -941,7 +992,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
   std::vector<int32_t> g_iters(nf, 0);
   int64_t swept = 0;
-  if (!force_global && ctx->shape_ms > 0 && key == ctx->shape) {
+  if (!force_global && !ctx->shard_front && ctx->shape_ms > 0 && key == ctx->shape) {
     // ---- optimistic path: the whole run with no host round trip, replayed from a CUDA graph
     //      when the caller's buffers allow it (pinned or device memory)
     const bool graphed = ctx->use_graphs && (in->on_device || graph_safe(in->points)) &&
@@ -1098,7 +1149,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     int ms_run = 32;
     while (ms_run < ml) ms_run <<= 1;
     ms_run = std::min(ms_run, ms_cap);
-    if (iter == 0 && !force_global) {  // K8 straight from binning: later runs go optimistic
+    if (iter == 0 && !force_global && !ctx->shard_front) {  // later runs go optimistic
       ctx->shape = key;
       ctx->shape_ms = std::min(ms_cap, 2 * ms_run);  // headroom for data-dependent m0
       ctx->shape_box = b;
@@ -1232,7 +1283,8 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->fiters, &ctx->fconv, &ctx->fk, &ctx->hist, &ctx->counters, &ctx->errflag,
                     &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes, &ctx->tiles,
                     &ctx->dbox, &ctx->erec, &ctx->lprod, &ctx->rden, &ctx->lvl,
-                    &ctx->lsucc, &ctx->order})
+                    &ctx->lsucc, &ctx->order, &ctx->xsum, &ctx->pkeys, &ctx->pcounts,
+                    &ctx->psums, &ctx->epoch_dev, &ctx->fswept, &ctx->fout, &ctx->ctl})
     b->release();
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
@@ -1306,6 +1358,171 @@ gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out) {
   }
   *out = ctx->stats;
   return GS_OK;
+}
+
+gs_status gs_shard_keybounds(gs_ctx* ctx, const gs_input* in, double h, int64_t* klo,
+                             int64_t* khi) {
+  gs_config cfg{h, 1, 0};
+  gs_status s = validate(in, &cfg);
+  if (s != GS_OK) return s;
+  if (!ctx || !klo || !khi) return GS_E_INVALID_PARAMETER;
+  if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "a shard is one frame");
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int d = in->d;
+  const int64_t n = in->n;
+  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
+  const void* dpts = in->points;
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice, st));
+    dpts = ctx->pts.p;
+  }
+  const unsigned nblk = blocks_for(n, 256 * 4, (int64_t)ctx->num_sms * 2);
+  GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
+  GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
+  GS_TRY(ensure_frames(ctx, 1));
+  if (!ctx->epoch_dev.p) {
+    GS_TRY(grow(ctx, ctx->epoch_dev, 16));
+    GS_CK(cudaMemsetAsync(ctx->epoch_dev.p, 0, 16, st));
+  }
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, in->dtype, d, n, true, nblk, h, n, 1));
+  int hdr[8];
+  GsBox b;
+  GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(&b, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+  if (hdr[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+  for (int c = 0; c < d; ++c) {
+    klo[c] = b.kmin[c] + GS_APRON;
+    khi[c] = b.kmin[c] + b.ext[c] - 1 - GS_APRON;
+  }
+  return GS_OK;
+}
+
+gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_global,
+                       const int64_t* klo, const int64_t* khi, int64_t cap, int64_t* m_out,
+                       uint32_t* keys, uint32_t* counts, int64_t* sums) {
+  gs_config cfg{h, 1, 0};
+  gs_status s = validate(in, &cfg);
+  if (s != GS_OK) return s;
+  if (!ctx || !klo || !khi || !m_out || (cap > 0 && (!keys || !counts || !sums)))
+    return GS_E_INVALID_PARAMETER;
+  if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "a shard is one frame");
+  if (n_global < in->n) return fail(ctx, GS_E_INVALID_PARAMETER, "n_global < shard size");
+  ctx->err.clear();
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int d = in->d;
+  const int64_t n = in->n;
+  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
+  // the global box: same keys, strides and fixed-point exponent on every rank
+  GsBox b;
+  std::memset(&b, 0, sizeof(b));
+  b.d = d;
+  b.h = h;
+  b.inv_h = 1.0 / h;  // == __drcp_rn(h): both correctly rounded
+  b.F = gs_fixed_shift(n_global, h);
+  b.scale = std::ldexp(1.0, b.F);
+  b.inv_scale = std::ldexp(1.0, -b.F);
+  b.n = n;
+  b.nframes = 1;
+  double vol = 1.0;
+  for (int c = 0; c < d; ++c) {
+    if (khi[c] < klo[c]) return fail(ctx, GS_E_INVALID_PARAMETER, "empty key range");
+    b.kmin[c] = klo[c] - GS_APRON;
+    b.ext[c] = khi[c] - klo[c] + 1 + 2 * GS_APRON;
+    vol *= (double)b.ext[c];
+  }
+  if (vol > (double)kMaxDenseCells)
+    return fail(ctx, GS_E_KEY_RANGE, "key box exceeds the dense cell grid (2^28)");
+  int64_t sv = 1;
+  for (int c = d - 1; c >= 0; --c) {
+    b.stride[c] = sv;
+    sv *= b.ext[c];
+  }
+  b.vol_frame = b.vol_total = sv;
+  GS_TRY(ensure_dense(ctx, std::max<int64_t>(ctx->dense_cap, sv), d));
+  GS_TRY(ensure_cells(ctx, std::min<int64_t>(n, sv), d));
+  GS_TRY(ensure_frames(ctx, 1));
+  GS_TRY(grow(ctx, ctx->slot, sizeof(uint32_t) * n));
+  GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
+  GS_TRY(grow(ctx, ctx->xsum, 8 * (size_t)d * std::min<int64_t>(n, sv)));
+  const int64_t ntiles = ctx->dense_cap / gs::kOccTile + 1;
+  if (ctx->tiles.bytes < sizeof(unsigned long long) * ntiles) {
+    GS_TRY(grow(ctx, ctx->tiles, sizeof(unsigned long long) * ntiles));
+    GS_CK(cudaMemsetAsync(ctx->tiles.p, 0, ctx->tiles.bytes, st));
+  }
+  if (!ctx->epoch_dev.p) {
+    GS_TRY(grow(ctx, ctx->epoch_dev, 16));
+    GS_CK(cudaMemsetAsync(ctx->epoch_dev.p, 0, 16, st));
+  }
+  const void* dpts = in->points;
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice, st));
+    dpts = ctx->pts.p;
+  }
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_CK(cudaMemcpyAsync(ctx->dbox.p, &b, sizeof(GsBox), cudaMemcpyHostToDevice, st));
+  GS_TRY(dispatch_bounds_bin(ctx, dpts, in->dtype, d, n, false, 0));
+  k_epoch_bump<<<1, 1, 0, st>>>(ctx->epoch_dev.as<unsigned>());
+  GS_LAUNCHED("k_epoch_bump");
+  unsigned* cnt32 = ctx->counters.as<unsigned>();
+  const unsigned tg = (unsigned)std::min<int64_t>(sv / gs::kOccTile + 1, (int64_t)ctx->num_sms * 4);
+  gs::k_occ<<<tg, 256, 0, st>>>(
+      ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>(), ctx->tiles.as<unsigned long long>(),
+      cnt32 + 5, cnt32, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+      ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(), ctx->S[0].as<double>(),
+      ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(),
+      ctx->ifirst.as<int32_t>(), ctx->errflag.as<int>(), ctx->xsum.as<long long>());
+  GS_LAUNCHED("k_occ");
+  int hdr[8];
+  unsigned ctr[16];
+  GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  if (hdr[0] & 2)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "shard points outside the given key bounds");
+  const int64_t m = ctr[0];
+  *m_out = m;
+  if (m > cap) return fail(ctx, GS_E_INVALID_PARAMETER, "partial-cell buffers too small");
+  GS_CK(cudaMemcpyAsync(keys, ctx->ckey[0].p, 4 * m, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(counts, ctx->ccnt[0].p, 4 * m, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(sums, ctx->xsum.p, 8 * d * m, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  ctx->box = b;
+  ctx->shard_box = true;
+  return GS_OK;
+}
+
+gs_status gs_shard_run(gs_ctx* ctx, int64_t m_all, const uint32_t* keys, const uint32_t* counts,
+                       const int64_t* sums, int64_t n_shard, const gs_config* cfg,
+                       gs_result* out) {
+  if (!ctx || !cfg || !out || m_all < 1 || !keys || !counts || !sums)
+    return GS_E_INVALID_PARAMETER;
+  if (!ctx->shard_box) return fail(ctx, GS_E_INVALID_PARAMETER, "gs_shard_bin first");
+  if (cfg->h != ctx->box.h) return fail(ctx, GS_E_INVALID_PARAMETER, "h differs from gs_shard_bin");
+  if (n_shard != ctx->box.n) return fail(ctx, GS_E_INVALID_PARAMETER, "shard size differs");
+  gs_input in{keys, n_shard, ctx->box.d, GS_F64, 1, 1, 0};  // points unused: cells given
+  gs_status s = validate(&in, cfg);
+  if (s != GS_OK) return s;
+  ctx->err.clear();
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GS_E_CUDA, "cudaSetDevice");
+  ctx->shard_front = true;
+  ctx->shard_m = m_all;
+  ctx->shard_keys = keys;
+  ctx->shard_counts = counts;
+  ctx->shard_sums = sums;
+  s = run_impl(ctx, &in, cfg, out);
+  ctx->shard_front = false;
+  ctx->shard_box = false;
+  ctx->shard_keys = ctx->shard_counts = nullptr;
+  ctx->shard_sums = nullptr;
+  return s;
 }
 
 gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_m,

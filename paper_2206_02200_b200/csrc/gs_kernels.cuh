@@ -377,7 +377,9 @@ __global__ void __launch_bounds__(256) k_occ(
     unsigned long long* __restrict__ qs, uint32_t* __restrict__ ckey,
     uint32_t* __restrict__ ccnt, double* __restrict__ S, int32_t* __restrict__ idx,
     int32_t* __restrict__ root, uint32_t* __restrict__ initkey, int32_t* __restrict__ ifirst,
-    const int* __restrict__ err) {
+    const int* __restrict__ err, long long* __restrict__ xsum = nullptr) {
+  // xsum != null: export mode (a shard's partial cells for the multi-GPU exchange): keys,
+  // counts and the raw fixed-point sums, no centroids, no index / root / label entries
   if (*err & (1 | 32 | 64)) return;
   __shared__ int sh[8];
   __shared__ GsBox b;
@@ -457,18 +459,39 @@ __global__ void __launch_bounds__(256) k_occ(
       if (c8[k] == 0u) continue;
       for (int q = 0; q < b.d; ++q) {
         const long long sq = (long long)qs[L * b.d + q];
-        S[(int64_t)pos * b.d + q] = gs_fix_centroid(gs_key_of(b, L, q), sq, c8[k], b.h, b.inv_scale);
+        if (xsum)
+          xsum[(int64_t)pos * b.d + q] = sq;
+        else
+          S[(int64_t)pos * b.d + q] =
+              gs_fix_centroid(gs_key_of(b, L, q), sq, c8[k], b.h, b.inv_scale);
         qs[L * b.d + q] = 0ull;
       }
       cnt[L] = 0u;
       ckey[pos] = (uint32_t)L;
       ccnt[pos] = c8[k];
-      idx[L] = pos;
-      root[pos] = pos;
-      initkey[pos] = (uint32_t)L;
+      if (!xsum) {
+        idx[L] = pos;
+        root[pos] = pos;
+        initkey[pos] = (uint32_t)L;
+      }
       ++pos;
     }
     __syncthreads();  // s_tile / s_excl are rewritten by the next round
+  }
+}
+
+// Multi-GPU (one cloud over R ranks): accumulate every rank's partial cells into the dense
+// grid.  Counts and fixed-point sums are integers, so the merged grid equals the one a single
+// GPU binning all points would build, bit for bit, in any order.
+__global__ void k_scatter_partials(int64_t m, int d, const uint32_t* __restrict__ keys,
+                                   const uint32_t* __restrict__ counts,
+                                   const long long* __restrict__ sums, uint32_t* __restrict__ cnt,
+                                   unsigned long long* __restrict__ qs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t L = keys[i];
+    atomicAdd(&cnt[L], counts[i]);
+    for (int c = 0; c < d; ++c) atomicAdd(&qs[L * d + c], (unsigned long long)sums[i * d + c]);
   }
 }
 

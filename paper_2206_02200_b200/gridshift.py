@@ -71,7 +71,8 @@ GS_DEBUG_GLOBAL_PATH = 0x80000000
 EXPORTED = [
     "gs_validate", "gs_create", "gs_destroy", "gs_run", "gs_get_centroids", "gs_get_history",
     "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
-    "gs_debug_iterate_once", "gs_fixed_shift",
+    "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
+    "gs_shard_run",
 ]
 
 
@@ -128,6 +129,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.gs_debug_iterate_once.argtypes = [P, I32, D, I64, P, P, P, P, P, P, P, P, P, P, P, P]
     lib.gs_fixed_shift.argtypes = [I64, D]
     lib.gs_fixed_shift.restype = I32
+    lib.gs_shard_keybounds.argtypes = [P, C.POINTER(GsInput), D, P, P]
+    lib.gs_shard_bin.argtypes = [P, C.POINTER(GsInput), D, I64, P, P, I64, P, P, P, P]
+    lib.gs_shard_run.argtypes = [P, I64, P, P, P, I64, C.POINTER(GsConfig), C.POINTER(GsResult)]
     _lib = lib
     return lib
 
@@ -277,6 +281,68 @@ class Engine:
         out["sweep_modes"] = list(out["sweep_modes"])
         out["resident_cycles"] = list(out["resident_cycles"])
         return out
+
+    # -- one point cloud over several ranks (gridshift_c.h gs_shard_*; driven by dist.py) ----
+    @staticmethod
+    def _shard_input(X):
+        """numpy (host) or a contiguous torch CUDA tensor (device-resident shard)."""
+        if hasattr(X, "is_cuda") and X.is_cuda:
+            import torch
+            assert X.is_contiguous() and X.dtype in (torch.float32, torch.float64)
+            n, d = X.shape
+            dt = GS_F32 if X.dtype == torch.float32 else GS_F64
+            return X, GsInput(X.data_ptr(), n, d, dt, 1, 1, 0)
+        X = np.ascontiguousarray(X)
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        n, d = X.shape
+        dt = GS_F32 if X.dtype == np.float32 else GS_F64
+        return X, GsInput(_ptr(X), n, d, dt, 1, 0, 0)
+
+    def shard_keybounds(self, X: np.ndarray, h: float):
+        """Per-dim cell-key range [klo, khi] of this rank's shard (to be all-reduced)."""
+        X, inp = self._shard_input(X)
+        d = X.shape[1]
+        lo, hi = np.zeros(d, np.int64), np.zeros(d, np.int64)
+        self._check(self._lib.gs_shard_keybounds(self._ctx, C.byref(inp), h, _ptr(lo), _ptr(hi)))
+        return lo, hi
+
+    def shard_bin(self, X: np.ndarray, h: float, n_global: int, klo, khi):
+        """This shard's partial cells over the global key box: (keys u32, counts u32,
+        sums int64 [m, d]) -- integers, merged exactly by shard_run."""
+        X, inp = self._shard_input(X)
+        n, d = X.shape
+        klo = np.ascontiguousarray(klo, np.int64)
+        khi = np.ascontiguousarray(khi, np.int64)
+        cap = max(1, n)
+        keys = np.zeros(cap, np.uint32)
+        counts = np.zeros(cap, np.uint32)
+        sums = np.zeros((cap, d), np.int64)
+        m = C.c_int64()
+        self._check(self._lib.gs_shard_bin(self._ctx, C.byref(inp), h, int(n_global), _ptr(klo),
+                                           _ptr(khi), cap, C.byref(m), _ptr(keys),
+                                           _ptr(counts), _ptr(sums)))
+        m = m.value
+        return keys[:m].copy(), counts[:m].copy(), sums[:m].copy()
+
+    def shard_run(self, keys, counts, sums, n_shard: int, cfg: EngineConfig) -> ClusterLabeling:
+        """Merge every rank's partial cells, iterate, label this rank's shard."""
+        keys = np.ascontiguousarray(keys, np.uint32)
+        counts = np.ascontiguousarray(counts, np.uint32)
+        sums = np.ascontiguousarray(sums, np.int64)
+        d = sums.shape[1]
+        labels = np.zeros(n_shard, np.int32)
+        k = np.zeros(1, np.int64)
+        it = np.zeros(1, np.int32)
+        cv = np.zeros(1, np.int32)
+        flags = (GS_RECORD_HISTORY if cfg.record_history else 0) | cfg.debug_flags
+        c = GsConfig(cfg.h, cfg.max_iterations, flags)
+        res = GsResult(_ptr(labels), _ptr(k), _ptr(it), _ptr(cv))
+        self._check(self._lib.gs_shard_run(self._ctx, len(keys), _ptr(keys), _ptr(counts),
+                                           _ptr(sums), n_shard, C.byref(c), C.byref(res)))
+        hist = self.history(0, int(it[0])) if cfg.record_history else None
+        return ClusterLabeling(labels, self.centroids(0, int(k[0]), d), int(it[0]),
+                               bool(cv[0]), hist)
 
     # -- test hooks --------------------------------------------------------------------------
     def debug_build(self, X: np.ndarray, h: float):

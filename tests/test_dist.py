@@ -78,3 +78,129 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
         assert float(z["tmax"]) == float(world)   # max over ranks
         seen += c
     assert seen == nframes
+
+
+# ---------------------------------------------------------------- one cloud over ranks (cfg5)
+class CpuShardEngine:
+    """CPU replica of the engine's gs_shard_* calls (test infrastructure: numpy fixed-point
+    binning exactly as gs_fixq / gs_fix_centroid, then the oracle's iterate_once loop), so the
+    rank orchestration in dist.run_cloud runs without a GPU."""
+    APRON = 2
+
+    def shard_keybounds(self, X, h):
+        k = np.floor(np.asarray(X, np.float64) / h)
+        return k.min(0).astype(np.int64), k.max(0).astype(np.int64)
+
+    def _geometry(self, klo, khi):
+        ext = (khi - klo + 1 + 2 * self.APRON).astype(np.int64)
+        strides = np.ones(len(ext), np.int64)
+        for c in range(len(ext) - 2, -1, -1):
+            strides[c] = strides[c + 1] * ext[c + 1]
+        return klo - self.APRON, ext, strides
+
+    def shard_bin(self, X, h, n_global, klo, khi):
+        from oracle import oracle as O
+        X = np.asarray(X, np.float64)
+        F = O.fixed_shift(n_global, h)
+        kmin, ext, strides = self._geometry(np.asarray(klo), np.asarray(khi))
+        k = np.floor(X / h).astype(np.int64)
+        L = ((k - kmin) * strides).sum(1)
+        q = np.rint((X - k.astype(np.float64) * h) * np.ldexp(1.0, F)).astype(np.int64)
+        keys, inv = np.unique(L, return_inverse=True)
+        counts = np.bincount(inv, minlength=len(keys)).astype(np.uint32)
+        sums = np.zeros((len(keys), X.shape[1]), np.int64)
+        np.add.at(sums, inv, q)
+        self.h, self.F, self.kmin, self.ext, self.strides, self.slot = h, F, kmin, ext, strides, L
+        return keys.astype(np.uint32), counts, sums
+
+    def shard_run(self, keys, counts, sums, n_shard, cfg):
+        from oracle import oracle as O
+        from paper_2206_02200_b200.gridshift import ClusterLabeling
+        L, inv = np.unique(keys.astype(np.int64), return_inverse=True)
+        cnt = np.bincount(inv, weights=None, minlength=len(L)).astype(np.int64) * 0
+        np.add.at(cnt, inv, counts.astype(np.int64))
+        qs = np.zeros((len(L), sums.shape[1]), np.int64)
+        np.add.at(qs, inv, sums)
+        kk = (L[:, None] // self.strides) % self.ext + self.kmin
+        cent = kk.astype(np.float64) * self.h + (qs.astype(np.float64) / cnt[:, None]) * np.ldexp(1.0, -self.F)
+        root = np.arange(len(L))
+        state = dict(keys=kk, counts=cnt, centroids=cent)
+        it, conv = 0, False
+        while True:  # do-while (SPEC.md:141): converged, unchanged, or max_iter
+            r = O.iterate_once(state["keys"], state["counts"], state["centroids"], self.h)
+            root = r["parent"][root]
+            it += 1
+            state = r
+            conv = r["converged"] or not r["changed"]
+            if conv or it >= cfg.max_iterations:
+                break
+        labels = root[np.searchsorted(L, self.slot)].astype(np.int32)
+        return ClusterLabeling(labels, state["centroids"], it, conv)
+
+
+def _cloud(n=6000, seed=5, kind="small"):
+    if kind == "cfg5":  # a 3% cfg5 cloud: m0 in the tens of thousands (the global path first)
+        from paper_2206_02200_b200 import configs as CF
+        return CF.generate("cfg5", scale=0.03)[0]
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0, 10, size=(6, 3))
+    lab = rng.integers(0, 6, n)
+    return (centres[lab] + rng.normal(0, 0.6, size=(n, 3))).astype(np.float32)
+
+
+def _cloud_worker(rank, world, port, outdir, use_gpu, kind="small"):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2206_02200_b200.dist import point_shard, run_cloud
+    X = _cloud(kind=kind)
+    p0, c = point_shard(X.shape[0], world, rank)
+    if use_gpu:
+        from paper_2206_02200_b200 import gridshift as G
+        eng = G.Engine(0)
+    else:
+        eng = CpuShardEngine()
+    r = run_cloud(eng, X[p0:p0 + c], 1.0, 100)
+    np.savez(os.path.join(outdir, f"c{rank}.npz"), labels=r.labels, cent=r.centroids,
+             it=r.iterations, p0=p0, c=c)
+    dist.destroy_process_group()
+
+
+def _check_cloud(outdir, world, ref_labels, ref_cent, ref_it):
+    seen = 0
+    for r in range(world):
+        z = np.load(os.path.join(outdir, f"c{r}.npz"))
+        p0, c = int(z["p0"]), int(z["c"])
+        assert np.array_equal(z["labels"], ref_labels[p0:p0 + c])
+        assert np.array_equal(z["cent"].view(np.int64), ref_cent.view(np.int64))
+        assert int(z["it"]) == ref_it
+        seen += c
+    assert seen == len(ref_labels)
+
+
+def test_cloud_two_rank_gloo_matches_single_process(tmp_path):
+    """One cloud over 2 gloo ranks (CPU replica of the shard calls): every rank's labels and
+    the common centroids equal the oracle's single-process run bit for bit."""
+    import torch.multiprocessing as mp
+    from oracle import oracle as O
+    world = 2
+    mp.spawn(_cloud_worker, args=(world, _free_port(), str(tmp_path), False), nprocs=world,
+             join=True)
+    ref = O.run(_cloud().astype(np.float64), 1.0, 100, O.BUILD_FIXED)
+    _check_cloud(str(tmp_path), world, ref["labels"], ref["centroids"], ref["iterations"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,world", [("small", 2), ("small", 3), ("cfg5", 2)])
+def test_cloud_multi_rank_engine_matches_single_gpu(tmp_path, kind, world):
+    """The engine's gs_shard_* path: R ranks (all on cuda:0, host-side gloo exchange -- the
+    ranks' kernels never wait on each other) equal one GPU clustering the whole cloud."""
+    import torch.multiprocessing as mp
+    from paper_2206_02200_b200 import gridshift as G
+    mp.spawn(_cloud_worker, args=(world, _free_port(), str(tmp_path), True, kind), nprocs=world,
+             join=True)
+    eng = G.Engine(0)
+    ref = eng.run(_cloud(kind=kind), G.EngineConfig(1.0, 100))
+    _check_cloud(str(tmp_path), world, ref.labels, ref.centroids, ref.iterations)
+    eng.close()
