@@ -57,6 +57,8 @@ typedef struct {
 
 #define GS_RECORD_HISTORY 0x1u  /* keep per-iteration (m, max displacement)   */
 #define GS_DEVICE_OUTPUTS 0x2u  /* result.labels is a device pointer                          */
+#define GS_TIME_PHASES 0x4u    /* record phase events: gs_stats ms_* (costs ~30 us per run)  */
+#define GS_TIME_KERNEL 0x8u    /* record the binning kernel's events only: gs_stats ms_k_bin  */
 #define GS_DEBUG_GLOBAL_PATH 0x80000000u /* test hook: iterate on the multi-CTA path only */
 
 /* EngineConfig. */
@@ -99,7 +101,8 @@ gs_status gs_get_centroids(gs_ctx* ctx, int64_t frame, double* out, int64_t cap_
 gs_status gs_get_history(gs_ctx* ctx, int64_t frame, int64_t* m_t, double* maxdisp_t,
                          int32_t cap);
 
-/* Per-run counters of the last gs_run (device-timed with CUDA events on the ctx stream). */
+/* Per-run counters of the last gs_run.  The ms_* times are CUDA events on the ctx stream and
+ * are only recorded with GS_TIME_PHASES (ms_k_bin also with GS_TIME_KERNEL); else 0. */
 typedef struct {
   double ms_total;       /* first kernel to last kernel (device-resident input/outputs)   */
   double ms_bin;         /* bounds + binning + compaction (n-scale)                        */

@@ -150,6 +150,7 @@ struct gs_ctx {
   bool have_run = false;
   gs_stats stats{};
   bool stats_times_pending = false;
+  unsigned ev_mask = 0;  // which phase events this run records
   cudaEvent_t ev[12] = {};
 };
 
@@ -193,7 +194,11 @@ gs_status grow(gs_ctx* ctx, DevBuf& b, size_t bytes) {
 
 // Phase events; recorded as external event nodes while the stream is being captured so the
 // graph replay records them too (elapsed times keep working on the graph path).
+// Events cost ~3.5 us each as graph nodes (measured: 8 events = 28 us of a 170 us cfg2 run),
+// so they are recorded only when the caller asks: GS_TIME_KERNEL (the binning kernel's pair,
+// 6/7) or GS_TIME_PHASES (all).
 gs_status rec_event(gs_ctx* ctx, int i) {
+  if (!((ctx->ev_mask >> i) & 1u)) return GS_OK;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   GS_CK(cudaStreamIsCapturing(ctx->stream, &cs));
   GS_CK(cudaEventRecordWithFlags(ctx->ev[i], ctx->stream,
@@ -566,6 +571,55 @@ gs_status launch_sweep_levels(gs_ctx* ctx, int d, int64_t m, const int32_t* eoff
   return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
 }
 
+// Global path, d <= 6: neighbour lists at a fixed stride, then the single-CTA Kahn sweep with
+// the operand rows in L2 (gs_global.cuh).  Q = ctx->S1: rows [0, m) = S1 after the sweep.
+template <int D>
+gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
+  cudaStream_t st = ctx->stream;
+  const GsBox& b = ctx->box;
+  const int KP = (K + 3) & ~3;
+  GS_TRY(grow(ctx, ctx->erec, 4 * (size_t)m * KP));  // the lists (u32 rows)
+  GS_TRY(grow(ctx, ctx->rden, 8 * (size_t)m));
+  GS_TRY(grow(ctx, ctx->S1, 8 * (size_t)(2 * m + 2) * D));
+  GS_TRY(grow(ctx, ctx->lvl, 4 * (size_t)(m / 4 + 2)));  // pending counts (global fallback)
+  GS_TRY(grow(ctx, ctx->order, 4 * (size_t)m));          // queue (global fallback)
+  uint32_t* lists = ctx->erec.as<uint32_t>();
+  double* Q = ctx->S1.as<double>();
+  const int cur = ctx->cur;
+  gs::k_nbr_lists<D><<<blocks_for(m, 256), 256, 0, st>>>(
+      (int)m, b, K, KP, ctx->ckey[cur].as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(),
+      ctx->S[cur].as<double>(), ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(), lists,
+      ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(), ctx->den.as<uint32_t>(),
+      ctx->rden.as<double>(), Q, ctx->fm.as<int32_t>());
+  GS_LAUNCHED("k_nbr_lists");
+  constexpr size_t kBudget = 220 * 1024;
+  const size_t smem = 4 * ((size_t)(m + 3) / 4 + 1) + 2 * (size_t)m;
+  const int in_smem = (m < 65536 && smem <= kBudget) ? 1 : 0;
+  static bool configured = false;
+  if (!configured) {
+    GS_CK(cudaFuncSetAttribute(gs::k_sweep_global<D>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
+    configured = true;
+  }
+  gs::k_sweep_global<D><<<1, gs::sweep_global_threads<D>(), in_smem ? smem : 0, st>>>(
+      (int)m, KP, lists, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
+      ctx->ccnt[cur].as<uint32_t>(), ctx->den.as<uint32_t>(), ctx->rden.as<double>(), Q,
+      ctx->lvl.as<unsigned>(), ctx->order.as<unsigned>(), in_smem);
+  GS_LAUNCHED("k_sweep_global");
+  return GS_OK;
+}
+
+gs_status launch_global_sweep(gs_ctx* ctx, int d, int64_t m, int K) {
+  switch (d) {
+#define GS_CASE(D) \
+  case D:          \
+    return launch_global_sweep_d<D>(ctx, m, K);
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+#undef GS_CASE
+  }
+  return fail(ctx, GS_E_INVALID_PARAMETER, "d out of range");
+}
+
 // One iterate_once over all frames (frozen frames excluded).  Cells in buffer `cur`; the new
 // cells land in buffer 1-cur.  Per-frame changed/adjacency/m/disp land in the f* arrays.
 gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
@@ -580,6 +634,10 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, st));
   GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, st));
   const unsigned mb = blocks_for(m, 256);
+  if (d <= 6) {
+    // (1) fixed-stride neighbour lists (all SMs), (2) the single-CTA Kahn sweep over L2
+    GS_TRY(launch_global_sweep(ctx, d, m, K));
+  } else {
   // (1) neighbour census -> scanned record offsets -> records (all SMs)
   gs::k_nbr_count<<<mb, 256, 0, st>>>((int)m, b, K, ctx->ckey[cur].as<uint32_t>(),
                                       ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(),
@@ -617,13 +675,14 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   GS_LAUNCHED("k_nbr_fill");
   // (2) the sweep: one CTA, DAG levels, level-synchronous exact Eq. (5)
   GS_TRY(launch_sweep_levels(ctx, d, m, eoff, loff));
+  }
   gs::k_rehome<<<mb, 256, 0, ctx->stream>>>(
       (int)m, b, ctx->ckey[cur].as<uint32_t>(), ctx->S[cur].as<double>(), ctx->S1.as<double>(),
       ctx->fdone.as<int32_t>(), ctx->nkey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
       ctx->fchanged.as<int32_t>(), ctx->fdisp.as<unsigned long long>(), ctx->errflag.as<int>());
   GS_LAUNCHED("k_rehome");
   const int kb = bits_for(b.vol_total);
-  tb = ctx->cub_tmp.bytes;
+  size_t tb = ctx->cub_tmp.bytes;
   GS_CK(cub::DeviceRadixSort::SortPairs(ctx->cub_tmp.p, tb, ctx->nkey.as<uint32_t>(),
                                         ctx->skey.as<uint32_t>(), ctx->vals.as<uint32_t>(),
                                         ctx->sval.as<uint32_t>(), (int)m, 0, kb, ctx->stream));
@@ -964,6 +1023,8 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   ctx->have_run = false;
   ctx->stats = gs_stats{};
   ctx->stats_times_pending = false;
+  ctx->ev_mask = ((cfg->flags & GS_TIME_PHASES) ? 0x3ffu : 0u) |
+                 ((cfg->flags & GS_TIME_KERNEL) ? 0xc0u : 0u);
   ctx->cur = 0;
   cudaGetLastError();  // a stale error from an unrelated earlier call must not fail this run
   cudaStream_t st = ctx->stream;
@@ -1343,7 +1404,8 @@ gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out) {
     gs_stats& s = ctx->stats;
     auto el = [&](int a, int b) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+      if (((ctx->ev_mask >> a) & 1u) && ((ctx->ev_mask >> b) & 1u))
+        cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
       return (double)ms;
     };
     s.ms_h2d = el(0, 1);

@@ -16,6 +16,197 @@
 
 namespace gs {
 
+__device__ __forceinline__ double gl_div(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double fa = fabs(a);
+  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return gs_ddiv_slow(a, b);
+  const double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, y, q0);
+}
+
+// Neighbour lists at a fixed stride of KP entries (no census, no scan, no host round trip):
+// per cell the Q-row of every active neighbour in lex order (earlier neighbour j -> P1 row
+// m+1+j = C'*S_new, itself / later -> row j = C'*S_old), padded with the zero row m; #active,
+// #earlier, ΣC' and RN(1/ΣC'); Q row i = C'*S_old (S_old itself when the cell has no active
+// neighbour but itself, pin P3).  Frozen frames: nbn = 0, Q row = S_old.
+template <int D>
+__global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __restrict__ ckey,
+                            const uint32_t* __restrict__ ccnt, const double* __restrict__ S0,
+                            const int32_t* __restrict__ idx, const int32_t* __restrict__ fdone,
+                            uint32_t* __restrict__ lists, int32_t* __restrict__ nbn,
+                            int32_t* __restrict__ nbe, uint32_t* __restrict__ den,
+                            double* __restrict__ rden, double* __restrict__ Q,
+                            int32_t* __restrict__ fm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0)
+    for (int c = 0; c < D; ++c) Q[(int64_t)m * D + c] = 0.0;  // the zero row
+  if (i >= m) return;
+  const int64_t L = ckey[i];
+  const int64_t f = L / b.vol_frame;
+  uint32_t* li = lists + (int64_t)i * KP;
+  if (fdone[f]) {
+    nbn[i] = nbe[i] = 0;
+    den[i] = ccnt[i];
+    for (int c = 0; c < D; ++c) Q[(int64_t)i * D + c] = S0[(int64_t)i * D + c];
+    return;
+  }
+  atomicAdd(&fm[f], 1);
+  GsNbrOdometer od;
+  od.init(b);
+  int n = 0, e = 0;
+  uint32_t s = 0;
+  const uint32_t P1ROW = (uint32_t)m + 1u, ZROW = (uint32_t)m;
+  for (int t = 0; t < K; ++t) {
+    const int32_t j = __ldg(&idx[L + od.off]);
+    od.next(b);
+    if (j < 0) continue;
+    s += ccnt[j];
+    li[n++] = j < i ? P1ROW + (uint32_t)j : (uint32_t)j;
+    e += j < i;
+  }
+  for (int t = n; t < KP; ++t) li[t] = ZROW;
+  nbn[i] = n;
+  nbe[i] = e;
+  den[i] = s;
+  rden[i] = __drcp_rn((double)s);
+  const double ci = (double)ccnt[i];
+  for (int c = 0; c < D; ++c)
+    Q[(int64_t)i * D + c] =
+        n <= 1 ? S0[(int64_t)i * D + c] : __dmul_rn(ci, S0[(int64_t)i * D + c]);
+}
+
+// The global path's sweep: ONE CTA runs Kahn frontiers over the whole (multi-frame) cell set
+// with the state in L2 (`Q`, lists, per-cell metadata; operands read with ld.global.cg since
+// they are written during the kernel).  Per level: every warp updates the frontier's cells,
+// one lane per (cell, coordinate) -- the serial sweep's operands in lex order, +0.0 padding --
+// then every thread releases the successors of one frontier cell (pending counts packed as
+// bytes in shared memory, the queue in shared memory as u16 when the cells fit, else both in
+// global scratch).  Two block barriers per level.
+template <int D>
+constexpr int sweep_global_threads() { return D <= 3 ? 1024 : 512; }  // d > 3: 128 registers
+
+template <int D>
+__global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
+    int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
+    const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
+    const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q,
+    unsigned* pend_g, unsigned* queue_g, int in_smem) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = T >> 5;
+  unsigned* pend = in_smem ? (unsigned*)dsm : pend_g;                  // (m + 3) / 4 words
+  uint16_t* q16 = (uint16_t*)(dsm + 4 * (((size_t)m + 3) / 4 + 1));   // m entries (u16)
+  __shared__ int tail;
+  auto q_get = [&](int k) -> int { return in_smem ? (int)q16[k] : (int)queue_g[k]; };
+  auto q_put = [&](int k, int v) {
+    if (in_smem)
+      q16[k] = (uint16_t)v;
+    else
+      queue_g[k] = (unsigned)v;
+  };
+  if (tid == 0) tail = 0;
+  for (int w = tid; w < (m + 3) / 4; w += T) pend[w] = 0u;
+  __syncthreads();
+  for (int i = tid; i < m; i += T) {
+    const int e = nbe[i];
+    if (e > 0) atomicAdd(&pend[i >> 2], (unsigned)e << (8 * (i & 3)));
+    else q_put(atomicAdd(&tail, 1), i);
+  }
+  constexpr int CPW = 32 / D;
+  const int q = lane / D, c = lane - (lane / D) * D;
+  const uint32_t P1ROW = (uint32_t)m + 1u;
+  int qhead = 0;
+  for (;;) {
+    __syncthreads();  // the previous level's appends are complete
+    const int lev_end = *(volatile int*)&tail;
+    if (qhead >= lev_end) break;
+    // ---- update the frontier
+    for (int base = qhead + warp * CPW; base < lev_end; base += nwarps * CPW) {
+      const int k = base + q;
+      const bool act = q < CPW && k < lev_end;
+      const int i = act ? q_get(k) : 0;
+      const int n = act ? nbn[i] : 0;
+      if (n > 1) {  // else: frozen or no active neighbour but itself (Q row = S_old, P3)
+        const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
+        double num = 0.0;
+        if constexpr (D <= 3) {
+          // every word and operand up front (L2 latency dominates), then the whole padded
+          // chain: the zero-row padding adds +0.0
+          constexpr int NW = (D == 1 ? 3 : D == 2 ? 9 : 27) / 4 + 1;
+          uint4 r[NW];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) r[w] = __ldg(&ls[w]);
+          double v[NW][4];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            v[w][0] = __ldcg(&Q[(int64_t)r[w].x * D + c]);
+            v[w][1] = __ldcg(&Q[(int64_t)r[w].y * D + c]);
+            v[w][2] = __ldcg(&Q[(int64_t)r[w].z * D + c]);
+            v[w][3] = __ldcg(&Q[(int64_t)r[w].w * D + c]);
+          }
+#pragma unroll
+          for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
+        } else {
+          // blocks of 4 words (16 terms): each block's loads issued together, the next
+          // block's in flight while this one is added (L2 latency, not the adds, is the cost)
+          const int nq = (n + 3) >> 2;
+          constexpr int WB = 4;
+          uint4 ra[WB], rb[WB];
+          double va[WB][4], vb[WB][4];
+          auto fetch = [&](uint4 (&r)[WB], double (&v)[WB][4], int w0) {
+#pragma unroll
+            for (int w = 0; w < WB; ++w) r[w] = __ldg(&ls[min(w0 + w, KP / 4 - 1)]);
+#pragma unroll
+            for (int w = 0; w < WB; ++w) {
+              const bool in = w0 + w < nq;  // beyond the list: +0.0 terms
+              v[w][0] = in ? __ldcg(&Q[(int64_t)r[w].x * D + c]) : 0.0;
+              v[w][1] = in ? __ldcg(&Q[(int64_t)r[w].y * D + c]) : 0.0;
+              v[w][2] = in ? __ldcg(&Q[(int64_t)r[w].z * D + c]) : 0.0;
+              v[w][3] = in ? __ldcg(&Q[(int64_t)r[w].w * D + c]) : 0.0;
+            }
+          };
+          auto fold = [&](const double (&v)[WB][4]) {
+#pragma unroll
+            for (int w = 0; w < WB; ++w)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
+          };
+          fetch(ra, va, 0);
+          for (int w0 = 0; w0 < nq; w0 += 2 * WB) {
+            if (w0 + WB < nq) fetch(rb, vb, w0 + WB);
+            fold(va);
+            if (w0 + WB >= nq) break;
+            if (w0 + 2 * WB < nq) fetch(ra, va, w0 + 2 * WB);
+            fold(vb);
+          }
+        }
+        const double s1 = gl_div(num, (double)den[i], rden[i]);
+        __stcg(&Q[((int64_t)P1ROW + i) * D + c], __dmul_rn((double)ccnt[i], s1));
+        __stcg(&Q[(int64_t)i * D + c], s1);
+      }
+    }
+    __syncthreads();  // the frontier's rows are final for every later reader
+    // ---- release the frontier's later neighbours: d <= 3 a thread per frontier cell (<= 13
+    //      successors), d > 3 a warp per cell with its lanes over the successors (up to 121
+    //      for d = 5: a thread per cell would serialise them)
+    constexpr int RW = D <= 3 ? 1 : 32;  // lanes per frontier cell
+    for (int k = qhead + tid / RW; k < lev_end; k += T / RW) {
+      const int i = q_get(k);
+      const int n = nbn[i], e = nbe[i];
+      const uint32_t* li = lists + (int64_t)i * KP;
+      for (int t = e + 1 + (RW == 1 ? 0 : lane); t < n; t += RW) {  // entry e: the cell itself
+        const int j = (int)__ldg(&li[t]);
+        const unsigned sh = 8 * (j & 3);
+        const unsigned old = atomicSub(&pend[j >> 2], 1u << sh);
+        if (((old >> sh) & 0xffu) == 1u) q_put(atomicAdd(&tail, 1), j);
+      }
+    }
+    qhead = lev_end;
+  }
+}
+
 // census: number of active neighbours and of lex-earlier ones; frozen frames -> 0
 __global__ void k_nbr_count(int m, GsBox b, int K, const uint32_t* __restrict__ ckey,
                             const int32_t* __restrict__ idx, const int32_t* __restrict__ fdone,
@@ -85,13 +276,6 @@ __global__ void k_nbr_fill(int m, GsBox b, int K, const uint32_t* __restrict__ c
   rden[i] = __drcp_rn((double)s);
 }
 
-__device__ __forceinline__ double gl_div(double a, double b, double y) {
-  const double q0 = __dmul_rn(a, y);
-  const double fa = fabs(a);
-  if (!(fa < 0x1p+1000) || (fa < 0x1p-900 && a != 0.0)) return gs_ddiv_slow(a, b);
-  const double r = __fma_rn(-q0, b, a);
-  return __fma_rn(r, y, q0);
-}
 
 // Lanes per cell in the cooperative update.
 template <int D>

@@ -65,6 +65,7 @@ STATUS_NAMES = {
 
 GS_F32, GS_F64 = 0, 1
 GS_RECORD_HISTORY, GS_DEVICE_OUTPUTS = 0x1, 0x2
+GS_TIME_PHASES, GS_TIME_KERNEL = 0x4, 0x8
 GS_DEBUG_GLOBAL_PATH = 0x80000000
 
 # every symbol include/gridshift_c.h declares (checked by tests/test_abi.py)
