@@ -194,6 +194,11 @@ __device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned lon
   if (hi) atomicAdd(&w[1], hi);
 }
 
+// Probe budget of the privatised table: when a CTA sees more distinct cells than the table
+// holds (cfg5: shuffled, ~45K cells), a full table made every new key walk 16 slots (~36 % of
+// K2's time); after 4 the point takes the global atomics.
+constexpr int kBinProbes = 4;
+
 template <int D>
 __host__ __device__ constexpr int bin_table_entries() {
   return D <= 3 ? 4096 : (D <= 5 ? 2048 : 1024);
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     uint32_t h = (key * 2654435761u) & (TBL - 1);
     int hit = -1;
 #pragma unroll 1
-    for (int probe = 0; probe < 16; ++probe) {
+    for (int probe = 0; probe < kBinProbes; ++probe) {
       uint32_t k = tk[h];
       if (k == EMPTY) k = atomicCAS(&tk[h], EMPTY, key);
       if (k == EMPTY || k == key) {
