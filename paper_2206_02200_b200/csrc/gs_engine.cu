@@ -421,26 +421,33 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
           ctx->epoch_dev.as<unsigned>());
     GS_LAUNCHED("k_bounds_box");
   } else {
-    // privatised binning: one 1024-thread CTA per SM at most, >= 4096 points per CTA
-    constexpr int TBL = gs::bin_table_entries<D>();
+    // privatised binning: one 768-thread CTA per SM at most, >= 1024 points per CTA; the
+    // table sized to the CTA's points (2 entries per point, at least 256)
+    constexpr int TBL_MAX = gs::bin_table_entries<D>();
+    const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
+    const int64_t per_cta = (ntot + grid - 1) / grid;
+    int TBL = 256;
+    while (TBL < TBL_MAX && TBL < 2 * per_cta) TBL <<= 1;
     const size_t smem = (size_t)TBL * (8 * D + 8);
     static bool configured = false;
     if (!configured) {
+      const int smax = (int)((size_t)TBL_MAX * (8 * D + 8));
       GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, double>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       configured = true;
     }
-    const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
     if (dtype == GS_F32)
       gs::k_bin_priv<D, float><<<grid, 768, smem, ctx->stream>>>(
           (const float*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
+          TBL);
     else
       gs::k_bin_priv<D, double><<<grid, 768, smem, ctx->stream>>>(
           (const double*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>());
+          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
+          TBL);
     GS_LAUNCHED("k_bin_priv");
   }
   return GS_OK;

@@ -209,12 +209,25 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
                                                    const GsBox* __restrict__ pb,
                                                    uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
-                                                   uint32_t* __restrict__ slot, int* err) {
-  constexpr int TBL = bin_table_entries<D>();
+                                                   uint32_t* __restrict__ slot, int* err,
+                                                   int TBL) {
+  // TBL: table entries, a power of two <= bin_table_entries<D>() sized to the CTA's points
+  // (initialising and flushing a table costs O(TBL) per CTA)
   constexpr uint32_t EMPTY = 0xffffffffu;
-  if (*err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
+  // the first round's coordinates, the error word and the box are all requested before any
+  // of them is waited for (after an L2 flush each is a cold HBM round trip)
+  const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = (int64_t)blockIdx.x * per;
+  const int64_t p1 = min(ntot, p0 + per);
+  T xn[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * D + c] : T(0);
   __shared__ GsBox b;
-  if (threadIdx.x == 0) b = *pb;
+  __shared__ int s_err;
+  if (threadIdx.x == 0) {
+    s_err = *err;
+    b = *pb;
+  }
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned long long* ts = (unsigned long long*)smem;      // TBL * D sums
   uint32_t* tk = (uint32_t*)(ts + (size_t)TBL * D);        // TBL keys
@@ -226,17 +239,12 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     for (int c = 0; c < D; ++c) ts[j * D + c] = 0ull;
   }
   __syncthreads();
-  const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
-  const int64_t p0 = (int64_t)blockIdx.x * per;
-  const int64_t p1 = min(ntot, p0 + per);
+  if (s_err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
   const unsigned lane = threadIdx.x & 31;
   // frame of this thread's point, tracked incrementally (no 64-bit division per point)
   int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
   // warp-uniform trip count so every lane takes part in the warp aggregation; the next
   // round's coordinates are loaded before this round is processed (twice the bytes in flight)
-  T xn[D];
-#pragma unroll
-  for (int c = 0; c < D; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * D + c] : T(0);
   for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
     const int64_t p = pb + threadIdx.x;
     const bool valid = p < p1;
