@@ -1,12 +1,14 @@
-// gs_kernels.cuh — sm_100a kernels of the GridShift hot path.
+// gs_kernels.cuh — sm_100a kernels of the GridShift hot path (n-scale and global path).
 //
-//   K1 k_bounds        key bounding box + non-finite check
-//   K2 k_bin           grid_index + build_active_grid fixed-point sums
-//   K3 k_make_cells    occupied cells -> lex-ordered cell list
-//   K4 k_nbr, k_sweep  Eq. (5) sequential-semantics sweep (dataflow)   (SPEC.md:120(a-c))
-//   K5 k_rehome, k_seg, k_fold, k_idx_*, k_adjacent, k_compose
-//                      rehome + merge_into (Eq. 3-4) + has_converged   (SPEC.md:67-75, :120(d-f), :126-134)
-//   K7 k_label         label propagation through the root map
+//   K1 k_bounds_box     bounds, non-finite check, device key box
+//   K2 k_bin_priv       grid_index + build_active_grid fixed-point sums
+//   K3 k_occ            occupied cells -> lex-ordered cell list, frames
+//      k_scatter_partials  multi-GPU: merge every rank's partial cells
+//   K5 k_rehome, k_heads, k_seg, k_fold, k_idx_*, k_adjacent, k_compose
+//                       global path: rehome + merge_into (Eq. 3-4) + has_converged
+//                       (SPEC.md:67-75, :120(d-f), :126-134); the sweep is in gs_global.cuh
+//   K7 k_label          label propagation through the label table
+// K8 (the CTA-resident iteration engine) is gs_resident.cuh.
 #pragma once
 
 #include "gs_common.cuh"
@@ -138,44 +140,7 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
 }
 
 // ---------------------------------------------------------------- K2: binning
-// One pass over the points: cell key -> dense linear index L, count and fixed-point sums by
-// atomics (int64 sums are order-independent, so the result is deterministic), slot[p] = L,
-// first touch appends L to the occupied list.
-template <int D, typename T>
-__global__ void __launch_bounds__(256) k_bin(const T* __restrict__ pts, int64_t ntot, GsBox b,
-                                             uint32_t* __restrict__ cnt,
-                                             unsigned long long* __restrict__ qs,
-                                             uint32_t* __restrict__ slot,
-                                             uint32_t* __restrict__ occ, unsigned int* m0,
-                                             int* err) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ntot;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t f = p / b.n;
-    int64_t L = f * b.vol_frame;
-    long long q[D];
-    bool bad = false;
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      double x = (double)pts[p * D + c];
-      int64_t k = gs_grid_coord(x, b.h, b.inv_h);
-      int64_t rel = k - b.kmin[c];
-      bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
-      L += rel * b.stride[c];
-      q[c] = gs_fixq(x, k, b.h, b.scale);
-    }
-    if (bad) {  // cannot happen after k_bounds; guards the dense grid
-      atomicOr(err, 2);
-      continue;
-    }
-    uint32_t old = atomicAdd(&cnt[L], 1u);
-    if (old == 0) occ[atomicAdd(m0, 1u)] = (uint32_t)L;
-#pragma unroll
-    for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], (unsigned long long)q[c]);
-    slot[p] = (uint32_t)L;
-  }
-}
-
-// K2 with shared-memory privatisation.  Hot cells take tens of thousands of points (cfg2:
+// Shared-memory privatisation.  Hot cells take tens of thousands of points (cfg2:
 // 16K in one cell, cfg5: 415K), so per-point global atomics serialise at one L2 slice.  Each
 // CTA bins a contiguous range of points into a shared-memory open-addressing table of cell
 // accumulators (count + D int64 fixed-point sums); a point whose probe run finds no room falls
@@ -508,135 +473,6 @@ __global__ void k_scatter_partials(int64_t m, int d, const uint32_t* __restrict_
   }
 }
 
-// ---------------------------------------------------------------- K3: cells
-// Lex-ordered cell list from the sorted occupied list; restores the clean-grid invariant
-// (cnt = 0, qs = 0) for the cells it consumes.
-__global__ void k_make_cells(int m0, GsBox b, const uint32_t* __restrict__ occ_sorted,
-                             uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs,
-                             uint32_t* __restrict__ ckey, uint32_t* __restrict__ ccnt,
-                             double* __restrict__ S, int32_t* __restrict__ idx,
-                             int32_t* __restrict__ root, uint32_t* __restrict__ initkey) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m0) return;
-  uint32_t L = occ_sorted[i];
-  uint32_t c = cnt[L];
-  for (int k = 0; k < b.d; ++k) {
-    long long s = (long long)qs[(int64_t)L * b.d + k];
-    S[(int64_t)i * b.d + k] = gs_fix_centroid(gs_key_of(b, L, k), s, c, b.h, b.inv_scale);
-    qs[(int64_t)L * b.d + k] = 0ull;
-  }
-  cnt[L] = 0u;
-  ckey[i] = L;
-  ccnt[i] = c;
-  idx[L] = i;
-  root[i] = i;
-  initkey[i] = L;
-}
-
-// ---------------------------------------------------------------- K4: neighbour lists
-// For each cell, its active 1-neighbourhood in lexicographic v order (slot order), the number
-// of lex-earlier neighbours, and the snapshot-count denominator ΣC' (SPEC.md:120(a), :165).
-// Cells of frames that already terminated get nbn = 0 (frozen).
-__global__ void k_nbr(int m, GsBox b, int K, const uint32_t* __restrict__ ckey,
-                      const uint32_t* __restrict__ ccnt, const int32_t* __restrict__ idx,
-                      const int32_t* __restrict__ fdone, int32_t* __restrict__ nbl,
-                      int32_t* __restrict__ nbn, int32_t* __restrict__ nbe,
-                      unsigned long long* __restrict__ den, int32_t* __restrict__ fm) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  int64_t L = ckey[i];
-  int64_t f = L / b.vol_frame;
-  if (fdone[f]) {
-    nbn[i] = 0;
-    return;
-  }
-  atomicAdd(&fm[f], 1);
-  GsNbrOdometer od;
-  od.init(b);
-  int n = 0, e = 0;
-  unsigned long long s = 0;
-  int32_t* out = nbl + (int64_t)i * K;
-  for (int t = 0; t < K; ++t) {
-    int32_t j = idx[L + od.off];
-    if (j >= 0) {
-      out[n++] = j;
-      e += (j < i);
-      s += ccnt[j];
-    }
-    od.next(b);
-  }
-  nbn[i] = n;
-  nbe[i] = e;
-  den[i] = s;
-}
-
-// ---------------------------------------------------------------- K4: sweep
-// Eq. (5) with the exact sequential (Gauss-Seidel) semantics of the lexicographic sweep:
-// each cell waits for its lex-earlier active neighbours (dataflow over the static DAG of one
-// sweep), then sums C'*S over its neighbourhood in lex v order — earlier neighbours' NEW
-// centroids, its own and later neighbours' OLD ones — and divides by ΣC' (pin P2).  Cells are
-// claimed in lex order through a ticket, so a warp only ever waits on cells owned by warps that
-// are already running: deadlock-free for any grid size.  Isolated and frozen cells keep their
-// centroid bit-for-bit (pin P3).
-__global__ void __launch_bounds__(256) k_sweep(int m, int d, int K,
-                                               const uint32_t* __restrict__ ccnt,
-                                               const double* __restrict__ S0, double* S1,
-                                               const int32_t* __restrict__ nbl,
-                                               const int32_t* __restrict__ nbn,
-                                               const int32_t* __restrict__ nbe,
-                                               const unsigned long long* __restrict__ den,
-                                               uint32_t* flag, uint32_t epoch,
-                                               unsigned int* ticket, int* err) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(ticket, 32u);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= (unsigned)m) return;
-    const int i = (int)base + lane;
-    bool pending = i < m;
-    int n_nb = 0, n_e = 0, t_ok = 0;
-    if (pending) {
-      n_nb = nbn[i];
-      n_e = nbe[i];
-      if (n_nb <= 1) {
-        for (int c = 0; c < d; ++c) S1[(int64_t)i * d + c] = S0[(int64_t)i * d + c];
-        gs_st_release(&flag[i], epoch);
-        pending = false;
-      }
-    }
-    const int32_t* lst = nbl + (int64_t)(pending ? i : 0) * K;
-    unsigned spins = 0;
-    while (__any_sync(kFull, pending)) {
-      if (pending) {
-        while (t_ok < n_e && gs_ld_acquire(&flag[lst[t_ok]]) == epoch) ++t_ok;
-        if (++spins > (1u << 26)) {  // watchdog: a broken DAG must not hang the device
-          atomicOr(err, 8);
-          pending = false;
-        } else if (t_ok == n_e) {
-          double num[GS_DMAX];
-          for (int c = 0; c < d; ++c) num[c] = 0.0;
-          for (int t = 0; t < n_nb; ++t) {
-            const int32_t j = lst[t];
-            const double w = (double)ccnt[j];
-            if (t < n_e) {
-              for (int c = 0; c < d; ++c)
-                num[c] = __dadd_rn(num[c], __dmul_rn(w, __ldcg(&S1[(int64_t)j * d + c])));
-            } else {
-              for (int c = 0; c < d; ++c)
-                num[c] = __dadd_rn(num[c], __dmul_rn(w, S0[(int64_t)j * d + c]));
-            }
-          }
-          const double dd = (double)den[i];
-          for (int c = 0; c < d; ++c) S1[(int64_t)i * d + c] = __ddiv_rn(num[c], dd);
-          gs_st_release(&flag[i], epoch);
-          pending = false;
-        }
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------- K5: rehome
 // New key floor(S/h) per cell (SPEC.md:120(d)), per-frame `changed` (SPEC.md:120(e)) and max
 // sweep displacement.  Frozen frames keep their keys.
@@ -757,25 +593,6 @@ __global__ void k_adjacent(int m, GsBox b, int K, const uint32_t* __restrict__ k
 __global__ void k_compose(int m0, const int32_t* __restrict__ parent, int32_t* __restrict__ root) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m0) root[i] = parent[root[i]];
-}
-
-// first final cell of every frame (cells are frame-major)
-__global__ void k_frame_first(int k, int64_t vol_frame, const uint32_t* __restrict__ key,
-                              int32_t* __restrict__ ffirst) {
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= k) return;
-  const int64_t f = key[g] / vol_frame;
-  if (g == 0 || (int64_t)(key[g - 1] / vol_frame) != f) ffirst[f] = g;
-}
-
-// label table over the initial cells' dense indices: lab[L0] = cluster id within the frame
-__global__ void k_labtab(int m0, int64_t vol_frame, const uint32_t* __restrict__ initkey,
-                         const int32_t* __restrict__ root, const int32_t* __restrict__ ffirst,
-                         int32_t* __restrict__ lab) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m0) return;
-  const uint32_t L = initkey[i];
-  lab[L] = root[i] - ffirst[L / vol_frame];
 }
 
 // K7: labels[p] = lab[slot[p]]

@@ -897,11 +897,5 @@ __global__ void k_frame_counts(int64_t nf, const int32_t* __restrict__ first,
   if (f < nf) count[f] -= first[f];
 }
 
-// label table from frame-local final ids
-__global__ void k_labtab_local(int m0, const uint32_t* __restrict__ initkey,
-                               const int32_t* __restrict__ root, int32_t* __restrict__ lab) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m0) lab[initkey[i]] = root[i];
-}
 
 }  // namespace gs
