@@ -40,7 +40,11 @@ typedef enum {
   GS_E_NO_DEVICE = 10          /* Error: no sm_100 device visible                               */
 } gs_status;
 
-typedef enum { GS_F32 = 0, GS_F64 = 1 } gs_dtype;
+/* GS_U8: 8-bit RGB pixels, 3 bytes per point, turned into features on the device exactly as
+ * the segmentation front end does: d = 3 -> (r,g,b)/255; d = 5 -> (r,g,b)/255
+ * followed by x = col/(W-1), y = row/(H-1) with the image width W in gs_input.reserved
+ * (n = W*H, row-major).  Reads 3 B/pixel instead of 12-20 B of fp32 features. */
+typedef enum { GS_F32 = 0, GS_F64 = 1, GS_U8 = 2 } gs_dtype;
 
 /* A dataset: `batch` independent frames of n points each, d coordinates,
  * row-major [batch][n][d].  Frames are clustered independently.  With
@@ -52,7 +56,7 @@ typedef struct {
   int32_t dtype;  /* gs_dtype */
   int64_t batch;  /* frames, >= 1 */
   int32_t on_device;
-  int32_t reserved;
+  int32_t reserved;  /* GS_U8 with d = 5: the image width W; else 0 */
 } gs_input;
 
 #define GS_RECORD_HISTORY 0x1u  /* keep per-iteration (m, max displacement)   */
@@ -129,6 +133,12 @@ gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out);
 
 const char* gs_last_error(const gs_ctx* ctx); /* valid until the next call on ctx */
 const char* gs_status_string(gs_status s);
+
+/* Segmentation render (fused K7 epilogue) for `frame` of the last gs_run:
+ * every pixel replaced by its segment's mean colour, the centroid's first three components
+ * times 255 rounded half-up, clamped to 0..255.  out: n*3 bytes, host memory
+ * or (on_device) device memory. */
+gs_status gs_render(gs_ctx* ctx, int64_t frame, uint8_t* out, int32_t on_device);
 
 /* ---- multi-GPU: one point cloud split over R ranks ----
  * Each rank calls, on its own contiguous shard of the cloud (batch = 1):

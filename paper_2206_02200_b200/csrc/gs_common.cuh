@@ -48,6 +48,53 @@ __device__ __forceinline__ int64_t gs_grid_coord(double x, double h, double inv_
   return (int64_t)fl;
 }
 
+// ---- segmentation front end fused into the point readers: 8-bit RGB
+// pixels are read as 3 bytes and turned into features on the fly -- rgb: channel / 255;
+// rgbxy: + x = col / (W-1), y = row / (H-1) -- instead of a 12-24 B/pixel fp32 feature array.
+// Every quotient is RN(a / b) for a small non-negative integer a: Markstein's form from
+// y = RN(1/b) is the correctly rounded quotient there (see rs_div), so the features equal the
+// oracle's `img / 255.0` bit for bit.
+struct GsImg {
+  int W = 0, H = 0;       // rgbxy image width / height (0: rgb only)
+  double wm1 = 0, hm1 = 0, rw = 0, rh = 0;
+};
+
+__device__ __forceinline__ double gs_div_small(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  return __fma_rn(__fma_rn(-q0, b, a), y, q0);
+}
+
+template <typename T, int D>
+__host__ __device__ constexpr int gs_raw_cols() {
+  return sizeof(T) == 1 ? 3 : D;  // uint8_t: r, g, b bytes per pixel
+}
+
+// feature c of a point from its raw row; pl = the point's index within its frame
+template <typename T, int D>
+__device__ __forceinline__ double gs_feature(const T* raw, int c, int64_t pl, const GsImg& im) {
+  if constexpr (sizeof(T) == 1) {
+    if (c < 3) return gs_div_small((double)raw[c], 255.0, 1.0 / 255.0);
+    const uint32_t ul = (uint32_t)pl, col = ul % (uint32_t)im.W, row = ul / (uint32_t)im.W;
+    return c == 3 ? gs_div_small((double)col, im.wm1, im.rw)
+                  : gs_div_small((double)row, im.hm1, im.rh);
+  } else {
+    return (double)raw[c];
+  }
+}
+
+__device__ __forceinline__ GsImg gs_img(int W, int64_t n) {
+  GsImg im;
+  if (W > 1) {
+    im.W = W;
+    im.H = (int)(n / W);
+    im.wm1 = (double)(W - 1);
+    im.hm1 = (double)(im.H - 1);
+    im.rw = __drcp_rn(im.wm1);
+    im.rh = __drcp_rn(im.hm1);
+  }
+  return im;
+}
+
 // Fixed-point offset of coordinate x inside its cell k (oracle build mode 1):
 // nearbyint((x - k*h) * 2^F) as int64.
 __device__ __forceinline__ long long gs_fixq(double x, int64_t k, double h, double scale) {

@@ -94,6 +94,7 @@ struct gs_ctx {
   int64_t ctl_nf = 0;
   // bumped whenever a device buffer is (re)allocated: a cached graph holds raw pointers
   uint64_t alloc_gen = 0;
+  int img_w = 0;  // GS_U8 rgbxy: image width of the current call
   // multi-GPU shard state (gs_shard_*): the global key box from gs_shard_bin, and for
   // gs_shard_run the merged partial cells the run starts from instead of binning
   bool shard_box = false;
@@ -113,9 +114,10 @@ struct gs_ctx {
     int d = 0, dtype = 0;
     double h = 0;
     int max_iter = 0;
+    int img_w = 0;
     bool operator==(const ShapeKey& o) const {
       return n == o.n && nf == o.nf && d == o.d && dtype == o.dtype && h == o.h &&
-             max_iter == o.max_iter;
+             max_iter == o.max_iter && img_w == o.img_w;
     }
   } shape;
   int shape_ms = 0;
@@ -228,11 +230,23 @@ gs_status validate(const gs_input* in, const gs_config* cfg) {
   if (!(cfg->h > 0.0) || !std::isfinite(cfg->h)) return GS_E_INVALID_BANDWIDTH;
   if (in->n < 1 || in->batch < 1) return in->n < 1 ? GS_E_EMPTY_INPUT : GS_E_INVALID_PARAMETER;
   if (in->d < 1 || in->d > GS_MAX_DIM) return GS_E_INVALID_PARAMETER;
-  if (in->dtype != GS_F32 && in->dtype != GS_F64) return GS_E_INVALID_PARAMETER;
+  if (in->dtype != GS_F32 && in->dtype != GS_F64 && in->dtype != GS_U8)
+    return GS_E_INVALID_PARAMETER;
+  if (in->dtype == GS_U8) {  // pixels: rgb (d = 3) or rgbxy (d = 5, width in `reserved`)
+    if (in->d != 3 && in->d != 5) return GS_E_INVALID_PARAMETER;
+    if (in->d == 5 && (in->reserved < 2 || in->n % in->reserved != 0 || in->n / in->reserved < 2))
+      return GS_E_INVALID_PARAMETER;
+  }
   if (cfg->max_iter < 1) return GS_E_INVALID_PARAMETER;
   if (!in->points) return GS_E_INVALID_PARAMETER;
   if (in->n * in->batch > (int64_t(1) << 40)) return GS_E_INVALID_PARAMETER;
   return GS_OK;
+}
+
+// bytes of the raw point array of `in` (GS_U8: 3 bytes per pixel whatever d is)
+size_t input_bytes(const gs_input* in) {
+  const size_t per = in->dtype == GS_U8 ? 3 : (in->dtype == GS_F32 ? 4 : 8) * (size_t)in->d;
+  return per * (size_t)in->n * (size_t)in->batch;
 }
 
 // Dense grid: grow to hold `cells` cells of dimension d; fresh memory gets the clean state.
@@ -402,23 +416,18 @@ gs_status make_box_from_cells(gs_ctx* ctx, int d, double h, int64_t m, const int
   return GS_OK;
 }
 
-template <int D>
-gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t ntot, bool bounds,
-                            unsigned nblk, double h = 0, int64_t n = 0, int64_t nf = 0) {
+template <int D, typename T>
+gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool bounds,
+                              unsigned nblk, double h, int64_t n, int64_t nf) {
+  const int img_w = ctx->img_w;
   if (bounds) {
     unsigned* ctr = ctx->counters.as<unsigned>();
     int* err = ctx->errflag.as<int>();
     const int F = gs_fixed_shift(n, h);
-    if (dtype == GS_F32)
-      gs::k_bounds_box<D, float><<<nblk, 256, 0, ctx->stream>>>(
-          (const float*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
-          ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
-          ctx->epoch_dev.as<unsigned>());
-    else
-      gs::k_bounds_box<D, double><<<nblk, 256, 0, ctx->stream>>>(
-          (const double*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
-          ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
-          ctx->epoch_dev.as<unsigned>());
+    gs::k_bounds_box<D, T><<<nblk, 256, 0, ctx->stream>>>(
+        (const T*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
+        ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
+        ctx->epoch_dev.as<unsigned>(), img_w);
     GS_LAUNCHED("k_bounds_box");
   } else {
     // privatised binning: one 768-thread CTA per SM at most, >= 1024 points per CTA; the
@@ -432,25 +441,27 @@ gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t nto
     static bool configured = false;
     if (!configured) {
       const int smax = (int)((size_t)TBL_MAX * (8 * D + 8));
-      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, float>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, double>,
+      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
       configured = true;
     }
-    if (dtype == GS_F32)
-      gs::k_bin_priv<D, float><<<grid, 768, smem, ctx->stream>>>(
-          (const float*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
-          TBL);
-    else
-      gs::k_bin_priv<D, double><<<grid, 768, smem, ctx->stream>>>(
-          (const double*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-          ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
-          TBL);
+    gs::k_bin_priv<D, T><<<grid, 768, smem, ctx->stream>>>(
+        (const T*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
+        ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
+        TBL, img_w);
     GS_LAUNCHED("k_bin_priv");
   }
   return GS_OK;
+}
+
+template <int D>
+gs_status launch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int64_t ntot, bool bounds,
+                            unsigned nblk, double h = 0, int64_t n = 0, int64_t nf = 0) {
+  if (dtype == GS_F32) return launch_bounds_bin_t<D, float>(ctx, pts, ntot, bounds, nblk, h, n, nf);
+  if (dtype == GS_F64) return launch_bounds_bin_t<D, double>(ctx, pts, ntot, bounds, nblk, h, n, nf);
+  if constexpr (D == 3 || D == 5)  // GS_U8 pixels: rgb / rgbxy
+    return launch_bounds_bin_t<D, uint8_t>(ctx, pts, ntot, bounds, nblk, h, n, nf);
+  return fail(ctx, GS_E_INVALID_PARAMETER, "8-bit pixels need d = 3 or 5");
 }
 
 gs_status dispatch_bounds_bin(gs_ctx* ctx, const void* pts, int dtype, int d, int64_t ntot,
@@ -1016,14 +1027,18 @@ struct HostProf {
   }
 };
 
+int img_width(const gs_input* in) {
+  return (in->dtype == GS_U8 && in->d == 5) ? in->reserved : 0;
+}
+
 gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
   HostProf hp;
   GS_TRY(validate(in, cfg));
+  if (!ctx->shard_front) ctx->img_w = img_width(in);
   if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
     return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
   const int d = in->d;
   const int64_t n = in->n, nf = in->batch, ntot = n * nf;
-  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
   const bool rec = (cfg->flags & GS_RECORD_HISTORY) != 0;
   const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
   const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
@@ -1044,20 +1059,20 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   GS_TRY(map_readback(ctx, nf, cfg->max_iter, &rb));
   ctx->hist_m.assign(rec ? nf : 0, {});
   ctx->hist_d.assign(rec ? nf : 0, {});
-  if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, esz * d * ntot));
+  if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
   const void* dpts = in->on_device ? in->points : ctx->pts.p;
   int64_t vol_hint = 0;  // the cached shape's grid volume (sizes the compaction launch)
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
     if (ctx->shard_front) return launch_shard_front(ctx, d);
     GS_TRY(rec_event(ctx, 0));
     if (!in->on_device)
-      GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * ntot, cudaMemcpyHostToDevice, st));
+      GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
     GS_TRY(rec_event(ctx, 1));
     GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint));
     GS_TRY(rec_event(ctx, 2));
     return GS_OK;
   };
-  const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter};
+  const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter, ctx->img_w};
   std::vector<int32_t> g_iters(nf, 0);
   int64_t swept = 0;
   if (!force_global && !ctx->shard_front && ctx->shape_ms > 0 && key == ctx->shape) {
@@ -1436,16 +1451,17 @@ gs_status gs_shard_keybounds(gs_ctx* ctx, const gs_input* in, double h, int64_t*
   if (s != GS_OK) return s;
   if (!ctx || !klo || !khi) return GS_E_INVALID_PARAMETER;
   if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "a shard is one frame");
+  if (img_width(in)) return fail(ctx, GS_E_INVALID_PARAMETER, "rgbxy pixels cannot be sharded");
   ctx->err.clear();
+  ctx->img_w = 0;
   cudaSetDevice(ctx->device);
   cudaStream_t st = ctx->stream;
   const int d = in->d;
   const int64_t n = in->n;
-  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
   const void* dpts = in->points;
   if (!in->on_device) {
-    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
-    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice, st));
+    GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
     dpts = ctx->pts.p;
   }
   const unsigned nblk = blocks_for(n, 256 * 4, (int64_t)ctx->num_sms * 2);
@@ -1482,12 +1498,13 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_glob
     return GS_E_INVALID_PARAMETER;
   if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "a shard is one frame");
   if (n_global < in->n) return fail(ctx, GS_E_INVALID_PARAMETER, "n_global < shard size");
+  if (img_width(in)) return fail(ctx, GS_E_INVALID_PARAMETER, "rgbxy pixels cannot be sharded");
   ctx->err.clear();
+  ctx->img_w = 0;
   cudaSetDevice(ctx->device);
   cudaStream_t st = ctx->stream;
   const int d = in->d;
   const int64_t n = in->n;
-  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
   // the global box: same keys, strides and fixed-point exponent on every rank
   GsBox b;
   std::memset(&b, 0, sizeof(b));
@@ -1531,8 +1548,8 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_glob
   }
   const void* dpts = in->points;
   if (!in->on_device) {
-    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
-    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice, st));
+    GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
     dpts = ctx->pts.p;
   }
   GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
@@ -1594,6 +1611,34 @@ gs_status gs_shard_run(gs_ctx* ctx, int64_t m_all, const uint32_t* keys, const u
   return s;
 }
 
+gs_status gs_render(gs_ctx* ctx, int64_t frame, uint8_t* out, int32_t on_device) {
+  if (!ctx || !out) return GS_E_INVALID_PARAMETER;
+  if (!ctx->have_run || frame < 0 || frame >= ctx->nframes)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "no such frame in the last run");
+  if (ctx->box.d < 3) return fail(ctx, GS_E_INVALID_PARAMETER, "render needs rgb features");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->box.n, k = ctx->h_k[frame];
+  GS_TRY(grow(ctx, ctx->pkeys, 4 * (size_t)std::max<int64_t>(k, 1)));  // colour table
+  uint8_t* dout = out;
+  if (!on_device) {
+    GS_TRY(grow(ctx, ctx->labels, 3 * (size_t)n));
+    dout = ctx->labels.as<uint8_t>();
+  }
+  gs::k_segment_colours<<<blocks_for(k, 128), 128, 0, st>>>(
+      k, ctx->box.d, ctx->S[ctx->cur].as<double>() + (size_t)ctx->h_ffirst[frame] * ctx->box.d,
+      ctx->pkeys.as<uint32_t>());
+  GS_LAUNCHED("k_segment_colours");
+  gs::k_render<<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+      n, ctx->slot.as<uint32_t>() + (size_t)frame * n, ctx->lab.as<int32_t>(),
+      ctx->pkeys.as<uint32_t>(), dout);
+  GS_LAUNCHED("k_render");
+  if (!on_device)
+    GS_CK(cudaMemcpyAsync(out, dout, 3 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  return GS_OK;
+}
+
 gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_m,
                          int64_t* m_out, int64_t* keys, int64_t* counts, double* centroids,
                          int64_t* slot) {
@@ -1601,14 +1646,14 @@ gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_
   GS_TRY(validate(in, &cfg));
   if (!ctx) return GS_E_INVALID_PARAMETER;
   if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "debug build takes one frame");
+  ctx->img_w = img_width(in);
   cudaSetDevice(ctx->device);
   const int d = in->d;
   const int64_t n = in->n;
-  const size_t esz = in->dtype == GS_F32 ? 4 : 8;
   const void* dpts = in->points;
   if (!in->on_device) {
-    GS_TRY(grow(ctx, ctx->pts, esz * d * n));
-    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, esz * d * n, cudaMemcpyHostToDevice,
+    GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice,
                           ctx->stream));
     dpts = ctx->pts.p;
   }

@@ -29,7 +29,10 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
                                                     int64_t n, int64_t nframes,
                                                     int64_t cap_cells, GsBox* __restrict__ out,
                                                     int* err, long long* need,
-                                                    unsigned* ticket, unsigned* epoch) {
+                                                    unsigned* ticket, unsigned* epoch,
+                                                    int img_w = 0) {
+  constexpr int RC = gs_raw_cols<T, D>();
+  const GsImg im = gs_img(img_w, n);
   double mn[D], mx[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) {
@@ -39,9 +42,13 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
   bool bad = false;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ntot;
        p += (int64_t)gridDim.x * blockDim.x) {
+    T raw[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) raw[c] = pts[p * RC + c];
+    const int64_t pl = (sizeof(T) == 1 && D > 3) ? p % n : 0;  // rgbxy needs the pixel index
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      double x = (double)pts[p * D + c];
+      double x = gs_feature<T, D>(raw, c, pl, im);
       bad |= !isfinite(x);
       mn[c] = fmin(mn[c], x);
       mx[c] = fmax(mx[c], x);
@@ -175,7 +182,8 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
                                                    uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
                                                    uint32_t* __restrict__ slot, int* err,
-                                                   int TBL) {
+                                                   int TBL, int img_w = 0) {
+  constexpr int RC = gs_raw_cols<T, D>();
   // TBL: table entries, a power of two <= bin_table_entries<D>() sized to the CTA's points
   // (initialising and flushing a table costs O(TBL) per CTA)
   constexpr uint32_t EMPTY = 0xffffffffu;
@@ -184,9 +192,9 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
   const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
   const int64_t p0 = (int64_t)blockIdx.x * per;
   const int64_t p1 = min(ntot, p0 + per);
-  T xn[D];
+  T xn[RC];
 #pragma unroll
-  for (int c = 0; c < D; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * D + c] : T(0);
+  for (int c = 0; c < RC; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * RC + c] : T(0);
   __shared__ GsBox b;
   __shared__ int s_err;
   if (threadIdx.x == 0) {
@@ -206,6 +214,7 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
   __syncthreads();
   if (s_err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
   const unsigned lane = threadIdx.x & 31;
+  const GsImg im = gs_img(img_w, b.n);
   // frame of this thread's point, tracked incrementally (no 64-bit division per point)
   int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
   // warp-uniform trip count so every lane takes part in the warp aggregation; the next
@@ -213,12 +222,12 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
   for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
     const int64_t p = pb + threadIdx.x;
     const bool valid = p < p1;
-    T xc[D];
+    T xc[RC];
 #pragma unroll
-    for (int c = 0; c < D; ++c) xc[c] = xn[c];
+    for (int c = 0; c < RC; ++c) xc[c] = xn[c];
     const int64_t pn = p + blockDim.x;
 #pragma unroll
-    for (int c = 0; c < D; ++c) xn[c] = pn < p1 ? pts[pn * D + c] : T(0);
+    for (int c = 0; c < RC; ++c) xn[c] = pn < p1 ? pts[pn * RC + c] : T(0);
     int64_t L = 0;
     long long q[D];
     bool bad = false;
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
       L = fr * b.vol_frame;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double x = (double)xc[c];
+        const double x = gs_feature<T, D>(xc, c, p - fr * b.n, im);
         const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
         const int64_t rel = k - b.kmin[c];
         bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
@@ -605,6 +614,35 @@ __global__ void __launch_bounds__(256) k_label(int64_t ntot, const uint32_t* __r
 }
 
 // test hook: rank of every point's initial cell
+// Segmentation render: a segment's colour is its centroid's first three
+// components times 255, rounded half-up, clamped to 0..255 (packed r | g<<8 | b<<16)
+__global__ void k_segment_colours(int64_t k, int d, const double* __restrict__ cent,
+                                  uint32_t* __restrict__ rgb) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= k) return;
+  uint32_t packed = 0;
+  for (int c = 0; c < 3; ++c) {
+    double v = floor(__dadd_rn(__dmul_rn(cent[g * d + c], 255.0), 0.5));
+    v = fmin(fmax(v, 0.0), 255.0);
+    packed |= (uint32_t)v << (8 * c);
+  }
+  rgb[g] = packed;
+}
+
+// every pixel -> its segment's colour (label = lab[slot[p]], as K7)
+__global__ void __launch_bounds__(256) k_render(int64_t n, const uint32_t* __restrict__ slot,
+                                                const int32_t* __restrict__ lab,
+                                                const uint32_t* __restrict__ rgb,
+                                                uint8_t* __restrict__ out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = rgb[lab[slot[p]]];
+    out[3 * p] = (uint8_t)(v & 0xffu);
+    out[3 * p + 1] = (uint8_t)((v >> 8) & 0xffu);
+    out[3 * p + 2] = (uint8_t)((v >> 16) & 0xffu);
+  }
+}
+
 __global__ void k_slot_rank(int64_t ntot, const uint32_t* __restrict__ slot,
                             const int32_t* __restrict__ idx, int64_t* __restrict__ out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

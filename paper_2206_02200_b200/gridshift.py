@@ -63,7 +63,7 @@ STATUS_NAMES = {
     7: "GS_E_CUDA", 8: "GS_E_OOM", 9: "GS_E_NCCL", 10: "GS_E_NO_DEVICE",
 }
 
-GS_F32, GS_F64 = 0, 1
+GS_F32, GS_F64, GS_U8 = 0, 1, 2
 GS_RECORD_HISTORY, GS_DEVICE_OUTPUTS = 0x1, 0x2
 GS_TIME_PHASES, GS_TIME_KERNEL = 0x4, 0x8
 GS_DEBUG_GLOBAL_PATH = 0x80000000
@@ -73,7 +73,7 @@ EXPORTED = [
     "gs_validate", "gs_create", "gs_destroy", "gs_run", "gs_get_centroids", "gs_get_history",
     "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
     "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
-    "gs_shard_run",
+    "gs_shard_run", "gs_render",
 ]
 
 
@@ -130,6 +130,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.gs_debug_iterate_once.argtypes = [P, I32, D, I64, P, P, P, P, P, P, P, P, P, P, P, P]
     lib.gs_fixed_shift.argtypes = [I64, D]
     lib.gs_fixed_shift.restype = I32
+    lib.gs_render.argtypes = [P, I64, P, I32]
     lib.gs_shard_keybounds.argtypes = [P, C.POINTER(GsInput), D, P, P]
     lib.gs_shard_bin.argtypes = [P, C.POINTER(GsInput), D, I64, P, P, I64, P, P, P, P]
     lib.gs_shard_run.argtypes = [P, I64, P, P, P, I64, C.POINTER(GsConfig), C.POINTER(GsResult)]
@@ -227,6 +228,7 @@ class Engine:
         c = GsConfig(cfg.h, cfg.max_iterations, flags)
         res = GsResult(labels_ptr, _ptr(k), _ptr(it), _ptr(cv))
         self._check(self._lib.gs_run(self._ctx, C.byref(inp), C.byref(c), C.byref(res)))
+        self._last_n = n
         return k, it, cv
 
     def run_batch(self, X: np.ndarray, cfg: EngineConfig, want_centroids: bool = True
@@ -281,6 +283,42 @@ class Engine:
         out = {name: getattr(s, name) for name, _ in GsStats._fields_}
         out["sweep_modes"] = list(out["sweep_modes"])
         out["resident_cycles"] = list(out["resident_cycles"])
+        return out
+
+    # -- segmentation front end / render, fused into K1/K2 and K7 ---------
+    def run_image(self, img: np.ndarray, cfg: EngineConfig, mode: str = "rgb") -> ClusterLabeling:
+        """segment(): 8-bit RGB image [H, W, 3] (or a batch [B, H, W, 3]); features (r,g,b)/255
+        (mode "rgb", d = 3) or + (col/(W-1), row/(H-1)) ("rgbxy", d = 5) are formed on the
+        device from the 3-byte pixels.  Returns frame 0's labelling (labels [H*W])."""
+        img = np.ascontiguousarray(img, np.uint8)
+        if img.ndim == 3:
+            img = img[None]
+        if img.ndim != 4 or img.shape[3] != 3:
+            raise InvalidParameterError("image must be [H, W, 3] or [B, H, W, 3] uint8")
+        B, H, W, _ = img.shape
+        d = 3 if mode == "rgb" else 5
+        if mode not in ("rgb", "rgbxy"):
+            raise InvalidParameterError("mode is rgb or rgbxy")
+        n = H * W
+        labels = np.zeros((B, n), np.int32)
+        k = np.zeros(B, np.int64)
+        it = np.zeros(B, np.int32)
+        cv = np.zeros(B, np.int32)
+        flags = (GS_RECORD_HISTORY if cfg.record_history else 0) | cfg.debug_flags
+        inp = GsInput(_ptr(img), n, d, GS_U8, B, 0, W if d == 5 else 0)
+        c = GsConfig(cfg.h, cfg.max_iterations, flags)
+        res = GsResult(_ptr(labels), _ptr(k), _ptr(it), _ptr(cv))
+        self._check(self._lib.gs_run(self._ctx, C.byref(inp), C.byref(c), C.byref(res)))
+        self._last_n = n
+        return ClusterLabeling(labels[0], self.centroids(0, int(k[0]), d), int(it[0]),
+                               bool(cv[0]), None)
+
+    def render(self, frame: int = 0) -> np.ndarray:
+        """render(): every pixel of `frame` replaced by its segment's mean colour (uint8
+        [n, 3]; centroid rgb * 255 rounded half-up)."""
+        n = getattr(self, "_last_n", 0)
+        out = np.zeros((n, 3), np.uint8)
+        self._check(self._lib.gs_render(self._ctx, frame, _ptr(out), 0))
         return out
 
     # -- one point cloud over several ranks (gridshift_c.h gs_shard_*; driven by dist.py) ----

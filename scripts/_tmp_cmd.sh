@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for W in cfg5 cfg4 cfg2; do timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${W}_r1J.log 2>&1; echo "bench $W rc=$?"; done
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log | cut -c1-300
+for W in cfg2 cfg4; do timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${W}_r1L.log 2>&1; echo "bench $W rc=$?"; done

@@ -234,3 +234,60 @@ def test_graph_replay_new_data_same_shape():
         cen = eng.centroids(0, int(k[0]), 3)
         assert np.array_equal(_bits(cen), _bits(o["centroids"])), rep
     eng.close()
+
+
+# ---------------------------------------------------------------- segmentation front end (§8(f)1)
+def _u8_image(H=96, W=128, seed=3):
+    """Voronoi regions of random colours + noise, quantised to 8 bits (a cfg2-like image)."""
+    rng = np.random.default_rng(seed)
+    sites = rng.uniform(0, 1, size=(10, 2)) * [H, W]
+    cols = rng.integers(0, 256, size=(10, 3))
+    yy, xx = np.mgrid[0:H, 0:W]
+    reg = np.argmin(((yy[..., None] - sites[:, 0]) ** 2 + (xx[..., None] - sites[:, 1]) ** 2), -1)
+    img = cols[reg] + rng.normal(0, 6, size=(H, W, 3))
+    return np.clip(np.rint(img), 0, 255).astype(np.uint8)
+
+
+def _features(img, mode):
+    H, W, _ = img.shape
+    f = img.reshape(-1, 3).astype(np.float64) / 255.0       # SPEC.md:390: channel / 255
+    if mode == "rgbxy":
+        yy, xx = np.mgrid[0:H, 0:W]
+        f = np.concatenate([f, (xx.reshape(-1, 1) / (W - 1)), (yy.reshape(-1, 1) / (H - 1))], 1)
+    return f
+
+
+@pytest.mark.parametrize("mode,h", [("rgb", 0.08), ("rgbxy", 0.1)])
+def test_u8_pixels_bit_exact(engine, mode, h):
+    """8-bit pixels turned into features on the device (3 B/pixel read) equal the oracle run
+    on the host-made features img / 255 (and x/(W-1), y/(H-1)) bit for bit."""
+    img = _u8_image()
+    g = engine.run_image(img, G.EngineConfig(h, 100), mode)
+    o = O.run(_features(img, mode), h, 100, O.BUILD_FIXED)
+    assert np.array_equal(g.labels, o["labels"])
+    assert np.array_equal(_bits(g.centroids), _bits(o["centroids"]))
+    assert g.iterations == o["iterations"]
+
+
+def test_u8_spec_feature_examples(engine):
+    """black -> (0,0,0), white -> (1,1,1); rgbxy pixel (1,0) of a 2x2 image
+    -> x = 1, y = 0.  With h > 1 every pixel shares one cell whose fixed-point mean is exact
+    here, so the single centroid is the mean of the features."""
+    img = np.array([[[0, 0, 0], [255, 255, 255]], [[0, 0, 0], [255, 255, 255]]], np.uint8)
+    g = engine.run_image(img, G.EngineConfig(4.0, 10), "rgbxy")
+    assert g.centroids.shape == (1, 5)
+    assert np.allclose(g.centroids[0], [0.5, 0.5, 0.5, 0.5, 0.5], rtol=0, atol=1e-15)
+
+
+def test_render_mean_colours(engine):
+    """render: every pixel gets its segment's centroid rgb * 255, rounded
+    half-up; a 1-segment image renders uniform."""
+    img = _u8_image()
+    g = engine.run_image(img, G.EngineConfig(0.08, 100), "rgb")
+    out = engine.render(0)
+    col = np.clip(np.floor(g.centroids[:, :3] * 255.0 + 0.5), 0, 255).astype(np.uint8)
+    assert np.array_equal(out, col[g.labels])
+    flat = np.full((8, 8, 3), 77, np.uint8)
+    g1 = engine.run_image(flat, G.EngineConfig(0.08, 20), "rgb")
+    out1 = engine.render(0)
+    assert len(g1.centroids) == 1 and (out1 == out1[0]).all()
