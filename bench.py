@@ -183,6 +183,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--input", default="features", choices=["features", "u8"],
+                    help="u8: the image workloads (cfg2, cfg4) as 8-bit RGB pixels, features "
+                         "formed on the device (segmentation front end, SURVEY.md §8(f)1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -210,8 +213,12 @@ def main():
         from paper_2206_02200_b200.dist import point_shard, run_cloud
         p0, cnt_local = point_shard(n_global, world, rank)
         X = np.ascontiguousarray(X[:, p0:p0 + cnt_local])
+    if args.input == "u8":
+        if args.workload not in ("cfg2", "cfg4") or shard_cloud:
+            raise SystemExit("--input u8 applies to the image workloads cfg2 and cfg4")
+        X = np.clip(np.rint(X.astype(np.float64) * 255.0), 0, 255).astype(np.uint8)
     B, n, d = X.shape
-    dt = G.GS_F32 if X.dtype == np.float32 else G.GS_F64
+    dt = G.GS_U8 if X.dtype == np.uint8 else (G.GS_F32 if X.dtype == np.float32 else G.GS_F64)
     # timed steps record only the binning kernel's CUDA events (the roofline's kernel time);
     # the per-phase times come from a separate, untimed diagnostic pass (events cost ~30 us)
     econf = G.EngineConfig(cfg.h, cfg.max_iter, debug_flags=G.GS_TIME_KERNEL)
@@ -285,7 +292,7 @@ def main():
 
     # roofline of the n-scale binning kernel K2: algorithmic bytes = points read + slot write
     peak, peak_kind = peaks()
-    s_in = 4 if dt == G.GS_F32 else 8
+    s_in = {G.GS_F32: 4, G.GS_F64: 8, G.GS_U8: 1}[dt]
     kbin_ms = float(np.mean([s["ms_k_bin"] for s in st_dev]))
     kbin_bytes = B * n * (d * s_in + 4)
     kbin_gbs = kbin_bytes / (kbin_ms / 1e3) / 1e9
@@ -302,7 +309,8 @@ def main():
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "desc": cfg.desc, "n": n, "d": d, "batch": B,
-                   "h": cfg.h, "max_iter": cfg.max_iter, "input_dtype": "f32" if s_in == 4 else "f64",
+                   "h": cfg.h, "max_iter": cfg.max_iter,
+                   "input_dtype": {4: "f32", 8: "f64", 1: "u8 rgb pixels"}[s_in],
                    "l2": "flushed (512 MiB write) before every timed step",
                    "parallelism": (f"one cloud in {world} point shards (partial cells "
                                    f"all-gathered, replicated iteration)") if shard_cloud else
@@ -316,7 +324,8 @@ def main():
                      "frac": kbin_gbs / peak,
                      # dram read+write of one K2 launch from the committed ncu --set full
                      # capture of this workload (profiles/r1_ncu_kernels.md), or null
-                     "traffic": NCU_TRAFFIC.get(args.workload) if not shard_cloud else None,
+                     "traffic": (NCU_TRAFFIC.get(args.workload)
+                                 if not shard_cloud and args.input == "features" else None),
                      "algorithmic_bytes": kbin_bytes},
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
                 "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},

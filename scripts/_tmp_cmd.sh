@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_gpu.log | cut -c1-300
-for W in cfg2 cfg4; do timeout 300 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${W}_r1L.log 2>&1; echo "bench $W rc=$?"; done
+for W in cfg2 cfg4; do timeout 300 python bench.py --workload $W --input u8 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${W}_u8_r1L.log 2>&1; echo "bench $W rc=$?"; tail -2 gpurun_out/bench_${W}_u8_r1L.log | cut -c1-300; done
