@@ -104,9 +104,13 @@ struct gs_ctx {
   const uint32_t* shard_counts = nullptr;
   const int64_t* shard_sums = nullptr;
   DevBuf xsum, pkeys, pcounts, psums;
-  // pinned readback area (one async D2H per result array, one sync per run)
+  // pinned, device-mapped readback area: K7 stores the control block there (zero copy)
   void* pin = nullptr;
+  void* pin_dev = nullptr;
   size_t pin_bytes = 0;
+  // the control block's zero region is zero (K7 re-zeroes it at the end of every run; any
+  // other user of the block, or a run that stopped early, clears this and a memset follows)
+  bool ctl_clean = false;
   // shape cache: a run whose frames all went straight to K8 lets later runs of the same
   // shape launch K8 optimistically (no host round trip between binning and labels)
   struct ShapeKey {
@@ -315,6 +319,7 @@ gs_status ensure_ctl(gs_ctx* ctx, int64_t nf) {
   ctx->ctl.release();
   GS_TRY(grow(ctx, ctx->ctl, ctl_bytes(nf)));
   GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_bytes(nf), ctx->stream));
+  ctx->ctl_clean = true;
   char* p = ctx->ctl.as<char>();
   ctx->errflag.view(p, 32);
   ctx->counters.view(p + 32, 64);
@@ -499,6 +504,19 @@ gs_status grow_dense_for(gs_ctx* ctx, long long need, int d) {
   return ensure_dense(ctx, (int64_t)need, d);
 }
 
+// The control block's zero region must be zero when a run starts; K7 leaves it so.  Outside
+// a graph capture a dirty block is cleared here; a captured run relies on the invariant (the
+// caller clears before launching the graph).
+gs_status clean_ctl(gs_ctx* ctx) {
+  if (ctx->ctl_clean) return GS_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  GS_CK(cudaStreamIsCapturing(ctx->stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive) return GS_OK;
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), ctx->stream));
+  ctx->ctl_clean = true;
+  return GS_OK;
+}
+
 // n-scale phase with no host round trip: control block cleared -> bounds + device box ->
 // privatised binning -> single-pass compaction (cells come out lexicographically sorted, with
 // per-frame first indices).  Errors (non-finite input, key box beyond the grid) surface in
@@ -523,7 +541,8 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
     GS_TRY(grow(ctx, ctx->epoch_dev, 16));
     GS_CK(cudaMemsetAsync(ctx->epoch_dev.p, 0, 16, st));
   }
-  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_TRY(clean_ctl(ctx));
+  ctx->ctl_clean = false;  // until K7 of this run re-zeroes it
   GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
   GS_TRY(rec_event(ctx, 6));
   GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk));
@@ -813,9 +832,10 @@ gs_status map_readback(gs_ctx* ctx, int64_t nf_run, int max_iter, Readback* rb) 
   const size_t need = ctl_bytes(nf) + 16 * (size_t)nf_run * max_iter + 64;
   if (need > ctx->pin_bytes) {
     if (ctx->pin) cudaFreeHost(ctx->pin);
-    ctx->pin = nullptr;
+    ctx->pin = ctx->pin_dev = nullptr;
     ctx->pin_bytes = 0;
-    GS_CK(cudaMallocHost(&ctx->pin, need));
+    GS_CK(cudaHostAlloc(&ctx->pin, need, cudaHostAllocMapped));
+    GS_CK(cudaHostGetDevicePointer(&ctx->pin_dev, ctx->pin, 0));
     ctx->pin_bytes = need;
     ++ctx->alloc_gen;
   }
@@ -917,14 +937,16 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
     dlabels = ctx->labels.as<int32_t>();
   }
   gs::k_label<<<blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
-      ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels);
+      ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels, ctx->ctl.as<unsigned>(),
+      (unsigned*)ctx->pin_dev, (int)(ctl_bytes(ctx->ctl_nf) / 4),
+      (int)(ctl_zero_bytes(ctx->ctl_nf) / 4));
   GS_LAUNCHED("k_label");
+  ctx->ctl_clean = true;  // K7 re-zeroes the control block (stream order: before any later use)
   GS_TRY(rec_event(ctx, 4));
   if (!direct)
     GS_CK(cudaMemcpyAsync(user_labels, dlabels, sizeof(int32_t) * ntot, cudaMemcpyDeviceToHost,
                           st));
   GS_TRY(rec_event(ctx, 5));
-  GS_CK(cudaMemcpyAsync(rb.err, ctx->ctl.p, ctl_bytes(ctx->ctl_nf), cudaMemcpyDeviceToHost, st));
   if (rec) {
     GS_CK(cudaMemcpyAsync(rb.hm, ra.hist_m, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
     GS_CK(cudaMemcpyAsync(rb.hd, ra.hist_d, 8 * nf * cfg->max_iter, cudaMemcpyDeviceToHost, st));
@@ -1087,6 +1109,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
                          rec, rb);
     };
     if (graphed) {
+      GS_TRY(clean_ctl(ctx));  // the graph has no memset node: it starts from a clean block
       const gs_ctx::GraphKey gk{key, in->points, out->labels, cfg->flags, in->on_device,
                                 ctx->alloc_gen};
       if (!(ctx->gexec && ctx->gkey == gk)) {
@@ -1122,6 +1145,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
     if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+    if (rb.err[0] & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep schedule watchdog fired");
     if ((rb.err[0] & 32) || rb.ctr[4] != 0) {  // grid too small / a frame too big: redo it
       ctx->shape_ms = 0;                        // synchronously below
       if (rb.err[0] & 32) GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
@@ -1242,6 +1266,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
                        rec, rb));
     GS_CK(cudaStreamSynchronize(st));
     dump_trace(ctx);
+    if (rb.err[0] & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep schedule watchdog fired");
     if (rb.err[0] & 16)
       return fail(ctx, GS_E_INTERNAL_INVARIANT, "frame exceeded the resident capacity");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
@@ -1473,6 +1498,7 @@ gs_status gs_shard_keybounds(gs_ctx* ctx, const gs_input* in, double h, int64_t*
     GS_CK(cudaMemsetAsync(ctx->epoch_dev.p, 0, 16, st));
   }
   GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  ctx->ctl_clean = false;
   GS_TRY(dispatch_bounds_bin(ctx, dpts, in->dtype, d, n, true, nblk, h, n, 1));
   int hdr[8];
   GsBox b;
@@ -1485,6 +1511,7 @@ gs_status gs_shard_keybounds(gs_ctx* ctx, const gs_input* in, double h, int64_t*
     klo[c] = b.kmin[c] + GS_APRON;
     khi[c] = b.kmin[c] + b.ext[c] - 1 - GS_APRON;
   }
+  ctx->ctl_clean = false;
   return GS_OK;
 }
 
@@ -1553,6 +1580,7 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_glob
     dpts = ctx->pts.p;
   }
   GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  ctx->ctl_clean = false;
   GS_CK(cudaMemcpyAsync(ctx->dbox.p, &b, sizeof(GsBox), cudaMemcpyHostToDevice, st));
   GS_TRY(dispatch_bounds_bin(ctx, dpts, in->dtype, d, n, false, 0));
   k_epoch_bump<<<1, 1, 0, st>>>(ctx->epoch_dev.as<unsigned>());
@@ -1582,6 +1610,7 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_glob
   GS_CK(cudaStreamSynchronize(st));
   ctx->box = b;
   ctx->shard_box = true;
+  ctx->ctl_clean = false;
   return GS_OK;
 }
 
@@ -1723,6 +1752,7 @@ gs_status gs_debug_iterate_once(gs_ctx* ctx, int32_t d, double h, int64_t m, con
   GS_TRY(grow(ctx, ctx->errflag, sizeof(int) * 4));
   GS_TRY(grow(ctx, ctx->counters, sizeof(unsigned int) * 16));
   GS_CK(cudaMemsetAsync(ctx->errflag.p, 0, sizeof(int) * 4, ctx->stream));
+  ctx->ctl_clean = false;
   std::vector<uint32_t> hk(m), hc(m);
   std::vector<int32_t> hidx(m);
   for (int64_t i = 0; i < m; ++i) {

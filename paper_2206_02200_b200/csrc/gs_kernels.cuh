@@ -605,15 +605,24 @@ __global__ void k_compose(int m0, const int32_t* __restrict__ parent, int32_t* _
 }
 
 // K7: labels[p] = lab[slot[p]]
+// K7.  Block 0 also hands the run's control block to the host: it stores the words into
+// mapped pinned memory (no copy node, ~12 us per run on the graph path) and then re-zeroes
+// the part every run starts from zero, so the next run needs no memset node either.
 __global__ void __launch_bounds__(256) k_label(int64_t ntot, const uint32_t* __restrict__ slot,
                                                const int32_t* __restrict__ lab,
-                                               int32_t* __restrict__ labels) {
+                                               int32_t* __restrict__ labels,
+                                               unsigned* __restrict__ ctl, unsigned* ctl_host,
+                                               int ctl_words, int zero_words) {
+  if (blockIdx.x == 0 && ctl_host) {
+    for (int w = threadIdx.x; w < ctl_words; w += blockDim.x) ctl_host[w] = ctl[w];
+    __syncthreads();
+    for (int w = threadIdx.x; w < zero_words; w += blockDim.x) ctl[w] = 0u;
+  }
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ntot;
        p += (int64_t)gridDim.x * blockDim.x)
     labels[p] = __ldg(&lab[slot[p]]);
 }
 
-// test hook: rank of every point's initial cell
 // Segmentation render: a segment's colour is its centroid's first three
 // components times 255, rounded half-up, clamped to 0..255 (packed r | g<<8 | b<<16)
 __global__ void k_segment_colours(int64_t k, int d, const double* __restrict__ cent,
@@ -643,6 +652,7 @@ __global__ void __launch_bounds__(256) k_render(int64_t n, const uint32_t* __res
   }
 }
 
+// test hook: rank of every point's initial cell
 __global__ void k_slot_rank(int64_t ntot, const uint32_t* __restrict__ slot,
                             const int32_t* __restrict__ idx, int64_t* __restrict__ out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

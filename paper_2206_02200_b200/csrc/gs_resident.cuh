@@ -191,10 +191,17 @@ __device__ int rs_scan(int* a, int n, int* wtmp) {
 template <int D>
 __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   __shared__ GsBox sbox;
+  __shared__ int s_err0;
   const int f = blockIdx.x;
   const int tid = threadIdx.x, T = blockDim.x;
-  if (tid == 0) sbox = *a.pbox;
+  if (tid == 0) {
+    sbox = *a.pbox;
+    s_err0 = *a.err;
+  }
   __syncthreads();
+  // non-finite input / key box beyond the grid or the int64 range: binning did not run and the
+  // box is not valid (the host reports the error; on the optimistic path K8 is already queued)
+  if (s_err0 & (1 | 32 | 64)) return;
   const GsBox& b = sbox;
   // dense cell index of this frame: smem int16 table when the host reserved room for this
   // box's frame volume, else the global grid (L2-resident)
@@ -538,7 +545,13 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         while (qhead < m) {
           long long tt1 = 0;
           int v;
+          long long spins = 0;  // watchdog: a schedule that stops short is a bug, not a hang
           while ((v = (int)rs_ld_acquire((const uint32_t*)&levend[lev])) == 0) {
+            if (++spins > (1ll << 26)) break;
+          }
+          if (v == 0) {
+            if (lane == 0) atomicOr(a.err, 8);
+            break;
           }
           if (trace) tt1 = clock64();
           const int lev_end = v - 1;

@@ -291,3 +291,35 @@ def test_render_mean_colours(engine):
     g1 = engine.run_image(flat, G.EngineConfig(0.08, 20), "rgb")
     out1 = engine.render(0)
     assert len(g1.centroids) == 1 and (out1 == out1[0]).all()
+
+
+def test_graph_replay_after_other_calls(engine):
+    """The replayed graph has no memset: K7 leaves the control block clean.  Calls that use
+    the block in between (debug build, shard binning, a failing run) must not leak state
+    into the next replay."""
+    import torch
+    X = CF.generate("cfg2", scale=0.2)[0]
+    o = O.run(X.astype(np.float64), 0.08, 100, O.BUILD_FIXED)
+    Xp = torch.from_numpy(X).pin_memory()
+    lab = torch.empty(X.shape[0], dtype=torch.int32).pin_memory()
+    eng = G.Engine(0)
+
+    def replay():
+        k, it, cv = eng.run_raw(Xp.data_ptr(), X.shape[0], 3, G.GS_F32, 1, False,
+                                G.EngineConfig(0.08, 100), lab.data_ptr())
+        assert int(k[0]) == o["k"] and int(it[0]) == o["iterations"]
+        assert np.array_equal(lab.numpy(), o["labels"])
+
+    for _ in range(2):
+        replay()
+    eng.debug_build(X.astype(np.float64), 0.08)
+    replay()
+    lo, hi = eng.shard_keybounds(X, 0.08)
+    eng.shard_bin(X, 0.08, X.shape[0], lo, hi)
+    replay()
+    bad = X.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(G.InvalidInputError):
+        eng.run(bad, G.EngineConfig(0.08, 100))
+    replay()
+    eng.close()
