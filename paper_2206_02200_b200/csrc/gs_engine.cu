@@ -95,6 +95,7 @@ struct gs_ctx {
   // bumped whenever a device buffer is (re)allocated: a cached graph holds raw pointers
   uint64_t alloc_gen = 0;
   int img_w = 0;  // GS_U8 rgbxy: image width of the current call
+  const void* host_src = nullptr;  // pinned caller points read by K1 directly (zero copy)
   // multi-GPU shard state (gs_shard_*): the global key box from gs_shard_bin, and for
   // gs_shard_run the merged partial cells the run starts from instead of binning
   bool shard_box = false;
@@ -429,10 +430,13 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
     unsigned* ctr = ctx->counters.as<unsigned>();
     int* err = ctx->errflag.as<int>();
     const int F = gs_fixed_shift(n, h);
+    // zero copy: read the caller's pinned points, store the device copy K2 reads
+    const void* src = ctx->host_src ? ctx->host_src : pts;
+    T* copy = ctx->host_src ? (T*)pts : nullptr;
     gs::k_bounds_box<D, T><<<nblk, 256, 0, ctx->stream>>>(
-        (const T*)pts, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
+        (const T*)src, ntot, ctx->bpart.as<double>(), h, F, n, nf, ctx->dense_cap,
         ctx->dbox.as<GsBox>(), err, (long long*)(err + 2), ctr + 6,
-        ctx->epoch_dev.as<unsigned>(), img_w);
+        ctx->epoch_dev.as<unsigned>(), img_w, copy);
     GS_LAUNCHED("k_bounds_box");
   } else {
     // privatised binning: one 768-thread CTA per SM at most, >= 1024 points per CTA; the
@@ -992,6 +996,20 @@ bool graph_safe(const void* p) {
          at.type == cudaMemoryTypeManaged;
 }
 
+// Pinned inputs up to this size are read by K1 over the bus instead of copied (cfg2: e2e
+// 728 -> 755 M points/s); above it the copy engine wins (cfg4, 943 MB: 3.15 -> 2.96 G).
+constexpr size_t kZeroCopyMaxBytes = size_t(16) << 20;
+
+// The device address of pinned host memory a kernel may read directly, or null.
+const void* pinned_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 __global__ void k_epoch_bump(unsigned* e) { *e += 1u; }
 
 // The front of gs_shard_run: every rank's partial cells (host) -> the dense grid of the
@@ -1087,10 +1105,19 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
     if (ctx->shard_front) return launch_shard_front(ctx, d);
     GS_TRY(rec_event(ctx, 0));
-    if (!in->on_device)
-      GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
+    // pinned caller points: K1 reads them over the bus and stores the device copy (the copy
+    // and the bounds pass overlap; no copy node); pageable points: an explicit copy
+    ctx->host_src = nullptr;
+    if (!in->on_device) {
+      // (large inputs go by DMA: measured, K1's bus reads lose to the copy engine past ~MBs)
+      if (input_bytes(in) <= kZeroCopyMaxBytes) ctx->host_src = pinned_device_ptr(in->points);
+      if (!ctx->host_src)
+        GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
+    }
     GS_TRY(rec_event(ctx, 1));
-    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint));
+    const gs_status sf = launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint);
+    ctx->host_src = nullptr;
+    GS_TRY(sf);
     GS_TRY(rec_event(ctx, 2));
     return GS_OK;
   };

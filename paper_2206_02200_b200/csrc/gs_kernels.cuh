@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
                                                     int64_t cap_cells, GsBox* __restrict__ out,
                                                     int* err, long long* need,
                                                     unsigned* ticket, unsigned* epoch,
-                                                    int img_w = 0) {
+                                                    int img_w = 0, T* __restrict__ copy = nullptr) {
+  // copy != null: `pts` is pinned host memory read over the bus (zero copy) and every point is
+  // stored to `copy` (device) for K2 -- the host-to-device copy and the bounds pass are one
   constexpr int RC = gs_raw_cols<T, D>();
   const GsImg im = gs_img(img_w, n);
   double mn[D], mx[D];
@@ -45,6 +47,10 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
     T raw[RC];
 #pragma unroll
     for (int c = 0; c < RC; ++c) raw[c] = pts[p * RC + c];
+    if (copy) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c) copy[p * RC + c] = raw[c];
+    }
     const int64_t pl = (sizeof(T) == 1 && D > 3) ? p % n : 0;  // rgbxy needs the pixel index
 #pragma unroll
     for (int c = 0; c < D; ++c) {
