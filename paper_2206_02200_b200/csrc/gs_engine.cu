@@ -744,10 +744,18 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
                         cudaMemcpyDeviceToHost, ctx->stream));
   GS_CK(cudaStreamSynchronize(ctx->stream));
   const unsigned nb = blocks_for(mnew, 256);
-  gs::k_fold<<<nb, 256, 0, ctx->stream>>>(
-      mnew, (int)m, d, ctx->segstart.as<int32_t>(), ctx->skey.as<uint32_t>(),
-      ctx->sval.as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(), ctx->S1.as<double>(),
-      ctx->ckey[nxt].as<uint32_t>(), ctx->ccnt[nxt].as<uint32_t>(), ctx->S[nxt].as<double>());
+  switch (d) {
+#define GS_CASE(D)                                                                            \
+  case D:                                                                                     \
+    gs::k_fold<D><<<nb, 256, 0, ctx->stream>>>(                                               \
+        mnew, (int)m, ctx->segstart.as<int32_t>(), ctx->skey.as<uint32_t>(),                 \
+        ctx->sval.as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(), ctx->S1.as<double>(),       \
+        ctx->ckey[nxt].as<uint32_t>(), ctx->ccnt[nxt].as<uint32_t>(), ctx->S[nxt].as<double>()); \
+    break;
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+    GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
+#undef GS_CASE
+  }
   GS_LAUNCHED("k_fold");
   gs::k_idx_clear<<<mb, 256, 0, ctx->stream>>>((int)m, ctx->ckey[cur].as<uint32_t>(),
                                                ctx->idx.as<int32_t>());

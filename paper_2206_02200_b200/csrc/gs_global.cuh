@@ -81,7 +81,7 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
 // one lane per (cell, coordinate) -- the serial sweep's operands in lex order, +0.0 padding --
 // then every thread releases the successors of one frontier cell (pending counts packed as
 // bytes in shared memory, the queue in shared memory as u16 when the cells fit, else both in
-// global scratch).  Two block barriers per level.
+// global scratch).  One block barrier per level.
 template <int D>
 constexpr int sweep_global_threads() { return D <= 3 ? 1024 : 512; }  // d > 3: 128 registers
 
@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
         __stcg(&Q[(int64_t)i * D + c], s1);
       }
     }
-    __syncthreads();  // the frontier's rows are final for every later reader
+    // (no barrier here: the release only prepares the NEXT frontier, which starts after the
+    // loop-top barrier, by when every row of this one is final)
     // ---- release the frontier's later neighbours: d <= 3 a thread per frontier cell (<= 13
     //      successors), d > 3 a warp per cell with its lanes over the successors (up to 121
     //      for d = 5: a thread per cell would serialise them)

@@ -547,7 +547,12 @@ __global__ void k_seg(int m, const int32_t* __restrict__ head, const int32_t* __
 
 // merge_into folded in visit order (Eq. 3-4, pin P4): members of a segment are in increasing
 // old rank because the sort is stable and ranks were fed in order.
-__global__ void k_fold(int mnew, int m, int d, const int32_t* __restrict__ segstart,
+// Ordered Eq. (3) fold of each new cell's members in visit order (pin P4), one thread per new
+// cell: s = RN(RN(RN(a*s) + RN(w*S_i)) / tot) with the division from y = RN(1/tot) (Markstein,
+// correctly rounded for integer tot; y does not depend on s, so it leaves the chain); an
+// operand outside the theorem's range redoes the group with IEEE divisions.
+template <int D>
+__global__ void k_fold(int mnew, int m, const int32_t* __restrict__ segstart,
                        const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sval,
                        const uint32_t* __restrict__ ccnt, const double* __restrict__ S1,
                        uint32_t* __restrict__ okey, uint32_t* __restrict__ ocnt,
@@ -557,20 +562,45 @@ __global__ void k_fold(int mnew, int m, int d, const int32_t* __restrict__ segst
   const int start = segstart[g];
   const int end = (g + 1 < mnew) ? segstart[g + 1] : m;
   const uint32_t i0 = sval[start];
-  double s[GS_DMAX];
-  for (int c = 0; c < d; ++c) s[c] = S1[(int64_t)i0 * d + c];
+  double s[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) s[c] = S1[(int64_t)i0 * D + c];
   uint64_t cnt = ccnt[i0];
+  bool slow = false;
   for (int j = start + 1; j < end; ++j) {
     const uint32_t i = sval[j];
     const uint64_t ci = ccnt[i];
     const double a = (double)cnt, w = (double)ci, tot = (double)(cnt + ci);
-    for (int c = 0; c < d; ++c)
-      s[c] = __ddiv_rn(__dadd_rn(__dmul_rn(a, s[c]), __dmul_rn(w, S1[(int64_t)i * d + c])), tot);
+    const double y = __drcp_rn(tot);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double num = __dadd_rn(__dmul_rn(a, s[c]), __dmul_rn(w, S1[(int64_t)i * D + c]));
+      const double fa = fabs(num);
+      slow |= !(fa < 0x1p+1000) || (fa < 0x1p-900 && num != 0.0);
+      const double q0 = __dmul_rn(num, y);
+      s[c] = __fma_rn(__fma_rn(-q0, tot, num), y, q0);
+    }
     cnt += ci;
+  }
+  if (slow) {
+    cnt = ccnt[i0];
+#pragma unroll
+    for (int c = 0; c < D; ++c) s[c] = S1[(int64_t)i0 * D + c];
+    for (int j = start + 1; j < end; ++j) {
+      const uint32_t i = sval[j];
+      const uint64_t ci = ccnt[i];
+      const double a = (double)cnt, w = (double)ci, tot = (double)(cnt + ci);
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        s[c] = gs_ddiv_slow(__dadd_rn(__dmul_rn(a, s[c]), __dmul_rn(w, S1[(int64_t)i * D + c])),
+                            tot);
+      cnt += ci;
+    }
   }
   okey[g] = skey[start];
   ocnt[g] = (uint32_t)cnt;
-  for (int c = 0; c < d; ++c) oS[(int64_t)g * d + c] = s[c];
+#pragma unroll
+  for (int c = 0; c < D; ++c) oS[(int64_t)g * D + c] = s[c];
 }
 
 __global__ void k_idx_clear(int m, const uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
