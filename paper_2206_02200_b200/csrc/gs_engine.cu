@@ -444,8 +444,7 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
     constexpr int TBL_MAX = gs::bin_table_entries<D>();
     const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
     const int64_t per_cta = (ntot + grid - 1) / grid;
-    int TBL = 256;
-    while (TBL < TBL_MAX && TBL < 2 * per_cta) TBL <<= 1;
+    const int TBL = (int)std::max<int64_t>(256, std::min<int64_t>(TBL_MAX, (2 * per_cta + 31) & ~31ll));
     const size_t smem = (size_t)TBL * (8 * D + 8);
     static bool configured = false;
     if (!configured) {

@@ -173,13 +173,32 @@ __device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned lon
 }
 
 // Probe budget of the privatised table: when a CTA sees more distinct cells than the table
-// holds (cfg5: shuffled, ~45K cells), a full table made every new key walk 16 slots (~36 % of
-// K2's time); after 4 the point takes the global atomics.
+// holds (cfg5: shuffled, ~15K cells per CTA slice), a full table made every new key walk 16
+// slots (~36 % of K2's time); after 4 the point takes the global atomics.
 constexpr int kBinProbes = 4;
+// Warp aggregation is used when a warp's 32 keys form at most this many runs of equal keys.
+constexpr int kAggRuns = 4;
 
+// Table entries (key u32 + count u32 + D int64 sums = 8D+8 B) filling the shared memory of one
+// CTA per SM (cfg5: 7168 entries catch 89 % of a CTA's points, 4096 caught 78 %).
 template <int D>
 __host__ __device__ constexpr int bin_table_entries() {
-  return D <= 3 ? 4096 : (D <= 5 ? 2048 : 1024);
+  return (229376 / (8 * D + 8)) & ~31;
+}
+
+// grid_index + fixed-point offset of one coordinate (build mode 1), lean form of
+// gs_grid_coord + gs_fixq: fl = floor(RN(x*RN(1/h))) is taken when |q| < 2^20 and q is more
+// than 2^-30 from an integer (|q - x/h| <= 2^-32 there, so fl == floor(RN(x/h))); otherwise the
+// IEEE quotient (x == 0 is exact either way).  rel = fl - kmin (exact in fp64); q = RN(RN(x - RN(fl*h)) * 2^F) (== gs_fixq:
+// fl is (double)k).  Bit-identical to the oracle's build mode 1.
+__device__ __forceinline__ void gs_bin_coord(double x, double h, double inv_h, double scale,
+                                             double kmin, int& rel, long long& q) {
+  const double qd = __dmul_rn(x, inv_h);
+  double fl = floor(qd);
+  const double t = __dsub_rn(__dsub_rn(qd, fl), 0.5);
+  if (!(fabs(t) < 0.5 - 0x1p-30 && fabs(qd) < 0x1p20) && x != 0.0) fl = floor(gs_ddiv_slow(x, h));
+  rel = __double2int_rz(__dsub_rn(fl, kmin));
+  q = __double2ll_rn(__dmul_rn(__dsub_rn(x, __dmul_rn(fl, h)), scale));
 }
 
 template <int D, typename T>
@@ -188,10 +207,10 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
                                                    uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
                                                    uint32_t* __restrict__ slot, int* err,
-                                                   int TBL, int img_w = 0) {
+                                                   int TBL, int img_w) {
   constexpr int RC = gs_raw_cols<T, D>();
-  // TBL: table entries, a power of two <= bin_table_entries<D>() sized to the CTA's points
-  // (initialising and flushing a table costs O(TBL) per CTA)
+  // TBL: table entries (a multiple of 32, <= bin_table_entries<D>()) sized to the CTA's points
+  // (initialising and flushing a table costs O(TBL) per CTA).
   constexpr uint32_t EMPTY = 0xffffffffu;
   // the first round's coordinates, the error word and the box are all requested before any
   // of them is waited for (after an L2 flush each is a cold HBM round trip)
@@ -221,8 +240,24 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
   if (s_err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
   const unsigned lane = threadIdx.x & 31;
   const GsImg im = gs_img(img_w, b.n);
+  // per-dimension constants in registers; 32-bit cell arithmetic (the grid holds <= 2^28 cells)
+  const double h = b.h, inv_h = b.inv_h, scale = b.scale;
+  // per-point |q| <= h*2^F < 2^(ilogb(h)+1+F): when that is <= 2^51 (n >= 513 points per frame)
+  // a 32-lane sum splits into a 26-bit unsigned piece and a signed high piece, neither of which
+  // can overflow 32 bits
+  const bool two_piece = ilogb(h) + 1 + b.F <= 51;
+  double kminD[D];
+  uint32_t span[D], strd[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    kminD[c] = (double)b.kmin[c];
+    span[c] = (uint32_t)(b.ext[c] - 2 * GS_APRON);
+    strd[c] = (uint32_t)b.stride[c];
+  }
   // frame of this thread's point, tracked incrementally (no 64-bit division per point)
   int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
+  uint32_t Lf = (uint32_t)(fr * b.vol_frame);
+  const uint32_t vf = (uint32_t)b.vol_frame;
   // warp-uniform trip count so every lane takes part in the warp aggregation; the next
   // round's coordinates are loaded before this round is processed (twice the bytes in flight)
   for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
@@ -234,81 +269,97 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     const int64_t pn = p + blockDim.x;
 #pragma unroll
     for (int c = 0; c < RC; ++c) xn[c] = pn < p1 ? pts[pn * RC + c] : T(0);
-    int64_t L = 0;
-    long long q[D];
-    bool bad = false;
     while (p >= fr_end) {
       ++fr;
       fr_end += b.n;
+      Lf += vf;
     }
-    if (valid) {
-      L = fr * b.vol_frame;
+    uint32_t key = EMPTY;
+    long long q[D];
+    {
+      uint32_t L = Lf;
+      bool bad = false;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double x = gs_feature<T, D>(xc, c, p - fr * b.n, im);
-        const int64_t k = gs_grid_coord(x, b.h, b.inv_h);
-        const int64_t rel = k - b.kmin[c];
-        bad |= (rel < GS_APRON) | (rel >= b.ext[c] - GS_APRON);
-        L += rel * b.stride[c];
-        q[c] = gs_fixq(x, k, b.h, b.scale);
+        const double x = gs_feature<T, D>(xc, c, (sizeof(T) == 1 && D > 3) ? p - fr * b.n : 0, im);
+        int rel;
+        gs_bin_coord(x, h, inv_h, scale, kminD[c], rel, q[c]);
+        bad |= (uint32_t)(rel - GS_APRON) >= span[c];
+        L += (uint32_t)rel * strd[c];
       }
-      if (bad) atomicOr(err, 2);
-      else slot[p] = (uint32_t)L;
-    } else {
-#pragma unroll
-      for (int c = 0; c < D; ++c) q[c] = 0;
+      if (valid) {
+        if (bad) atomicOr(err, 2);
+        else {
+          slot[p] = L;
+          key = L;
+        }
+      }
     }
-    const uint32_t key = (valid && !bad) ? (uint32_t)L : EMPTY;
-    // ---- warp aggregation: lanes binning into the same cell (pixel-ordered images put most
-    // of a warp into 1-4 cells) reduce to their group leader before any atomic: per group,
-    // hardware reductions (REDUX) of the fixed-point sums in three 26/26/12-bit pieces (no
-    // piece sum of <= 32 lanes can overflow; the u64 recombination is exact mod 2^64).  Many
-    // small groups skip it: their atomics hardly contend.
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const bool leader = (peers & ((1u << lane) - 1u)) == 0u;
-    const unsigned leaders = __ballot_sync(0xffffffffu, leader);
+    // ---- warp aggregation over runs of equal keys (pixel-ordered images put most of a warp
+    // into 1-4 runs): a run's sums reduce to its first lane with hardware reductions (REDUX)
+    // before any atomic.  Runs come from one shuffle + ballot (MATCH.ANY costs 2 cycles per
+    // distinct key).  A warp of many runs (shuffled clouds, noisy backgrounds) skips it: its
+    // lanes' atomics hardly contend.
+    const uint32_t prev = __shfl_up_sync(kFull, key, 1);
+    const bool head = lane == 0 || key != prev;
+    const unsigned heads = __ballot_sync(kFull, head);
     uint32_t my_cnt = 1;
-    if (__popc(leaders) <= 4) {
-      unsigned rem = leaders;
+    if (__popc(heads) <= kAggRuns) {
+      // my run: lanes [s, e) with s = my head, e = the next head (or 32)
+      const unsigned upto = heads & (0xffffffffu >> (31 - lane));      // heads <= lane
+      const unsigned after = heads & ~(0xffffffffu >> (31 - lane));    // heads > lane
+      const int s = 31 - __clz(upto);
+      const int e = after ? __ffs(after) - 1 : 32;
+      const unsigned gm = (e == 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((1u << s) - 1u);
+      my_cnt = (uint32_t)__popc(gm);
+      unsigned rem = heads;
       while (rem) {
         const int ld = __ffs(rem) - 1;
         rem &= rem - 1u;
-        const unsigned gm = __shfl_sync(0xffffffffu, peers, ld);
-        if ((gm >> lane) & 1u) {
+        if (ld == s) {
+          if (two_piece) {
 #pragma unroll
-          for (int c = 0; c < D; ++c) {
-            const unsigned long long u = (unsigned long long)q[c];
-            const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
-            const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
-            const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
-            q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
+            for (int c = 0; c < D; ++c) {
+              const long long u = q[c];
+              const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffff));
+              const long long s1 = __reduce_add_sync(gm, (int)(u >> 26));
+              q[c] = (long long)s0 + s1 * 67108864ll;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const unsigned long long u = (unsigned long long)q[c];
+              const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
+              const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
+              const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
+              q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
+            }
           }
         }
       }
-      my_cnt = (uint32_t)__popc(peers);
-      if (!leader) continue;  // only the group leader carries the group's sums
+      if (!head) continue;  // only the run's first lane carries the run's sums
     }
     if (key == EMPTY) continue;
-    uint32_t h = (key * 2654435761u) & (TBL - 1);
+    uint32_t hsh = __umulhi(key * 2654435761u, (unsigned)TBL);
     int hit = -1;
 #pragma unroll 1
     for (int probe = 0; probe < kBinProbes; ++probe) {
-      uint32_t k = tk[h];
-      if (k == EMPTY) k = atomicCAS(&tk[h], EMPTY, key);
+      uint32_t k = tk[hsh];
+      if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, key);
       if (k == EMPTY || k == key) {
-        hit = (int)h;
+        hit = (int)hsh;
         break;
       }
-      h = (h + 1) & (TBL - 1);
+      hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
     }
     if (hit >= 0) {
       atomicAdd(&tc[hit], my_cnt);
 #pragma unroll
       for (int c = 0; c < D; ++c) smem_add_u64(&ts[hit * D + c], (unsigned long long)q[c]);
     } else {
-      atomicAdd(&cnt[L], my_cnt);
+      atomicAdd(&cnt[key], my_cnt);
 #pragma unroll
-      for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], (unsigned long long)q[c]);
+      for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)q[c]);
     }
   }
   __syncthreads();
