@@ -42,16 +42,7 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
     mx[c] = -INFINITY;
   }
   bool bad = false;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ntot;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    T raw[RC];
-#pragma unroll
-    for (int c = 0; c < RC; ++c) raw[c] = pts[p * RC + c];
-    if (copy) {
-#pragma unroll
-      for (int c = 0; c < RC; ++c) copy[p * RC + c] = raw[c];
-    }
-    const int64_t pl = (sizeof(T) == 1 && D > 3) ? p % n : 0;  // rgbxy needs the pixel index
+  auto point = [&](const T* raw, int64_t pl) {
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       double x = gs_feature<T, D>(raw, c, pl, im);
@@ -59,6 +50,61 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
       mn[c] = fmin(mn[c], x);
       mx[c] = fmax(mx[c], x);
     }
+  };
+  // 16-byte vector loads: a chunk of RC words is PPC whole points (4 fp32 / 2 fp64 points,
+  // 16 pixels); two chunks per thread are in flight before either is reduced
+  constexpr int PPC = 16 / sizeof(T);
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((uintptr_t)pts & 15) == 0 && ((uintptr_t)copy & 15) == 0;
+  const int64_t nch = vec ? ntot / PPC : 0;
+  const uint4* src = reinterpret_cast<const uint4*>(pts);
+  uint4* dst = reinterpret_cast<uint4*>(copy);
+  for (int64_t ch = gtid; ch < nch; ch += 2 * gstride) {
+    const int64_t ch1 = ch + gstride;
+    const bool two = ch1 < nch;
+    uint4 w0[RC], w1[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) w0[r] = src[ch * RC + r];
+    if (two) {
+#pragma unroll
+      for (int r = 0; r < RC; ++r) w1[r] = src[ch1 * RC + r];
+    }
+    if (copy) {
+#pragma unroll
+      for (int r = 0; r < RC; ++r) dst[ch * RC + r] = w0[r];
+      if (two) {
+#pragma unroll
+        for (int r = 0; r < RC; ++r) dst[ch1 * RC + r] = w1[r];
+      }
+    }
+    int64_t pl = (sizeof(T) == 1 && D > 3) ? (ch * PPC) % n : 0;  // rgbxy needs the pixel index
+    const T* e0 = reinterpret_cast<const T*>(w0);
+#pragma unroll
+    for (int j = 0; j < PPC; ++j) {
+      point(e0 + j * RC, pl);
+      if (sizeof(T) == 1 && D > 3 && ++pl == n) pl = 0;
+    }
+    if (two) {
+      pl = (sizeof(T) == 1 && D > 3) ? (ch1 * PPC) % n : 0;
+      const T* e1 = reinterpret_cast<const T*>(w1);
+#pragma unroll
+      for (int j = 0; j < PPC; ++j) {
+        point(e1 + j * RC, pl);
+        if (sizeof(T) == 1 && D > 3 && ++pl == n) pl = 0;
+      }
+    }
+  }
+  // points after the last whole chunk (all of them when the pointers are not 16-byte aligned)
+  for (int64_t p = nch * PPC + gtid; p < ntot; p += gstride) {
+    T raw[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) raw[c] = pts[p * RC + c];
+    if (copy) {
+#pragma unroll
+      for (int c = 0; c < RC; ++c) copy[p * RC + c] = raw[c];
+    }
+    point(raw, (sizeof(T) == 1 && D > 3) ? p % n : 0);
   }
   if (bad) atomicOr(err, 1);
   __shared__ double smn[8][D], smx[8][D];
@@ -169,7 +215,7 @@ __device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned lon
   const unsigned old = atomicAdd(&w[0], lo);
   const unsigned carry = (old + lo < old) ? 1u : 0u;
   const unsigned hi = (unsigned)(v >> 32) + carry;
-  if (hi) atomicAdd(&w[1], hi);
+  atomicAdd(&w[1], hi);  // unconditional: a branch here costs more than the (rare) zero add
 }
 
 // Probe budget of the privatised table: when a CTA sees more distinct cells than the table
@@ -186,19 +232,15 @@ __host__ __device__ constexpr int bin_table_entries() {
   return (229376 / (8 * D + 8)) & ~31;
 }
 
-// grid_index + fixed-point offset of one coordinate (build mode 1), lean form of
-// gs_grid_coord + gs_fixq: fl = floor(RN(x*RN(1/h))) is taken when |q| < 2^20 and q is more
-// than 2^-30 from an integer (|q - x/h| <= 2^-32 there, so fl == floor(RN(x/h))); otherwise the
-// IEEE quotient (x == 0 is exact either way).  rel = fl - kmin (exact in fp64); q = RN(RN(x - RN(fl*h)) * 2^F) (== gs_fixq:
-// fl is (double)k).  Bit-identical to the oracle's build mode 1.
-__device__ __forceinline__ void gs_bin_coord(double x, double h, double inv_h, double scale,
-                                             double kmin, int& rel, long long& q) {
+// grid_index of one coordinate (build mode 1), lean form of gs_grid_coord: fl =
+// floor(RN(x*RN(1/h))) is final when |q| < 2^20 and q is more than 2^-30 from an integer
+// (|q - x/h| <= 2^-32 there, so fl == floor(RN(x/h))), or when x == 0; otherwise the caller
+// takes the IEEE quotient (gs_bin_floor_exact).  Returns whether fl needs that.
+__device__ __forceinline__ bool gs_bin_floor(double x, double inv_h, double& fl) {
   const double qd = __dmul_rn(x, inv_h);
-  double fl = floor(qd);
+  fl = floor(qd);
   const double t = __dsub_rn(__dsub_rn(qd, fl), 0.5);
-  if (!(fabs(t) < 0.5 - 0x1p-30 && fabs(qd) < 0x1p20) && x != 0.0) fl = floor(gs_ddiv_slow(x, h));
-  rel = __double2int_rz(__dsub_rn(fl, kmin));
-  q = __double2ll_rn(__dmul_rn(__dsub_rn(x, __dmul_rn(fl, h)), scale));
+  return !(fabs(t) < 0.5 - 0x1p-30 && fabs(qd) < 0x1p20) && x != 0.0;
 }
 
 template <int D, typename T>
@@ -277,15 +319,31 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     uint32_t key = EMPTY;
     long long q[D];
     {
+      // keys: floor(x/h) per coordinate with one (rare) exact-division branch per point;
+      // rel = fl - kmin is exact in fp64; fixed-point offset q = RN(RN(x - RN(fl*h)) * 2^F)
+      // (== gs_fixq: fl is (double)k) -- bit-identical to the oracle's build mode 1
+      double xs[D], fl[D];
+      bool slow = false;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        xs[c] = gs_feature<T, D>(xc, c, (sizeof(T) == 1 && D > 3) ? p - fr * b.n : 0, im);
+        slow |= gs_bin_floor(xs[c], inv_h, fl[c]);
+      }
+      if (slow) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          double f;
+          if (gs_bin_floor(xs[c], inv_h, f)) fl[c] = floor(gs_ddiv_slow(xs[c], h));
+        }
+      }
       uint32_t L = Lf;
       bool bad = false;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double x = gs_feature<T, D>(xc, c, (sizeof(T) == 1 && D > 3) ? p - fr * b.n : 0, im);
-        int rel;
-        gs_bin_coord(x, h, inv_h, scale, kminD[c], rel, q[c]);
+        const int rel = __double2int_rz(__dsub_rn(fl[c], kminD[c]));
         bad |= (uint32_t)(rel - GS_APRON) >= span[c];
         L += (uint32_t)rel * strd[c];
+        q[c] = __double2ll_rn(__dmul_rn(__dsub_rn(xs[c], __dmul_rn(fl[c], h)), scale));
       }
       if (valid) {
         if (bad) atomicOr(err, 2);
@@ -304,6 +362,7 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     const bool head = lane == 0 || key != prev;
     const unsigned heads = __ballot_sync(kFull, head);
     uint32_t my_cnt = 1;
+    bool act = key != EMPTY;
     if (__popc(heads) <= kAggRuns) {
       // my run: lanes [s, e) with s = my head, e = the next head (or 32)
       const unsigned upto = heads & (0xffffffffu >> (31 - lane));      // heads <= lane
@@ -337,29 +396,34 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
           }
         }
       }
-      if (!head) continue;  // only the run's first lane carries the run's sums
+      act = act && head;  // only the run's first lane carries the run's sums
     }
-    if (key == EMPTY) continue;
-    uint32_t hsh = __umulhi(key * 2654435761u, (unsigned)TBL);
-    int hit = -1;
-#pragma unroll 1
-    for (int probe = 0; probe < kBinProbes; ++probe) {
-      uint32_t k = tk[hsh];
-      if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, key);
-      if (k == EMPTY || k == key) {
-        hit = (int)hsh;
-        break;
+    // ---- table update.  The probe loop is predicated (no early exit) and the active lanes
+    // reconverge before the atomics, so the warp issues each atomic once (an early-exit loop
+    // let the compiler replay the whole atomic sequence once per exit group).
+    const unsigned am = __ballot_sync(kFull, act);
+    if (act) {
+      uint32_t hsh = __umulhi(key * 2654435761u, (unsigned)TBL);
+      int hit = -1;
+#pragma unroll
+      for (int probe = 0; probe < kBinProbes; ++probe) {
+        if (hit < 0) {
+          uint32_t k = tk[hsh];
+          if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, key);
+          if (k == EMPTY || k == key) hit = (int)hsh;
+          hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
+        }
       }
-      hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
-    }
-    if (hit >= 0) {
-      atomicAdd(&tc[hit], my_cnt);
+      __syncwarp(am);
+      if (hit >= 0) {
+        atomicAdd(&tc[hit], my_cnt);
 #pragma unroll
-      for (int c = 0; c < D; ++c) smem_add_u64(&ts[hit * D + c], (unsigned long long)q[c]);
-    } else {
-      atomicAdd(&cnt[key], my_cnt);
+        for (int c = 0; c < D; ++c) smem_add_u64(&ts[hit * D + c], (unsigned long long)q[c]);
+      } else {
+        atomicAdd(&cnt[key], my_cnt);
 #pragma unroll
-      for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)q[c]);
+        for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)q[c]);
+      }
     }
   }
   __syncthreads();
