@@ -173,13 +173,119 @@ def run_reference(args):
     print(json.dumps(line))
     return 0
 
+TUNE_GRID = [round(0.05 * i, 2) for i in range(1, 21)]  # SPEC.md:347 default grid
+TUNE_CAP, TUNE_SEED, TUNE_MAX_ITER = 10_000, 2206, 100
+
+
+def run_tune(args):
+    """--workload tune: tune_bandwidth over the cfg2 image features with the
+    SPEC's default 20-value grid and silhouette_subsampled (cap 10,000).  A step = one whole
+    sweep.  value = points x grid values clustered per second (device-resident input), e2e =
+    the same through gs_tune_bandwidth from host memory; --impl reference / cpu_baseline = the
+    oracle's gso_tune on the host (bounded: the first grid values that fit ~10 s)."""
+    from paper_2206_02200_b200 import configs as CF
+    X = CF.voronoi_rgb(seed=2208)  # cfg2 (481 x 321, rgb in [0,1])
+    n, d = X.shape
+    nh = len(TUNE_GRID)
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as O
+        Xd = X.astype(np.float64)
+        times = []
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.tune(Xd, TUNE_GRID[:4], TUNE_MAX_ITER, TUNE_CAP, TUNE_SEED, O.BUILD_SPEC)
+            if s >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        value = n * 4 * args.steps / sum(times)
+        print(json.dumps({
+            "impl": "reference", "metric": "bandwidth sweep: points x h values per second",
+            "value": value, "unit": "points*h/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps * nh / 4,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "tune", "n": n, "d": d, "grid": nh,
+                                            "cap": TUNE_CAP},
+            "cpu_baseline": {"value": value, "unit": "points*h/s", "cores": 1, "kind": "port",
+                             "sample": "oracle gso_tune over the first 4 grid values per step"},
+            "e2e": {"value": value, "unit": "points*h/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return 0
+    import torch
+    from paper_2206_02200_b200 import gridshift as G
+    torch.cuda.set_device(0)
+    tuner = G.Tuner(0, max_concurrent=8)
+    Xd = torch.from_numpy(X).cuda()
+    lib = G.load_library()
+    inp_dev = G.GsInput(Xd.data_ptr(), n, d, G.GS_F32, 1, 1, 0)
+    hs = np.ascontiguousarray(TUNE_GRID, np.float64)
+    out = (G.GsSweepEntry * nh)()
+    best = G.C.c_double()
+
+    def sweep_dev():
+        tuner._check(lib.gs_tune_bandwidth(tuner._t, G.C.byref(inp_dev), hs.ctypes.data, nh,
+                                           TUNE_MAX_ITER, TUNE_CAP, TUNE_SEED, out,
+                                           G.C.byref(best)))
+
+    def sweep_host():
+        tuner.tune_bandwidth(X, TUNE_GRID, TUNE_MAX_ITER, TUNE_CAP, TUNE_SEED)
+
+    for _ in range(args.warmup):
+        sweep_dev()
+        sweep_host()
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sweep_dev()
+    torch.cuda.synchronize()
+    t_dev = (time.perf_counter() - t0) / args.steps
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sweep_host()
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    clk = clocks.stop()
+    ents = [dict(h=e.h, score=e.score if e.valid else None, k=e.k, iterations=e.iterations)
+            for e in out]
+    line = {
+        "metric": "bandwidth sweep: points x h values per second", "value": n * nh / t_dev,
+        "unit": "points*h/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_dev, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "tune", "desc": "cfg2 image features, SPEC.md:347 grid",
+                   "n": n, "d": d, "grid": nh, "cap": TUNE_CAP, "seed": TUNE_SEED,
+                   "max_iter": TUNE_MAX_ITER, "concurrent_entries": 8,
+                   "timing": "host wall clock around the synchronous sweep call"},
+        "best_h": best.value, "entries": ents,
+        "e2e": {"value": n * nh / t_e2e, "unit": "points*h/s", "ms_per_step": 1e3 * t_e2e,
+                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": 0},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        O.tune(X.astype(np.float64), TUNE_GRID[:4], TUNE_MAX_ITER, TUNE_CAP, TUNE_SEED,
+               O.BUILD_SPEC)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n * 4 / dt, "unit": "points*h/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"oracle gso_tune over the first 4 grid values "
+                                          f"({dt:.1f} s, 1 thread)"}
+    print(json.dumps(line))
+    tuner.close()
+    return 0
+
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg2",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune"],
+                    help="tune: the bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -187,6 +293,8 @@ def main():
                     help="u8: the image workloads (cfg2, cfg4) as 8-bit RGB pixels, features "
                          "formed on the device (segmentation front end, SURVEY.md §8(f)1)")
     args = ap.parse_args()
+    if args.workload == "tune":
+        return run_tune(args)
     if args.impl == "reference":
         return run_reference(args)
 

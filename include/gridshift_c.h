@@ -37,7 +37,9 @@ typedef enum {
   GS_E_CUDA = 7,               /* Error: CUDA runtime failure                                   */
   GS_E_OOM = 8,                /* Error: device allocation failed                               */
   GS_E_NCCL = 9,               /* Error: collective failure (multi-GPU driver)                  */
-  GS_E_NO_DEVICE = 10          /* Error: no sm_100 device visible                               */
+  GS_E_NO_DEVICE = 10,         /* Error: no sm_100 device visible                               */
+  GS_E_TUNING_FAILED = 11,     /* TuningFailureError: no bandwidth gave a scorable clustering   */
+  GS_E_UNDEFINED_SCORE = 12    /* UndefinedScoreError: silhouette of < 2 clusters */
 } gs_status;
 
 /* GS_U8: 8-bit RGB pixels, 3 bytes per point, turned into features on the device exactly as
@@ -162,6 +164,40 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* shard, double h, int64_t n_g
 gs_status gs_shard_run(gs_ctx* ctx, int64_t m_all, const uint32_t* keys, const uint32_t* counts,
                        const int64_t* sums, int64_t n_shard, const gs_config* cfg,
                        gs_result* out);
+
+/* ---- bandwidth sweep (reference module `metrics`) ----
+ * gs_tune_bandwidth replaces tune_bandwidth(X, clusterer, h_grid) with the
+ * GridShift engine as the clusterer and silhouette_subsampled as the score:
+ * per grid value one engine.run on the GPU, then the silhouette of a seeded subsample of
+ * min(n, cap) points.  Entries with < 2 clusters in the sample are recorded with valid = 0
+ * and skipped; best_h = argmax score, ties -> smallest h; no valid entry ->
+ * GS_E_TUNING_FAILED.  Grid values must lie in (0, 1] (GS_E_INVALID_BANDWIDTH), X is one
+ * dataset (batch 1) of fp32/fp64 features, normalised to [0,1] by the caller.
+ * Subsample and summation order are pinned (oracle/gs_oracle.cpp S1-S3): results equal the
+ * CPU oracle's bit for bit.  A gs_tuner runs up to `max_concurrent` entries at once, each on
+ * its own engine context and stream (entries may evaluate concurrently). */
+typedef struct {
+  double h;
+  double score;       /* subsample silhouette; 0 when !valid                      */
+  int64_t k;          /* clusters of the whole dataset                            */
+  int32_t iterations;
+  int32_t converged;
+  int32_t valid;      /* 0: fewer than 2 clusters in the sample (undefined entry) */
+  int32_t reserved;
+} gs_sweep_entry;
+
+typedef struct gs_tuner gs_tuner;
+gs_status gs_tuner_create(int device, int32_t max_concurrent, gs_tuner** out);
+void gs_tuner_destroy(gs_tuner* t);
+const char* gs_tuner_last_error(const gs_tuner* t);
+gs_status gs_tune_bandwidth(gs_tuner* t, const gs_input* X, const double* h_grid, int32_t nh,
+                            int32_t max_iter, int64_t cap, uint64_t seed, gs_sweep_entry* out,
+                            double* best_h);
+/* silhouette_subsampled(X, labels, cap, seed): labels n int32 (host, or
+ * device with labels_on_device); < 2 clusters in the sample -> GS_E_UNDEFINED_SCORE. */
+gs_status gs_silhouette_subsampled(gs_tuner* t, const gs_input* X, const int32_t* labels,
+                                   int32_t labels_on_device, int64_t cap, uint64_t seed,
+                                   double* score);
 
 /* ---- test hooks (parity harness; not needed by callers) ---- */
 

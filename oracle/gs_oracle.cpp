@@ -48,6 +48,8 @@ enum {
   E_EMPTY_INPUT = 3,
   E_INVALID_PARAMETER = 4,
   E_INTERNAL_INVARIANT = 5,
+  E_TUNING_FAILED = 11,
+  E_UNDEFINED_SCORE = 12,
 };
 
 using Key = std::array<int64_t, kMaxD>;  // GridIndex; unused tail is zero
@@ -443,6 +445,140 @@ int gso_run(const double* X, int64_t n, int32_t d, double h, int32_t max_iter, i
   *k_out = (int64_t)e.cells.size();
   *iters_out = iters;
   *converged_out = conv ? 1 : 0;
+  return OK;
+}
+
+}  // extern "C"
+
+// ---- metrics: silhouette_subsampled + tune_bandwidth (ledger :342-348) ----
+// Pins the SPEC leaves open (DESIGN.md §"Bandwidth sweep"):
+//   S1 subsample ("seeded uniform subsample of min(n, cap) points"): n <= cap
+//      takes every point; else a partial Fisher-Yates over [0, n) driven by SplitMix64(seed)
+//      (j = i + next() % (n - i), swap), the first cap positions, sorted ascending;
+//   S2 silhouette: dist = sqrt(sum_c (xi_c - xj_c)^2), terms in c order, no
+//      FMA; for point i the clusters of the sample are walked in ascending label order and
+//      their members in ascending sample position, each cluster's distances summed in that
+//      order (i itself skipped); a = sum/(size-1) over i's own cluster, b = min over the others
+//      of sum/size; s_i = (b - a)/max(a, b), 0 when i's cluster is a singleton or max(a,b)==0;
+//      score = (sum of s_i in sample order) / s;
+//   S3 a sweep entry is undefined when the sample holds < 2 clusters;
+//      best_h = max score, ties -> smallest h (first in grid order after sorting by h).
+namespace {
+uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+double sq_dist(const double* a, const double* b, int d) {
+  double acc = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double t = a[c] - b[c];
+    acc = acc + t * t;
+  }
+  return std::sqrt(acc);
+}
+}  // namespace
+
+extern "C" {
+
+int64_t gso_sample_indices(int64_t n, int64_t cap, uint64_t seed, int64_t* out) {
+  if (n <= cap) {
+    for (int64_t i = 0; i < n; ++i) out[i] = i;
+    return n;
+  }
+  std::unordered_map<int64_t, int64_t> sw;  // sparse Fisher-Yates: only touched slots
+  auto at = [&](int64_t i) {
+    auto it = sw.find(i);
+    return it == sw.end() ? i : it->second;
+  };
+  uint64_t st = seed;
+  for (int64_t i = 0; i < cap; ++i) {
+    const int64_t j = i + (int64_t)(splitmix64(st) % (uint64_t)(n - i));
+    const int64_t vi = at(i), vj = at(j);
+    sw[i] = vj;
+    sw[j] = vi;
+    out[i] = vj;
+  }
+  std::sort(out, out + cap);
+  return cap;
+}
+
+// silhouette (pin S2) of s points (row-major s x d) with labels.
+// Returns E_INVALID_PARAMETER-free status; *valid = 0 when fewer than 2 clusters.
+int gso_silhouette(const double* X, const int32_t* labels, int64_t s, int32_t d, double* score,
+                   int32_t* valid, double* per_point) {
+  std::vector<int64_t> ord(s);
+  for (int64_t i = 0; i < s; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(),
+                   [&](int64_t a, int64_t b) { return labels[a] < labels[b]; });
+  std::vector<int64_t> seg;  // cluster starts in ord
+  for (int64_t t = 0; t < s; ++t)
+    if (t == 0 || labels[ord[t]] != labels[ord[t - 1]]) seg.push_back(t);
+  const int64_t kc = (int64_t)seg.size();
+  seg.push_back(s);
+  *valid = kc >= 2 ? 1 : 0;
+  *score = 0.0;
+  if (kc < 2) return OK;
+  double total = 0.0;
+  for (int64_t i = 0; i < s; ++i) {
+    double a = 0.0, b = INFINITY;
+    bool single = false;
+    for (int64_t c = 0; c < kc; ++c) {
+      double sum = 0.0;
+      for (int64_t t = seg[c]; t < seg[c + 1]; ++t) {
+        const int64_t j = ord[t];
+        if (j == i) continue;
+        sum = sum + sq_dist(X + i * d, X + j * d, d);
+      }
+      const int64_t size = seg[c + 1] - seg[c];
+      if (labels[ord[seg[c]]] == labels[i]) {
+        if (size == 1) single = true;
+        else a = sum / (double)(size - 1);
+      } else {
+        const double mean = sum / (double)size;
+        if (mean < b) b = mean;
+      }
+    }
+    const double mx = a > b ? a : b;
+    const double si = (single || mx == 0.0) ? 0.0 : (b - a) / mx;
+    if (per_point) per_point[i] = si;
+    total = total + si;
+  }
+  *score = total / (double)s;
+  return OK;
+}
+
+// tune_bandwidth with silhouette_subsampled: per h the
+// engine run (build `mode`), its cluster count and iterations, the subsample silhouette.
+int gso_tune(const double* X, int64_t n, int32_t d, const double* hs, int32_t nh,
+             int32_t max_iter, int64_t cap, uint64_t seed, int32_t mode, double* scores,
+             int64_t* ks, int32_t* iters, int32_t* valid, double* best_h) {
+  if (nh < 1 || cap < 2) return E_INVALID_PARAMETER;
+  for (int32_t i = 0; i < nh; ++i)
+    if (!(hs[i] > 0.0 && hs[i] <= 1.0)) return E_INVALID_BANDWIDTH;
+  std::vector<int64_t> idx((size_t)std::min(n, cap));
+  const int64_t s = gso_sample_indices(n, cap, seed, idx.data());
+  std::vector<double> xs((size_t)(s * d));
+  for (int64_t t = 0; t < s; ++t)
+    for (int c = 0; c < d; ++c) xs[t * d + c] = X[idx[t] * d + c];
+  std::vector<int32_t> lab(n), ls(s);
+  std::vector<double> cent((size_t)(n * d));
+  int best = -1;
+  for (int32_t i = 0; i < nh; ++i) {
+    int32_t conv;
+    int st = gso_run(X, n, d, hs[i], max_iter, mode, lab.data(), &ks[i], &iters[i], &conv,
+                     cent.data(), nullptr, nullptr);
+    if (st) return st;
+    for (int64_t t = 0; t < s; ++t) ls[t] = lab[idx[t]];
+    gso_silhouette(xs.data(), ls.data(), s, d, &scores[i], &valid[i], nullptr);
+    if (valid[i] && (best < 0 || scores[i] > scores[best] ||
+                     (scores[i] == scores[best] && hs[i] < hs[best])))
+      best = i;
+  }
+  if (best < 0) return E_TUNING_FAILED;
+  *best_h = hs[best];
   return OK;
 }
 

@@ -35,6 +35,10 @@ def lib():
         L.gso_has_converged.argtypes = [I32, I64, P, P]
         L.gso_run.argtypes = [P, I64, I32, D, I32, I32, P, P, P, P, P, P, P]
         L.gso_fixed_shift.argtypes = [I64, D]
+        L.gso_sample_indices.argtypes = [I64, I64, C.c_uint64, P]
+        L.gso_sample_indices.restype = I64
+        L.gso_silhouette.argtypes = [P, P, I64, I32, P, P, P]
+        L.gso_tune.argtypes = [P, I64, I32, P, I32, I32, I64, C.c_uint64, I32, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -114,3 +118,42 @@ def run(X: np.ndarray, h: float, max_iter: int = 1000, mode: int = BUILD_SPEC) -
 
 def fixed_shift(n: int, h: float) -> int:
     return int(lib().gso_fixed_shift(n, h))
+
+
+def sample_indices(n: int, cap: int, seed: int) -> np.ndarray:
+    """Pin S1 of silhouette_subsampled."""
+    out = np.zeros(min(n, cap), np.int64)
+    lib().gso_sample_indices(n, cap, seed, _p(out))
+    return out
+
+
+def silhouette(X: np.ndarray, labels: np.ndarray):
+    """silhouette (pin S2): (score, valid, per-point values)."""
+    X = np.ascontiguousarray(X, np.float64)
+    lab = np.ascontiguousarray(labels, np.int32)
+    s, d = X.shape
+    sc, va = C.c_double(), C.c_int32()
+    per = np.zeros(s, np.float64)
+    _chk(lib().gso_silhouette(_p(X), _p(lab), s, d, C.byref(sc), C.byref(va), _p(per)))
+    return sc.value, bool(va.value), per
+
+
+def silhouette_subsampled(X: np.ndarray, labels: np.ndarray, cap: int, seed: int = 0):
+    idx = sample_indices(X.shape[0], cap, seed)
+    return silhouette(np.asarray(X, np.float64)[idx], np.asarray(labels)[idx])
+
+
+def tune(X: np.ndarray, hs, max_iter: int = 1000, cap: int = 10000, seed: int = 0,
+         mode: int = BUILD_FIXED) -> dict:
+    """tune_bandwidth with the oracle engine (build `mode`)."""
+    X = np.ascontiguousarray(X, np.float64)
+    n, d = X.shape
+    hs = np.ascontiguousarray(hs, np.float64)
+    nh = len(hs)
+    sc = np.zeros(max(nh, 1)); ks = np.zeros(max(nh, 1), np.int64)
+    it = np.zeros(max(nh, 1), np.int32); va = np.zeros(max(nh, 1), np.int32)
+    best = C.c_double()
+    _chk(lib().gso_tune(_p(X), n, d, _p(hs), nh, max_iter, cap, seed, mode, _p(sc), _p(ks),
+                        _p(it), _p(va), C.byref(best)))
+    return dict(scores=sc[:nh], k=ks[:nh], iterations=it[:nh], valid=va[:nh].astype(bool),
+                best_h=best.value)

@@ -22,6 +22,8 @@ void throw_for_status(gs_status s, const char* detail) {
     case GS_E_INVALID_PARAMETER: throw InvalidParameterError(msg);
     case GS_E_KEY_RANGE: throw InvalidParameterError(msg);
     case GS_E_INTERNAL_INVARIANT: throw InternalInvariantError(msg);
+    case GS_E_TUNING_FAILED: throw TuningFailureError(msg);
+    case GS_E_UNDEFINED_SCORE: throw UndefinedScoreError(msg);
     default: throw Error(msg);
   }
 }

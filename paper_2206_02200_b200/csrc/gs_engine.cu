@@ -528,7 +528,7 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
                         double h, int64_t vol_hint = 0) {
   cudaStream_t st = ctx->stream;
   const int64_t ntot = n * nf;
-  const unsigned nblk = blocks_for(ntot, 256 * 8, (int64_t)ctx->num_sms * 4);
+  const unsigned nblk = blocks_for(ntot, 256 * 4, (int64_t)ctx->num_sms * 4);
   GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
   GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
   GS_TRY(ensure_dense(ctx, std::max<int64_t>(ctx->dense_cap, kDefaultDenseCells), d));
@@ -1372,6 +1372,8 @@ const char* gs_status_string(gs_status s) {
     case GS_E_INVALID_PARAMETER: return "invalid parameter";
     case GS_E_INTERNAL_INVARIANT: return "internal invariant violated";
     case GS_E_KEY_RANGE: return "key range exceeds the dense cell grid";
+    case GS_E_TUNING_FAILED: return "tuning failure";
+    case GS_E_UNDEFINED_SCORE: return "undefined score";
     case GS_E_CUDA: return "CUDA error";
     case GS_E_OOM: return "device out of memory";
     case GS_E_NCCL: return "NCCL error";

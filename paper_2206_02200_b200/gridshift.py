@@ -44,6 +44,14 @@ class InternalInvariantError(Error):
     """errors.hpp:31-33."""
 
 
+class UndefinedScoreError(Error):
+    """errors.hpp:36-38 (silhouette of fewer than 2 clusters)."""
+
+
+class TuningFailureError(Error):
+    """errors.hpp:41-43 (no bandwidth gave a scorable clustering)."""
+
+
 GS_OK = 0
 _STATUS = {
     1: InvalidInputError,
@@ -56,11 +64,14 @@ _STATUS = {
     8: Error,  # GS_E_OOM
     9: Error,  # GS_E_NCCL
     10: Error,  # GS_E_NO_DEVICE
+    11: TuningFailureError,
+    12: UndefinedScoreError,
 }
 STATUS_NAMES = {
     0: "GS_OK", 1: "GS_E_INVALID_INPUT", 2: "GS_E_INVALID_BANDWIDTH", 3: "GS_E_EMPTY_INPUT",
     4: "GS_E_INVALID_PARAMETER", 5: "GS_E_INTERNAL_INVARIANT", 6: "GS_E_KEY_RANGE",
     7: "GS_E_CUDA", 8: "GS_E_OOM", 9: "GS_E_NCCL", 10: "GS_E_NO_DEVICE",
+    11: "GS_E_TUNING_FAILED", 12: "GS_E_UNDEFINED_SCORE",
 }
 
 GS_F32, GS_F64, GS_U8 = 0, 1, 2
@@ -73,7 +84,8 @@ EXPORTED = [
     "gs_validate", "gs_create", "gs_destroy", "gs_run", "gs_get_centroids", "gs_get_history",
     "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
     "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
-    "gs_shard_run", "gs_render",
+    "gs_shard_run", "gs_render", "gs_tuner_create", "gs_tuner_destroy", "gs_tuner_last_error",
+    "gs_tune_bandwidth", "gs_silhouette_subsampled",
 ]
 
 
@@ -100,6 +112,12 @@ class GsStats(C.Structure):
                 ("fixed_shift", C.c_int32), ("dense_cells", C.c_int64),
                 ("ms_k_bin", C.c_double), ("ms_k_label", C.c_double), ("lib_calls", C.c_int64),
                 ("sweep_modes", C.c_int64 * 3), ("resident_cycles", C.c_int64 * 8)]
+
+
+class GsSweepEntry(C.Structure):
+    _fields_ = [("h", C.c_double), ("score", C.c_double), ("k", C.c_int64),
+                ("iterations", C.c_int32), ("converged", C.c_int32), ("valid", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -134,6 +152,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.gs_shard_keybounds.argtypes = [P, C.POINTER(GsInput), D, P, P]
     lib.gs_shard_bin.argtypes = [P, C.POINTER(GsInput), D, I64, P, P, I64, P, P, P, P]
     lib.gs_shard_run.argtypes = [P, I64, P, P, P, I64, C.POINTER(GsConfig), C.POINTER(GsResult)]
+    lib.gs_tuner_create.argtypes = [C.c_int, I32, C.POINTER(P)]
+    lib.gs_tuner_destroy.argtypes = [P]
+    lib.gs_tuner_destroy.restype = None
+    lib.gs_tuner_last_error.argtypes = [P]
+    lib.gs_tuner_last_error.restype = C.c_char_p
+    lib.gs_tune_bandwidth.argtypes = [P, C.POINTER(GsInput), P, I32, I32, I64, C.c_uint64,
+                                      C.POINTER(GsSweepEntry), C.POINTER(D)]
+    lib.gs_silhouette_subsampled.argtypes = [P, C.POINTER(GsInput), P, I32, I64, C.c_uint64,
+                                             C.POINTER(D)]
     _lib = lib
     return lib
 
@@ -443,3 +470,83 @@ def run(X, cfg: EngineConfig) -> ClusterLabeling:
 
 def fixed_shift(n: int, h: float) -> int:
     return int(load_library().gs_fixed_shift(n, h))
+
+
+# ----------------------------------------------------------------------------- metrics
+@dataclass
+class SweepEntry:
+    """One (h, silhouette score, cluster count) pair of BandwidthSweepResult."""
+    h: float
+    score: Optional[float]   # None: undefined (< 2 clusters in the sample), skipped
+    k: int
+    iterations: int
+    converged: bool
+
+
+@dataclass
+class BandwidthSweepResult:
+    """evaluated pairs and best_h."""
+    entries: List[SweepEntry]
+    best_h: float
+
+
+class Tuner:
+    """tune_bandwidth with the GPU engine as the clusterer and
+    silhouette_subsampled as the score, over gs_tune_bandwidth: up to
+    ``max_concurrent`` sweep entries run at once on one GPU, each on its own engine context."""
+
+    def __init__(self, device: int = 0, max_concurrent: int = 8):
+        self._lib = load_library()
+        h = C.c_void_p()
+        _raise(self._lib.gs_tuner_create(device, max_concurrent, C.byref(h)), "gs_tuner_create")
+        self._t = h
+
+    def close(self) -> None:
+        if self._t:
+            self._lib.gs_tuner_destroy(self._t)
+            self._t = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, status: int) -> None:
+        if status != GS_OK:
+            _raise(status, (self._lib.gs_tuner_last_error(self._t) or b"").decode())
+
+    @staticmethod
+    def _input(X: np.ndarray):
+        if X.ndim != 2:
+            raise InvalidParameterError("X must be n x d")
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        dt = GS_F32 if X.dtype == np.float32 else GS_F64
+        return X, GsInput(X.ctypes.data, X.shape[0], X.shape[1], dt, 1, 0, 0)
+
+    def tune_bandwidth(self, X: np.ndarray, h_grid=None, max_iter: int = 1000, cap: int = 10000,
+                       seed: int = 0) -> BandwidthSweepResult:
+        if h_grid is None:  # SPEC.md:347 default grid {0.05, 0.10, ..., 1.00}
+            h_grid = [round(0.05 * i, 2) for i in range(1, 21)]
+        X, inp = self._input(X)
+        hs = np.ascontiguousarray(h_grid, np.float64)
+        out = (GsSweepEntry * max(len(hs), 1))()
+        best = C.c_double()
+        self._check(self._lib.gs_tune_bandwidth(self._t, C.byref(inp), hs.ctypes.data, len(hs),
+                                                max_iter, cap, seed, out, C.byref(best)))
+        ents = [SweepEntry(e.h, e.score if e.valid else None, e.k, e.iterations,
+                           bool(e.converged)) for e in out[:len(hs)]]
+        return BandwidthSweepResult(ents, best.value)
+
+    def silhouette_subsampled(self, X: np.ndarray, labels: np.ndarray, cap: int,
+                              seed: int = 0) -> float:
+        X, inp = self._input(X)
+        lab = np.ascontiguousarray(labels, np.int32)
+        if lab.shape != (X.shape[0],):
+            raise InvalidInputError("labels must have one entry per point")
+        sc = C.c_double()
+        self._check(self._lib.gs_silhouette_subsampled(self._t, C.byref(inp), lab.ctypes.data, 0,
+                                                       cap, seed, C.byref(sc)))
+        return sc.value
