@@ -39,7 +39,9 @@ typedef enum {
   GS_E_NCCL = 9,               /* Error: collective failure (multi-GPU driver)                  */
   GS_E_NO_DEVICE = 10,         /* Error: no sm_100 device visible                               */
   GS_E_TUNING_FAILED = 11,     /* TuningFailureError: no bandwidth gave a scorable clustering   */
-  GS_E_UNDEFINED_SCORE = 12    /* UndefinedScoreError: silhouette of < 2 clusters */
+  GS_E_UNDEFINED_SCORE = 12,   /* UndefinedScoreError: silhouette of < 2 clusters */
+  GS_E_INVALID_WINDOW = 13,    /* InvalidWindowError: tracking window outside the frame         */
+  GS_E_SELECTION = 14          /* SelectionError: selected cluster id does not exist            */
 } gs_status;
 
 /* GS_U8: 8-bit RGB pixels, 3 bytes per point, turned into features on the device exactly as
@@ -198,6 +200,41 @@ gs_status gs_tune_bandwidth(gs_tuner* t, const gs_input* X, const double* h_grid
 gs_status gs_silhouette_subsampled(gs_tuner* t, const gs_input* X, const int32_t* labels,
                                    int32_t labels_on_device, int64_t cap, uint64_t seed,
                                    double* score);
+
+/* ---- tracker (reference module `tracker`, Algorithm 2) ----
+ * init_tracker -> gs_track_init: engine.run on the (r,g,b)/255 colours of the
+ * window's pixels of frame0 (H x W x 3 u8, row-major), selection of the top_k largest clusters
+ * (or n_ids explicit ids), reference bin B = colour cells of the selected pixels.
+ * track_sequence -> gs_track_sequence: track_frame on each
+ * of T frames in order, continuing the tracker's state across calls; out[t] = emitted window,
+ * lost[t] = 1 when the target was not found in any inner iteration, inner[t] = iterations.
+ * Window, colour-cell and inner-loop semantics are pinned (oracle/gs_oracle.cpp T1-T5); the
+ * results equal the CPU oracle's bit for bit.  The whole sequence runs in one kernel launch. */
+typedef struct {
+  double ox, oy;  /* centre (x = column, y = row), pixels */
+  double l, w;    /* length (x extent) and width (y extent), pixels, > 0 */
+} gs_window;
+
+typedef struct {
+  double h;                /* colour bandwidth, > 0 (and >= ~1/72: the cell bitmap is on chip) */
+  double f;                /* increment factor >= 1 (search region W(o, l/f, w/f)); SPEC default 1 */
+  double eta;              /* centre tolerance in pixels, > 0; SPEC default 1 */
+  int32_t max_inner_iters; /* SPEC default 20 */
+  int32_t engine_max_iter; /* engine.run max_iterations for init (SPEC default 1000) */
+  int32_t top_k;           /* selection: k largest clusters (SPEC default 1) when n_ids == 0 */
+  int32_t n_ids;
+  const int32_t* ids;      /* explicit cluster ids (n_ids > 0) */
+} gs_tracker_config;
+
+typedef struct gs_tracker gs_tracker;
+gs_status gs_tracker_create(int device, gs_tracker** out);
+void gs_tracker_destroy(gs_tracker* t);
+const char* gs_tracker_last_error(const gs_tracker* t);
+gs_status gs_track_init(gs_tracker* t, const uint8_t* frame0, int32_t H, int32_t W,
+                        int32_t on_device, const gs_window* win, const gs_tracker_config* cfg,
+                        int64_t* k_out);
+gs_status gs_track_sequence(gs_tracker* t, const uint8_t* frames, int64_t T, int32_t on_device,
+                            gs_window* out, int32_t* lost, int32_t* inner);
 
 /* ---- test hooks (parity harness; not needed by callers) ---- */
 

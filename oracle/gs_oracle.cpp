@@ -50,6 +50,8 @@ enum {
   E_INTERNAL_INVARIANT = 5,
   E_TUNING_FAILED = 11,
   E_UNDEFINED_SCORE = 12,
+  E_INVALID_WINDOW = 13,
+  E_SELECTION = 14,
 };
 
 using Key = std::array<int64_t, kMaxD>;  // GridIndex; unused tail is zero
@@ -579,6 +581,159 @@ int gso_tune(const double* X, int64_t n, int32_t d, const double* hs, int32_t nh
   }
   if (best < 0) return E_TUNING_FAILED;
   *best_h = hs[best];
+  return OK;
+}
+
+}  // extern "C"
+
+// ---- tracker: GridShift object tracking, Algorithm 2 ----
+// Pins the SPEC leaves open (DESIGN.md §"Tracker"):
+//   T1 window W(o, l, w) = pixels (x, y) with ceil(ox - l*0.5) <= x <= floor(ox + l*0.5) and
+//      ceil(oy - w*0.5) <= y <= floor(oy + w*0.5), clipped to the frame;
+//   T2 colour cell of a pixel: k_c = floor((v_c / 255.0) / h) per channel (the segmentation
+//      features, and grid_index); id (k_r*K + k_g)*K + k_b, K = floor(1/h)+1;
+//   T3 init: engine.run on the window's (r,g,b)/255 in row-major pixel order;
+//      top_k = the k largest clusters by pixel count (ties -> smaller id) or explicit ids;
+//      B = colour cells of the selected pixels;
+//   T4 track_frame: per inner iteration: region W(o, l/f, w/f); R = region
+//      pixels whose cell is in B; R empty -> l, w *= 1.1; else o' = (sum x / |R|, sum y / |R|),
+//      B = cells of R, l *= (max x - min x < l) ? 0.99 : 1.01 (w likewise on y), and the loop
+//      ends when sqrt(dx*dx + dy*dy) < eta; at most max_inner iterations; lost = R was empty
+//      in every iteration;
+//   T5 track_sequence: frames[0] initialises, frames 1..T-1 are tracked.
+namespace {
+struct TrackState {
+  double ox, oy, l, w;
+  std::vector<uint8_t> B;  // K^3 cell bitmap (one byte per cell here)
+};
+
+int track_cells(double h, int* K_out) {
+  const double K = std::floor(1.0 / h) + 1.0;
+  if (!(K >= 1.0) || K * K * K > (double)(1 << 22)) return E_INVALID_PARAMETER;
+  *K_out = (int)K;
+  return OK;
+}
+
+inline int pixel_cell(const uint8_t* px, double h, int K) {
+  int id = 0;
+  for (int c = 0; c < 3; ++c) id = id * K + (int)std::floor(((double)px[c] / 255.0) / h);
+  return id;
+}
+
+bool window_range(double o, double len, int lim, int* lo, int* hi) {
+  const double a = std::ceil(o - len * 0.5), b = std::floor(o + len * 0.5);
+  const double ca = std::max(a, 0.0), cb = std::min(b, (double)(lim - 1));
+  if (!(ca <= cb)) return false;
+  *lo = (int)ca;
+  *hi = (int)cb;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+int gso_track(const uint8_t* frames, int64_t T, int32_t H, int32_t W, const double* win0,
+              double h, double f, double eta, int32_t max_inner, int32_t engine_max_iter,
+              int32_t top_k, const int32_t* ids, int32_t n_ids, int32_t mode, double* out_win,
+              int32_t* out_lost, int32_t* out_inner) {
+  if (!(h > 0.0) || !std::isfinite(h)) return E_INVALID_BANDWIDTH;
+  if (T < 1 || H < 1 || W < 1 || !(f >= 1.0) || !(eta > 0.0) || max_inner < 1 ||
+      engine_max_iter < 1 || (n_ids == 0 && top_k < 1) || !(win0[2] > 0.0) || !(win0[3] > 0.0))
+    return E_INVALID_PARAMETER;
+  int K;
+  if (track_cells(h, &K)) return E_INVALID_PARAMETER;
+  const int64_t fpx = (int64_t)H * W;
+  // ---- T3: init on frames[0]
+  int x0, x1, y0, y1;
+  if (!window_range(win0[0], win0[2], W, &x0, &x1) || !window_range(win0[1], win0[3], H, &y0, &y1))
+    return E_INVALID_WINDOW;
+  const int cw = x1 - x0 + 1, ch = y1 - y0 + 1;
+  const int64_t np = (int64_t)cw * ch;
+  std::vector<double> X((size_t)(np * 3));
+  for (int y = y0; y <= y1; ++y)
+    for (int x = x0; x <= x1; ++x) {
+      const uint8_t* px = frames + ((int64_t)y * W + x) * 3;
+      const int64_t q = (int64_t)(y - y0) * cw + (x - x0);
+      for (int c = 0; c < 3; ++c) X[q * 3 + c] = (double)px[c] / 255.0;
+    }
+  std::vector<int32_t> lab(np);
+  std::vector<double> cent((size_t)(np * 3));
+  int64_t k;
+  int32_t it, cv;
+  int st = gso_run(X.data(), np, 3, h, engine_max_iter, mode, lab.data(), &k, &it, &cv,
+                   cent.data(), nullptr, nullptr);
+  if (st) return st;
+  std::vector<int64_t> size(k, 0);
+  for (int64_t q = 0; q < np; ++q) ++size[lab[q]];
+  std::vector<uint8_t> sel(k, 0);
+  if (n_ids > 0) {
+    for (int32_t i = 0; i < n_ids; ++i) {
+      if (ids[i] < 0 || ids[i] >= k) return E_SELECTION;
+      sel[ids[i]] = 1;
+    }
+  } else {
+    std::vector<int64_t> ord(k);
+    for (int64_t c = 0; c < k; ++c) ord[c] = c;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return size[a] > size[b]; });
+    for (int64_t r = 0; r < std::min<int64_t>(top_k, k); ++r) sel[ord[r]] = 1;
+  }
+  TrackState s{win0[0], win0[1], win0[2], win0[3], std::vector<uint8_t>((size_t)K * K * K, 0)};
+  for (int y = y0; y <= y1; ++y)
+    for (int x = x0; x <= x1; ++x)
+      if (sel[lab[(int64_t)(y - y0) * cw + (x - x0)]])
+        s.B[pixel_cell(frames + ((int64_t)y * W + x) * 3, h, K)] = 1;
+  // ---- T4/T5
+  std::vector<uint8_t> nb(s.B.size());
+  for (int64_t t = 1; t < T; ++t) {
+    const uint8_t* fr = frames + t * fpx * 3;
+    bool found = false;
+    int inner = 0;
+    for (int itn = 0; itn < max_inner; ++itn) {
+      ++inner;
+      int64_t cnt = 0, sx = 0, sy = 0;
+      int mnx = W, mxx = -1, mny = H, mxy = -1;
+      std::fill(nb.begin(), nb.end(), 0);
+      int a0, a1, b0, b1;
+      const double lr = s.l / f, wr = s.w / f;
+      if (window_range(s.ox, lr, W, &a0, &a1) && window_range(s.oy, wr, H, &b0, &b1)) {
+        for (int y = b0; y <= b1; ++y)
+          for (int x = a0; x <= a1; ++x) {
+            const int cell = pixel_cell(fr + ((int64_t)y * W + x) * 3, h, K);
+            if (!s.B[cell]) continue;
+            ++cnt;
+            sx += x;
+            sy += y;
+            mnx = std::min(mnx, x);
+            mxx = std::max(mxx, x);
+            mny = std::min(mny, y);
+            mxy = std::max(mxy, y);
+            nb[cell] = 1;
+          }
+      }
+      if (cnt == 0) {  // target lost in this region: grow the window (Alg. 2 lines 9-10)
+        s.l = s.l * 1.1;
+        s.w = s.w * 1.1;
+        continue;
+      }
+      found = true;
+      const double nx = (double)sx / (double)cnt, ny = (double)sy / (double)cnt;
+      s.B.swap(nb);
+      s.l = ((double)(mxx - mnx) < s.l) ? s.l * 0.99 : s.l * 1.01;
+      s.w = ((double)(mxy - mny) < s.w) ? s.w * 0.99 : s.w * 1.01;
+      const double dx = nx - s.ox, dy = ny - s.oy;
+      const double disp = std::sqrt(dx * dx + dy * dy);
+      s.ox = nx;
+      s.oy = ny;
+      if (disp < eta) break;
+    }
+    double* o = out_win + (t - 1) * 4;
+    o[0] = s.ox;
+    o[1] = s.oy;
+    o[2] = s.l;
+    o[3] = s.w;
+    out_lost[t - 1] = found ? 0 : 1;
+    out_inner[t - 1] = inner;
+  }
   return OK;
 }
 

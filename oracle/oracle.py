@@ -38,6 +38,7 @@ def lib():
         L.gso_sample_indices.argtypes = [I64, I64, C.c_uint64, P]
         L.gso_sample_indices.restype = I64
         L.gso_silhouette.argtypes = [P, P, I64, I32, P, P, P]
+        L.gso_track.argtypes = [P, I64, I32, I32, P, D, D, D, I32, I32, I32, P, I32, I32, P, P, P]
         L.gso_tune.argtypes = [P, I64, I32, P, I32, I32, I64, C.c_uint64, I32, P, P, P, P, P]
         _lib = L
     return _lib
@@ -157,3 +158,21 @@ def tune(X: np.ndarray, hs, max_iter: int = 1000, cap: int = 10000, seed: int = 
                         _p(it), _p(va), C.byref(best)))
     return dict(scores=sc[:nh], k=ks[:nh], iterations=it[:nh], valid=va[:nh].astype(bool),
                 best_h=best.value)
+
+
+def track(frames: np.ndarray, window, h: float, f: float = 1.0, eta: float = 1.0,
+          max_inner: int = 20, engine_max_iter: int = 1000, top_k: int = 1, ids=None,
+          mode: int = BUILD_FIXED) -> dict:
+    """tracker (pins T1-T5): frames [T][H][W][3] u8; frames[0] initialises.
+    Returns per tracked frame the window (ox, oy, l, w), the lost flag and inner iterations."""
+    fr = np.ascontiguousarray(frames, np.uint8)
+    T, H, W, _ = fr.shape
+    w0 = np.ascontiguousarray(window, np.float64)
+    ida = np.ascontiguousarray([] if ids is None else ids, np.int32)
+    out = np.zeros((max(T - 1, 1), 4))
+    lost = np.zeros(max(T - 1, 1), np.int32)
+    inner = np.zeros(max(T - 1, 1), np.int32)
+    _chk(lib().gso_track(_p(fr), T, H, W, _p(w0), h, f, eta, max_inner, engine_max_iter, top_k,
+                         _p(ida) if len(ida) else None, len(ida), mode, _p(out), _p(lost),
+                         _p(inner)))
+    return dict(windows=out[:T - 1], lost=lost[:T - 1].astype(bool), inner=inner[:T - 1])

@@ -24,6 +24,8 @@ void throw_for_status(gs_status s, const char* detail) {
     case GS_E_INTERNAL_INVARIANT: throw InternalInvariantError(msg);
     case GS_E_TUNING_FAILED: throw TuningFailureError(msg);
     case GS_E_UNDEFINED_SCORE: throw UndefinedScoreError(msg);
+    case GS_E_INVALID_WINDOW: throw InvalidWindowError(msg);
+    case GS_E_SELECTION: throw SelectionError(msg);
     default: throw Error(msg);
   }
 }

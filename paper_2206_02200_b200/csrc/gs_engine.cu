@@ -1374,6 +1374,8 @@ const char* gs_status_string(gs_status s) {
     case GS_E_KEY_RANGE: return "key range exceeds the dense cell grid";
     case GS_E_TUNING_FAILED: return "tuning failure";
     case GS_E_UNDEFINED_SCORE: return "undefined score";
+    case GS_E_INVALID_WINDOW: return "invalid window";
+    case GS_E_SELECTION: return "selection error";
     case GS_E_CUDA: return "CUDA error";
     case GS_E_OOM: return "device out of memory";
     case GS_E_NCCL: return "NCCL error";

@@ -52,6 +52,14 @@ class TuningFailureError(Error):
     """errors.hpp:41-43 (no bandwidth gave a scorable clustering)."""
 
 
+class InvalidWindowError(InvalidInputError):
+    """errors.hpp:55-57 (tracking window outside the frame)."""
+
+
+class SelectionError(InvalidInputError):
+    """errors.hpp:59-61 (selected cluster does not exist)."""
+
+
 GS_OK = 0
 _STATUS = {
     1: InvalidInputError,
@@ -66,12 +74,15 @@ _STATUS = {
     10: Error,  # GS_E_NO_DEVICE
     11: TuningFailureError,
     12: UndefinedScoreError,
+    13: InvalidWindowError,
+    14: SelectionError,
 }
 STATUS_NAMES = {
     0: "GS_OK", 1: "GS_E_INVALID_INPUT", 2: "GS_E_INVALID_BANDWIDTH", 3: "GS_E_EMPTY_INPUT",
     4: "GS_E_INVALID_PARAMETER", 5: "GS_E_INTERNAL_INVARIANT", 6: "GS_E_KEY_RANGE",
     7: "GS_E_CUDA", 8: "GS_E_OOM", 9: "GS_E_NCCL", 10: "GS_E_NO_DEVICE",
-    11: "GS_E_TUNING_FAILED", 12: "GS_E_UNDEFINED_SCORE",
+    11: "GS_E_TUNING_FAILED", 12: "GS_E_UNDEFINED_SCORE", 13: "GS_E_INVALID_WINDOW",
+    14: "GS_E_SELECTION",
 }
 
 GS_F32, GS_F64, GS_U8 = 0, 1, 2
@@ -85,7 +96,8 @@ EXPORTED = [
     "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
     "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
     "gs_shard_run", "gs_render", "gs_tuner_create", "gs_tuner_destroy", "gs_tuner_last_error",
-    "gs_tune_bandwidth", "gs_silhouette_subsampled",
+    "gs_tune_bandwidth", "gs_silhouette_subsampled", "gs_tracker_create", "gs_tracker_destroy",
+    "gs_tracker_last_error", "gs_track_init", "gs_track_sequence",
 ]
 
 
@@ -118,6 +130,16 @@ class GsSweepEntry(C.Structure):
     _fields_ = [("h", C.c_double), ("score", C.c_double), ("k", C.c_int64),
                 ("iterations", C.c_int32), ("converged", C.c_int32), ("valid", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class GsWindow(C.Structure):
+    _fields_ = [("ox", C.c_double), ("oy", C.c_double), ("l", C.c_double), ("w", C.c_double)]
+
+
+class GsTrackerConfig(C.Structure):
+    _fields_ = [("h", C.c_double), ("f", C.c_double), ("eta", C.c_double),
+                ("max_inner_iters", C.c_int32), ("engine_max_iter", C.c_int32),
+                ("top_k", C.c_int32), ("n_ids", C.c_int32), ("ids", C.c_void_p)]
 
 
 _lib = None
@@ -161,6 +183,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                       C.POINTER(GsSweepEntry), C.POINTER(D)]
     lib.gs_silhouette_subsampled.argtypes = [P, C.POINTER(GsInput), P, I32, I64, C.c_uint64,
                                              C.POINTER(D)]
+    lib.gs_tracker_create.argtypes = [C.c_int, C.POINTER(P)]
+    lib.gs_tracker_destroy.argtypes = [P]
+    lib.gs_tracker_destroy.restype = None
+    lib.gs_tracker_last_error.argtypes = [P]
+    lib.gs_tracker_last_error.restype = C.c_char_p
+    lib.gs_track_init.argtypes = [P, P, I32, I32, I32, C.POINTER(GsWindow),
+                                  C.POINTER(GsTrackerConfig), C.POINTER(I64)]
+    lib.gs_track_sequence.argtypes = [P, P, I64, I32, C.POINTER(GsWindow), P, P]
     _lib = lib
     return lib
 
@@ -550,3 +580,70 @@ class Tuner:
         self._check(self._lib.gs_silhouette_subsampled(self._t, C.byref(inp), lab.ctypes.data, 0,
                                                        cap, seed, C.byref(sc)))
         return sc.value
+
+
+# ----------------------------------------------------------------------------- tracker
+@dataclass
+class TrackerConfig:
+    """TrackerConfig with the ledger defaults."""
+    h: float
+    f: float = 1.0
+    eta: float = 1.0
+    max_inner_iters: int = 20
+    engine_max_iter: int = 1000
+    top_k: int = 1
+    ids: Optional[List[int]] = None
+
+
+class Tracker:
+    """init_tracker / track_frame / track_sequence over gs_track_*: the
+    engine on the GPU for init, the whole tracked sequence in one kernel launch."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        h = C.c_void_p()
+        _raise(self._lib.gs_tracker_create(device, C.byref(h)), "gs_tracker_create")
+        self._t = h
+        self._ids = None
+
+    def close(self) -> None:
+        if self._t:
+            self._lib.gs_tracker_destroy(self._t)
+            self._t = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, status: int) -> None:
+        if status != GS_OK:
+            _raise(status, (self._lib.gs_tracker_last_error(self._t) or b"").decode())
+
+    def init(self, frame0: np.ndarray, window, cfg: TrackerConfig) -> int:
+        """init_tracker: returns the number of clusters found in the window."""
+        fr = np.ascontiguousarray(frame0, np.uint8)
+        if fr.ndim != 3 or fr.shape[2] != 3:
+            raise InvalidInputError("frame must be H x W x 3 uint8")
+        ids = np.ascontiguousarray(cfg.ids or [], np.int32)
+        self._ids = ids
+        c = GsTrackerConfig(cfg.h, cfg.f, cfg.eta, cfg.max_inner_iters, cfg.engine_max_iter,
+                            cfg.top_k, len(ids), ids.ctypes.data if len(ids) else None)
+        w = GsWindow(*[float(v) for v in window])
+        k = C.c_int64()
+        self._check(self._lib.gs_track_init(self._t, fr.ctypes.data, fr.shape[0], fr.shape[1], 0,
+                                            C.byref(w), C.byref(c), C.byref(k)))
+        return k.value
+
+    def track_sequence(self, frames: np.ndarray):
+        """track_sequence over frames [T][H][W][3]: (windows T x 4, lost T, inner T)."""
+        fr = np.ascontiguousarray(frames, np.uint8)
+        T = fr.shape[0]
+        out = (GsWindow * T)()
+        lost = np.zeros(T, np.int32)
+        inner = np.zeros(T, np.int32)
+        self._check(self._lib.gs_track_sequence(self._t, fr.ctypes.data, T, 0, out,
+                                                lost.ctypes.data, inner.ctypes.data))
+        win = np.array([[o.ox, o.oy, o.l, o.w] for o in out])
+        return win, lost.astype(bool), inner
