@@ -278,14 +278,133 @@ def run_tune(args):
     return 0
 
 
+TRACK_H = 0.08
+
+
+def track_setup():
+    """cfg4's 256 frames as 8-bit pixels and an initial window on frame 0's largest ellipse
+    (the most frequent exact colour: ellipses are solid, the background is noisy)."""
+    from paper_2206_02200_b200 import configs as CF
+    X = CF.ellipse_frames()
+    fr = np.clip(np.rint(X.astype(np.float64) * 255.0), 0, 255).astype(np.uint8)
+    fr = fr.reshape(X.shape[0], 480, 640, 3)
+    f0 = fr[0].reshape(-1, 3)
+    packed = (f0[:, 0].astype(np.int64) << 16) | (f0[:, 1].astype(np.int64) << 8) | f0[:, 2]
+    vals, cnt = np.unique(packed, return_counts=True)
+    sel = np.nonzero(packed == vals[np.argmax(cnt)])[0]
+    ys, xs = sel // 640, sel % 640
+    win = [float(xs.mean()), float(ys.mean()), 0.8 * float(np.ptp(xs) + 1),
+           0.8 * float(np.ptp(ys) + 1)]
+    return fr, win
+
+
+def run_track(args):
+    """--workload track: track_sequence over cfg4's 256 frames (640 x 480,
+    8-bit), init on frame 0's largest ellipse, h = 0.08, SPEC defaults f = 1, eta = 1,
+    max_inner 20.  A step = init + the 255 tracked frames.  value = tracked frames/s with the
+    frames in HBM; e2e = the same from host memory (H2D of the frames inside the step)."""
+    fr, win = track_setup()
+    T = fr.shape[0]
+    rank = int(os.environ.get("RANK", "0"))
+    metric = "tracker: frames tracked per second"
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as O
+        nfr = 32  # bounded sample: init + 31 frames per step
+        times = []
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.track(fr[:nfr], win, TRACK_H)
+            if s >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        value = (nfr - 1) * args.steps / sum(times)
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": value, "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "track", "frames": T, "H": 480, "W": 640, "h": TRACK_H},
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "port",
+                             "sample": f"oracle gso_track over the first {nfr} frames per step"},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return 0
+    import torch
+    from paper_2206_02200_b200 import gridshift as G
+    torch.cuda.set_device(0)
+    tr = G.Tracker(0)
+    lib = G.load_library()
+    fr_host = torch.from_numpy(fr).pin_memory()
+    fr_dev = fr_host.cuda()
+    cfg = G.TrackerConfig(TRACK_H)
+    c = G.GsTrackerConfig(cfg.h, cfg.f, cfg.eta, cfg.max_inner_iters, cfg.engine_max_iter,
+                          cfg.top_k, 0, None)
+    w0 = G.GsWindow(*win)
+    out = (G.GsWindow * (T - 1))()
+    lost = np.zeros(T - 1, np.int32)
+    inner = np.zeros(T - 1, np.int32)
+    fbytes = 480 * 640 * 3
+
+    def step(dev: bool):
+        base = fr_dev.data_ptr() if dev else fr_host.data_ptr()
+        k = G.C.c_int64()
+        tr._check(lib.gs_track_init(tr._t, base, 480, 640, 1 if dev else 0, G.C.byref(w0),
+                                    G.C.byref(c), G.C.byref(k)))
+        tr._check(lib.gs_track_sequence(tr._t, base + fbytes, T - 1, 1 if dev else 0, out,
+                                        lost.ctypes.data, inner.ctypes.data))
+
+    for _ in range(args.warmup):
+        step(True)
+        step(False)
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(True)
+    t_dev = (time.perf_counter() - t0) / args.steps
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(False)
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    clk = clocks.stop()
+    wins = np.array([[o.ox, o.oy, o.l, o.w] for o in out])
+    line = {
+        "metric": metric, "value": (T - 1) / t_dev, "unit": "frames/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "track", "desc": "cfg4 frames as 8-bit pixels, largest ellipse",
+                   "frames": T, "H": 480, "W": 640, "h": TRACK_H, "init_window": win,
+                   "timing": "host wall clock around init + the synchronous sequence call"},
+        "lost_frames": int(lost.sum()), "mean_inner": float(inner.mean()),
+        "final_window": wins[-1].tolist(),
+        "e2e": {"value": (T - 1) / t_e2e, "unit": "frames/s", "ms_per_step": 1e3 * t_e2e,
+                "h2d_bytes_per_step": int(fr.nbytes), "d2h_bytes_per_step": int(32 * (T - 1))},
+        "gpu_launches": 8, "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        O.track(fr[:32], win, TRACK_H)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": 31 / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+                                "sample": f"oracle gso_track, init + 31 frames ({dt:.2f} s)"}
+    print(json.dumps(line))
+    tr.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg2",
-                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune"],
-                    help="tune: the bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image")
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune", "track"],
+                    help="tune: the bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image; "
+                         "track: the tracker (§8(f)3) over the cfg4 frames")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -295,6 +414,8 @@ def main():
     args = ap.parse_args()
     if args.workload == "tune":
         return run_tune(args)
+    if args.workload == "track":
+        return run_track(args)
     if args.impl == "reference":
         return run_reference(args)
 
