@@ -641,11 +641,94 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
     configured = true;
   }
+  // the cluster sweep (NC CTAs on NC SMs, DSMEM pending counts and queues) when the owned
+  // share of 3 words per cell fits each CTA; GS_SWEEP_CLUSTER=0 forces the single-CTA sweep
+  {
+    static int nc_env = -1;
+    if (nc_env < 0) {
+      const char* v = getenv("GS_SWEEP_CLUSTER");
+      nc_env = v ? atoi(v) : 16;
+    }
+    int NC = nc_env;
+    const size_t csmem = 12 * (size_t)((m + NC - 1) / std::max(NC, 1));
+    static int cl_cfg = 0;  // 1: 16-CTA clusters allowed, 2: refused (use 8)
+    if (NC >= 2 && csmem <= kBudget) {
+      if (!cl_cfg) {
+        GS_CK(cudaFuncSetAttribute(gs::k_sweep_cluster<D>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
+        cl_cfg = cudaFuncSetAttribute(gs::k_sweep_cluster<D>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                         cudaSuccess
+                     ? 1
+                     : 2;
+        cudaGetLastError();
+      }
+      if (NC > 8 && cl_cfg != 1) NC = 8;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3((unsigned)NC);
+      lc.blockDim = dim3(gs::sweep_global_threads<D>());
+      lc.dynamicSmemBytes = 12 * (size_t)((m + NC - 1) / NC);
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)NC;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaError_t le = cudaLaunchKernelEx(&lc, gs::k_sweep_cluster<D>, (int)m, KP,
+                                          (const uint32_t*)lists, (const int32_t*)ctx->nbn.as<int32_t>(),
+                                          (const int32_t*)ctx->nbe.as<int32_t>(),
+                                          (const uint32_t*)ctx->ccnt[cur].as<uint32_t>(),
+                                          (const uint32_t*)ctx->den.as<uint32_t>(),
+                                          (const double*)ctx->rden.as<double>(), Q);
+      if (le == cudaSuccess) {
+        GS_LAUNCHED("k_sweep_cluster");
+        return GS_OK;
+      }
+      cudaGetLastError();  // a cluster this size cannot be scheduled: single-CTA sweep below
+      nc_env = NC > 8 ? 8 : 0;
+    }
+  }
+  long long* prof = nullptr;
+  const bool trace = getenv("GS_TRACE_GLOBAL") != nullptr;
+  if (trace) {
+    GS_TRY(grow(ctx, ctx->dbg, 8 * (2000 * 66 + 8)));
+    GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * (2000 * 66 + 8), st));
+    prof = (long long*)ctx->dbg.p;
+  }
   gs::k_sweep_global<D><<<1, gs::sweep_global_threads<D>(), in_smem ? smem : 0, st>>>(
       (int)m, KP, lists, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
       ctx->ccnt[cur].as<uint32_t>(), ctx->den.as<uint32_t>(), ctx->rden.as<double>(), Q,
-      ctx->lvl.as<unsigned>(), ctx->order.as<unsigned>(), in_smem);
+      ctx->lvl.as<unsigned>(), ctx->order.as<unsigned>(), in_smem, prof);
   GS_LAUNCHED("k_sweep_global");
+  if (trace) {  // diagnostics: per-level update / release / barrier split of this sweep
+    std::vector<long long> h(2000 * 66 + 8);
+    GS_CK(cudaMemcpyAsync(h.data(), prof, 8 * h.size(), cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaStreamSynchronize(st));
+    const int nl = (int)std::min<long long>(h[2000 * 66], 2000);
+    const int nw = gs::sweep_global_threads<D>() / 32;
+    double su = 0, sr = 0, sb = 0, sw = 0;
+    for (int l = 0; l < nl; ++l) {
+      const long long* p = &h[(size_t)l * 66];
+      long long ue = 0, re = 0;
+      for (int w = 0; w < nw; ++w) {
+        ue = std::max(ue, p[2 + w]);
+        re = std::max(re, p[34 + w]);
+      }
+      const long long nxt = l + 1 < nl ? h[(size_t)(l + 1) * 66 + 1] : re;
+      su += ue - p[1];
+      sr += re - ue;
+      sb += nxt - re;
+      sw += p[0];
+      if (l < 8 || l % 20 == 0)
+        fprintf(stderr, "gsweep m %lld level %4d width %5lld update %6lld release %6lld barrier %5lld\n",
+                (long long)m, l, p[0], ue - p[1], re - ue, nxt - re);
+    }
+    fprintf(stderr, "gsweep m %lld levels %d mean width %.1f | mean cycles: update %.0f release %.0f barrier %.0f\n",
+            (long long)m, nl, sw / std::max(nl, 1), su / std::max(nl, 1), sr / std::max(nl, 1),
+            sb / std::max(nl, 1));
+  }
   return GS_OK;
 }
 

@@ -12,6 +12,8 @@
 // Operands and order of the fp64 adds are exactly the serial sweep's (pins P2/P3).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -90,7 +92,9 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
     const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
     const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q,
-    unsigned* pend_g, unsigned* queue_g, int in_smem) {
+    unsigned* pend_g, unsigned* queue_g, int in_smem, long long* prof = nullptr) {
+  // prof (diagnostics, GS_TRACE_GLOBAL): per level [width, start, per-warp update end x 32,
+  // per-warp release end x 32] clock stamps, plain stores (no atomics on the path)
   extern __shared__ __align__(16) unsigned char dsm[];
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = T >> 5;
@@ -115,11 +119,16 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
   constexpr int CPW = 32 / D;
   const int q = lane / D, c = lane - (lane / D) * D;
   const uint32_t P1ROW = (uint32_t)m + 1u;
-  int qhead = 0;
+  int qhead = 0, plev = 0;
   for (;;) {
     __syncthreads();  // the previous level's appends are complete
     const int lev_end = *(volatile int*)&tail;
     if (qhead >= lev_end) break;
+    long long* pl = (prof && plev < 2000) ? prof + (int64_t)plev * 66 : nullptr;
+    if (pl && tid == 0) {
+      pl[0] = lev_end - qhead;
+      pl[1] = clock64();
+    }
     // ---- update the frontier
     for (int base = qhead + warp * CPW; base < lev_end; base += nwarps * CPW) {
       const int k = base + q;
@@ -187,6 +196,7 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
         __stcg(&Q[(int64_t)i * D + c], s1);
       }
     }
+    if (pl && lane == 0) pl[2 + warp] = clock64();
     // (no barrier here: the release only prepares the NEXT frontier, which starts after the
     // loop-top barrier, by when every row of this one is final)
     // ---- release the frontier's later neighbours: d <= 3 a thread per frontier cell (<= 13
@@ -204,8 +214,11 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
         if (((old >> sh) & 0xffu) == 1u) q_put(atomicAdd(&tail, 1), j);
       }
     }
+    if (pl && lane == 0) pl[34 + warp] = clock64();
+    ++plev;
     qhead = lev_end;
   }
+  if (prof && tid == 0) prof[2000 * 66] = plev;
 }
 
 // census: number of active neighbours and of lex-earlier ones; frozen frames -> 0
@@ -368,6 +381,157 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
       atomicAdd((unsigned long long*)&dbg[2], (unsigned long long)(clock64() - tl0));
     qhead = lev_end;
   }
+}
+
+// ---------------------------------------------------------------- cluster sweep
+// The same Kahn-frontier sweep spread over a thread-block cluster of NC CTAs (one per SM):
+// the single-CTA sweep above is bound by one SM's bandwidth to L2 (every term of a cell is a
+// scattered 8-byte row read: cfg5's 316-cell frontiers took ~14 K cycles per level to update,
+// cfg3's d = 5 lists ~18 K).  Cell j is owned by CTA j % NC, which keeps j's pending count and
+// its frontier queue in its shared memory; a CTA updates the frontier cells it owns (operand
+// rows and lists in L2, exactly the single-CTA update) and releases their successors with
+// atomics on the OWNER's shared memory (DSMEM); a cluster barrier separates levels (its
+// release/acquire orders the row stores and the queue appends).  Termination: every CTA adds
+// the number of cells it updated to a per-level counter in CTA 0 (three buffers, so a counter
+// is read by everyone before it is reused), and all CTAs stop when the running total reaches m.
+// Operands and add order are the serial sweep's: bit-identical results.
+template <int D>
+__global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
+    int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
+    const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
+    const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int NC = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = T >> 5;
+  const int mloc = (m + NC - 1) / NC;          // cells owned by this CTA: j = rank + NC*t
+  unsigned* pend = (unsigned*)dsm;              // mloc pending counts
+  // two frontier buffers by level parity: level L reads qbuf[L & 1] (filled during level L-1)
+  // while its releases append to qbuf[(L + 1) & 1], so a CTA's level boundary never moves
+  // under it; the buffer is emptied by its owner after its last read, before the barrier
+  unsigned* qbuf0 = pend + mloc;
+  unsigned* qbuf1 = pend + 2 * mloc;
+  __shared__ unsigned tails[2];
+  __shared__ unsigned done_cnt[3];
+  if (tid == 0) {
+    tails[0] = tails[1] = 0;
+    done_cnt[0] = done_cnt[1] = done_cnt[2] = 0;
+  }
+  __syncthreads();
+  for (int t = tid; t < mloc; t += T) {
+    const int i = rank + NC * t;
+    if (i >= m) break;
+    const int e = nbe[i];
+    pend[t] = (unsigned)e;
+    if (e == 0) qbuf0[atomicAdd(&tails[0], 1u)] = (unsigned)i;
+  }
+  unsigned* cnt0 = cluster.map_shared_rank(&done_cnt[0], 0);
+  constexpr int CPW = 32 / D;
+  const int q = lane / D, c = lane - (lane / D) * D;
+  const uint32_t P1ROW = (uint32_t)m + 1u;
+  int level = 0;
+  long long total = 0;
+  cluster.sync();  // every CTA's pending counts and initial queue are in place
+  for (;;) {
+    const int cur = level & 1;
+    unsigned* queue = cur ? qbuf1 : qbuf0;
+    const int lev_end = (int)*(volatile unsigned*)&tails[cur];
+    const int qhead = 0;
+    // ---- update the frontier cells this CTA owns
+    for (int base = qhead + warp * CPW; base < lev_end; base += nwarps * CPW) {
+      const int k = base + q;
+      const bool act = q < CPW && k < lev_end;
+      const int i = act ? (int)queue[k] : 0;
+      const int n = act ? nbn[i] : 0;
+      if (n > 1) {  // else: frozen or no active neighbour but itself (Q row = S_old, P3)
+        const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
+        double num = 0.0;
+        if constexpr (D <= 3) {
+          constexpr int NW = (D == 1 ? 3 : D == 2 ? 9 : 27) / 4 + 1;
+          uint4 r[NW];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) r[w] = __ldg(&ls[w]);
+          double v[NW][4];
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            v[w][0] = __ldcg(&Q[(int64_t)r[w].x * D + c]);
+            v[w][1] = __ldcg(&Q[(int64_t)r[w].y * D + c]);
+            v[w][2] = __ldcg(&Q[(int64_t)r[w].z * D + c]);
+            v[w][3] = __ldcg(&Q[(int64_t)r[w].w * D + c]);
+          }
+#pragma unroll
+          for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
+        } else {
+          const int nq = (n + 3) >> 2;
+          constexpr int WB = 4;
+          uint4 ra[WB], rb[WB];
+          double va[WB][4], vb[WB][4];
+          auto fetch = [&](uint4 (&r)[WB], double (&v)[WB][4], int w0) {
+#pragma unroll
+            for (int w = 0; w < WB; ++w) r[w] = __ldg(&ls[min(w0 + w, KP / 4 - 1)]);
+#pragma unroll
+            for (int w = 0; w < WB; ++w) {
+              const bool in = w0 + w < nq;
+              v[w][0] = in ? __ldcg(&Q[(int64_t)r[w].x * D + c]) : 0.0;
+              v[w][1] = in ? __ldcg(&Q[(int64_t)r[w].y * D + c]) : 0.0;
+              v[w][2] = in ? __ldcg(&Q[(int64_t)r[w].z * D + c]) : 0.0;
+              v[w][3] = in ? __ldcg(&Q[(int64_t)r[w].w * D + c]) : 0.0;
+            }
+          };
+          auto fold = [&](const double (&v)[WB][4]) {
+#pragma unroll
+            for (int w = 0; w < WB; ++w)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
+          };
+          fetch(ra, va, 0);
+          for (int w0 = 0; w0 < nq; w0 += 2 * WB) {
+            if (w0 + WB < nq) fetch(rb, vb, w0 + WB);
+            fold(va);
+            if (w0 + WB >= nq) break;
+            if (w0 + 2 * WB < nq) fetch(ra, va, w0 + 2 * WB);
+            fold(vb);
+          }
+        }
+        const double s1 = gl_div(num, (double)den[i], rden[i]);
+        __stcg(&Q[((int64_t)P1ROW + i) * D + c], __dmul_rn((double)ccnt[i], s1));
+        __stcg(&Q[(int64_t)i * D + c], s1);
+      }
+    }
+    // ---- release the successors into their owners' pending counts / next queues (DSMEM)
+    constexpr int RW = D <= 3 ? 1 : 32;
+    const int nxt = cur ^ 1;
+    for (int k = qhead + tid / RW; k < lev_end; k += T / RW) {
+      const int i = (int)queue[k];
+      const int n = nbn[i], e = nbe[i];
+      const uint32_t* li = lists + (int64_t)i * KP;
+      for (int t = e + 1 + (RW == 1 ? 0 : lane); t < n; t += RW) {
+        const int j = (int)__ldg(&li[t]);
+        const int own = j % NC;
+        unsigned* pj = cluster.map_shared_rank(pend + j / NC, own);
+        if (atomicSub(pj, 1u) == 1u) {
+          unsigned* tl = cluster.map_shared_rank(&tails[nxt], own);
+          unsigned* qd = cluster.map_shared_rank(nxt ? qbuf1 : qbuf0, own);
+          qd[atomicAdd(tl, 1u)] = (unsigned)j;
+        }
+      }
+    }
+    __syncthreads();  // this CTA is done reading queue[cur]
+    if (tid == 0) {
+      tails[cur] = 0u;  // refilled only during the next level, after the barrier
+      if (lev_end > 0) atomicAdd(cnt0 + level % 3, (unsigned)lev_end);
+    }
+    cluster.sync();  // rows, releases and counts of this level are complete and visible
+    total += *(volatile unsigned*)(cnt0 + level % 3);
+    if (rank == 0 && tid == 0) done_cnt[(level + 2) % 3] = 0u;  // everyone read it before this
+    ++level;
+    if (total >= m) break;
+  }
+  cluster.sync();  // no CTA exits while others may still read its shared memory
 }
 
 }  // namespace gs
