@@ -666,7 +666,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       if (NC > 8 && cl_cfg != 1) NC = 8;
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3((unsigned)NC);
-      lc.blockDim = dim3(gs::sweep_global_threads<D>());
+      lc.blockDim = dim3(gs::sweep_cluster_threads<D>());
       lc.dynamicSmemBytes = 12 * (size_t)((m + NC - 1) / NC);
       lc.stream = st;
       cudaLaunchAttribute at[1];
@@ -676,14 +676,47 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       at[0].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
+      long long* cprof = nullptr;
+      const bool ctrace = getenv("GS_TRACE_GLOBAL") != nullptr;
+      if (ctrace) {
+        GS_TRY(grow(ctx, ctx->dbg, 8 * (1000 * 16 * 5 + 8)));
+        GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * (1000 * 16 * 5 + 8), st));
+        cprof = (long long*)ctx->dbg.p;
+      }
       cudaError_t le = cudaLaunchKernelEx(&lc, gs::k_sweep_cluster<D>, (int)m, KP,
                                           (const uint32_t*)lists, (const int32_t*)ctx->nbn.as<int32_t>(),
                                           (const int32_t*)ctx->nbe.as<int32_t>(),
                                           (const uint32_t*)ctx->ccnt[cur].as<uint32_t>(),
                                           (const uint32_t*)ctx->den.as<uint32_t>(),
-                                          (const double*)ctx->rden.as<double>(), Q);
+                                          (const double*)ctx->rden.as<double>(), Q, cprof);
       if (le == cudaSuccess) {
         GS_LAUNCHED("k_sweep_cluster");
+        if (ctrace) {  // diagnostics: per-level split, max over CTAs
+          std::vector<long long> h(1000 * 16 * 5 + 8);
+          GS_CK(cudaMemcpyAsync(h.data(), cprof, 8 * h.size(), cudaMemcpyDeviceToHost, st));
+          GS_CK(cudaStreamSynchronize(st));
+          const int nl = (int)std::min<long long>(h[1000 * 16 * 5], 1000);
+          double su = 0, sr = 0, sb = 0;
+          for (int l = 0; l < nl; ++l) {
+            long long wmax = 0, u = 0, r = 0, bq = 0, wsum = 0;
+            for (int c = 0; c < NC; ++c) {
+              const long long* p = &h[((size_t)l * 16 + c) * 5];
+              wmax = std::max(wmax, p[0]);
+              wsum += p[0];
+              u = std::max(u, p[2] - p[1]);
+              r = std::max(r, p[3] - p[2]);
+              bq = std::max(bq, p[4] - p[3]);
+            }
+            su += u;
+            sr += r;
+            sb += bq;
+            if (l < 6 || l % 25 == 0)
+              fprintf(stderr, "csweep m %lld level %4d width %5lld (max/CTA %4lld) update %6lld release %6lld barrier %5lld\n",
+                      (long long)m, l, wsum, wmax, u, r, bq);
+          }
+          fprintf(stderr, "csweep m %lld NC %d levels %d | mean max-over-CTA cycles: update %.0f release %.0f barrier %.0f\n",
+                  (long long)m, NC, nl, su / std::max(nl, 1), sr / std::max(nl, 1), sb / std::max(nl, 1));
+        }
         return GS_OK;
       }
       cudaGetLastError();  // a cluster this size cannot be scheduled: single-CTA sweep below

@@ -396,10 +396,16 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
 // is read by everyone before it is reused), and all CTAs stop when the running total reaches m.
 // Operands and add order are the serial sweep's: bit-identical results.
 template <int D>
-__global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
+constexpr int sweep_cluster_threads() { return 512; }  // 128 registers: no spills at d = 3
+
+template <int D>
+__global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster(
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
     const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
-    const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q) {
+    const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q,
+    long long* prof = nullptr) {
+  // prof (diagnostics, GS_TRACE_GLOBAL): per level and CTA [width, start, update end,
+  // release end, barrier end] clock stamps (an extra block barrier after the update)
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int NC = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
@@ -439,21 +445,32 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
     unsigned* queue = cur ? qbuf1 : qbuf0;
     const int lev_end = (int)*(volatile unsigned*)&tails[cur];
     const int qhead = 0;
+    long long* pl = (prof && level < 1000) ? prof + ((int64_t)level * 16 + rank) * 5 : nullptr;
+    if (pl && tid == 0) {
+      pl[0] = lev_end;
+      pl[1] = clock64();
+    }
     // ---- update the frontier cells this CTA owns
     for (int base = qhead + warp * CPW; base < lev_end; base += nwarps * CPW) {
       const int k = base + q;
       const bool act = q < CPW && k < lev_end;
       const int i = act ? (int)queue[k] : 0;
+      // every load that depends only on i is issued together (nbn, the per-cell scalars, the
+      // list words and -- for d <= 3 all, for d > 3 the first block of -- operand rows): the
+      // rows beyond the list's end are the zero row (lists are padded to KP), so they need
+      // not wait for n
       const int n = act ? nbn[i] : 0;
-      if (n > 1) {  // else: frozen or no active neighbour but itself (Q row = S_old, P3)
-        const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
-        double num = 0.0;
-        if constexpr (D <= 3) {
-          constexpr int NW = (D == 1 ? 3 : D == 2 ? 9 : 27) / 4 + 1;
-          uint4 r[NW];
+      const uint32_t dn = act ? den[i] : 1u, cn = act ? ccnt[i] : 0u;
+      const double rd = act ? rden[i] : 1.0;
+      const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
+      double num = 0.0;
+      if constexpr (D <= 3) {
+        constexpr int NW = (D == 1 ? 3 : D == 2 ? 9 : 27) / 4 + 1;
+        uint4 r[NW];
+        double v[NW][4];
+        if (act) {
 #pragma unroll
           for (int w = 0; w < NW; ++w) r[w] = __ldg(&ls[w]);
-          double v[NW][4];
 #pragma unroll
           for (int w = 0; w < NW; ++w) {
             v[w][0] = __ldcg(&Q[(int64_t)r[w].x * D + c]);
@@ -461,15 +478,30 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
             v[w][2] = __ldcg(&Q[(int64_t)r[w].z * D + c]);
             v[w][3] = __ldcg(&Q[(int64_t)r[w].w * D + c]);
           }
+        }
+        if (n > 1) {
 #pragma unroll
           for (int w = 0; w < NW; ++w)
 #pragma unroll
             for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
-        } else {
+        }
+      } else {
+        constexpr int WB = 4;
+        uint4 ra[WB], rb[WB];
+        double va[WB][4], vb[WB][4];
+        if (act) {  // first block: no dependence on n
+#pragma unroll
+          for (int w = 0; w < WB; ++w) ra[w] = __ldg(&ls[min(w, KP / 4 - 1)]);
+#pragma unroll
+          for (int w = 0; w < WB; ++w) {
+            va[w][0] = __ldcg(&Q[(int64_t)ra[w].x * D + c]);
+            va[w][1] = __ldcg(&Q[(int64_t)ra[w].y * D + c]);
+            va[w][2] = __ldcg(&Q[(int64_t)ra[w].z * D + c]);
+            va[w][3] = __ldcg(&Q[(int64_t)ra[w].w * D + c]);
+          }
+        }
+        if (n > 1) {
           const int nq = (n + 3) >> 2;
-          constexpr int WB = 4;
-          uint4 ra[WB], rb[WB];
-          double va[WB][4], vb[WB][4];
           auto fetch = [&](uint4 (&r)[WB], double (&v)[WB][4], int w0) {
 #pragma unroll
             for (int w = 0; w < WB; ++w) r[w] = __ldg(&ls[min(w0 + w, KP / 4 - 1)]);
@@ -488,7 +520,6 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
 #pragma unroll
               for (int t = 0; t < 4; ++t) num = __dadd_rn(num, v[w][t]);
           };
-          fetch(ra, va, 0);
           for (int w0 = 0; w0 < nq; w0 += 2 * WB) {
             if (w0 + WB < nq) fetch(rb, vb, w0 + WB);
             fold(va);
@@ -497,13 +528,21 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
             fold(vb);
           }
         }
-        const double s1 = gl_div(num, (double)den[i], rden[i]);
-        __stcg(&Q[((int64_t)P1ROW + i) * D + c], __dmul_rn((double)ccnt[i], s1));
+      }
+      if (n > 1) {  // else: frozen or no active neighbour but itself (Q row = S_old, P3)
+        const double s1 = gl_div(num, (double)dn, rd);
+        __stcg(&Q[((int64_t)P1ROW + i) * D + c], __dmul_rn((double)cn, s1));
         __stcg(&Q[(int64_t)i * D + c], s1);
       }
     }
-    // ---- release the successors into their owners' pending counts / next queues (DSMEM)
-    constexpr int RW = D <= 3 ? 1 : 32;
+    if (prof) {
+      __syncthreads();
+      if (pl && tid == 0) pl[2] = clock64();
+    }
+    // ---- release the successors into their owners' pending counts / next queues (DSMEM):
+    //      a warp per frontier cell, one lane per successor (the remote atomic chains of a
+    //      cell's successors run in parallel)
+    constexpr int RW = 32;
     const int nxt = cur ^ 1;
     for (int k = qhead + tid / RW; k < lev_end; k += T / RW) {
       const int i = (int)queue[k];
@@ -521,16 +560,19 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_cluster(
       }
     }
     __syncthreads();  // this CTA is done reading queue[cur]
+    if (pl && tid == 0) pl[3] = clock64();
     if (tid == 0) {
       tails[cur] = 0u;  // refilled only during the next level, after the barrier
       if (lev_end > 0) atomicAdd(cnt0 + level % 3, (unsigned)lev_end);
     }
     cluster.sync();  // rows, releases and counts of this level are complete and visible
+    if (pl && tid == 0) pl[4] = clock64();
     total += *(volatile unsigned*)(cnt0 + level % 3);
     if (rank == 0 && tid == 0) done_cnt[(level + 2) % 3] = 0u;  // everyone read it before this
     ++level;
     if (total >= m) break;
   }
+  if (prof && rank == 0 && tid == 0) prof[1000 * 16 * 5] = level;
   cluster.sync();  // no CTA exits while others may still read its shared memory
 }
 
