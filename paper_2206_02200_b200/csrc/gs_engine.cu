@@ -650,7 +650,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       nc_env = v ? atoi(v) : 16;
     }
     int NC = nc_env;
-    const size_t csmem = 12 * (size_t)((m + NC - 1) / std::max(NC, 1));
+    const size_t csmem = gs::sweep_cluster_smem<D>((int)((m + NC - 1) / std::max(NC, 1)));
     static int cl_cfg = 0;  // 1: 16-CTA clusters allowed, 2: refused (use 8)
     if (NC >= 2 && csmem <= kBudget) {
       if (!cl_cfg) {
@@ -667,7 +667,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3((unsigned)NC);
       lc.blockDim = dim3(gs::sweep_cluster_threads<D>());
-      lc.dynamicSmemBytes = 12 * (size_t)((m + NC - 1) / NC);
+      lc.dynamicSmemBytes = gs::sweep_cluster_smem<D>((int)((m + NC - 1) / NC));
       lc.stream = st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;

@@ -398,6 +398,14 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_kahn(
 template <int D>
 constexpr int sweep_cluster_threads() { return 512; }  // 128 registers: no spills at d = 3
 
+// dynamic shared memory of the cluster sweep: pending counts + two queues per owned cell,
+// and for d > 3 a 128-entry staging tile of operand rows per warp
+template <int D>
+__host__ __device__ constexpr size_t sweep_cluster_smem(int mloc) {
+  return (((size_t)12 * mloc + 15) & ~(size_t)15) +
+         (D > 3 ? (size_t)(sweep_cluster_threads<D>() / 32) * 128 * D * 8 : 0);
+}
+
 template <int D>
 __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster(
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
   // under it; the buffer is emptied by its owner after its last read, before the barrier
   unsigned* qbuf0 = pend + mloc;
   unsigned* qbuf1 = pend + 2 * mloc;
+  const size_t stage_off = ((size_t)12 * mloc + 15) & ~(size_t)15;  // d > 3: per-warp tiles
   __shared__ unsigned tails[2];
   __shared__ unsigned done_cnt[3];
   if (tid == 0) {
@@ -450,6 +459,67 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
       pl[0] = lev_end;
       pl[1] = clock64();
     }
+    const int nxt = cur ^ 1;
+    auto release_one = [&](int j) {  // successor j: its owner's pending count, next queue
+      const int own = j % NC;
+      unsigned* pj = cluster.map_shared_rank(pend + j / NC, own);
+      if (atomicSub(pj, 1u) == 1u) {
+        unsigned* tl = cluster.map_shared_rank(&tails[nxt], own);
+        unsigned* qd = cluster.map_shared_rank(nxt ? qbuf1 : qbuf0, own);
+        qd[atomicAdd(tl, 1u)] = (unsigned)j;
+      }
+    };
+    if constexpr (D > 3) {
+      // ---- d > 3: a warp per frontier cell.  Lane l loads list word l of each 128-entry
+      // chunk (one L2 round trip for the whole chunk instead of one per 16 entries), releases
+      // the successors among its 4 entries right away (they are processed after the level's
+      // cluster barrier, by when this cell's row is stored), loads the 4 entries' operand rows
+      // into a per-warp staging tile, and lane c < D then adds the chunk's terms in list order.
+      double* stg = (double*)(dsm + stage_off) + (size_t)warp * 128 * D;
+      for (int k = warp; k < lev_end; k += nwarps) {
+        const int i = (int)queue[k];
+        const int n = nbn[i], e = nbe[i];
+        const uint32_t dn = den[i], cn = ccnt[i];
+        const double rd = rden[i];
+        const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
+        double num = 0.0;
+        for (int t0 = 0; t0 < n; t0 += 128) {
+          const int tb = t0 + 4 * lane;
+          uint4 r = make_uint4(0u, 0u, 0u, 0u);
+          if (tb < n) r = __ldg(&ls[tb >> 2]);
+          const uint32_t ent[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (tb + jj > e && tb + jj < n) release_one((int)ent[jj]);
+          double v[4][D];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc)
+              v[jj][cc] = (tb + jj < n) ? __ldcg(&Q[(int64_t)ent[jj] * D + cc]) : 0.0;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) stg[(4 * lane + jj) * D + cc] = v[jj][cc];
+          __syncwarp();
+          if (lane < D && n > 1) {
+            const int len = min(128, n - t0);
+#pragma unroll 8
+            for (int u = 0; u < len; ++u) num = __dadd_rn(num, stg[u * D + lane]);
+          }
+          __syncwarp();
+        }
+        if (n > 1 && lane < D) {  // else: frozen or isolated (Q row = S_old, P3)
+          const double s1 = gl_div(num, (double)dn, rd);
+          __stcg(&Q[((int64_t)P1ROW + i) * D + lane], __dmul_rn((double)cn, s1));
+          __stcg(&Q[(int64_t)i * D + lane], s1);
+        }
+      }
+      if (prof) {
+        __syncthreads();
+        if (pl && tid == 0) pl[2] = clock64();
+      }
+    } else {
     // ---- update the frontier cells this CTA owns
     for (int base = qhead + warp * CPW; base < lev_end; base += nwarps * CPW) {
       const int k = base + q;
@@ -543,7 +613,6 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
     //      a warp per frontier cell, one lane per successor (the remote atomic chains of a
     //      cell's successors run in parallel)
     constexpr int RW = 32;
-    const int nxt = cur ^ 1;
     for (int k = qhead + tid / RW; k < lev_end; k += T / RW) {
       const int i = (int)queue[k];
       const int n = nbn[i], e = nbe[i];
@@ -558,6 +627,7 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
           qd[atomicAdd(tl, 1u)] = (unsigned)j;
         }
       }
+    }
     }
     __syncthreads();  // this CTA is done reading queue[cur]
     if (pl && tid == 0) pl[3] = clock64();
