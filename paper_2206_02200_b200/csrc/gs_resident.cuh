@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       t_prev = t;
     }
   };
+  auto stamp = [&](int k) {  // diagnostics (GS_TRACE_LEVELS): thread 0 sub-phase stamps
+    if (a.trace && tid == 0 && f == 0 && iters < 64) a.trace[9700 + 16 * iters + k] = clock64();
+  };
   lap(7);
   while (!done) {
     if (a.trace && tid == 0 && f == 0 && iters < 64) a.trace[4096 + 8 * iters + 7] = clock64();
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       levend[i] = 0;
     };
     int mode, n_all = 0;
+    stamp(0);
     if (D <= 3 && 2 * KP * m + 16 <= a.pool_bytes) {
       mode = 0;
       for (int i = tid; i < m; i += T) {
@@ -395,15 +399,29 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         uint32_t s = 0;
         const int64_t Li = key[i];
         uint16_t* li = lst + i * KP;
+        // branch-free: all 27 index loads (the index kind hoisted out of the loop), then all
+        // count loads, then unconditional list stores at the running position (a dropped
+        // entry is overwritten by the next one or by the padding).  With a branch per probe
+        // a lone warp paid ~100 cycles per neighbour (~3 K cycles per iteration).
+        int jn[K];
+        if (sdense) {
+#pragma unroll
+          for (int t = 0; t < K; ++t) jn[t] = sidx[Li + it.at(t)];
+        } else {
+#pragma unroll
+          for (int t = 0; t < K; ++t) jn[t] = gidx[Li + it.at(t)];
+        }
+        uint32_t cn[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) cn[t] = cnt[jn[t] >= 0 ? jn[t] : 0];
 #pragma unroll
         for (int t = 0; t < K; ++t) {
-          const int j = idx_get(Li + it.at(t));
-          it.step(b);
-          if (j >= 0) {
-            s += cnt[j];
-            li[n++] = (uint16_t)(j < i ? P1ROW + j : j);
-            e += j < i;
-          }
+          const int j = jn[t];
+          const bool ok = j >= 0;
+          s += ok ? cn[t] : 0u;
+          li[n] = (uint16_t)(j < i ? P1ROW + j : j);
+          n += ok ? 1 : 0;
+          e += (ok && j < i) ? 1 : 0;
         }
 #pragma unroll
         for (int t = 1; t < KP; ++t)  // (entry 0 is the cell itself or an earlier neighbour)
@@ -452,6 +470,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       }
       if (mode == 1 && tid < 4) lst[n_all + tid] = (uint16_t)ZROW;  // slack word (prefetch)
     }
+    stamp(1);
     for (int c = tid; c < D; c += T) Q[ZROW * D + c] = 0.0;
     if (tid == 0) {
       s_dmax = 0ull;
@@ -769,17 +788,42 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 
     lap(3);
     // ---- (5) segments -> new cells; parent map
-    for (int j = tid; j < m; j += T)
-      tmp[j] = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32)) ? 1 : 0;
-    __syncthreads();
-    const int mnew = rs_scan(tmp, m, wtmp);
-    for (int j = tid; j < m; j += T) {
-      const bool head = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32));
-      const int g = tmp[j] + (head ? 1 : 0) - 1;
-      par[(uint32_t)sk[j]] = g;
-      if (head) eoff[g] = j;  // segment start (eoff is free after the sweep)
+    int mnew;
+    stamp(2);
+    if (m <= T) {  // heads are 0/1: the group ids from one ballot per warp, one barrier
+      const int j = tid;
+      const bool head = j < m && (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32));
+      const unsigned bm = __ballot_sync(0xffffffffu, head);
+      const int wex = __popc(bm & ((1u << (tid & 31)) - 1u));
+      if ((tid & 31) == 0) wtmp[tid >> 5] = __popc(bm);
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int w = 0; w < (T >> 5); ++w) {
+        const int cw = wtmp[w];
+        before += (w < (tid >> 5)) ? cw : 0;
+        tot += cw;
+      }
+      mnew = tot;
+      if (j < m) {
+        const int g = before + wex + (head ? 1 : 0) - 1;
+        par[(uint32_t)sk[j]] = g;
+        if (head) eoff[g] = j;  // segment start (eoff is free after the sweep)
+      }
+    } else {
+      for (int j = tid; j < m; j += T)
+        tmp[j] = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32)) ? 1 : 0;
+      __syncthreads();
+      mnew = rs_scan(tmp, m, wtmp);
+      for (int j = tid; j < m; j += T) {
+        const bool head = (j == 0 || (sk[j] >> 32) != (sk[j - 1] >> 32));
+        const int g = tmp[j] + (head ? 1 : 0) - 1;
+        par[(uint32_t)sk[j]] = g;
+        if (head) eoff[g] = j;  // segment start (eoff is free after the sweep)
+      }
     }
+    stamp(3);
     __syncthreads();
+    stamp(4);
     // merge_into folded in visit order (Eq. 3, pin P4): s = RN(RN(RN(x*s) + RN(w*S_i)) / tot),
     // the division from RN(1/tot) (Markstein; the reciprocal does not depend on s, so it
     // leaves the chain); an operand outside the theorem's range redoes the group exactly
@@ -826,6 +870,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 #pragma unroll
       for (int c = 0; c < D; ++c) S0[g * D + c] = s[c];
     }
+    stamp(5);
     // member union (Eq. 4) as root composition
     for (int c = tid; c < icnt; c += T) {
       if (rsm)
@@ -834,7 +879,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         a.root[ifirst + c] = par[a.root[ifirst + c]];
     }
     for (int i = tid; i < m; i += T) idx_put(key[i], -1);  // retire the old keys
+    stamp(6);
     __syncthreads();
+    stamp(7);
     {
       uint32_t* t1 = key;
       key = nkey;
@@ -855,10 +902,18 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
       NbrIt it = nbr_begin();
       const int64_t Li = key[i];
       int hits = 0;
+      if (sdense) {  // the index kind hoisted: no branch per probe
 #pragma unroll 27
-      for (int t = 0; t < K; ++t) {
-        hits += (t != (K - 1) / 2) && idx_get(Li + it.at(t)) >= 0;
-        it.step(b);
+        for (int t = 0; t < K; ++t) {
+          hits += (t != (K - 1) / 2) && sidx[Li + it.at(t)] >= 0;
+          it.step(b);
+        }
+      } else {
+#pragma unroll 27
+        for (int t = 0; t < K; ++t) {
+          hits += (t != (K - 1) / 2) && gidx[Li + it.at(t)] >= 0;
+          it.step(b);
+        }
       }
       adj = hits > 0;
     }
