@@ -86,8 +86,9 @@ class ClockSampler:
                 "samples": len(busy)}
 
 
-# K2 dram bytes (read + write) per launch, ncu --set full (profiles/r1_ncu_kernels.md)
-NCU_TRAFFIC = {"cfg2": 1_903_616, "cfg4": 961_585_408 + 305_048_320}
+# K2 dram bytes (read + write) per launch, ncu --set full of the current K2
+# (profiles/r1_ncu_kernels.md, session-2 captures)
+NCU_TRAFFIC = {"cfg2": 1_901_312, "cfg4": 950_866_432 + 297_167_872}
 
 
 def workload_input(name: str, rank: int):
@@ -556,6 +557,22 @@ def main():
                      "traffic": (NCU_TRAFFIC.get(args.workload)
                                  if not shard_cloud and args.input == "features" else None),
                      "algorithmic_bytes": kbin_bytes},
+        # the dominant kernel of the step: on the image-sized workloads the iteration phase
+        # (K8 / the cluster sweep) -- latency-bound by the Gauss-Seidel sweep's DAG depth, so
+        # its HBM fraction is tiny by construction; reported beside the K2 roofline above
+        "roofline_dominant": {
+            "kernel": ("k_resident (K8) / k_sweep_cluster (iteration phase)"
+                       if phase["ms_iterate"] >= phase["ms_bin"] else "binning phase (K1+K2+K3)"),
+            "bound": "latency (sweep DAG depth x per-level round trips)"
+                     if phase["ms_iterate"] >= phase["ms_bin"] else "hbm",
+            "algorithmic_bytes": int(s0["cells_swept"] * (24 + 16 * d)),
+            "ms": phase["ms_iterate"],
+            "achieved": (s0["cells_swept"] * (24 + 16 * d)) / (phase["ms_iterate"] / 1e3) / 1e9
+                        if phase["ms_iterate"] > 0 else None,
+            "peak": peak, "unit": "GB/s",
+            "frac": (s0["cells_swept"] * (24 + 16 * d)) / (phase["ms_iterate"] / 1e3) / 1e9 / peak
+                    if phase["ms_iterate"] > 0 else None,
+            "note": "B_c = 24 + 16d bytes per cell-iteration (SURVEY.md 8(d)); per-run sum"},
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
                 "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},
         "gpu_launches": launches, "lib_calls": lib_calls,
