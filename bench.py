@@ -532,6 +532,20 @@ def main():
     dominant = max(("binning phase (K1+K2+K3)", phase["ms_bin"]),
                    ("iteration phase (K4+K5)", phase["ms_iterate"]),
                    ("label phase (K7)", phase["ms_label"]), key=lambda x: x[1])[0]
+    # the dominant kernel of the step: when the iteration phase dominates (the image-sized
+    # workloads) it is K8 / the cluster sweep, latency-bound by the Gauss-Seidel sweep's DAG
+    # depth, so its HBM fraction is tiny by construction; else the binning kernel K2
+    it_bytes = int(s0["cells_swept"] * (24 + 16 * d))  # B_c = 24 + 16d
+    if phase["ms_iterate"] >= phase["ms_bin"] and phase["ms_iterate"] > 0:
+        ach = it_bytes / (phase["ms_iterate"] / 1e3) / 1e9
+        dominant_roofline = {
+            "kernel": "k_resident (K8) / k_sweep_cluster: the iteration phase",
+            "bound": "latency (sweep DAG depth x per-level round trips), not hbm",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "algorithmic_bytes": it_bytes, "ms": phase["ms_iterate"],
+            "note": "sum over the run of m_t x (24 + 16d) bytes / iteration-phase time"}
+    else:
+        dominant_roofline = {"kernel": "k_bin (K2 binning)", "same_as": "roofline"}
     out = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_dev / args.steps,
@@ -560,19 +574,7 @@ def main():
         # the dominant kernel of the step: on the image-sized workloads the iteration phase
         # (K8 / the cluster sweep) -- latency-bound by the Gauss-Seidel sweep's DAG depth, so
         # its HBM fraction is tiny by construction; reported beside the K2 roofline above
-        "roofline_dominant": {
-            "kernel": ("k_resident (K8) / k_sweep_cluster (iteration phase)"
-                       if phase["ms_iterate"] >= phase["ms_bin"] else "binning phase (K1+K2+K3)"),
-            "bound": "latency (sweep DAG depth x per-level round trips)"
-                     if phase["ms_iterate"] >= phase["ms_bin"] else "hbm",
-            "algorithmic_bytes": int(s0["cells_swept"] * (24 + 16 * d)),
-            "ms": phase["ms_iterate"],
-            "achieved": (s0["cells_swept"] * (24 + 16 * d)) / (phase["ms_iterate"] / 1e3) / 1e9
-                        if phase["ms_iterate"] > 0 else None,
-            "peak": peak, "unit": "GB/s",
-            "frac": (s0["cells_swept"] * (24 + 16 * d)) / (phase["ms_iterate"] / 1e3) / 1e9 / peak
-                    if phase["ms_iterate"] > 0 else None,
-            "note": "B_c = 24 + 16d bytes per cell-iteration (SURVEY.md 8(d)); per-run sum"},
+        "roofline_dominant": dominant_roofline,
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
                 "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},
         "gpu_launches": launches, "lib_calls": lib_calls,
