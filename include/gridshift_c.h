@@ -236,6 +236,19 @@ gs_status gs_track_init(gs_tracker* t, const uint8_t* frame0, int32_t H, int32_t
 gs_status gs_track_sequence(gs_tracker* t, const uint8_t* frames, int64_t T, int32_t on_device,
                             gs_window* out, int32_t* lost, int32_t* inner);
 
+/* ---- MS++ baseline (reference module `baselines`, mspp_run SPEC.md:197-203)
+ * Per-point grid mean shift with parallel (Jacobi, Eq. 6) updates: every iteration re-grids the
+ * current positions and moves every point to the count-weighted mean of its cell's
+ * 1-neighbourhood centroids computed from the previous state; stop when the max displacement
+ * < tol (SPEC default 1e-6*h) or after max_iter (SPEC default 300); clusters = points sharing a
+ * final cell, ids by lexicographic key.  Pins M1-M5 (oracle/gs_oracle.cpp): results equal the
+ * oracle's bit for bit.  One dataset (batch 1) of fp32/fp64 features, d <= 6, whose first grid
+ * fits one CTA's shared memory (~2K cells at d = 3).  out->k/iterations/converged get one
+ * entry; disp_hist (nullable, max_iter entries) the per-iteration displacement;
+ * gs_get_centroids(ctx, 0, ...) the final centroids. */
+gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, double tol, int32_t max_iter,
+                      gs_result* out, double* disp_hist);
+
 /* ---- test hooks (parity harness; not needed by callers) ---- */
 
 /* build_active_grid only on one frame: m0 cells in lex order.

@@ -738,3 +738,154 @@ int gso_track(const uint8_t* frames, int64_t T, int32_t H, int32_t W, const doub
 }
 
 }  // extern "C"
+
+// ---- baselines: MS++ per-point grid mean shift, parallel (Jacobi) updates ----
+// Pins the SPEC leaves open (DESIGN.md §"MS++"):
+//   M1 cell centroids are the fixed-point means of build mode 1 (F = fixed_shift(n, h)), for the
+//      first grid over the points and every re-grid over the moved particles (a particle of
+//      count c adds c*q);
+//   M2 update (Eq. 6): every cell j at once from the previous state:
+//      num = 0.0; num = num + (double)C(j+v)*S(j+v) over active neighbours in lex v order;
+//      S'(j) = num / (double)sum C; a cell with no active neighbour but itself keeps S (P3);
+//   M3 every point / particle of cell j moves to S'(j); the iteration's displacement is the max
+//      over points (first iteration) or particles of sqrt(sum_c (S'_c - x_c)^2);
+//   M4 particles that share a cell coincide after the move and merge (counts add); the loop is a
+//      do-while: stop when displacement < tol or after max_iter iterations;
+//   M5 final clusters: the cells of the final particles, ids by lex key order,
+//      centroids their fixed-point means.
+namespace {
+struct MsCells {
+  std::vector<Key> key;
+  std::vector<int64_t> cnt;
+  std::vector<double> S;  // m x d
+};
+
+// re-grid particles (pos m_p x d, counts) into lex-sorted cells; cell_of[i] = cell rank
+void ms_regrid(const std::vector<double>& pos, const std::vector<int64_t>& pc, int d, double h,
+               int F, MsCells* out, std::vector<int64_t>* cell_of) {
+  const int64_t mp = (int64_t)pc.size();
+  const double scale = std::ldexp(1.0, F);
+  std::vector<std::pair<Key, int64_t>> kp(mp);
+  for (int64_t i = 0; i < mp; ++i) {
+    Key k{};
+    for (int c = 0; c < d; ++c) k[c] = grid_coord(pos[i * d + c], h);
+    kp[i] = {k, i};
+  }
+  std::sort(kp.begin(), kp.end());
+  out->key.clear();
+  out->cnt.clear();
+  out->S.clear();
+  cell_of->assign(mp, -1);
+  std::vector<int64_t> qs;
+  for (int64_t t = 0; t < mp; ++t) {
+    const Key& k = kp[t].first;
+    const int64_t i = kp[t].second;
+    if (t == 0 || !(kp[t - 1].first == k)) {
+      out->key.push_back(k);
+      out->cnt.push_back(0);
+      qs.resize(qs.size() + d, 0);
+    }
+    const int64_t r = (int64_t)out->key.size() - 1;
+    (*cell_of)[i] = r;
+    out->cnt[r] += pc[i];
+    for (int c = 0; c < d; ++c) {
+      const double off = pos[i * d + c] - (double)k[c] * h;
+      qs[r * d + c] += pc[i] * (int64_t)std::nearbyint(off * scale);
+    }
+  }
+  const int64_t m = (int64_t)out->key.size();
+  out->S.resize(m * d);
+  for (int64_t r = 0; r < m; ++r)
+    for (int c = 0; c < d; ++c)
+      out->S[r * d + c] = (double)out->key[r][c] * h +
+                          std::ldexp((double)qs[r * d + c] / (double)out->cnt[r], -F);
+}
+
+void ms_jacobi(const MsCells& g, int d, std::vector<double>* Snew) {
+  const int64_t m = (int64_t)g.cnt.size();
+  std::unordered_map<Key, int64_t, KeyHash> index;
+  for (int64_t r = 0; r < m; ++r) index.emplace(g.key[r], r);
+  const auto offs = Engine::offsets(d);
+  Snew->assign(m * d, 0.0);
+  for (int64_t j = 0; j < m; ++j) {
+    double num[kMaxD] = {0};
+    int64_t den = 0;
+    int act = 0;
+    for (const auto& v : offs) {
+      Key nk = g.key[j];
+      for (int c = 0; c < d; ++c) nk[c] += v[c];
+      auto it = index.find(nk);
+      if (it == index.end()) continue;
+      const int64_t r = it->second;
+      ++act;
+      den += g.cnt[r];
+      for (int c = 0; c < d; ++c) num[c] = num[c] + (double)g.cnt[r] * g.S[r * d + c];
+    }
+    for (int c = 0; c < d; ++c)
+      (*Snew)[j * d + c] = act <= 1 ? g.S[j * d + c] : num[c] / (double)den;
+  }
+}
+
+double ms_dist(const double* a, const double* b, int d) {
+  double acc = 0.0;
+  for (int c = 0; c < d; ++c) {
+    const double t = a[c] - b[c];
+    acc = acc + t * t;
+  }
+  return std::sqrt(acc);
+}
+}  // namespace
+
+extern "C" {
+
+// mspp_run.  labels n; centroids capacity n*d (first k*d written);
+// disp_hist capacity max_iter (per-iteration displacement).
+int gso_mspp(const double* X, int64_t n, int32_t d, double h, double tol, int32_t max_iter,
+             int32_t* labels, int64_t* k_out, int32_t* iters_out, int32_t* conv_out,
+             double* cent_out, double* disp_hist) {
+  int st = check_common(n, d, h);
+  if (st) return st;
+  if (max_iter < 1 || !(tol > 0.0)) return E_INVALID_PARAMETER;
+  const int F = fixed_shift(n, h);
+  // the first grid: points as particles of count 1
+  std::vector<double> pos(X, X + n * d);
+  std::vector<int64_t> pc(n, 1), cell_of, root(n);
+  for (int64_t p = 0; p < n; ++p)
+    for (int c = 0; c < d; ++c)
+      if (!std::isfinite(X[p * d + c])) return E_INVALID_INPUT;
+  for (int64_t p = 0; p < n; ++p) root[p] = p;  // point -> particle
+  MsCells g;
+  ms_regrid(pos, pc, d, h, F, &g, &cell_of);
+  int it = 0;
+  bool conv = false;
+  std::vector<double> Snew;
+  do {
+    ms_jacobi(g, d, &Snew);
+    double disp = 0.0;
+    const int64_t mp = (int64_t)pc.size();
+    for (int64_t i = 0; i < mp; ++i)
+      disp = std::max(disp, ms_dist(&Snew[cell_of[i] * d], &pos[i * d], d));
+    for (int64_t p = 0; p < n; ++p) root[p] = cell_of[root[p]];  // particle -> its cell
+    pos = Snew;  // the cells become the particles (M4)
+    pc = g.cnt;
+    if (disp_hist) disp_hist[it] = disp;
+    ++it;
+    if (disp < tol) {
+      conv = true;
+      break;
+    }
+    if (it >= max_iter) break;
+    ms_regrid(pos, pc, d, h, F, &g, &cell_of);
+  } while (true);
+  MsCells fin;  // M5: the cells of the final particles
+  ms_regrid(pos, pc, d, h, F, &fin, &cell_of);
+  for (int64_t p = 0; p < n; ++p) labels[p] = (int32_t)cell_of[root[p]];
+  const int64_t k = (int64_t)fin.cnt.size();
+  for (int64_t r = 0; r < k * d; ++r) cent_out[r] = fin.S[r];
+  *k_out = k;
+  *iters_out = it;
+  *conv_out = conv ? 1 : 0;
+  return OK;
+}
+
+}  // extern "C"

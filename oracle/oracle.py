@@ -39,6 +39,7 @@ def lib():
         L.gso_sample_indices.restype = I64
         L.gso_silhouette.argtypes = [P, P, I64, I32, P, P, P]
         L.gso_track.argtypes = [P, I64, I32, I32, P, D, D, D, I32, I32, I32, P, I32, I32, P, P, P]
+        L.gso_mspp.argtypes = [P, I64, I32, D, D, I32, P, P, P, P, P, P]
         L.gso_tune.argtypes = [P, I64, I32, P, I32, I32, I64, C.c_uint64, I32, P, P, P, P, P]
         _lib = L
     return _lib
@@ -176,3 +177,18 @@ def track(frames: np.ndarray, window, h: float, f: float = 1.0, eta: float = 1.0
                          _p(ida) if len(ida) else None, len(ida), mode, _p(out), _p(lost),
                          _p(inner)))
     return dict(windows=out[:T - 1], lost=lost[:T - 1].astype(bool), inner=inner[:T - 1])
+
+
+def mspp(X: np.ndarray, h: float, tol: float = None, max_iter: int = 300) -> dict:
+    """mspp_run (pins M1-M5): MS++ parallel grid mean shift."""
+    X = np.ascontiguousarray(X, np.float64)
+    n, d = X.shape
+    tol = 1e-6 * h if tol is None else tol
+    labels = np.zeros(n, np.int32)
+    cen = np.zeros((n, d))
+    disp = np.zeros(max(max_iter, 1))
+    k, it, cv = C.c_int64(), C.c_int32(), C.c_int32()
+    _chk(lib().gso_mspp(_p(X), n, d, h, tol, max_iter, _p(labels), C.byref(k), C.byref(it),
+                        C.byref(cv), _p(cen), _p(disp)))
+    return dict(labels=labels, k=k.value, iterations=it.value, converged=bool(cv.value),
+                centroids=cen[:k.value], disp=disp[:it.value])

@@ -23,6 +23,7 @@
 #include "gs_kernels.cuh"
 #include "gs_global.cuh"
 #include "gs_resident.cuh"
+#include "gs_mspp.cuh"
 
 namespace {
 
@@ -1474,6 +1475,180 @@ results:
 }
 
 
+// ---- MS++ baseline (gs_mspp.cuh) ----
+template <int D, typename T>
+gs_status mspp_launch(gs_ctx* ctx, const void* dpts, int64_t n, int64_t m0, double tol,
+                      int32_t max_iter, int MS, int vol_small, double* snew0,
+                      unsigned long long* disp0, int* outw, double* dhist, double* cent) {
+  cudaStream_t st = ctx->stream;
+  gs::k_mspp_jacobi<D><<<blocks_for(m0, 128), 128, 0, st>>>(
+      (int)m0, ctx->dbox.as<GsBox>(), ctx->ckey[0].as<uint32_t>(), ctx->ccnt[0].as<uint32_t>(),
+      ctx->S[0].as<double>(), ctx->idx.as<int32_t>(), snew0);
+  GS_LAUNCHED("k_mspp_jacobi");
+  gs::k_mspp_disp0<D, T><<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+      n, (const T*)dpts, ctx->slot.as<uint32_t>(), ctx->idx.as<int32_t>(), snew0, disp0);
+  GS_LAUNCHED("k_mspp_disp0");
+  gs::MsppArgs a;
+  a.m0 = (int)m0;
+  a.MS = MS;
+  a.F = ctx->box.F;
+  a.max_iter = max_iter;
+  a.vol_small = vol_small;
+  a.tol = tol;
+  a.scale = ctx->box.scale;
+  a.inv_scale = ctx->box.inv_scale;
+  a.pb = ctx->dbox.as<GsBox>();
+  a.ckey0 = ctx->ckey[0].as<uint32_t>();
+  a.ccnt0 = ctx->ccnt[0].as<uint32_t>();
+  a.Snew0 = snew0;
+  a.idx = ctx->idx.as<int32_t>();
+  a.lab = ctx->lab.as<int32_t>();
+  a.disp0 = disp0;
+  a.cent_out = cent;
+  a.out = outw;
+  a.disp_hist = dhist;
+  const size_t smem = (size_t)MS * gs::mspp_bytes_per_slot<D>() +
+                      (vol_small ? 2 * (size_t)ctx->box.vol_frame : 0);
+  static bool configured = false;
+  if (!configured) {
+    GS_CK(cudaFuncSetAttribute(gs::k_mspp_loop<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024));
+    configured = true;
+  }
+  gs::k_mspp_loop<D><<<1, 512, smem, st>>>(a);
+  GS_LAUNCHED("k_mspp_loop");
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, double tol,
+                                 int32_t max_iter, gs_result* out, double* disp_hist) {
+  gs_config cfg{h, max_iter, 0};
+  gs_status s0 = validate(in, &cfg);
+  if (s0 != GS_OK) {
+    if (ctx) ctx->err = gs_status_string(s0);
+    return s0;
+  }
+  if (!ctx || !out || !out->labels || !out->k || !out->iterations || !out->converged)
+    return GS_E_INVALID_PARAMETER;
+  ctx->err.clear();
+  if (in->batch != 1) return fail(ctx, GS_E_INVALID_PARAMETER, "MS++ runs one dataset (batch 1)");
+  if (in->dtype != GS_F32 && in->dtype != GS_F64)
+    return fail(ctx, GS_E_INVALID_PARAMETER, "MS++ takes fp32/fp64 features");
+  if (in->d > 6) return fail(ctx, GS_E_INVALID_PARAMETER, "MS++ baseline: d <= 6");
+  if (!(tol > 0.0) || !std::isfinite(tol))
+    return fail(ctx, GS_E_INVALID_PARAMETER, "tol must be > 0 (SPEC.md:242)");
+  cudaSetDevice(ctx->device);
+  ctx->have_run = false;
+  ctx->img_w = 0;
+  cudaGetLastError();
+  const int d = in->d;
+  const int64_t n = in->n;
+  const void* dpts = in->points;
+  if (!in->on_device) {
+    GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
+    GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice,
+                          ctx->stream));
+    dpts = ctx->pts.p;
+  }
+  GS_TRY(grow(ctx, ctx->errflag, 32));
+  GS_TRY(grow(ctx, ctx->counters, 64));
+  GS_TRY(ensure_frames(ctx, 1));
+  int64_t m0 = 0;
+  for (int attempt = 0;; ++attempt) {  // the first grid (pin M1) = the engine's n-scale phase
+    GS_TRY(launch_nscale(ctx, dpts, in->dtype, d, n, 1, h));
+    int hdr[8];
+    unsigned ctr[16];
+    GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaMemcpyAsync(ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+    GS_CK(cudaStreamSynchronize(ctx->stream));
+    if ((hdr[0] & 32) && attempt < 3) {
+      GS_TRY(grow_dense_for(ctx, *(long long*)(hdr + 2), d));
+      continue;
+    }
+    if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    if (hdr[0] & (32 | 64)) return fail(ctx, GS_E_KEY_RANGE, "key box too large");
+    m0 = ctr[0];
+    break;
+  }
+  ctx->ctl_clean = false;
+  // one CTA holds the particles: the largest power-of-two slot count that fits with the
+  // frame's dense index (in shared memory when it fits, else the global grid index)
+  const size_t budget = 226 * 1024;
+  const size_t bps = (size_t)(d == 1 ? gs::mspp_bytes_per_slot<1>() : d == 2 ? gs::mspp_bytes_per_slot<2>()
+                              : d == 3 ? gs::mspp_bytes_per_slot<3>() : d == 4 ? gs::mspp_bytes_per_slot<4>()
+                              : d == 5 ? gs::mspp_bytes_per_slot<5>() : gs::mspp_bytes_per_slot<6>());
+  int MS = 1;
+  while ((size_t)(2 * MS) * bps <= budget) MS *= 2;
+  int vol_small = 0;
+  if (2 * (size_t)ctx->box.vol_frame + (size_t)MS * bps <= budget) vol_small = 1;
+  else if (2 * (size_t)ctx->box.vol_frame + (size_t)(MS / 2) * bps <= budget && m0 <= MS / 2) {
+    MS /= 2;
+    vol_small = 1;
+  }
+  if (m0 > MS)
+    return fail(ctx, GS_E_INVALID_PARAMETER,
+                "MS++ baseline: the first grid (" + std::to_string((long long)m0) +
+                    " cells) exceeds one CTA's shared memory (" + std::to_string(MS) + ")");
+  GS_TRY(grow(ctx, ctx->S1, sizeof(double) * (size_t)m0 * d));
+  GS_TRY(grow(ctx, ctx->dbg, 64 + sizeof(double) * (size_t)max_iter));
+  GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 64, ctx->stream));
+  unsigned long long* disp0 = (unsigned long long*)ctx->dbg.p;
+  int* outw = (int*)((char*)ctx->dbg.p + 16);
+  double* dhist = (double*)((char*)ctx->dbg.p + 64);
+  double* cent = ctx->S[1].as<double>();
+  double* snew0 = ctx->S1.as<double>();
+  gs_status ls = GS_OK;
+  const bool f64 = in->dtype == GS_F64;
+  switch (d) {
+#define GS_CASE(D)                                                                              \
+  case D:                                                                                       \
+    ls = f64 ? mspp_launch<D, double>(ctx, dpts, n, m0, tol, max_iter, MS, vol_small, snew0,   \
+                                      disp0, outw, dhist, cent)                                 \
+             : mspp_launch<D, float>(ctx, dpts, n, m0, tol, max_iter, MS, vol_small, snew0,    \
+                                     disp0, outw, dhist, cent);                                 \
+    break;
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
+#undef GS_CASE
+  }
+  GS_TRY(ls);
+  GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * n));
+  int32_t* dl = ctx->labels.as<int32_t>();
+  gs::k_label<<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+      n, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dl, nullptr, nullptr, 0, 0);
+  GS_LAUNCHED("k_label");
+  GS_CK(cudaMemcpyAsync(out->labels, dl, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                        ctx->stream));
+  int ow[4];
+  GS_CK(cudaMemcpyAsync(ow, outw, sizeof(ow), cudaMemcpyDeviceToHost, ctx->stream));
+  if (disp_hist)
+    GS_CK(cudaMemcpyAsync(disp_hist, dhist, sizeof(double) * max_iter, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  int err = 0;
+  GS_CK(cudaMemcpyAsync(&err, ctx->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CK(cudaStreamSynchronize(ctx->stream));
+  GS_CK(cudaGetLastError());
+  if (err & ~0) {
+    if (err & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    if (err & 2) return fail(ctx, GS_E_INTERNAL_INVARIANT, "a point's key left the box");
+  }
+  out->k[0] = ow[0];
+  out->iterations[0] = ow[1];
+  out->converged[0] = ow[2];
+  ctx->cur = 1;  // gs_get_centroids reads the final centroids from S[1]
+  ctx->nframes = 1;
+  ctx->h_k.assign(1, ow[0]);
+  ctx->h_ffirst.assign(1, 0);
+  ctx->hist_m.clear();
+  ctx->hist_d.clear();
+  ctx->have_run = true;
+  return GS_OK;
+}
+
+namespace {
 }  // namespace
 
 extern "C" {

@@ -97,7 +97,7 @@ EXPORTED = [
     "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
     "gs_shard_run", "gs_render", "gs_tuner_create", "gs_tuner_destroy", "gs_tuner_last_error",
     "gs_tune_bandwidth", "gs_silhouette_subsampled", "gs_tracker_create", "gs_tracker_destroy",
-    "gs_tracker_last_error", "gs_track_init", "gs_track_sequence",
+    "gs_tracker_last_error", "gs_track_init", "gs_track_sequence", "gs_mspp_run",
 ]
 
 
@@ -183,6 +183,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                       C.POINTER(GsSweepEntry), C.POINTER(D)]
     lib.gs_silhouette_subsampled.argtypes = [P, C.POINTER(GsInput), P, I32, I64, C.c_uint64,
                                              C.POINTER(D)]
+    lib.gs_mspp_run.argtypes = [P, C.POINTER(GsInput), D, D, I32, C.POINTER(GsResult), P]
     lib.gs_tracker_create.argtypes = [C.c_int, C.POINTER(P)]
     lib.gs_tracker_destroy.argtypes = [P]
     lib.gs_tracker_destroy.restype = None
@@ -322,6 +323,29 @@ class Engine:
         r = self.run_batch(X[None], cfg)
         return ClusterLabeling(r.labels[0], r.centroids[0], int(r.iterations[0]),
                                bool(r.converged[0]), r.history[0] if r.history else None)
+
+    def mspp(self, X: np.ndarray, h: float, tol: Optional[float] = None,
+             max_iter: int = 300) -> ClusterLabeling:
+        """MS++ baseline, mspp_run on the GPU: Jacobi grid mean shift."""
+        X = np.ascontiguousarray(X)
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        n, d = X.shape
+        tol = 1e-6 * h if tol is None else tol
+        dt = GS_F32 if X.dtype == np.float32 else GS_F64
+        inp = GsInput(X.ctypes.data, n, d, dt, 1, 0, 0)
+        labels = np.zeros(n, np.int32)
+        k = np.zeros(1, np.int64)
+        it = np.zeros(1, np.int32)
+        cv = np.zeros(1, np.int32)
+        disp = np.zeros(max(max_iter, 1), np.float64)
+        res = GsResult(labels.ctypes.data, k.ctypes.data, it.ctypes.data, cv.ctypes.data)
+        self._check(self._lib.gs_mspp_run(self._ctx, C.byref(inp), h, tol, max_iter, C.byref(res),
+                                          disp.ctypes.data))
+        cen = self.centroids(0, int(k[0]), d)
+        return ClusterLabeling(labels=labels, centroids=cen, iterations=int(it[0]),
+                               converged=bool(cv[0]),
+                               history=[(None, float(v)) for v in disp[:int(it[0])]])
 
     def centroids(self, frame: int, k: int, d: int) -> np.ndarray:
         out = np.zeros((k, d), np.float64)
