@@ -1509,12 +1509,8 @@ gs_status mspp_launch(gs_ctx* ctx, const void* dpts, int64_t n, int64_t m0, doub
   a.disp_hist = dhist;
   const size_t smem = (size_t)MS * gs::mspp_bytes_per_slot<D>() +
                       (vol_small ? 2 * (size_t)ctx->box.vol_frame : 0);
-  static bool configured = false;
-  if (!configured) {
-    GS_CK(cudaFuncSetAttribute(gs::k_mspp_loop<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               227 * 1024));
-    configured = true;
-  }
+  GS_CK(cudaFuncSetAttribute(gs::k_mspp_loop<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem));
   gs::k_mspp_loop<D><<<1, 512, smem, st>>>(a);
   GS_LAUNCHED("k_mspp_loop");
   return GS_OK;
