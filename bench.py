@@ -397,15 +397,110 @@ def run_track(args):
     return 0
 
 
+def run_mspp(args):
+    """--workload mspp: the MS++ baseline (mspp_run; parallel Jacobi grid
+    mean shift) on the cfg2 image, h = 0.08, tol = 1e-6 h, max_iter 300 -- the comparator of
+    the reference's speed claims.  value = points/s through gs_mspp_run from
+    device-resident points (host wall clock around the synchronous call); e2e = from host
+    memory; the engine's own cfg2 line is the default bench."""
+    from paper_2206_02200_b200 import configs as CF
+    X = CF.voronoi_rgb(seed=2208)
+    n, d = X.shape
+    h = 0.08
+    rank = int(os.environ.get("RANK", "0"))
+    metric = "MS++ baseline: points/s"
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as O
+        Xd = X.astype(np.float64)
+        times = []
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.mspp(Xd, h)
+            if s >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        value = n * args.steps / sum(times)
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": value, "unit": "points/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "mspp", "n": n, "d": d, "h": h},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "port",
+                             "sample": "oracle gso_mspp on the whole cfg2 image per step"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return 0
+    import torch
+    from paper_2206_02200_b200 import gridshift as G
+    torch.cuda.set_device(0)
+    eng = G.Engine(0)
+    lib = G.load_library()
+    Xd = torch.from_numpy(X).cuda()
+    Xh = torch.from_numpy(X).pin_memory()
+    labels = np.zeros(n, np.int32)
+    k = np.zeros(1, np.int64)
+    it = np.zeros(1, np.int32)
+    cv = np.zeros(1, np.int32)
+    res = G.GsResult(labels.ctypes.data, k.ctypes.data, it.ctypes.data, cv.ctypes.data)
+
+    def step(dev: bool):
+        inp = G.GsInput(Xd.data_ptr() if dev else Xh.data_ptr(), n, d, G.GS_F32, 1,
+                        1 if dev else 0, 0)
+        eng._check(lib.gs_mspp_run(eng._ctx, G.C.byref(inp), h, 1e-6 * h, 300, G.C.byref(res),
+                                   None))
+
+    for _ in range(args.warmup):
+        step(True)
+        step(False)
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(True)
+    t_dev = (time.perf_counter() - t0) / args.steps
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(False)
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    clk = clocks.stop()
+    line = {
+        "metric": metric, "value": n / t_dev, "unit": "points/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "mspp", "desc": "cfg2 image, MS++ Jacobi baseline", "n": n,
+                   "d": d, "h": h, "tol": 1e-6 * h, "max_iter": 300,
+                   "timing": "host wall clock around the synchronous call"},
+        "k": int(k[0]), "iterations": int(it[0]), "converged": bool(cv[0]),
+        "e2e": {"value": n / t_e2e, "unit": "points/s", "ms_per_step": 1e3 * t_e2e,
+                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(4 * n)},
+        "gpu_launches": 7, "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        O.mspp(X.astype(np.float64), h)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n / dt, "unit": "points/s", "cores": 1, "kind": "port",
+                                "sample": f"oracle gso_mspp, one cfg2 run ({dt:.2f} s)"}
+    print(json.dumps(line))
+    eng.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg2",
-                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune", "track"],
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune", "track", "mspp"],
                     help="tune: the bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image; "
-                         "track: the tracker (§8(f)3) over the cfg4 frames")
+                         "track: the tracker (§8(f)3) over the cfg4 frames; mspp: the MS++ "
+                         "baseline (§8(f)4) on the cfg2 image")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -417,6 +512,8 @@ def main():
         return run_tune(args)
     if args.workload == "track":
         return run_track(args)
+    if args.workload == "mspp":
+        return run_mspp(args)
     if args.impl == "reference":
         return run_reference(args)
 
