@@ -96,6 +96,7 @@ struct gs_ctx {
   // bumped whenever a device buffer is (re)allocated: a cached graph holds raw pointers
   uint64_t alloc_gen = 0;
   int img_w = 0;  // GS_U8 rgbxy: image width of the current call
+  int bin_rep_log2 = 0;  // K2 table replicas per cell (2^x): batched frames use 4
   const void* host_src = nullptr;  // pinned caller points read by K1 directly (zero copy)
   // multi-GPU shard state (gs_shard_*): the global key box from gs_shard_bin, and for
   // gs_shard_run the merged partial cells the run starts from instead of binning
@@ -457,7 +458,7 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
     gs::k_bin_priv<D, T><<<grid, 768, smem, ctx->stream>>>(
         (const T*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
         ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
-        TBL, img_w);
+        TBL, img_w, ctx->bin_rep_log2);
     GS_LAUNCHED("k_bin_priv");
   }
   return GS_OK;
@@ -530,6 +531,12 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   cudaStream_t st = ctx->stream;
   const int64_t ntot = n * nf;
   const unsigned nblk = blocks_for(ntot, 256 * 4, (int64_t)ctx->num_sms * 4);
+  // batched frames (images): few distinct cells per warp -> 4 lane-chosen replicas per cell
+  // in K2's table (GS_BIN_REPLICAS overrides: 0, 1 or 2 = log2 of the replica count)
+  {
+    const char* v = getenv("GS_BIN_REPLICAS");
+    ctx->bin_rep_log2 = v ? std::max(0, std::min(2, atoi(v))) : (nf > 1 ? 2 : 0);
+  }
   GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
   GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
   GS_TRY(ensure_dense(ctx, std::max<int64_t>(ctx->dense_cap, kDefaultDenseCells), d));

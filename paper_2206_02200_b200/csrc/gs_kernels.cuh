@@ -249,10 +249,13 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
                                                    uint32_t* __restrict__ cnt,
                                                    unsigned long long* __restrict__ qs,
                                                    uint32_t* __restrict__ slot, int* err,
-                                                   int TBL, int img_w) {
+                                                   int TBL, int img_w, int rep_log2) {
   constexpr int RC = gs_raw_cols<T, D>();
   // TBL: table entries (a multiple of 32, <= bin_table_entries<D>()) sized to the CTA's points
-  // (initialising and flushing a table costs O(TBL) per CTA).
+  // (initialising and flushing a table costs O(TBL) per CTA).  rep_log2: each cell gets
+  // 2^rep_log2 replica entries, chosen by lane (batched image frames: a frame's noisy
+  // background puts few distinct cells in a warp, many lanes each, and same-address shared
+  // atomics serialise); the replicas are summed by the flush.
   constexpr uint32_t EMPTY = 0xffffffffu;
   // the first round's coordinates, the error word and the box are all requested before any
   // of them is waited for (after an L2 flush each is a cold HBM round trip)
@@ -403,14 +406,15 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
     // let the compiler replay the whole atomic sequence once per exit group).
     const unsigned am = __ballot_sync(kFull, act);
     if (act) {
-      uint32_t hsh = __umulhi(key * 2654435761u, (unsigned)TBL);
+      const uint32_t tkey = (key << rep_log2) | (lane & ((1u << rep_log2) - 1u));
+      uint32_t hsh = __umulhi(tkey * 2654435761u, (unsigned)TBL);
       int hit = -1;
 #pragma unroll
       for (int probe = 0; probe < kBinProbes; ++probe) {
         if (hit < 0) {
           uint32_t k = tk[hsh];
-          if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, key);
-          if (k == EMPTY || k == key) hit = (int)hsh;
+          if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, tkey);
+          if (k == EMPTY || k == tkey) hit = (int)hsh;
           hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
         }
       }
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, 
   for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
     const uint32_t key = tk[j];
     if (key == EMPTY) continue;
-    const int64_t L = key;
+    const int64_t L = key >> rep_log2;
     atomicAdd(&cnt[L], tc[j]);
 #pragma unroll
     for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], ts[j * D + c]);
