@@ -88,7 +88,8 @@ class ClockSampler:
 
 # K2 dram bytes (read + write) per launch, ncu --set full of the current K2
 # (profiles/r1_ncu_kernels.md, session-2 captures)
-NCU_TRAFFIC = {"cfg2": 1_901_312, "cfg4": 950_866_432 + 297_167_872}
+NCU_TRAFFIC = {"cfg2": 1_900_288, "cfg4": 952_078_592 + 298_366_208,
+               "cfg5": 771_519_744 + 237_712_896}
 
 
 def workload_input(name: str, rank: int):
