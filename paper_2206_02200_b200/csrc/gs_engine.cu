@@ -649,6 +649,62 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
     configured = true;
   }
+  // the dataflow cluster sweep (no levels: a cell is updated as soon as its predecessors are);
+  // GS_SWEEP_FLOW=0 falls back to the level-synchronous cluster sweep below
+  {
+    static int flow_env = -1;
+    if (flow_env < 0) {
+      const char* v = getenv("GS_SWEEP_FLOW");
+      flow_env = v ? atoi(v) : 1;
+    }
+    static int fl_cfg = 0;  // 1: 16-CTA clusters allowed, 2: refused
+    static const int flow_sleep = getenv("GS_FLOW_SLEEP") ? atoi(getenv("GS_FLOW_SLEEP")) : 0;
+    static const int flow_fence = getenv("GS_FLOW_FENCE") ? atoi(getenv("GS_FLOW_FENCE")) : 0;
+    // measured: d = 5 (cfg3) 2.17 -> 1.85 ms per run; d = 3 (cfg5) 2.33 -> 2.45 ms (the
+    // per-hop fence + remote release costs more than the level barrier saves when a cell has
+    // <= 27 terms), so d <= 3 keeps the level-synchronous sweep unless GS_SWEEP_FLOW=2
+    if (flow_env > 1 || (flow_env == 1 && D > 3)) {
+      int NC = 16;
+      if (!fl_cfg) {
+        GS_CK(cudaFuncSetAttribute(gs::k_sweep_flow<D>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
+        fl_cfg = cudaFuncSetAttribute(gs::k_sweep_flow<D>,
+                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                         cudaSuccess
+                     ? 1
+                     : 2;
+        cudaGetLastError();
+      }
+      if (fl_cfg != 1) NC = 8;
+      const size_t fsm = gs::sweep_flow_smem<D>((int)((m + NC - 1) / NC));
+      if (fsm <= kBudget) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)NC);
+        lc.blockDim = dim3(512);
+        lc.dynamicSmemBytes = fsm;
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)NC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        const cudaError_t le = cudaLaunchKernelEx(
+            &lc, gs::k_sweep_flow<D>, (int)m, KP, (const uint32_t*)lists,
+            (const int32_t*)ctx->nbn.as<int32_t>(), (const int32_t*)ctx->nbe.as<int32_t>(),
+            (const uint32_t*)ctx->ccnt[cur].as<uint32_t>(),
+            (const uint32_t*)ctx->den.as<uint32_t>(), (const double*)ctx->rden.as<double>(), Q,
+            ctx->errflag.as<int>(), flow_sleep, flow_fence);
+        if (le == cudaSuccess) {
+          GS_LAUNCHED("k_sweep_flow");
+          return GS_OK;
+        }
+        cudaGetLastError();
+        flow_env = 0;  // cannot be scheduled here: level-synchronous sweeps from now on
+      }
+    }
+  }
   // the cluster sweep (NC CTAs on NC SMs, DSMEM pending counts and queues) when the owned
   // share of 3 words per cell fits each CTA; GS_SWEEP_CLUSTER=0 forces the single-CTA sweep
   {

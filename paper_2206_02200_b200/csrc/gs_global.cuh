@@ -646,4 +646,149 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
   cluster.sync();  // no CTA exits while others may still read its shared memory
 }
 
+// ---------------------------------------------------------------- dataflow cluster sweep
+// The cluster sweep without levels: a cell is updated as soon as its last lex-earlier
+// neighbour is, by a warp of its owner CTA that waits on the next position of the owner's
+// queue (every owned cell is appended exactly once, after all of its predecessors were
+// processed, so a warp waiting on position k only waits for cells at earlier positions of some
+// queue: no deadlock).  A warp updates one cell (lane l loads list word l of each 128-entry
+// chunk, the operand rows are staged per warp, lanes c < D add them in list order), stores the
+// row, fences it (__threadfence: visible GPU-wide before the release), and releases the
+// successors with remote atomics on their owners' pending counts; the last releaser appends
+// the successor with an atomic on the owner's tail and a store of the cell id into the owner's
+// queue slot (initialised to -1; the consumer polls it with an acquire load).  No barrier, no
+// level skew: the critical path is the DAG depth x one update + one release.  A spin watchdog
+// sets err bit 8 instead of hanging.  Operands and add order are the serial sweep's.
+__device__ __forceinline__ int ld_acquire_cluster_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.shared::cta.s32 %0, [%1];"
+               : "=r"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+
+template <int D>
+__host__ __device__ constexpr size_t sweep_flow_smem(int mloc) {
+  return (((size_t)8 * mloc + 15) & ~(size_t)15) + (size_t)(512 / 32) * 128 * D * 8;
+}
+
+template <int D>
+__global__ void __launch_bounds__(512, 1) k_sweep_flow(
+    int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
+    const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
+    const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q, int* err,
+    int flow_sleep, int flow_fence) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int NC = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = T >> 5;
+  const int mloc = (m + NC - 1) / NC;
+  const int own_n = rank < m ? (m - rank + NC - 1) / NC : 0;  // cells rank, rank+NC, ...
+  unsigned* pend = (unsigned*)dsm;
+  int* queue = (int*)(pend + mloc);
+  double* stg = (double*)(dsm + (((size_t)8 * mloc + 15) & ~(size_t)15)) + (size_t)warp * 128 * D;
+  __shared__ unsigned tail;
+  if (tid == 0) tail = 0;
+  for (int t = tid; t < mloc; t += T) queue[t] = -1;
+  __syncthreads();
+  for (int t = tid; t < own_n; t += T) {
+    const int i = rank + NC * t;
+    const int e = nbe[i];
+    pend[t] = (unsigned)e;
+    if (e == 0) queue[atomicAdd(&tail, 1u)] = i;
+  }
+  const uint32_t P1ROW = (uint32_t)m + 1u;
+  cluster.sync();  // every CTA's pending counts and queue slots are initialised
+  bool dead = false;
+  for (int pos = warp; pos < own_n && !dead; pos += nwarps) {
+    int i = -1;
+    if (lane == 0) {
+      long long spins = 0;
+      while ((i = ld_acquire_cluster_s32(&queue[pos])) < 0) {
+        if (++spins > (1ll << 26)) {  // watchdog: never hang the GPU
+          atomicOr(err, 8);
+          break;
+        }
+        if (flow_sleep) __nanosleep(flow_sleep);
+      }
+    }
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i < 0) {
+      dead = true;
+      break;
+    }
+    const int n = nbn[i], e = nbe[i];
+    const uint32_t dn = den[i], cn = ccnt[i];
+    const double rd = rden[i];
+    const uint4* ls = (const uint4*)(lists + (int64_t)i * KP);
+    double num = 0.0;
+    uint32_t ent_keep[4];  // this lane's entries of the last chunk (for the release)
+    int tb_keep = 0;
+    for (int t0 = 0; t0 < max(n, 1); t0 += 128) {
+      const int tb = t0 + 4 * lane;
+      uint4 r = make_uint4(0u, 0u, 0u, 0u);
+      if (tb < n) r = __ldg(&ls[tb >> 2]);
+      const uint32_t ent[4] = {r.x, r.y, r.z, r.w};
+      double v[4][D];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc)
+          v[jj][cc] = (tb + jj < n) ? __ldcg(&Q[(int64_t)ent[jj] * D + cc]) : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) stg[(4 * lane + jj) * D + cc] = v[jj][cc];
+      __syncwarp();
+      if (lane < D && n > 1) {
+        const int len = min(128, n - t0);
+#pragma unroll 8
+        for (int u = 0; u < len; ++u) num = __dadd_rn(num, stg[u * D + lane]);
+      }
+      __syncwarp();
+      if (t0 + 128 >= n) {  // the last chunk's words stay in registers for the release
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) ent_keep[jj] = ent[jj];
+        tb_keep = tb;
+      }
+    }
+    if (n > 1 && lane < D) {  // else: frozen or isolated (Q row = S_old, P3)
+      const double s1 = gl_div(num, (double)dn, rd);
+      __stcg(&Q[((int64_t)P1ROW + i) * D + lane], __dmul_rn((double)cn, s1));
+      __stcg(&Q[(int64_t)i * D + lane], s1);
+      if (flow_fence)  // the row is visible before any successor is released
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      else
+        __threadfence();
+    }
+    __syncwarp();
+    auto release_one = [&](int j) {
+      const int own = j % NC;
+      unsigned* pj = cluster.map_shared_rank(pend + j / NC, own);
+      if (atomicSub(pj, 1u) == 1u) {
+        unsigned* tl = cluster.map_shared_rank(&tail, own);
+        int* qd = cluster.map_shared_rank(queue, own);
+        const unsigned slot = atomicAdd(tl, 1u);
+        atomicExch(&qd[slot], j);
+      }
+    };
+    // successors: entries e < t < n; the last chunk's from registers, earlier chunks reloaded
+    for (int t0 = 0; t0 + 128 < n; t0 += 128) {
+      const int tb = t0 + 4 * lane;
+      const uint4 r = __ldg(&ls[tb >> 2]);
+      const uint32_t ent[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        if (tb + jj > e && tb + jj < n) release_one((int)ent[jj]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (tb_keep + jj > e && tb_keep + jj < n) release_one((int)ent_keep[jj]);
+  }
+  cluster.sync();  // no CTA exits while others may still touch its shared memory
+}
+
 }  // namespace gs
