@@ -1158,13 +1158,15 @@ void dump_trace(gs_ctx* ctx) {
       cudaMemcpy(ti.data(), (long long*)ctx->dbg.p + 4096, 8 * 512, cudaMemcpyDeviceToHost);
       std::vector<long long> ts(1024);
       cudaMemcpy(ts.data(), (long long*)ctx->dbg.p + 9700, 8 * 1024, cudaMemcpyDeviceToHost);
-      for (int t = 0; t < 64 && ti[8 * t + 7]; ++t) {
+      for (int t = 0; t < 64; ++t) {
+        if (!ti[8 * t + 7]) continue;  // (iterations run on the global path have no stamps)
         const long long* y = &ts[16 * t];
         const long long* x = &ti[8 * t];
         fprintf(stderr, "sub %2d lists: top->loop %5lld loop(t0) %5lld barrier %5lld | fold: heads->scan %5lld seg %5lld fold(t0) %5lld roots+retire %5lld barrier %5lld\n",
                 t, y[0] - x[7], y[1] - y[0], x[0] - y[1], y[3] - y[2], y[4] - y[3], y[5] - y[4], y[6] - y[5], y[7] - y[6]);
       }
-      for (int t = 0; t < 64 && ti[8 * t + 7]; ++t) {
+      for (int t = 0; t < 64; ++t) {
+        if (!ti[8 * t + 7]) continue;
         const long long* x = &ti[8 * t];
         const long long* y = &((const long long*)tp9.data())[4 * t];
         fprintf(stderr, "iter %2d m %5lld lists %6lld sweep %6lld (levels %4lld: relax %6lld sort %5lld) rehome %6lld sort %6lld fold %6lld adj %6lld\n",

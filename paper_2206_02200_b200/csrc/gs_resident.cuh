@@ -347,6 +347,31 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   for (int i = tid; i < m; i += T) idx_put(key[i], i);
   __syncthreads();
 
+  // d > 3 with small frames: neighbours by pairwise comparison of byte-packed cell coordinates
+  // (|dk| <= 1 in every byte: two __vabsdiffu4) instead of 3^d index probes, which go to the
+  // global grid when the frame's box is too large for the shared-memory index (cfg3: 243 L2
+  // probes per cell).  Cells are lex-sorted, so ascending j is the lex neighbour order.
+  bool pairwise_ok = D > 3 && D <= 8;
+#pragma unroll
+  for (int c = 0; c < D; ++c) pairwise_ok = pairwise_ok && b.ext[c] <= 256;
+  auto pack_cells = [&](int mm) {  // sk[i] = byte-packed coordinates of cell i
+    for (int i = tid; i < mm; i += T) {
+      const uint32_t L = key[i];
+      uint64_t pk = 0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const uint32_t rel = (L / (uint32_t)b.stride[c]) % (uint32_t)b.ext[c];
+        pk |= (uint64_t)rel << (8 * c);
+      }
+      sk[i] = pk;
+    }
+  };
+  auto near = [](uint64_t x, uint64_t y) {
+    const uint32_t d0 = __vabsdiffu4((uint32_t)x, (uint32_t)y);
+    const uint32_t d1 = __vabsdiffu4((uint32_t)(x >> 32), (uint32_t)(y >> 32));
+    return ((d0 | d1) & 0xfefefefeu) == 0u;
+  };
+
   bool done = false;
   int64_t swept = 0;
   long long t_prev = clock64();
@@ -433,40 +458,104 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
         finish_cell(i, n, s, true);
       }
     } else {
-      for (int i = tid; i < m; i += T) {
-        NbrIt it = nbr_begin();
-        int n = 0, e = 0;
-        const int64_t Li = key[i];
+      // census and fill with the index kind hoisted out of the probe loops (a branch per probe
+      // serialised d = 5's 243 L2 probes: ~110 K cycles per cell when the frame's index is the
+      // global grid) and, in the fill, the probes of a batch issued before its list stores
+      constexpr int KB = K < 27 ? K : 27;
+      auto census = [&](const auto* ix) {
+        for (int i = tid; i < m; i += T) {
+          NbrIt it = nbr_begin();
+          int n = 0, e = 0;
+          const int64_t Li = key[i];
 #pragma unroll 27
-        for (int t = 0; t < K; ++t) {
-          const int j = idx_get(Li + it.at(t));
-          n += (j >= 0);
-          e += (j >= 0) & (j < i);
-          it.step(b);
+          for (int t = 0; t < K; ++t) {
+            const int j = (int)ix[Li + it.at(t)];
+            n += (j >= 0);
+            e += (j >= 0) & (j < i);
+            it.step(b);
+          }
+          nbn[i] = n;
+          nbe[i] = e;
+          tmp[i] = (n + 3) & ~3;  // list length padded to whole 4-entry words
         }
-        nbn[i] = n;
-        nbe[i] = e;
-        tmp[i] = (n + 3) & ~3;  // list length padded to whole 4-entry words
+      };
+      const bool pw = pairwise_ok && m <= T;
+      if (pw) {
+        pack_cells(m);
+        __syncthreads();
+        for (int i = tid; i < m; i += T) {
+          const uint64_t pi = sk[i];
+          int n = 0, e = 0;
+          for (int j = 0; j < m; ++j) {
+            const bool nb = near(pi, sk[j]);
+            n += nb;
+            e += nb & (j < i);
+          }
+          nbn[i] = n;
+          nbe[i] = e;
+          tmp[i] = (n + 3) & ~3;
+        }
+      } else if (sdense) {
+        census(sidx);
+      } else {
+        census(gidx);
       }
       __syncthreads();
       n_all = rs_scan(tmp, m, wtmp);
       mode = (2 * n_all + 8 <= a.pool_bytes) ? 1 : 2;
-      for (int i = tid; i < m; i += T) {
-        NbrIt it = nbr_begin();
-        int nn = 0;
-        uint32_t s = 0;
-        const int64_t Li = key[i];
-        uint16_t* li = lst + tmp[i];
-        for (int t = 0; t < K; ++t) {
-          const int j = idx_get(Li + it.at(t));
-          it.step(b);
-          if (j < 0) continue;
-          s += cnt[j];
-          if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+      auto fill = [&](const auto* ix) {
+        for (int i = tid; i < m; i += T) {
+          NbrIt it = nbr_begin();
+          int nn = 0;
+          uint32_t s = 0;
+          const int64_t Li = key[i];
+          uint16_t* li = lst + tmp[i];
+          if constexpr (kTable) {
+            for (int t0 = 0; t0 < K; t0 += KB) {
+              int jb[KB];
+#pragma unroll
+              for (int u = 0; u < KB; ++u) jb[u] = (int)ix[Li + it.at(t0 + u)];
+#pragma unroll
+              for (int u = 0; u < KB; ++u) {
+                const int j = jb[u];
+                if (j < 0) continue;
+                s += cnt[j];
+                if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+              }
+            }
+          } else {
+            for (int t = 0; t < K; ++t) {
+              const int j = (int)ix[Li + it.at(t)];
+              it.step(b);
+              if (j < 0) continue;
+              s += cnt[j];
+              if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+            }
+          }
+          if (mode == 1)
+            for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
+          finish_cell(i, nbn[i], s, mode == 1);
         }
-        if (mode == 1)
-          for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
-        finish_cell(i, nbn[i], s, mode == 1);
+      };
+      if (pw) {
+        for (int i = tid; i < m; i += T) {
+          const uint64_t pi = sk[i];
+          int nn = 0;
+          uint32_t s = 0;
+          uint16_t* li = lst + tmp[i];
+          for (int j = 0; j < m; ++j) {
+            if (!near(pi, sk[j])) continue;
+            s += cnt[j];
+            if (mode == 1) li[nn++] = (uint16_t)(j < i ? P1ROW + j : j);
+          }
+          if (mode == 1)
+            for (; nn & 3; ++nn) li[nn] = (uint16_t)ZROW;
+          finish_cell(i, nbn[i], s, mode == 1);
+        }
+      } else if (sdense) {
+        fill(sidx);
+      } else {
+        fill(gidx);
       }
       if (mode == 1 && tid < 4) lst[n_all + tid] = (uint16_t)ZROW;  // slack word (prefetch)
     }
@@ -898,6 +987,14 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 
     // ---- (6) has_converged on the new state
     bool adj = false;
+    if (pairwise_ok && m <= T) {
+      pack_cells(m);
+      __syncthreads();
+      for (int i = tid; i < m && !adj; i += T) {
+        const uint64_t pi = sk[i];
+        for (int j = 0; j < m && !adj; ++j) adj = j != i && near(pi, sk[j]);
+      }
+    } else
     for (int i = tid; i < m && !adj; i += T) {
       NbrIt it = nbr_begin();
       const int64_t Li = key[i];
