@@ -942,9 +942,18 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   gs::k_idx_set<<<nb, 256, 0, ctx->stream>>>(mnew, ctx->ckey[nxt].as<uint32_t>(),
                                              ctx->idx.as<int32_t>());
   GS_LAUNCHED("k_idx_set");
-  gs::k_adjacent<<<nb, 256, 0, ctx->stream>>>(mnew, b, K, ctx->ckey[nxt].as<uint32_t>(),
-                                              ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(),
-                                              ctx->fadj.as<int32_t>());
+  switch (d) {
+#define GS_ADJ(D)                                                                             \
+  case D:                                                                                     \
+    gs::k_adjacent<D><<<nb, 256, 0, ctx->stream>>>(mnew, b, K, ctx->ckey[nxt].as<uint32_t>(), \
+                                                   ctx->idx.as<int32_t>(),                    \
+                                                   ctx->fdone.as<int32_t>(),                  \
+                                                   ctx->fadj.as<int32_t>());                  \
+    break;
+    GS_ADJ(1) GS_ADJ(2) GS_ADJ(3) GS_ADJ(4) GS_ADJ(5) GS_ADJ(6) GS_ADJ(7) GS_ADJ(8) GS_ADJ(9)
+    GS_ADJ(10) GS_ADJ(11) GS_ADJ(12)
+#undef GS_ADJ
+  }
   GS_LAUNCHED("k_adjacent");
   ctx->cur = nxt;
   *mnew_out = mnew;

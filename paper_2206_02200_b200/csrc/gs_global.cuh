@@ -31,6 +31,21 @@ __device__ __forceinline__ double gl_div(double a, double b, double y) {
 // m+1+j = C'*S_new, itself / later -> row j = C'*S_old), padded with the zero row m; #active,
 // #earlier, ΣC' and RN(1/ΣC'); Q row i = C'*S_old (S_old itself when the cell has no active
 // neighbour but itself, pin P3).  Frozen frames: nbn = 0, Q row = S_old.
+// Lexicographic neighbour offsets (v in {-1,0,1}^D, dim 0 most significant: the odometer's
+// order) as linear deltas of the frame box, one per thread of the block (D <= 6: K <= 729).
+template <int D>
+__device__ __forceinline__ void nbr_offsets_smem(const GsBox& b, int K, int* offs) {
+  for (int t = threadIdx.x; t < K; t += blockDim.x) {
+    int r = t;
+    int64_t off = 0;
+    for (int c = D - 1; c >= 0; --c) {
+      off += (int64_t)(r % 3 - 1) * b.stride[c];
+      r /= 3;
+    }
+    offs[t] = (int)off;
+  }
+}
+
 template <int D>
 __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __restrict__ ckey,
                             const uint32_t* __restrict__ ccnt, const double* __restrict__ S0,
@@ -39,6 +54,13 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
                             int32_t* __restrict__ nbe, uint32_t* __restrict__ den,
                             double* __restrict__ rden, double* __restrict__ Q,
                             int32_t* __restrict__ fm) {
+  // probes in batches of 27 from a shared offset table: the loads of a batch are independent
+  // (one L2 round trip per batch instead of one per probe behind the odometer and the stores)
+  constexpr int KMAX = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 : 729;
+  constexpr int B = KMAX < 27 ? KMAX : 27;
+  __shared__ int offs[KMAX];
+  nbr_offsets_smem<D>(b, KMAX, offs);
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0)
     for (int c = 0; c < D; ++c) Q[(int64_t)m * D + c] = 0.0;  // the zero row
@@ -53,18 +75,24 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
     return;
   }
   atomicAdd(&fm[f], 1);
-  GsNbrOdometer od;
-  od.init(b);
   int n = 0, e = 0;
   uint32_t s = 0;
   const uint32_t P1ROW = (uint32_t)m + 1u, ZROW = (uint32_t)m;
-  for (int t = 0; t < K; ++t) {
-    const int32_t j = __ldg(&idx[L + od.off]);
-    od.next(b);
-    if (j < 0) continue;
-    s += ccnt[j];
-    li[n++] = j < i ? P1ROW + (uint32_t)j : (uint32_t)j;
-    e += j < i;
+  for (int t0 = 0; t0 < KMAX; t0 += B) {
+    int jb[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) jb[u] = __ldg(&idx[L + offs[t0 + u]]);
+    uint32_t cb[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) cb[u] = jb[u] >= 0 ? __ldg(&ccnt[jb[u]]) : 0u;
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int32_t j = jb[u];
+      if (j < 0) continue;
+      s += cb[u];
+      li[n++] = j < i ? P1ROW + (uint32_t)j : (uint32_t)j;
+      e += j < i;
+    }
   }
   for (int t = n; t < KP; ++t) li[t] = ZROW;
   nbn[i] = n;

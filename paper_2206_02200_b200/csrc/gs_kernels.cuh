@@ -686,14 +686,29 @@ __global__ void k_fold(int mnew, int m, const int32_t* __restrict__ segstart,
   for (int c = 0; c < D; ++c) s[c] = S1[(int64_t)i0 * D + c];
   uint64_t cnt = ccnt[i0];
   bool slow = false;
+  // software-pipelined: the next member's index, count and row are loaded before this member
+  // is folded (they do not depend on the fold), so only the fp64 chain is serial
+  uint32_t in = start + 1 < end ? sval[start + 1] : 0u;
+  uint64_t cin = start + 1 < end ? ccnt[in] : 0u;
+  double Sn[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) Sn[c] = start + 1 < end ? S1[(int64_t)in * D + c] : 0.0;
   for (int j = start + 1; j < end; ++j) {
-    const uint32_t i = sval[j];
-    const uint64_t ci = ccnt[i];
+    const uint64_t ci = cin;
+    double Si[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) Si[c] = Sn[c];
+    if (j + 1 < end) {
+      in = sval[j + 1];
+      cin = ccnt[in];
+#pragma unroll
+      for (int c = 0; c < D; ++c) Sn[c] = S1[(int64_t)in * D + c];
+    }
     const double a = (double)cnt, w = (double)ci, tot = (double)(cnt + ci);
     const double y = __drcp_rn(tot);
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      const double num = __dadd_rn(__dmul_rn(a, s[c]), __dmul_rn(w, S1[(int64_t)i * D + c]));
+      const double num = __dadd_rn(__dmul_rn(a, s[c]), __dmul_rn(w, Si[c]));
       const double fa = fabs(num);
       slow |= !(fa < 0x1p+1000) || (fa < 0x1p-900 && num != 0.0);
       const double q0 = __dmul_rn(num, y);
@@ -733,23 +748,55 @@ __global__ void k_idx_set(int m, const uint32_t* __restrict__ key, int32_t* __re
 }
 
 // has_converged per frame: fadj[f] = 1 if some cell of f has another
-// active cell in its 1-neighbourhood.
+// active cell in its 1-neighbourhood.  D <= 6: batched probes from a shared offset table.
+template <int D>
 __global__ void k_adjacent(int m, GsBox b, int K, const uint32_t* __restrict__ key,
                            const int32_t* __restrict__ idx, const int32_t* __restrict__ fdone,
                            int32_t* __restrict__ fadj) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const int64_t L = key[i];
-  const int64_t f = L / b.vol_frame;
-  if (fdone[f]) return;
-  GsNbrOdometer od;
-  od.init(b);
-  for (int t = 0; t < K; ++t) {
-    if (od.off != 0 && idx[L + od.off] >= 0) {
-      fadj[f] = 1;
-      return;
+  if constexpr (D <= 6) {
+    constexpr int KMAX = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 : 729;
+    constexpr int B = KMAX < 27 ? KMAX : 27;
+    __shared__ int offs[KMAX];
+    for (int t = threadIdx.x; t < KMAX; t += blockDim.x) {
+      int r = t;
+      int64_t off = 0;
+      for (int c = D - 1; c >= 0; --c) {
+        off += (int64_t)(r % 3 - 1) * b.stride[c];
+        r /= 3;
+      }
+      offs[t] = (int)off;
     }
-    od.next(b);
+    __syncthreads();
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t L = key[i];
+    const int64_t f = L / b.vol_frame;
+    if (fdone[f]) return;
+    for (int t0 = 0; t0 < KMAX; t0 += B) {
+      int hit = 0;
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        hit |= (t0 + u != (KMAX - 1) / 2) & (__ldg(&idx[L + offs[t0 + u]]) >= 0);
+      if (hit) {
+        fadj[f] = 1;
+        return;
+      }
+    }
+  } else {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const int64_t L = key[i];
+    const int64_t f = L / b.vol_frame;
+    if (fdone[f]) return;
+    GsNbrOdometer od;
+    od.init(b);
+    for (int t = 0; t < K; ++t) {
+      if (od.off != 0 && idx[L + od.off] >= 0) {
+        fadj[f] = 1;
+        return;
+      }
+      od.next(b);
+    }
   }
 }
 
