@@ -243,7 +243,7 @@ gs_status gs_track_sequence(gs_tracker* t, const uint8_t* frames, int64_t T, int
  * < tol (SPEC default 1e-6*h) or after max_iter (SPEC default 300); clusters = points sharing a
  * final cell, ids by lexicographic key.  Pins M1-M5 (oracle/gs_oracle.cpp): results equal the
  * oracle's bit for bit.  One dataset (batch 1) of fp32/fp64 features, d <= 6, whose first grid
- * fits one CTA's shared memory (~2K cells at d = 3).  out->k/iterations/converged get one
+ * fits one CTA's shared memory (2,048 cells at d = 3).  out->k/iterations/converged get one
  * entry; disp_hist (nullable, max_iter entries) the per-iteration displacement;
  * gs_get_centroids(ctx, 0, ...) the final centroids. */
 gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, double tol, int32_t max_iter,

@@ -106,8 +106,9 @@ struct MsppArgs {
 
 template <int D>
 __host__ __device__ constexpr int mspp_bytes_per_slot() {
-  // particles: pos D, count, sort key, cell-of | cells: S D, S' D, count, key, qsum D | root
-  return 8 * D + 4 + 8 + 4 + 8 * D + 8 * D + 4 + 4 + 8 * D + 4;
+  // particles: pos D, count, sort key, cell-of | cells: S D, S' D (aliased by the qsums),
+  // count, key | root
+  return 8 * D + 4 + 8 + 4 + 8 * D + 8 * D + 4 + 4 + 4;
 }
 
 template <int D>
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(512, 1) k_mspp_loop(MsppArgs a) {
   double* pos = (double*)p;          p += 8 * (size_t)MS * D;
   double* S = (double*)p;            p += 8 * (size_t)MS * D;
   double* Sn = (double*)p;           p += 8 * (size_t)MS * D;
-  long long* qs = (long long*)p;     p += 8 * (size_t)MS * D;
+  long long* qs = (long long*)Sn;    // the re-grid's integer sums die before the update writes S
   uint64_t* sk = (uint64_t*)p;       p += 8 * (size_t)MS;
   uint32_t* pc = (uint32_t*)p;       p += 4 * (size_t)MS;
   int* cof = (int*)p;                p += 4 * (size_t)MS;

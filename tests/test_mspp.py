@@ -77,6 +77,7 @@ CASES = [
     ("maxiter1", lambda: CF.generate("cfg1")[0], 0.5, dict(max_iter=1)),
     ("maxiter2", lambda: CF.generate("cfg2")[0], 0.08, dict(max_iter=2)),
     ("bigtol", lambda: CF.generate("cfg1")[0], 0.5, dict(tol=10.0)),
+    ("cells1700", lambda: np.random.default_rng(6).random((20000, 3)), 0.09, {}),
 ]
 
 
@@ -108,3 +109,6 @@ def test_gpu_mspp_errors(engine):
     bad[1, 1] = np.inf
     with pytest.raises(G.InvalidInputError):
         engine.mspp(bad, 0.5)
+    # a first grid beyond one CTA (8,000 cells at d = 3) is refused, never approximated
+    with pytest.raises(G.InvalidParameterError):
+        engine.mspp(np.random.default_rng(7).random((50000, 3)), 0.05)
