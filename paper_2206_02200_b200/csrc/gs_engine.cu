@@ -1659,10 +1659,14 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
     MS /= 2;
     vol_small = 1;
   }
-  if (m0 > MS)
+  if (m0 > MS) {  // restore the clean grid (K3 indexed the first grid's cells) before refusing
+    gs::k_idx_clear<<<blocks_for(m0, 256), 256, 0, ctx->stream>>>(
+        (int)m0, ctx->ckey[0].as<uint32_t>(), ctx->idx.as<int32_t>());
+    GS_CK(cudaStreamSynchronize(ctx->stream));
     return fail(ctx, GS_E_INVALID_PARAMETER,
                 "MS++ baseline: the first grid (" + std::to_string((long long)m0) +
                     " cells) exceeds one CTA's shared memory (" + std::to_string(MS) + ")");
+  }
   GS_TRY(grow(ctx, ctx->S1, sizeof(double) * (size_t)m0 * d));
   GS_TRY(grow(ctx, ctx->dbg, 64 + sizeof(double) * (size_t)max_iter));
   GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 64, ctx->stream));

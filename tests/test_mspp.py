@@ -112,3 +112,7 @@ def test_gpu_mspp_errors(engine):
     # a first grid beyond one CTA (8,000 cells at d = 3) is refused, never approximated
     with pytest.raises(G.InvalidParameterError):
         engine.mspp(np.random.default_rng(7).random((50000, 3)), 0.05)
+    # ... and leaves the context's grid clean for the next run
+    X = CF.generate("cfg2")[0]
+    r = engine.run(X, G.EngineConfig(0.08, 100))
+    assert np.array_equal(r.labels, O.run(X.astype(np.float64), 0.08, 100, O.BUILD_FIXED)["labels"])
