@@ -282,7 +282,12 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     flag[i] = 0u;
   }
   // initial cells of this frame -> current frame-local cell (shared memory when they fit)
+  // initial cells of a big frame (icnt > MS) keep their map to the K8-entry cells in global
+  // memory; the per-iteration composition then runs over the entry cells in shared memory
+  // (rootl[x] = current cell of entry cell x) and is applied to the initial cells once, at
+  // the end (a per-iteration pass over cfg5's 45 K initial cells cost ~27 K cycles)
   const bool rsm = icnt <= MS;
+  const int m_entry = m;
   for (int c = tid; c < icnt; c += T) {
     const int r = a.root[ifirst + c] - first;
     if (rsm)
@@ -290,6 +295,8 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     else
       a.root[ifirst + c] = r;
   }
+  if (!rsm)
+    for (int x = tid; x < m_entry; x += T) rootl[x] = x;
   constexpr int K = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 :
                     D == 6 ? 729 : D == 7 ? 2187 : D == 8 ? 6561 : D == 9 ? 19683 :
                     D == 10 ? 59049 : D == 11 ? 177147 : 531441;
@@ -961,12 +968,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     }
     stamp(5);
     // member union (Eq. 4) as root composition
-    for (int c = tid; c < icnt; c += T) {
-      if (rsm)
-        rootl[c] = par[rootl[c]];
-      else
-        a.root[ifirst + c] = par[a.root[ifirst + c]];
-    }
+    for (int c = tid; c < (rsm ? icnt : m_entry); c += T) rootl[c] = par[rootl[c]];
     for (int i = tid; i < m; i += T) idx_put(key[i], -1);  // retire the old keys
     stamp(6);
     __syncthreads();
@@ -1034,8 +1036,16 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
     for (int c = 0; c < D; ++c) a.oS[(int64_t)(first + i) * D + c] = S0[i * D + c];
     if (!sdense) gidx[key[i]] = -1;  // clean-grid invariant for the next run
   }
-  for (int c = tid; c < icnt; c += T)
-    a.lab[a.initkey[ifirst + c]] = rsm ? rootl[c] : a.root[ifirst + c];
+  for (int c = tid; c < icnt; c += T) {
+    int r;
+    if (rsm) {
+      r = rootl[c];
+    } else {
+      r = rootl[a.root[ifirst + c]];
+      a.root[ifirst + c] = r;
+    }
+    a.lab[a.initkey[ifirst + c]] = r;
+  }
   if (tid == 0) {
     a.fk[f] = m;
     a.fiters[f] = iters;
