@@ -1,0 +1,67 @@
+"""Randomised GPU parity: seeded mixtures over d = 1..6, point counts, bandwidths, dtypes and
+batches, on the default schedule (K8 after the global path), on the global path only (the
+16-CTA cluster sweep for d <= 3, the dataflow sweep for d > 3), and as batched frames (the K2
+table replicas).  Every case must equal the fixed-point-build oracle bit for bit."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2206_02200_b200 import gridshift as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.int64)
+
+
+def _mixture(rng, n, d):
+    # (the key box must stay within the dense grid's 2^28 cells: a smaller span for d >= 5)
+    k = int(rng.integers(1, 9))
+    centres = rng.uniform(0.0, 4.0 if d <= 4 else 2.0, (k, d))
+    sig = rng.uniform(0.05, 0.6, (k, 1))
+    lab = rng.integers(0, k, n)
+    return centres[lab] + sig[lab] * rng.standard_normal((n, d))
+
+
+def _cases():
+    out = []
+    for seed in range(64):
+        rng = np.random.default_rng(1000 + seed)
+        d = int(rng.integers(1, 7))
+        n = int(rng.integers(50, 6000 if d <= 3 else 2500))
+        h = float(rng.uniform(0.15, 0.6) if d <= 4 else rng.uniform(0.35, 0.6))
+        f32 = bool(rng.integers(0, 2))
+        out.append((f"s{seed}-d{d}-n{n}", seed, d, n, h, f32))
+    return out
+
+
+def _check(engine, X, h, flags, name):
+    g = engine.run(X, G.EngineConfig(h, 300, record_history=True, debug_flags=flags))
+    o = O.run(X.astype(np.float64), h, 300, O.BUILD_FIXED)
+    assert g.iterations == o["iterations"], name
+    assert np.array_equal(g.labels, o["labels"]), f"{name}: labels"
+    assert np.array_equal(_bits(g.centroids), _bits(o["centroids"])), f"{name}: centroids"
+    assert g.history == o["history"], f"{name}: history"
+
+
+@pytest.mark.parametrize("name,seed,d,n,h,f32", _cases(), ids=[c[0] for c in _cases()])
+def test_fuzz_default_and_global(engine, name, seed, d, n, h, f32):
+    rng = np.random.default_rng(seed)
+    X = _mixture(rng, n, d).astype(np.float32 if f32 else np.float64)
+    _check(engine, X, h, 0, name)
+    _check(engine, X, h, G.GS_DEBUG_GLOBAL_PATH, name + "-global")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_batched_frames(engine, seed):
+    rng = np.random.default_rng(500 + seed)
+    B, n, d = int(rng.integers(2, 6)), int(rng.integers(200, 3000)), 3
+    h = float(rng.uniform(0.2, 0.5))
+    X = np.stack([_mixture(rng, n, d) for _ in range(B)]).astype(np.float32)
+    rb = engine.run_batch(X, G.EngineConfig(h, 300))
+    for f in range(B):
+        o = O.run(X[f].astype(np.float64), h, 300, O.BUILD_FIXED)
+        assert np.array_equal(rb.labels[f], o["labels"]), f"frame {f}"
+        assert rb.iterations[f] == o["iterations"]
+        assert np.array_equal(_bits(rb.centroids[f]), _bits(o["centroids"])), f"frame {f}"
