@@ -323,3 +323,29 @@ def test_graph_replay_after_other_calls(engine):
         eng.run(bad, G.EngineConfig(0.08, 100))
     replay()
     eng.close()
+
+
+def test_cfg5_full_size_bit_exact(engine):
+    """cfg5 at its full size (64 M points, one cloud): global path (cluster sweeps) then K8,
+    bit-exact against the fixed-point-build oracle (labels, centroids, iterations, history)."""
+    cfg = CF.CONFIGS["cfg5"]
+    X = CF.generate("cfg5")[0]
+    g = engine.run(X, G.EngineConfig(cfg.h, cfg.max_iter, record_history=True))
+    o = O.run(X.astype(np.float64), cfg.h, cfg.max_iter, O.BUILD_FIXED)
+    assert g.iterations == o["iterations"]
+    assert np.array_equal(g.labels, o["labels"])
+    assert np.array_equal(_bits(g.centroids), _bits(o["centroids"]))
+    assert g.history == o["history"]
+
+
+def test_cfg4_all_frames_bit_exact(engine):
+    """cfg4 at its full size (256 frames of 640 x 480) in one batched call; every frame vs the
+    oracle."""
+    cfg = CF.CONFIGS["cfg4"]
+    X = CF.generate("cfg4")
+    r = engine.run_batch(X, G.EngineConfig(cfg.h, cfg.max_iter))
+    for f in range(X.shape[0]):
+        o = O.run(X[f].astype(np.float64), cfg.h, cfg.max_iter, O.BUILD_FIXED)
+        assert r.k[f] == o["k"] and r.iterations[f] == o["iterations"], f
+        assert np.array_equal(r.labels[f], o["labels"]), f
+        assert np.array_equal(_bits(r.centroids[f]), _bits(o["centroids"])), f
