@@ -65,3 +65,20 @@ def test_fuzz_batched_frames(engine, seed):
         assert np.array_equal(rb.labels[f], o["labels"]), f"frame {f}"
         assert rb.iterations[f] == o["iterations"]
         assert np.array_equal(_bits(rb.centroids[f]), _bits(o["centroids"])), f"frame {f}"
+
+
+@pytest.mark.parametrize("d", [2, 5])
+def test_fuzz_batched_frames_global_path(engine, d):
+    """Batched frames on the forced global path (cluster sweep d <= 3, dataflow sweep d > 3),
+    frames finishing at different iterations (frozen frames' cells stay in the sweep)."""
+    rng = np.random.default_rng(900 + d)
+    B, n = 4, 1500
+    frames = [_mixture(rng, n, d) for _ in range(B - 1)] + [np.full((n, d), 0.25)]
+    X = np.stack(frames).astype(np.float64)
+    h = 0.45
+    rb = engine.run_batch(X, G.EngineConfig(h, 300, debug_flags=G.GS_DEBUG_GLOBAL_PATH))
+    for f in range(B):
+        o = O.run(X[f], h, 300, O.BUILD_FIXED)
+        assert rb.iterations[f] == o["iterations"], f
+        assert np.array_equal(rb.labels[f], o["labels"]), f
+        assert np.array_equal(_bits(rb.centroids[f]), _bits(o["centroids"])), f
