@@ -1,14 +1,15 @@
 """GridShift hot-path benchmark (driver contract).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
 
 A step = one engine.run over one batch of the workload's synthetic input.
 `value` is whole-job points/s with the points already resident in HBM (device outputs);
 `e2e` is the same metric through the C-ABI with pinned HOST buffers, the H2D copy of the
 points and the D2H copy of the labels inside the timed region.  Each timed step is bracketed
 by CUDA events on the engine's stream; the L2 is flushed (512 MiB write) before every step.
-Under torchrun each rank clusters its own independent image(s) (frame sharding, no
-collective on the data path) and the time is the max over ranks.
+The default workload is cfg4, the largest single-GPU config: 256 frames of 640 x 480 colour
+features.  Under torchrun the 256 frames are split into contiguous frame shards (strong scaling,
+no collective on the data path) and the time is the max over ranks.
 `--impl reference` times the CPU oracle (the reference algorithm restated, oracle/) on all
 host threads instead, rank 0 only.
 """
@@ -86,89 +87,144 @@ class ClockSampler:
                 "samples": len(busy)}
 
 
-# K2 dram bytes (read + write) per launch, ncu --set full of the current K2
-# (profiles/r1_ncu_kernels.md, session-2 captures)
-NCU_TRAFFIC = {"cfg2": 1_900_288, "cfg4": 952_078_592 + 298_366_208,
-               "cfg5": 771_519_744 + 237_712_896}
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
-def workload_input(name: str, rank: int):
+def csrc_hash() -> str:
+    """Hash of the product kernel sources: a committed ncu traffic figure is only reported for
+    the sources it was captured from."""
+    import hashlib
+    d = os.path.join(ROOT, "paper_2206_02200_b200", "csrc")
+    hs = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".cpp")):
+            with open(os.path.join(d, f), "rb") as fh:
+                hs.update(f.encode() + fh.read())
+    return hs.hexdigest()[:16]
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """dram read+write bytes of one launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json, written by scripts/ncu_traffic.py on the GPU box); None when there
+    is no capture of the current kernel sources."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[workload][kernel]
+        if e["csrc_hash"] != csrc_hash():
+            return None, f"stale: captured from csrc {e['csrc_hash']} ({e['capture']})"
+        return int(e["dram_bytes"]), f"{e['capture']} (csrc {e['csrc_hash']})"
+    except (OSError, KeyError, ValueError):
+        return None, "no capture"
+
+
+def config_dict(name: str, input_kind: str = "features"):
+    """The workload description, identical in both arms (--impl ours / reference)."""
     from paper_2206_02200_b200 import configs as CF
     cfg = CF.CONFIGS[name]
-    if name == "cfg2":   # each rank its own independent image (seeded per rank)
-        X = CF.voronoi_rgb(seed=2208 + 1000 * rank)[None]
-    elif name == "cfg4":
-        X = CF.generate("cfg4", frames=cfg.batch, frame0=rank * cfg.batch)
-    else:
+    return {"workload": name, "desc": cfg.desc, "n": cfg.n, "d": cfg.d, "batch": cfg.batch,
+            "h": cfg.h, "max_iter": cfg.max_iter,
+            "input_dtype": "u8 rgb pixels" if input_kind == "u8" else cfg.dtype}
+
+
+def workload_input(name: str, rank: int, world: int):
+    """This rank's share of the workload.  cfg4: the 256 frames split into contiguous frame
+    shards (strong scaling, no collective on the data path); cfg5 under torchrun: a contiguous
+    point shard of the one cloud; cfg1-3: replicas (each rank its own copy)."""
+    from paper_2206_02200_b200 import configs as CF
+    from paper_2206_02200_b200.dist import frame_shard, point_shard
+    cfg = CF.CONFIGS[name]
+    if name == "cfg4":
+        f0, cnt = frame_shard(cfg.batch, world, rank)
+        return cfg, CF.generate("cfg4", frames=cnt, frame0=f0), "strong"
+    if name == "cfg5" and world > 1:
         X = CF.generate(name)
-    return cfg, X
+        p0, cnt = point_shard(X.shape[1], world, rank)
+        return cfg, np.ascontiguousarray(X[:, p0:p0 + cnt]), "strong"
+    if name == "cfg2":  # replicas: each rank its own independent image (seeded per rank)
+        return cfg, CF.voronoi_rgb(seed=2208 + 1000 * rank)[None], "weak"
+    return cfg, CF.generate(name), "weak"
+
+
+def oracle_frames(frames, h, max_iter, threads, budget_s=None):
+    """Independent oracle runs (SPEC-literal build) of `frames` over `threads` host threads
+    (one GridShift run is sequential; ctypes releases the GIL).  Repeats the
+    whole set until budget_s is spent (at least once).  Returns (points/s, points, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import oracle as O
+    pts, secs = 0, 0.0
+    with ThreadPoolExecutor(threads) as ex:
+        while True:
+            t0 = time.perf_counter()
+            list(ex.map(lambda x: O.run(x, h, max_iter, O.BUILD_SPEC), frames))
+            secs += time.perf_counter() - t0
+            pts += sum(x.shape[0] for x in frames)
+            if budget_s is None or secs >= budget_s:
+                break
+    return pts / secs, pts, secs
 
 
 def cpu_baseline(name: str, X: np.ndarray, h: float, max_iter: int, budget_s: float = 10.0):
-    """The oracle (SPEC-literal build) on one host core over a bounded sample of the workload."""
-    from oracle import oracle as O
-    frames = X.shape[0]
-    times, pts = [], 0
-    t_end = time.perf_counter() + budget_s
-    f = 0
-    cap = 4_000_000  # bounded sample: frames above 4M points are clustered on a prefix
-    while True:
-        x = np.ascontiguousarray(X[f % frames][:cap], np.float64)
-        t0 = time.perf_counter()
-        O.run(x, h, max_iter, O.BUILD_SPEC)
-        times.append(time.perf_counter() - t0)
-        pts += x.shape[0]
-        f += 1
-        if time.perf_counter() > t_end:
-            break
-    return {"value": pts / sum(times), "unit": "points/s", "cores": 1, "kind": "port",
-            "sample": f"{f} oracle runs of {name} frames ({pts} points, {sum(times):.1f} s, "
-                      f"SPEC-literal build, 1 thread"
-                      + (f", first {cap} points of each frame)" if X.shape[1] > cap else ")")}
+    """The oracle (SPEC-literal build) on this box's host cores over a bounded sample of the
+    workload: every frame on all cores (repeated to ~budget_s), plus a 1-core figure."""
+    hi = host_info()
+    cores = hi["nproc"] or 1
+    frames = [np.ascontiguousarray(X[f], np.float64) for f in range(X.shape[0])]
+    threads = max(1, min(cores, len(frames)))
+    v_all, pts, secs = oracle_frames(frames, h, max_iter, threads, budget_s)
+    v_one, pts1, secs1 = oracle_frames(frames[:max(1, min(len(frames), 8))], h, max_iter, 1)
+    return {"value": v_all, "unit": "points/s", "cores": threads, "kind": "port",
+            "sample": f"{name}: {len(frames)} frame(s) of {X.shape[1]} points as independent "
+                      f"oracle runs (SPEC-literal build) on {threads} thread(s), {pts} points in "
+                      f"{secs:.1f} s",
+            "single_core": {"value": v_one, "points": pts1, "seconds": round(secs1, 2)},
+            "host": hi}
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle (the reference's algorithm; the reference itself has no
-    code) on this arm's workload: the same frames, as independent runs spread over the host
-    threads -- one GridShift run is sequential, so a single frame uses one thread.
-    Rank 0 only.  Frames above 4M points are timed on a bounded prefix sample."""
+    code) on this arm's workload: the same frames, each step all of them as independent runs
+    spread over every host thread -- one GridShift run is sequential, so a
+    single-cloud workload (cfg5) runs on one thread.  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import oracle as O
-    cfg, X = workload_input(args.workload, 0)
+    from paper_2206_02200_b200 import configs as CF
+    cfg = CF.CONFIGS[args.workload]
+    X = CF.generate(args.workload)
     B, n = X.shape[0], X.shape[1]
-    cap = 4_000_000
-    frames = [np.ascontiguousarray(X[f][:cap], np.float64) for f in range(B)]
-    pts_step = sum(x.shape[0] for x in frames)
-    threads = max(1, min(os.cpu_count() or 1, B))
-
-    def one(f):
-        O.run(frames[f], cfg.h, cfg.max_iter, O.BUILD_SPEC)
-
-    from concurrent.futures import ThreadPoolExecutor
-    pool = ThreadPoolExecutor(threads)
+    frames = [np.ascontiguousarray(X[f], np.float64) for f in range(B)]
+    del X
+    hi = host_info()
+    threads = max(1, min(hi["nproc"] or 1, B))
     step_times = []
     for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        list(pool.map(one, range(B)))
-        dt = time.perf_counter() - t0
+        _, _, dt = oracle_frames(frames, cfg.h, cfg.max_iter, threads)
         if s >= args.warmup:
             step_times.append(dt)
     total = sum(step_times)
-    value = pts_step * args.steps / total
-    sample = (f"per step the workload's {B} frame(s) as independent oracle runs (SPEC-literal "
-              f"build) on {threads} thread(s)"
-              + (f", first {cap} points of each frame" if n > cap else ""))
+    value = B * n * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.workload in ("cfg4", "cfg5") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "n": n, "d": cfg.d, "h": cfg.h,
-                   "max_iter": cfg.max_iter, "batch": B},
+        "config": config_dict(args.workload),
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": f"per step all {B} frame(s) of {n} points as independent "
+                                   f"oracle runs (SPEC-literal build) on {threads} thread(s)",
+                         "host": hi},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -495,13 +551,14 @@ def run_mspp(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="cfg2",
+    ap.add_argument("--workload", default="cfg4",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tune", "track", "mspp"],
-                    help="tune: the bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image; "
-                         "track: the tracker (§8(f)3) over the cfg4 frames; mspp: the MS++ "
-                         "baseline (§8(f)4) on the cfg2 image")
+                    help="default cfg4: the largest single-GPU config (256 frames). tune: the "
+                         "bandwidth sweep (SURVEY.md §8(f)2) over the cfg2 image; track: the "
+                         "tracker (§8(f)3) over the cfg4 frames; mspp: the MS++ baseline "
+                         "(§8(f)4) on the cfg2 image")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -532,15 +589,12 @@ def main():
     stream = torch.cuda.Stream(device=dev)  # the engine and the timing events share it
     eng = G.Engine(local, stream.cuda_stream)
 
-    cfg, X = workload_input(args.workload, rank)
+    cfg, X, scaling = workload_input(args.workload, rank, world)
     # cfg5 over several GPUs: ONE cloud split into contiguous point shards (dist.run_cloud:
     # partial cells all-gathered, identical iteration on every rank, own points labelled)
     shard_cloud = args.workload == "cfg5" and world > 1
-    n_global = X.shape[1]
     if shard_cloud:
-        from paper_2206_02200_b200.dist import point_shard, run_cloud
-        p0, cnt_local = point_shard(n_global, world, rank)
-        X = np.ascontiguousarray(X[:, p0:p0 + cnt_local])
+        from paper_2206_02200_b200.dist import run_cloud
     if args.input == "u8":
         if args.workload not in ("cfg2", "cfg4") or shard_cloud:
             raise SystemExit("--input u8 applies to the image workloads cfg2 and cfg4")
@@ -550,6 +604,7 @@ def main():
     # timed steps record only the binning kernel's CUDA events (the roofline's kernel time);
     # the per-phase times come from a separate, untimed diagnostic pass (events cost ~30 us)
     econf = G.EngineConfig(cfg.h, cfg.max_iter, debug_flags=G.GS_TIME_KERNEL)
+    econf_e2e = G.EngineConfig(cfg.h, cfg.max_iter)
     econf_phases = G.EngineConfig(cfg.h, cfg.max_iter, debug_flags=G.GS_TIME_PHASES)
     X_host = torch.from_numpy(X).pin_memory()
     X_dev = X_host.to(dev)
@@ -565,8 +620,8 @@ def main():
         if device_resident:
             eng.run_raw(X_dev.data_ptr(), n, d, dt, B, True, conf, labels_dev.data_ptr(),
                         device_outputs=True)
-        else:
-            eng.run_raw(X_host.data_ptr(), n, d, dt, B, False, econf, labels_host.data_ptr())
+        else:  # the public call from pinned host memory (frame-group pipeline for batches)
+            eng.run_raw(X_host.data_ptr(), n, d, dt, B, False, econf_e2e, labels_host.data_ptr())
 
     def timed(device_resident: bool, steps: int):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -604,11 +659,16 @@ def main():
     torch.cuda.synchronize()
 
     tot_dev, tot_e2e = sum(ms_dev), sum(ms_e2e)
+    pts_rank = B * n * args.steps
     if world > 1:
         t = torch.tensor([tot_dev, tot_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_dev, tot_e2e = t.tolist()
-    pts_all = (n_global if shard_cloud else world * B * n) * args.steps
+        p = torch.tensor([float(pts_rank)], dtype=torch.float64, device=dev)
+        dist.all_reduce(p, op=dist.ReduceOp.SUM)
+        pts_all = cfg.n * args.steps if shard_cloud else int(p.item())
+    else:
+        pts_all = pts_rank
     value = pts_all / (tot_dev / 1e3)
     e2e = pts_all / (tot_e2e / 1e3)
     # cells x iterations (Σ m_t) per second over the iteration phase
@@ -616,71 +676,78 @@ def main():
     cells = sum(s["cells_swept"] for s in st_dev)
     it_ms = float(np.mean([s["ms_iterate"] for s in st_phase])) * len(st_dev)
     launches = int(np.median([s["kernel_launches"] for s in st_dev]))
+    launches_e2e = int(np.median([s["kernel_launches"] for s in st_e2e]))
     lib_calls = int(np.median([s["lib_calls"] for s in st_dev]))
 
     # roofline of the n-scale binning kernel K2: algorithmic bytes = points read + slot write
     peak, peak_kind = peaks()
     s_in = {G.GS_F32: 4, G.GS_F64: 8, G.GS_U8: 1}[dt]
+    slot_b = int(s0.get("slot_bytes", 4) or 4)
     kbin_ms = float(np.mean([s["ms_k_bin"] for s in st_dev]))
-    kbin_bytes = B * n * (d * s_in + 4)
+    kbin_bytes = B * n * ((3 if dt == G.GS_U8 else d * s_in) + slot_b)
     kbin_gbs = kbin_bytes / (kbin_ms / 1e3) / 1e9
     phase = {k: float(np.mean([s[k] for s in st_phase]))
              for k in ("ms_bin", "ms_iterate", "ms_label", "ms_k_bin", "ms_k_label")}
     phase["note"] = "untimed diagnostic pass with all phase events; timed steps record K2 only"
-    dominant = max(("binning phase (K1+K2+K3)", phase["ms_bin"]),
-                   ("iteration phase (K4+K5)", phase["ms_iterate"]),
+    dominant = max(("binning phase (K2+K3)", phase["ms_bin"]),
+                   ("iteration phase (K8 / global path)", phase["ms_iterate"]),
                    ("label phase (K7)", phase["ms_label"]), key=lambda x: x[1])[0]
-    # the dominant kernel of the step: when the iteration phase dominates (the image-sized
-    # workloads) it is K8 / the cluster sweep, latency-bound by the Gauss-Seidel sweep's DAG
-    # depth, so its HBM fraction is tiny by construction; else the binning kernel K2
-    it_bytes = int(s0["cells_swept"] * (24 + 16 * d))  # B_c = 24 + 16d (SURVEY.md 8(d))
+    # whole-step algorithmic bytes: n (d s_in + 4) + Σ m_t (24 + 16 d)
+    it_bytes = int(s0["cells_swept"] * (24 + 16 * d))  # B_c = 24 + 16d
+    step_bytes = B * n * ((3 if dt == G.GS_U8 else d * s_in) + 4) + it_bytes
+    step_ms = tot_dev / args.steps
     if phase["ms_iterate"] >= phase["ms_bin"] and phase["ms_iterate"] > 0:
         ach = it_bytes / (phase["ms_iterate"] / 1e3) / 1e9
         dominant_roofline = {
-            "kernel": "k_resident (K8) / k_sweep_cluster: the iteration phase",
+            "kernel": "k_resident (K8) / global-path sweeps: the iteration phase",
             "bound": "latency (sweep DAG depth x per-level round trips), not hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "algorithmic_bytes": it_bytes, "ms": phase["ms_iterate"],
             "note": "sum over the run of m_t x (24 + 16d) bytes / iteration-phase time"}
     else:
         dominant_roofline = {"kernel": "k_bin (K2 binning)", "same_as": "roofline"}
+    traffic, traffic_src = (ncu_traffic(args.workload, "k_bin")
+                            if not shard_cloud and args.input == "features" else (None, "n/a"))
     out = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_dev / args.steps,
-        "higher_is_better": True, "scaling": "strong" if shard_cloud else "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "desc": cfg.desc, "n": n, "d": d, "batch": B,
-                   "h": cfg.h, "max_iter": cfg.max_iter,
-                   "input_dtype": {4: "f32", 8: "f64", 1: "u8 rgb pixels"}[s_in],
-                   "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": (f"one cloud in {world} point shards (partial cells "
-                                   f"all-gathered, replicated iteration)") if shard_cloud else
-                                  f"frames x{world} (independent images per rank)"},
+        "config": config_dict(args.workload, args.input),
+        "l2": "flushed (512 MiB write) before every timed step",
+        "parallelism": (f"one cloud in {world} point shards (partial cells all-gathered, "
+                        f"replicated iteration)") if shard_cloud else
+                       (f"{B} of the {cfg.batch} frames on this rank (frame shards x{world})"
+                        if args.workload == "cfg4" else f"replicas x{world}"),
         "cell_updates_per_s": cells / (it_ms / 1e3) if it_ms > 0 else None,
         "cells_swept_per_step": s0["cells_swept"], "m0": s0["m0"], "k": s0["k_total"],
         "iterations": s0["max_iterations"],
         "phase_ms": phase, "dominant_phase": dominant,
         "roofline": {"kernel": "k_bin (K2 binning)", "bound": "hbm", "achieved": kbin_gbs,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": kbin_gbs / peak,
-                     # dram read+write of one K2 launch from the committed ncu --set full
-                     # capture of this workload (profiles/r1_ncu_kernels.md), or null
-                     "traffic": (NCU_TRAFFIC.get(args.workload)
-                                 if not shard_cloud and args.input == "features" else None),
-                     "algorithmic_bytes": kbin_bytes},
-        # the dominant kernel of the step: on the image-sized workloads the iteration phase
-        # (K8 / the cluster sweep) -- latency-bound by the Gauss-Seidel sweep's DAG depth, so
-        # its HBM fraction is tiny by construction; reported beside the K2 roofline above
+                     "frac": kbin_gbs / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": kbin_bytes,
+                     "bytes_per_point": (3 if dt == G.GS_U8 else d * s_in) + slot_b,
+                     "ms": kbin_ms},
+        "roofline_step": {"achieved": step_bytes / (step_ms / 1e3) / 1e9, "peak": peak,
+                          "unit": "GB/s", "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak,
+                          "algorithmic_bytes": step_bytes,
+                          "note": "whole step: n (d s_in + 4) + sum_t m_t (24 + 16 d) bytes"},
         "roofline_dominant": dominant_roofline,
         "e2e": {"value": e2e, "unit": "points/s", "h2d_bytes_per_step": int(X.nbytes),
-                "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps},
+                "d2h_bytes_per_step": int(B * n * 4), "ms_per_step": tot_e2e / args.steps,
+                "gpu_launches": launches_e2e,
+                "path": "gs_run from pinned host memory" +
+                        (" (frame-group pipeline)" if B >= 4 and X.nbytes >= (64 << 20) else "")},
         "gpu_launches": launches, "lib_calls": lib_calls,
         "sweep_modes": s0.get("sweep_modes"), "resident_cycles": s0.get("resident_cycles"),
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args.workload, X, cfg.h, cfg.max_iter, args.cpu_budget)
+        Xc = X if X.dtype != np.uint8 else X.astype(np.float64) / 255.0
+        out["cpu_baseline"] = cpu_baseline(args.workload, Xc, cfg.h, cfg.max_iter,
+                                           args.cpu_budget)
     if rank == 0:
         print(json.dumps(out))
     eng.close()

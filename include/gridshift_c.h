@@ -67,7 +67,12 @@ typedef struct {
 #define GS_DEVICE_OUTPUTS 0x2u  /* result.labels is a device pointer                          */
 #define GS_TIME_PHASES 0x4u    /* record phase events: gs_stats ms_* (costs ~30 us per run)  */
 #define GS_TIME_KERNEL 0x8u    /* record the binning kernel's events only: gs_stats ms_k_bin  */
+#define GS_NO_PIPELINE 0x10u     /* host frames: one whole-batch copy, no frame-group pipeline  */
 #define GS_DEBUG_GLOBAL_PATH 0x80000000u /* test hook: iterate on the multi-CTA path only */
+#define GS_DEBUG_PIPELINE 0x40000000u   /* test hook: pipeline host frames in groups of 2 */
+#define GS_DEBUG_SWEEP_FLOW 0x20000000u   /* test hook: global path sweeps use the dataflow sweep */
+#define GS_DEBUG_SWEEP_LEVELS 0x10000000u /* test hook: level-synchronous cluster sweep only */
+#define GS_DEBUG_SWEEP_SINGLE 0x08000000u /* test hook: the single-CTA sweep only */
 
 /* EngineConfig. */
 typedef struct {
@@ -98,7 +103,11 @@ gs_status gs_create(int device, void* cuda_stream, gs_ctx** out);
 void gs_destroy(gs_ctx* ctx);
 
 /* engine.run over every frame of `in`.  Synchronous w.r.t. the caller:
- * on return the result buffers are filled. */
+ * on return the result buffers are filled.  Host-resident batches of several frames larger
+ * than 64 MB are pipelined by frame groups (unless GS_NO_PIPELINE): the copy of group g+1
+ * overlaps the clustering of group g and the label write-back of group g-1; results are
+ * identical (frames are independent).  After such a run gs_render serves only
+ * the frames of the last group. */
 gs_status gs_run(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out);
 
 /* Cluster centroids of `frame` from the last gs_run: k x d fp64 in cluster-id order. */
@@ -132,6 +141,8 @@ typedef struct {
                             inline lookups */
   int64_t resident_cycles[8]; /* K8 SM cycles per phase with GS_PROF set (lists, sweep, rehome,
                                  sort, merge, converged, first sweep, load), summed over frames */
+  int32_t slot_bytes;     /* bytes per point of the point -> cell map (2: frames of <= 65536 cells) */
+  int32_t predicted_box;  /* 1: binned against the previous run's key box (no bounds pass)   */
 } gs_stats;
 gs_status gs_get_stats(gs_ctx* ctx, gs_stats* out);
 

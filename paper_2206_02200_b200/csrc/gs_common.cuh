@@ -10,6 +10,11 @@
 #define GS_APRON 2       // empty cells around the data key box on each side, every dim
 #define GS_DMAX 12
 
+// error bits (errflag[0]): 1 non-finite input, 2 point outside the key box (invariant), 4
+// centroid left the box, 8 watchdog, 16 frame beyond K8's capacity, 32 key box larger than the
+// grid, 64 keys beyond the int64 range, 128 point outside the PREDICTED box (rerun with bounds)
+constexpr int GS_ERR_SKIP = 1 | 32 | 64 | 128;  // binning did not complete: later kernels skip
+
 // The IEEE division as an out-of-line call for the rare-operand fallbacks of the reciprocal
 // divisions: inlined, the compiler if-converts it and runs its whole ~12-op FP64 sequence
 // speculatively on the common path (measured ~150 cycles per sweep level on a lone warp).
@@ -109,6 +114,13 @@ __device__ __forceinline__ double gs_fix_centroid(int64_t k, long long qsum, uin
   double base = __dmul_rn((double)k, h);
   double mq = __ddiv_rn(__ll2double_rn(qsum), (double)count);
   return __dadd_rn(base, __dmul_rn(mq, inv_scale));
+}
+
+// slot[] readers: a point's dense grid cell.  slot holds u16 frame-local cells when the frame
+// volume fits 16 bits (image frames: half the bytes), else u32 global cells.
+__device__ __forceinline__ uint32_t gs_slot_cell(const void* slot, bool s16, int64_t p,
+                                                 uint32_t fbase) {
+  return s16 ? fbase + ((const uint16_t*)slot)[p] : ((const uint32_t*)slot)[p];
 }
 
 // Key of dim c of a linear cell index (within its frame).

@@ -11,7 +11,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +61,41 @@ unsigned blocks_for(int64_t n, int threads, int64_t cap = 1 << 20) {
   if (b < 1) b = 1;
   if (b > cap) b = cap;
   return (unsigned)b;
+}
+
+// Diagnostics and schedule overrides read from the environment exist only in debug builds
+// (-DGS_DEBUG_KNOBS); the product library reads no environment variables.
+const char* knob(const char* name) {
+#ifdef GS_DEBUG_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+// Kernel attributes (dynamic shared memory above 48 KB, non-portable cluster sizes) are per
+// device: each launcher keeps a bitmask of the devices it has configured, set under a lock so a
+// concurrent context (gs_tune's worker threads) never launches before the attribute is in.
+std::mutex g_attr_mu;
+
+template <typename K>
+cudaError_t attr_once(std::atomic<uint64_t>& mask, int dev, K* kernel, int smem,
+                      bool nonportable_cluster = false, bool* cluster_ok = nullptr) {
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  if (nonportable_cluster) {
+    const bool ok = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                         1) == cudaSuccess;
+    cudaGetLastError();
+    if (cluster_ok) *cluster_ok = ok;
+  }
+  mask.fetch_or(bit, std::memory_order_release);
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -138,9 +175,10 @@ struct gs_ctx {
     uint32_t flags = 0;
     int on_device = 0;
     uint64_t gen = 0;
+    uint64_t pbox_gen = 0;  // the predicted box baked into the graph (~0: bounds pass)
     bool operator==(const GraphKey& o) const {
       return shape == o.shape && points == o.points && labels == o.labels && flags == o.flags &&
-             on_device == o.on_device && gen == o.gen;
+             on_device == o.on_device && gen == o.gen && pbox_gen == o.pbox_gen;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
@@ -157,6 +195,27 @@ struct gs_ctx {
   std::vector<std::vector<int64_t>> hist_m;
   std::vector<std::vector<double>> hist_d;
   bool have_run = false;
+  // frame-group pipeline (gs_run on host frames): the copy stream stages group g+1 while
+  // group g runs; the per-frame centroids of the whole call are kept on the host
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[2] = {};
+  DevBuf stage[2];
+  bool grouped = false;
+  int64_t group_f0 = 0;
+  // predicted key box: the box of the last successful run of this (n, frames, d, dtype, h)
+  // replaces the bounds pass (K2 flags any point outside it and the run is redone)
+  bool pbox_valid = false;
+  GsBox pbox{};
+  int64_t pbox_n = 0, pbox_nf = 0;
+  int pbox_d = 0, pbox_dtype = 0, pbox_w = 0;
+  double pbox_h = 0;
+  uint64_t pbox_gen = 0;
+  int predicted = 0;      // this launch of K2 bins against the predicted box
+  uint32_t sweep_flags = 0;  // GS_DEBUG_SWEEP_* of the current run
+  // per-context sweep schedule (a cluster shape the device refused is not retried)
+  bool flow_ok = true, cluster16_ok = true, cluster_ok = true;  // first frame of the last group (its slot/label state is live)
+  std::vector<double> g_cent;
+  std::vector<int64_t> g_cent_off;
   gs_stats stats{};
   bool stats_times_pending = false;
   unsigned ev_mask = 0;  // which phase events this run records
@@ -269,7 +328,8 @@ gs_status ensure_dense(gs_ctx* ctx, int64_t cells, int d) {
   GS_TRY(grow(ctx, ctx->cnt, sizeof(uint32_t) * cap));
   GS_TRY(grow(ctx, ctx->qs, sizeof(unsigned long long) * cap * qd));
   GS_TRY(grow(ctx, ctx->idx, sizeof(int32_t) * cap));
-  GS_TRY(grow(ctx, ctx->lab, sizeof(int32_t) * cap));
+  // (+65536: a u16 slot left by an aborted run can reach past the last frame; K7 reads it)
+  GS_TRY(grow(ctx, ctx->lab, sizeof(int32_t) * (cap + 65536)));
   GS_CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(uint32_t) * cap, ctx->stream));
   GS_CK(cudaMemsetAsync(ctx->qs.p, 0, sizeof(unsigned long long) * cap * qd, ctx->stream));
   GS_CK(cudaMemsetAsync(ctx->idx.p, 0xff, sizeof(int32_t) * cap, ctx->stream));
@@ -441,25 +501,16 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
         ctx->epoch_dev.as<unsigned>(), img_w, copy);
     GS_LAUNCHED("k_bounds_box");
   } else {
-    // privatised binning: one 768-thread CTA per SM at most, >= 1024 points per CTA; the
-    // table sized to the CTA's points (2 entries per point, at least 256)
-    constexpr int TBL_MAX = gs::bin_table_entries<D>();
+    // privatised binning: one 1024-thread CTA per SM at most, >= 1024 points per CTA
     const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
-    const int64_t per_cta = (ntot + grid - 1) / grid;
-    const int TBL = (int)std::max<int64_t>(256, std::min<int64_t>(TBL_MAX, (2 * per_cta + 31) & ~31ll));
-    const size_t smem = (size_t)TBL * (8 * D + 8);
-    static bool configured = false;
-    if (!configured) {
-      const int smax = (int)((size_t)TBL_MAX * (8 * D + 8));
-      GS_CK(cudaFuncSetAttribute(gs::k_bin_priv<D, T>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-      configured = true;
-    }
-    gs::k_bin_priv<D, T><<<grid, 768, smem, ctx->stream>>>(
+    static std::atomic<uint64_t> done{0};
+    GS_CK(attr_once(done, ctx->device, gs::k_bin<D, T>, gs::kBinSmemBytes));
+    const int hash_rep = ctx->bin_rep_log2;
+    gs::k_bin<D, T><<<grid, gs::kBinThreads, gs::kBinSmemBytes, ctx->stream>>>(
         (const T*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-        ctx->qs.as<unsigned long long>(), ctx->slot.as<uint32_t>(), ctx->errflag.as<int>(),
-        TBL, img_w, ctx->bin_rep_log2);
-    GS_LAUNCHED("k_bin_priv");
+        ctx->qs.as<unsigned long long>(), ctx->slot.p, ctx->errflag.as<int>(), img_w,
+        ctx->predicted, 4, hash_rep);
+    GS_LAUNCHED("k_bin");
   }
   return GS_OK;
 }
@@ -527,14 +578,14 @@ gs_status clean_ctl(gs_ctx* ctx) {
 // per-frame first indices).  Errors (non-finite input, key box beyond the grid) surface in
 // errflag at the next sync.  vol_hint sizes the compaction grid (any value is correct).
 gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t n, int64_t nf,
-                        double h, int64_t vol_hint = 0) {
+                        double h, int64_t vol_hint = 0, const GsBox* pbox = nullptr) {
   cudaStream_t st = ctx->stream;
   const int64_t ntot = n * nf;
   const unsigned nblk = blocks_for(ntot, 256 * 4, (int64_t)ctx->num_sms * 4);
   // batched frames (images): few distinct cells per warp -> 4 lane-chosen replicas per cell
   // in K2's table (GS_BIN_REPLICAS overrides: 0, 1 or 2 = log2 of the replica count)
   {
-    const char* v = getenv("GS_BIN_REPLICAS");
+    const char* v = knob("GS_BIN_REPLICAS");
     ctx->bin_rep_log2 = v ? std::max(0, std::min(2, atoi(v))) : (nf > 1 ? 2 : 0);
   }
   GS_TRY(grow(ctx, ctx->bpart, sizeof(double) * nblk * d * 2));
@@ -554,9 +605,17 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   }
   GS_TRY(clean_ctl(ctx));
   ctx->ctl_clean = false;  // until K7 of this run re-zeroes it
-  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
+  if (pbox) {  // the predicted box: no bounds pass (K2 checks every point against it)
+    gs::k_box_set<<<1, 1, 0, st>>>(*pbox, ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>());
+    GS_LAUNCHED("k_box_set");
+  } else {
+    GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
+  }
+  ctx->predicted = pbox ? 1 : 0;
   GS_TRY(rec_event(ctx, 6));
-  GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk));
+  const gs_status sb = dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, false, nblk);
+  ctx->predicted = 0;
+  GS_TRY(sb);
   GS_TRY(rec_event(ctx, 7));
   unsigned* cnt32 = ctx->counters.as<unsigned>();
   const int64_t vt = vol_hint > 0 ? std::min(vol_hint, ctx->dense_cap) : ctx->dense_cap;
@@ -578,25 +637,21 @@ gs_status launch_sweep_levels_d(gs_ctx* ctx, int64_t m, const int32_t* eoff,
   constexpr size_t kBudget = 220 * 1024;
   const size_t stage = (size_t)1024 * D * 8;
   const int smem_cells = (int)std::min<int64_t>(m, (int64_t)((kBudget - stage) / 8));
-  if (getenv("GS_DEBUG_KAHN")) {
+  if (knob("GS_DEBUG_KAHN")) {
     GS_TRY(grow(ctx, ctx->dbg, 64));
     GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 32, ctx->stream));
   }
   const size_t smem = stage + (size_t)smem_cells * 8;
-  static bool configured = false;
-  if (!configured) {
-    GS_CK(cudaFuncSetAttribute(gs::k_sweep_kahn<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kBudget));
-    configured = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  GS_CK(attr_once(done, ctx->device, gs::k_sweep_kahn<D>, (int)kBudget));
   gs::k_sweep_kahn<D><<<1, 1024, smem, ctx->stream>>>(
       (int)m, smem_cells, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(), eoff, loff,
       ctx->erec.as<unsigned long long>(), ctx->lprod.as<double>(), ctx->lsucc.as<int32_t>(),
       ctx->den.as<uint32_t>(), ctx->rden.as<double>(), ctx->S[ctx->cur].as<double>(),
       ctx->S1.as<double>(), ctx->lvl.as<int>(), ctx->order.as<int>(),
-      getenv("GS_DEBUG_KAHN") ? (long long*)ctx->dbg.p : nullptr);
+      knob("GS_DEBUG_KAHN") ? (long long*)ctx->dbg.p : nullptr);
   GS_LAUNCHED("k_sweep_kahn");
-  if (getenv("GS_DEBUG_KAHN")) {
+  if (knob("GS_DEBUG_KAHN")) {
     long long h[4];
     GS_CK(cudaMemcpyAsync(h, ctx->dbg.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
     GS_CK(cudaStreamSynchronize(ctx->stream));
@@ -643,39 +698,23 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
   constexpr size_t kBudget = 220 * 1024;
   const size_t smem = 4 * ((size_t)(m + 3) / 4 + 1) + 2 * (size_t)m;
   const int in_smem = (m < 65536 && smem <= kBudget) ? 1 : 0;
-  static bool configured = false;
-  if (!configured) {
-    GS_CK(cudaFuncSetAttribute(gs::k_sweep_global<D>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
-    configured = true;
-  }
-  // the dataflow cluster sweep (no levels: a cell is updated as soon as its predecessors are);
-  // GS_SWEEP_FLOW=0 falls back to the level-synchronous cluster sweep below
+  static std::atomic<uint64_t> done_g{0}, done_f{0}, done_c{0};
+  GS_CK(attr_once(done_g, ctx->device, gs::k_sweep_global<D>, (int)kBudget));
+  const uint32_t dbg = ctx->sweep_flags;
+  // the dataflow cluster sweep (no levels: a cell is updated as soon as its predecessors are).
+  // measured: d = 5 (cfg3) 2.17 -> 1.85 ms per run; d = 3 (cfg5) 2.33 -> 2.45 ms (the per-hop
+  // fence + remote release costs more than the level barrier saves when a cell has <= 27
+  // terms), so d <= 3 keeps the level-synchronous sweep (test hooks force either)
   {
-    static int flow_env = -1;
-    if (flow_env < 0) {
-      const char* v = getenv("GS_SWEEP_FLOW");
-      flow_env = v ? atoi(v) : 1;
-    }
-    static int fl_cfg = 0;  // 1: 16-CTA clusters allowed, 2: refused
-    static const int flow_sleep = getenv("GS_FLOW_SLEEP") ? atoi(getenv("GS_FLOW_SLEEP")) : 0;
-    static const int flow_fence = getenv("GS_FLOW_FENCE") ? atoi(getenv("GS_FLOW_FENCE")) : 0;
-    // measured: d = 5 (cfg3) 2.17 -> 1.85 ms per run; d = 3 (cfg5) 2.33 -> 2.45 ms (the
-    // per-hop fence + remote release costs more than the level barrier saves when a cell has
-    // <= 27 terms), so d <= 3 keeps the level-synchronous sweep unless GS_SWEEP_FLOW=2
-    if (flow_env > 1 || (flow_env == 1 && D > 3)) {
-      int NC = 16;
-      if (!fl_cfg) {
-        GS_CK(cudaFuncSetAttribute(gs::k_sweep_flow<D>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
-        fl_cfg = cudaFuncSetAttribute(gs::k_sweep_flow<D>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                         cudaSuccess
-                     ? 1
-                     : 2;
-        cudaGetLastError();
-      }
-      if (fl_cfg != 1) NC = 8;
+    int flow_sel = (dbg & GS_DEBUG_SWEEP_FLOW) ? 2 : (dbg & (GS_DEBUG_SWEEP_LEVELS | GS_DEBUG_SWEEP_SINGLE)) ? 0 : 1;
+    if (const char* v = knob("GS_SWEEP_FLOW")) flow_sel = atoi(v);
+    const int flow_sleep = knob("GS_FLOW_SLEEP") ? atoi(knob("GS_FLOW_SLEEP")) : 0;
+    const int flow_fence = knob("GS_FLOW_FENCE") ? atoi(knob("GS_FLOW_FENCE")) : 0;
+    if (ctx->flow_ok && (flow_sel > 1 || (flow_sel == 1 && D > 3))) {
+      bool c16 = true;
+      GS_CK(attr_once(done_f, ctx->device, gs::k_sweep_flow<D>, (int)kBudget, true, &c16));
+      if (!c16) ctx->cluster16_ok = false;
+      const int NC = ctx->cluster16_ok ? 16 : 8;
       const size_t fsm = gs::sweep_flow_smem<D>((int)((m + NC - 1) / NC));
       if (fsm <= kBudget) {
         cudaLaunchConfig_t lc = {};
@@ -701,33 +740,25 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
           return GS_OK;
         }
         cudaGetLastError();
-        flow_env = 0;  // cannot be scheduled here: level-synchronous sweeps from now on
+        ctx->flow_ok = false;  // cannot be scheduled here: level-synchronous sweeps from now on
       }
     }
   }
   // the cluster sweep (NC CTAs on NC SMs, DSMEM pending counts and queues) when the owned
-  // share of 3 words per cell fits each CTA; GS_SWEEP_CLUSTER=0 forces the single-CTA sweep
+  // share of 3 words per cell fits each CTA; else the single-CTA sweep
   {
-    static int nc_env = -1;
-    if (nc_env < 0) {
-      const char* v = getenv("GS_SWEEP_CLUSTER");
-      nc_env = v ? atoi(v) : 16;
+    int NC = (dbg & GS_DEBUG_SWEEP_SINGLE) || !ctx->cluster_ok ? 0 : 16;
+    if (const char* v = knob("GS_SWEEP_CLUSTER")) NC = atoi(v);
+    if (NC > 8) {
+      bool c16 = true;
+      GS_CK(attr_once(done_c, ctx->device, gs::k_sweep_cluster<D>, (int)kBudget, true, &c16));
+      if (!c16) ctx->cluster16_ok = false;
+      if (!ctx->cluster16_ok) NC = 8;
+    } else if (NC >= 2) {
+      GS_CK(attr_once(done_c, ctx->device, gs::k_sweep_cluster<D>, (int)kBudget, true));
     }
-    int NC = nc_env;
     const size_t csmem = gs::sweep_cluster_smem<D>((int)((m + NC - 1) / std::max(NC, 1)));
-    static int cl_cfg = 0;  // 1: 16-CTA clusters allowed, 2: refused (use 8)
     if (NC >= 2 && csmem <= kBudget) {
-      if (!cl_cfg) {
-        GS_CK(cudaFuncSetAttribute(gs::k_sweep_cluster<D>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBudget));
-        cl_cfg = cudaFuncSetAttribute(gs::k_sweep_cluster<D>,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                         cudaSuccess
-                     ? 1
-                     : 2;
-        cudaGetLastError();
-      }
-      if (NC > 8 && cl_cfg != 1) NC = 8;
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3((unsigned)NC);
       lc.blockDim = dim3(gs::sweep_cluster_threads<D>());
@@ -741,7 +772,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       lc.attrs = at;
       lc.numAttrs = 1;
       long long* cprof = nullptr;
-      const bool ctrace = getenv("GS_TRACE_GLOBAL") != nullptr;
+      const bool ctrace = knob("GS_TRACE_GLOBAL") != nullptr;
       if (ctrace) {
         GS_TRY(grow(ctx, ctx->dbg, 8 * (1000 * 16 * 5 + 8)));
         GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * (1000 * 16 * 5 + 8), st));
@@ -784,11 +815,12 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
         return GS_OK;
       }
       cudaGetLastError();  // a cluster this size cannot be scheduled: single-CTA sweep below
-      nc_env = NC > 8 ? 8 : 0;
+      if (NC > 8) ctx->cluster16_ok = false;
+      else ctx->cluster_ok = false;
     }
   }
   long long* prof = nullptr;
-  const bool trace = getenv("GS_TRACE_GLOBAL") != nullptr;
+  const bool trace = knob("GS_TRACE_GLOBAL") != nullptr;
   if (trace) {
     GS_TRY(grow(ctx, ctx->dbg, 8 * (2000 * 66 + 8)));
     GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * (2000 * 66 + 8), st));
@@ -987,12 +1019,8 @@ int resident_capacity(int d) {
 template <int D>
 gs_status launch_resident_d(gs_ctx* ctx, unsigned grid, int threads, size_t smem,
                             const gs::ResidentArgs& ra) {
-  static bool configured = false;
-  if (!configured) {
-    GS_CK(cudaFuncSetAttribute(gs::k_resident<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kResidentSmemBudget + 1024));
-    configured = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  GS_CK(attr_once(done, ctx->device, gs::k_resident<D>, (int)kResidentSmemBudget + 1024));
   gs::k_resident<D><<<grid, threads, smem, ctx->stream>>>(ra);
   GS_LAUNCHED("k_resident");
   return GS_OK;
@@ -1056,6 +1084,14 @@ gs_status map_readback(gs_ctx* ctx, int64_t nf_run, int max_iter, Readback* rb) 
   return GS_OK;
 }
 
+// K7 grid: frames along y, ~8 CTAs of 256 per SM in total
+dim3 label_grid(gs_ctx* ctx, int64_t n, int64_t nf) {
+  const int64_t y = std::min<int64_t>(nf, 65535);
+  const int64_t total = (int64_t)ctx->num_sms * 8;
+  const int64_t x = std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, (total + y - 1) / y));
+  return dim3((unsigned)x, (unsigned)y);
+}
+
 // K8 over every frame, then labels; results copied to the pinned readback area; one sync.
 // deferrable: the launch is optimistic (smem sized from the shape cache) and K8 may refuse.
 bool graph_safe(const void* p);
@@ -1114,11 +1150,11 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   ra.err = ctx->errflag.as<int>();
   ra.mode_count = ctx->modes.as<int64_t>();
   // per-phase cycle counters cost a global atomic per phase: opt-in diagnostics only
-  ra.prof = getenv("GS_PROF") ? (long long*)(ctx->modes.as<int64_t>() + 4) : nullptr;
+  ra.prof = knob("GS_PROF") ? (long long*)(ctx->modes.as<int64_t>() + 4) : nullptr;
   ra.gidx = ctx->idx.as<int32_t>();
   ra.sidx_bytes = (int)sidx;
   ra.trace = nullptr;
-  if (getenv("GS_TRACE_LEVELS")) {
+  if (knob("GS_TRACE_LEVELS")) {
     GS_TRY(grow(ctx, ctx->dbg, 8 * 12000));
     GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 8 * 12000, st));
     ra.trace = (long long*)ctx->dbg.p;
@@ -1136,9 +1172,9 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
   }
-  gs::k_label<<<blocks_for(ntot, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
-      ntot, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dlabels, ctx->ctl.as<unsigned>(),
-      (unsigned*)ctx->pin_dev, (int)(ctl_bytes(ctx->ctl_nf) / 4),
+  gs::k_label<<<label_grid(ctx, ntot / nf, nf), 256, 0, st>>>(
+      ntot / nf, nf, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->lab.as<int32_t>(), dlabels,
+      ctx->ctl.as<unsigned>(), (unsigned*)ctx->pin_dev, (int)(ctl_bytes(ctx->ctl_nf) / 4),
       (int)(ctl_zero_bytes(ctx->ctl_nf) / 4));
   GS_LAUNCHED("k_label");
   ctx->ctl_clean = true;  // K7 re-zeroes the control block (stream order: before any later use)
@@ -1157,7 +1193,7 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
 // GS_TRACE_LEVELS diagnostics: per-level timeline of frame 0's first sweep and per-iteration
 // phase timeline of frame 0 (K8 writes them into ctx->dbg)
 void dump_trace(gs_ctx* ctx) {
-  if (!getenv("GS_TRACE_LEVELS") || !ctx->dbg.p) return;
+  if (!knob("GS_TRACE_LEVELS") || !ctx->dbg.p) return;
   {
       std::vector<long long> tr(8 * 512);
       cudaMemcpy(tr.data(), ctx->dbg.p, 8 * 8 * 512, cudaMemcpyDeviceToHost);
@@ -1259,7 +1295,7 @@ gs_status launch_shard_front(gs_ctx* ctx, int d) {
 
 // opt-in host-side timeline of one run (GS_HOST_PROF): prep / launch / wait / results, in us
 struct HostProf {
-  bool on = getenv("GS_HOST_PROF") != nullptr;
+  bool on = knob("GS_HOST_PROF") != nullptr;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
   double seg[4] = {0, 0, 0, 0};
   void lap(int i) {
@@ -1289,6 +1325,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   const bool dev_out = (cfg->flags & GS_DEVICE_OUTPUTS) != 0;
   const bool force_global = (cfg->flags & GS_DEBUG_GLOBAL_PATH) != 0;
   ctx->have_run = false;
+  ctx->grouped = false;
   ctx->stats = gs_stats{};
   ctx->stats_times_pending = false;
   ctx->ev_mask = ((cfg->flags & GS_TIME_PHASES) ? 0x3ffu : 0u) |
@@ -1308,6 +1345,42 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   if (!in->on_device) GS_TRY(grow(ctx, ctx->pts, input_bytes(in)));
   const void* dpts = in->on_device ? in->points : ctx->pts.p;
   int64_t vol_hint = 0;  // the cached shape's grid volume (sizes the compaction launch)
+  ctx->sweep_flags = cfg->flags & (GS_DEBUG_SWEEP_FLOW | GS_DEBUG_SWEEP_LEVELS | GS_DEBUG_SWEEP_SINGLE);
+  // the predicted key box (no bounds pass): the last box at this (d, dtype, h, image width),
+  // re-based to this call's point and frame counts; not for pinned inputs small enough for the
+  // zero-copy bounds pass (it is the copy) or the shard / debug entry points
+  GsBox pbox_run{};
+  const GsBox* pb = nullptr;
+  auto choose_pbox = [&]() -> gs_status {
+    pb = nullptr;
+    if (ctx->shard_front || force_global || !ctx->pbox_valid || ctx->pbox_d != d ||
+        ctx->pbox_dtype != in->dtype || ctx->pbox_h != cfg->h || ctx->pbox_w != ctx->img_w)
+      return GS_OK;
+    if (!in->on_device && input_bytes(in) <= kZeroCopyMaxBytes && pinned_device_ptr(in->points))
+      return GS_OK;
+    pbox_run = ctx->pbox;
+    pbox_run.n = n;
+    pbox_run.nframes = nf;
+    pbox_run.F = gs_fixed_shift(n, cfg->h);
+    pbox_run.scale = std::ldexp(1.0, pbox_run.F);
+    pbox_run.inv_scale = std::ldexp(1.0, -pbox_run.F);
+    pbox_run.vol_total = pbox_run.vol_frame * nf;
+    if (pbox_run.vol_total > kMaxDenseCells) return GS_OK;
+    GS_TRY(ensure_dense(ctx, pbox_run.vol_total, d));
+    pb = &pbox_run;
+    return GS_OK;
+  };
+  // K2 binned against the predicted box and flagged a point outside it (128) or a non-finite
+  // coordinate (1): K3 skipped, so the grid holds K2's partial sums -- clear them
+  auto clear_predicted = [&]() -> gs_status {
+    GS_CK(cudaMemsetAsync(ctx->cnt.p, 0, sizeof(uint32_t) * pbox_run.vol_total, st));
+    GS_CK(cudaMemsetAsync(ctx->qs.p, 0, sizeof(unsigned long long) * pbox_run.vol_total * d, st));
+    GS_CK(cudaStreamSynchronize(st));
+    ctx->pbox_valid = false;
+    ctx->pbox_gen++;
+    pb = nullptr;
+    return GS_OK;
+  };
   auto enqueue_front = [&]() -> gs_status {  // points to HBM, then the n-scale phase
     if (ctx->shard_front) return launch_shard_front(ctx, d);
     GS_TRY(rec_event(ctx, 0));
@@ -1321,7 +1394,8 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
         GS_CK(cudaMemcpyAsync(ctx->pts.p, in->points, input_bytes(in), cudaMemcpyHostToDevice, st));
     }
     GS_TRY(rec_event(ctx, 1));
-    const gs_status sf = launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint);
+    const gs_status sf = launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint,
+                                       ctx->host_src ? nullptr : pb);
     ctx->host_src = nullptr;
     GS_TRY(sf);
     GS_TRY(rec_event(ctx, 2));
@@ -1330,6 +1404,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter, ctx->img_w};
   std::vector<int32_t> g_iters(nf, 0);
   int64_t swept = 0;
+  GS_TRY(choose_pbox());
   if (!force_global && !ctx->shard_front && ctx->shape_ms > 0 && key == ctx->shape) {
     // ---- optimistic path: the whole run with no host round trip, replayed from a CUDA graph
     //      when the caller's buffers allow it (pinned or device memory)
@@ -1344,7 +1419,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     if (graphed) {
       GS_TRY(clean_ctl(ctx));  // the graph has no memset node: it starts from a clean block
       const gs_ctx::GraphKey gk{key, in->points, out->labels, cfg->flags, in->on_device,
-                                ctx->alloc_gen};
+                                ctx->alloc_gen, pb ? ctx->pbox_gen : ~0ull};
       if (!(ctx->gexec && ctx->gkey == gk)) {
         if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
         ctx->gexec = nullptr;
@@ -1375,11 +1450,17 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     GS_CK(cudaStreamSynchronize(st));
     hp.lap(2);
     dump_trace(ctx);
+    if (pb && (rb.err[0] & (1 | 128))) {
+      GS_TRY(clear_predicted());
+      if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
+    }
     if (rb.err[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
     if (rb.err[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
     if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
     if (rb.err[0] & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep schedule watchdog fired");
-    if ((rb.err[0] & 32) || rb.ctr[4] != 0) {  // grid too small / a frame too big: redo it
+    if (rb.err[0] & 128) {
+      // a point outside the predicted box: redo the run with the bounds pass (below)
+    } else if ((rb.err[0] & 32) || rb.ctr[4] != 0) {  // grid too small / a frame too big: redo it
       ctx->shape_ms = 0;                        // synchronously below
       if (rb.err[0] & 32) GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
     } else {
@@ -1397,12 +1478,17 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     GS_CK(cudaMemcpyAsync(ctr, ctx->counters.p, 64, cudaMemcpyDeviceToHost, st));
     GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost, st));
     GS_CK(cudaStreamSynchronize(st));
+    if (pb && (hdr[0] & (1 | 128))) {
+      GS_TRY(clear_predicted());
+      if (hdr[0] & 128) continue;  // redo with the bounds pass
+    }
     if (hdr[0] & 32) {
       GS_TRY(grow_dense_for(ctx, *(long long*)(hdr + 2), d));
       continue;
     }
     if (hdr[0] & 1) return fail(ctx, GS_E_INVALID_INPUT, "non-finite coordinate in input");
     if (hdr[0] & 64) return fail(ctx, GS_E_KEY_RANGE, "cell keys exceed the int64 key range");
+    if (hdr[0] & 2) return fail(ctx, GS_E_INTERNAL_INVARIANT, "a point's key left the key box");
     const int64_t m0 = ctr[0];
     const GsBox& b = ctx->box;
     // (a) global path (K4/K5 kernels, host-driven) while some live frame has more active
@@ -1507,6 +1593,22 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   }
 results:
   ctx->cur = 1 - ctx->cur;  // K8 wrote the final cells to the other buffer
+  if (!ctx->shard_front && !force_global) {  // this run's key box predicts the next run's
+    if (!pb) {
+      GS_CK(cudaMemcpy(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost));
+      ctx->pbox = ctx->box;
+      ctx->pbox_valid = true;
+      ctx->pbox_gen++;
+      ctx->pbox_d = d;
+      ctx->pbox_dtype = in->dtype;
+      ctx->pbox_h = cfg->h;
+      ctx->pbox_w = ctx->img_w;
+    } else {
+      ctx->box = pbox_run;
+    }
+  }
+  ctx->stats.slot_bytes = ctx->box.vol_frame <= 65536 ? 2 : 4;
+  ctx->stats.predicted_box = pb ? 1 : 0;
   // ---- results
   if (ctx->hist_m.size() != (size_t)(rec ? nf : 0)) {
     ctx->hist_m.assign(rec ? nf : 0, {});
@@ -1549,6 +1651,156 @@ results:
 }
 
 
+// ---- frame-group pipeline for host-resident batches (e2e path of gs_run) ----
+// Frames are independent, so a host batch is clustered as consecutive groups of
+// frames: while group g runs on the engine stream, the copy stream stages group g+1 into the
+// other staging buffer, and K7 of group g writes its labels straight into the caller's pinned
+// memory (device->host, the other PCIe direction).  Each group is a complete engine run, so
+// the results are exactly those of one whole-batch run; the centroids of every frame are
+// collected on the host as the groups finish.
+constexpr size_t kPipelineMinBytes = size_t(64) << 20;
+constexpr size_t kPipelineGroupBytes = size_t(48) << 20;
+
+bool want_pipeline(const gs_input* in, const gs_config* cfg) {
+  if (in->on_device || in->batch < 2 || (cfg->flags & GS_NO_PIPELINE)) return false;
+  if (cfg->flags & GS_DEBUG_PIPELINE) return true;
+  return in->batch >= 4 && input_bytes(in) >= kPipelineMinBytes;
+}
+
+// frames per group: the largest divisor of nf whose group stays under the byte target (equal
+// groups keep every group on the cached-shape path), at least 2 groups
+int64_t group_frames(const gs_input* in, const gs_config* cfg) {
+  const int64_t nf = in->batch;
+  if (cfg->flags & GS_DEBUG_PIPELINE) return std::min<int64_t>(2, nf);
+  const size_t fb = input_bytes(in) / (size_t)nf;
+  int64_t cap = std::max<int64_t>(1, (int64_t)(kPipelineGroupBytes / std::max<size_t>(fb, 1)));
+  cap = std::min<int64_t>(cap, nf / 2);
+  for (int64_t g = cap; g >= std::max<int64_t>(1, cap / 2); --g)
+    if (nf % g == 0) return g;
+  return cap;
+}
+
+gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
+  const int64_t nf = in->batch, n = in->n, gf = group_frames(in, cfg);
+  const int64_t G = (nf + gf - 1) / gf;
+  const size_t fb = input_bytes(in) / (size_t)nf;
+  const int d = in->d;
+  cudaStream_t st = ctx->stream;
+  if (!ctx->copy_stream) {
+    GS_CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_copy) GS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  for (auto& b : ctx->stage) GS_TRY(grow(ctx, b, fb * (size_t)gf));
+  const char* src = static_cast<const char*>(in->points);
+  auto stage_in = [&](int64_t g) -> gs_status {
+    const int64_t f0 = g * gf, cnt = std::min(gf, nf - f0);
+    GS_CK(cudaMemcpyAsync(ctx->stage[g & 1].p, src + (size_t)f0 * fb, fb * (size_t)cnt,
+                          cudaMemcpyHostToDevice, ctx->copy_stream));
+    GS_CK(cudaEventRecord(ctx->ev_copy[g & 1], ctx->copy_stream));
+    return GS_OK;
+  };
+  std::vector<double> cent;
+  std::vector<int64_t> off(nf + 1, 0);
+  std::vector<int64_t> all_k(nf);
+  std::vector<int32_t> all_it(nf), all_cv(nf);
+  std::vector<std::vector<int64_t>> hm;
+  std::vector<std::vector<double>> hd;
+  const bool rec = (cfg->flags & GS_RECORD_HISTORY) != 0;
+  if (rec) {
+    hm.resize(nf);
+    hd.resize(nf);
+  }
+  gs_stats agg{};
+  const bool graphs = ctx->use_graphs;
+  ctx->use_graphs = false;  // the buffers change every group: plain launches, no re-capture
+  gs_status s = stage_in(0);
+  int64_t f0 = 0;
+  for (int64_t g = 0; g < G && s == GS_OK; ++g) {
+    f0 = g * gf;
+    const int64_t cnt = std::min(gf, nf - f0);
+    // the other staging buffer was last read by group g-1, which has completed (synchronous)
+    if (g + 1 < G && (s = stage_in(g + 1)) != GS_OK) break;
+    if (cudaStreamWaitEvent(st, ctx->ev_copy[g & 1], 0) != cudaSuccess) {
+      s = fail(ctx, GS_E_CUDA, "cudaStreamWaitEvent");
+      break;
+    }
+    gs_input sub = *in;
+    sub.points = ctx->stage[g & 1].p;
+    sub.batch = cnt;
+    sub.on_device = 1;
+    gs_result r{out->labels + (size_t)f0 * n, out->k + f0, out->iterations + f0,
+                out->converged + f0};
+    gs_config c = *cfg;
+    c.flags &= ~(uint32_t)(GS_DEBUG_PIPELINE | GS_DEVICE_OUTPUTS);
+    if ((s = run_impl(ctx, &sub, &c, &r)) != GS_OK) {
+      ctx->err = "frames " + std::to_string((long long)f0) + "-" +
+                 std::to_string((long long)(f0 + cnt - 1)) + ": " + ctx->err;
+      break;
+    }
+    // this group's centroids (rows h_ffirst[f] .. + h_k[f] of the final cell buffer)
+    int64_t lo = INT64_MAX, hi = 0;
+    for (int64_t f = 0; f < cnt; ++f) {
+      lo = std::min<int64_t>(lo, ctx->h_ffirst[f]);
+      hi = std::max<int64_t>(hi, ctx->h_ffirst[f] + ctx->h_k[f]);
+    }
+    std::vector<double> rows((size_t)std::max<int64_t>(hi - lo, 0) * d);
+    if (hi > lo &&
+        cudaMemcpy(rows.data(), ctx->S[ctx->cur].as<double>() + (size_t)lo * d,
+                   sizeof(double) * rows.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      s = fail(ctx, GS_E_CUDA, "centroid readback");
+      break;
+    }
+    for (int64_t f = 0; f < cnt; ++f) {
+      const int64_t k = ctx->h_k[f];
+      off[f0 + f] = (int64_t)(cent.size() / d);
+      const double* r0 = rows.data() + (size_t)(ctx->h_ffirst[f] - lo) * d;
+      cent.insert(cent.end(), r0, r0 + (size_t)k * d);
+      all_k[f0 + f] = k;
+      all_it[f0 + f] = ctx->h_iters[f];
+      all_cv[f0 + f] = ctx->h_conv[f];
+      if (rec) {
+        hm[f0 + f] = ctx->hist_m[f];
+        hd[f0 + f] = ctx->hist_d[f];
+      }
+    }
+    const gs_stats& gs1 = ctx->stats;
+    agg.cells_swept += gs1.cells_swept;
+    agg.m0 += gs1.m0;
+    agg.k_total += gs1.k_total;
+    agg.kernel_launches += gs1.kernel_launches;
+    agg.lib_calls += gs1.lib_calls;
+    agg.max_iterations = std::max(agg.max_iterations, gs1.max_iterations);
+    agg.fixed_shift = gs1.fixed_shift;
+    agg.dense_cells = std::max(agg.dense_cells, gs1.dense_cells);
+    for (int k = 0; k < 3; ++k) agg.sweep_modes[k] += gs1.sweep_modes[k];
+    for (int k = 0; k < 8; ++k) agg.resident_cycles[k] += gs1.resident_cycles[k];
+  }
+  ctx->use_graphs = graphs;
+  cudaStreamSynchronize(ctx->copy_stream);  // no staging copy outlives the call
+  if (s != GS_OK) {
+    ctx->have_run = false;
+    ctx->grouped = false;
+    return s;
+  }
+  off[nf] = (int64_t)(cent.size() / d);
+  ctx->g_cent.swap(cent);
+  ctx->g_cent_off.swap(off);
+  ctx->grouped = true;
+  ctx->group_f0 = f0;
+  ctx->nframes = nf;
+  ctx->h_k = all_k;
+  ctx->h_iters = all_it;
+  ctx->h_conv = all_cv;
+  if (rec) {
+    ctx->hist_m.swap(hm);
+    ctx->hist_d.swap(hd);
+  }
+  ctx->k_total = agg.k_total;
+  ctx->stats = agg;  // phase times: those of the last group's events
+  ctx->have_run = true;
+  return GS_OK;
+}
+
 // ---- MS++ baseline (gs_mspp.cuh) ----
 template <int D, typename T>
 gs_status mspp_launch(gs_ctx* ctx, const void* dpts, int64_t n, int64_t m0, double tol,
@@ -1560,7 +1812,7 @@ gs_status mspp_launch(gs_ctx* ctx, const void* dpts, int64_t n, int64_t m0, doub
       ctx->S[0].as<double>(), ctx->idx.as<int32_t>(), snew0);
   GS_LAUNCHED("k_mspp_jacobi");
   gs::k_mspp_disp0<D, T><<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
-      n, (const T*)dpts, ctx->slot.as<uint32_t>(), ctx->idx.as<int32_t>(), snew0, disp0);
+      n, (const T*)dpts, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->idx.as<int32_t>(), snew0, disp0);
   GS_LAUNCHED("k_mspp_disp0");
   gs::MsppArgs a;
   a.m0 = (int)m0;
@@ -1611,6 +1863,7 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
     return fail(ctx, GS_E_INVALID_PARAMETER, "tol must be > 0 (SPEC.md:242)");
   cudaSetDevice(ctx->device);
   ctx->have_run = false;
+  ctx->grouped = false;
   ctx->img_w = 0;
   cudaGetLastError();
   const int d = in->d;
@@ -1691,8 +1944,9 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
   GS_TRY(ls);
   GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * n));
   int32_t* dl = ctx->labels.as<int32_t>();
-  gs::k_label<<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-      n, ctx->slot.as<uint32_t>(), ctx->lab.as<int32_t>(), dl, nullptr, nullptr, 0, 0);
+  gs::k_label<<<label_grid(ctx, n, 1), 256, 0, ctx->stream>>>(
+      n, 1, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->lab.as<int32_t>(), dl, nullptr, nullptr, 0,
+      0);
   GS_LAUNCHED("k_label");
   GS_CK(cudaMemcpyAsync(out->labels, dl, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
                         ctx->stream));
@@ -1805,6 +2059,13 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->lsucc, &ctx->order, &ctx->xsum, &ctx->pkeys, &ctx->pcounts,
                     &ctx->psums, &ctx->epoch_dev, &ctx->fswept, &ctx->fout, &ctx->ctl})
     b->release();
+  for (auto& b : ctx->stage) b.release();
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (auto& e : ctx->ev_copy)
+    if (e) cudaEventDestroy(e);
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   for (auto& e : ctx->ev)
@@ -1824,6 +2085,12 @@ gs_status gs_run(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_resul
   if (!ctx) return GS_E_INVALID_PARAMETER;
   ctx->err.clear();
   if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GS_E_CUDA, "cudaSetDevice");
+  ctx->grouped = false;
+  if (want_pipeline(in, cfg)) {
+    if (!out || !out->labels || !out->k || !out->iterations || !out->converged)
+      return fail(ctx, GS_E_INVALID_PARAMETER, "null result buffer");
+    return run_grouped(ctx, in, cfg, out);
+  }
   return run_impl(ctx, in, cfg, out);
 }
 
@@ -1834,6 +2101,11 @@ gs_status gs_get_centroids(gs_ctx* ctx, int64_t frame, double* out, int64_t cap_
   const int64_t k = ctx->h_k[frame];
   if (cap_k < k) return fail(ctx, GS_E_INVALID_PARAMETER, "centroid buffer too small");
   const int d = ctx->box.d;
+  if (ctx->grouped) {  // pipelined run: collected on the host as the groups finished
+    std::memcpy(out, ctx->g_cent.data() + (size_t)ctx->g_cent_off[frame] * d,
+                sizeof(double) * k * d);
+    return GS_OK;
+  }
   GS_CK(cudaMemcpyAsync(out, ctx->S[ctx->cur].as<double>() + (size_t)ctx->h_ffirst[frame] * d,
                         sizeof(double) * k * d, cudaMemcpyDeviceToHost, ctx->stream));
   GS_CK(cudaStreamSynchronize(ctx->stream));
@@ -2056,9 +2328,13 @@ gs_status gs_render(gs_ctx* ctx, int64_t frame, uint8_t* out, int32_t on_device)
   if (!ctx->have_run || frame < 0 || frame >= ctx->nframes)
     return fail(ctx, GS_E_INVALID_PARAMETER, "no such frame in the last run");
   if (ctx->box.d < 3) return fail(ctx, GS_E_INVALID_PARAMETER, "render needs rgb features");
+  if (ctx->grouped && frame < ctx->group_f0)
+    return fail(ctx, GS_E_INVALID_PARAMETER,
+                "render after a pipelined run: only the last frame group is on the device");
   cudaSetDevice(ctx->device);
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->box.n, k = ctx->h_k[frame];
+  const int64_t lf = ctx->grouped ? frame - ctx->group_f0 : frame;  // frame of the live state
   GS_TRY(grow(ctx, ctx->pkeys, 4 * (size_t)std::max<int64_t>(k, 1)));  // colour table
   uint8_t* dout = out;
   if (!on_device) {
@@ -2066,11 +2342,11 @@ gs_status gs_render(gs_ctx* ctx, int64_t frame, uint8_t* out, int32_t on_device)
     dout = ctx->labels.as<uint8_t>();
   }
   gs::k_segment_colours<<<blocks_for(k, 128), 128, 0, st>>>(
-      k, ctx->box.d, ctx->S[ctx->cur].as<double>() + (size_t)ctx->h_ffirst[frame] * ctx->box.d,
+      k, ctx->box.d, ctx->S[ctx->cur].as<double>() + (size_t)ctx->h_ffirst[lf] * ctx->box.d,
       ctx->pkeys.as<uint32_t>());
   GS_LAUNCHED("k_segment_colours");
   gs::k_render<<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
-      n, ctx->slot.as<uint32_t>() + (size_t)frame * n, ctx->lab.as<int32_t>(),
+      n, ctx->slot.p, lf, ctx->dbox.as<GsBox>(), ctx->lab.as<int32_t>(),
       ctx->pkeys.as<uint32_t>(), dout);
   GS_LAUNCHED("k_render");
   if (!on_device)
@@ -2127,7 +2403,7 @@ gs_status gs_debug_build(gs_ctx* ctx, const gs_input* in, double h, int64_t cap_
                         ctx->stream));
   GS_TRY(grow(ctx, ctx->dbg, sizeof(int64_t) * n));
   gs::k_slot_rank<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(
-      n, ctx->slot.as<uint32_t>(), ctx->idx.as<int32_t>(), ctx->dbg.as<int64_t>());
+      n, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->idx.as<int32_t>(), ctx->dbg.as<int64_t>());
   GS_CK(cudaGetLastError());
   GS_CK(cudaMemcpyAsync(slot, ctx->dbg.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
                         ctx->stream));

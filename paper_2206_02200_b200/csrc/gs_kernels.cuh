@@ -199,43 +199,41 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
 }
 
 // ---------------------------------------------------------------- K2: binning
-// Shared-memory privatisation.  Hot cells take tens of thousands of points (cfg2:
-// 16K in one cell, cfg5: 415K), so per-point global atomics serialise at one L2 slice.  Each
-// CTA bins a contiguous range of points into a shared-memory open-addressing table of cell
-// accumulators (count + D int64 fixed-point sums); a point whose probe run finds no room falls
-// back to global atomics.  The table is flushed once per CTA.  int64 sums are associative, so
-// the result is bit-identical to k_bin for any schedule.
-// 64-bit add on shared memory as two native 32-bit atomics (sm_100 has no 64-bit shared
-// add: atomicAdd(u64) compiles to a CAS spin loop, which serialises under the contention of
-// image data).  The low word's wrap-around is carried into the high word, so the u64 read
-// after a barrier is the exact sum mod 2^64 (integer addition is associative).
-__device__ __forceinline__ void smem_add_u64(unsigned long long* p, unsigned long long v) {
-  unsigned* w = reinterpret_cast<unsigned*>(p);
-  const unsigned lo = (unsigned)v;
-  const unsigned old = atomicAdd(&w[0], lo);
-  const unsigned carry = (old + lo < old) ? 1u : 0u;
-  const unsigned hi = (unsigned)(v >> 32) + carry;
-  atomicAdd(&w[1], hi);  // unconditional: a branch here costs more than the (rare) zero add
+// Shared-memory privatisation: hot cells take tens of thousands of points (cfg2: 16K in one
+// cell, cfg5: 415K), so per-point global atomics would serialise at one L2 slice.  Each CTA bins
+// a contiguous range of points into a shared-memory table of cell accumulators (count + D int64
+// fixed-point sums) and flushes it to the dense grid with global atomics.  int64 sums are
+// associative, so the result is bit-identical to the oracle's build mode 1 for any schedule.
+//
+// Two table kinds, chosen per launch from the key box (uniformly by every CTA):
+//  * dense: the frame's data box (the key box without its apron) fits the table, possibly
+//    several times (replicas chosen by lane, so the hot cells of a warp spread over replica
+//    entries; summed by the flush).  The CTA's range is cut at frame boundaries and the table is
+//    flushed per frame.  No hashing, no probing, no key words: image frames (cfg2-4);
+//  * hash: open addressing over (global cell index), bounded probes, global atomics on a miss
+//    (clouds whose box is far larger than a CTA's table: cfg5).
+// 64-bit shared adds are two native 32-bit atomics with the carry of the low word (sm_100 has no
+// 64-bit shared add; atomicAdd(u64) compiles to a CAS loop).  Low and high words live in
+// separate arrays (SoA), so a warp's entries spread over the banks.
+//
+// Predicted box (`predicted` != 0): the key box is the one the previous run of this shape used
+// (no bounds pass); a point outside it sets err bit 128 (the host clears the grid and reruns
+// with the bounds pass) and a non-finite coordinate sets bit 1.
+constexpr int kBinThreads = 1024;
+constexpr int kBinProbes = 4;  // hash probe budget before the point takes the global atomics
+constexpr int kAggRuns = 4;    // warp aggregation when the warp's keys form <= this many runs
+constexpr int kBinSmemBytes = 200 * 1024;
+
+__device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned long long v) {
+  const unsigned l = (unsigned)v;
+  const unsigned old = atomicAdd(lo, l);
+  atomicAdd(hi, (unsigned)(v >> 32) + ((old + l < old) ? 1u : 0u));
 }
 
-// Probe budget of the privatised table: when a CTA sees more distinct cells than the table
-// holds (cfg5: shuffled, ~15K cells per CTA slice), a full table made every new key walk 16
-// slots (~36 % of K2's time); after 4 the point takes the global atomics.
-constexpr int kBinProbes = 4;
-// Warp aggregation is used when a warp's 32 keys form at most this many runs of equal keys.
-constexpr int kAggRuns = 4;
-
-// Table entries (key u32 + count u32 + D int64 sums = 8D+8 B) filling the shared memory of one
-// CTA per SM (cfg5: 7168 entries catch 89 % of a CTA's points, 4096 caught 78 %).
-template <int D>
-__host__ __device__ constexpr int bin_table_entries() {
-  return (229376 / (8 * D + 8)) & ~31;
-}
-
-// grid_index of one coordinate (build mode 1), lean form of gs_grid_coord: fl =
+// grid_index of one coordinate (build mode 1), lean fp64 form of gs_grid_coord: fl =
 // floor(RN(x*RN(1/h))) is final when |q| < 2^20 and q is more than 2^-30 from an integer
 // (|q - x/h| <= 2^-32 there, so fl == floor(RN(x/h))), or when x == 0; otherwise the caller
-// takes the IEEE quotient (gs_bin_floor_exact).  Returns whether fl needs that.
+// takes the IEEE quotient.  Returns whether fl needs that.
 __device__ __forceinline__ bool gs_bin_floor(double x, double inv_h, double& fl) {
   const double qd = __dmul_rn(x, inv_h);
   fl = floor(qd);
@@ -243,202 +241,345 @@ __device__ __forceinline__ bool gs_bin_floor(double x, double inv_h, double& fl)
   return !(fabs(t) < 0.5 - 0x1p-30 && fabs(qd) < 0x1p20) && x != 0.0;
 }
 
+// fp32 inputs: the same floor from fp32 arithmetic.  t = RN32(x * RN32(1/h)) is within
+// |t| 2^-22.9 of x/h, so when t's fractional part is farther than |t| 2^-20 + 2^-23 from 0 and
+// from 1 (and |t| < 2^22), floor(t) == floor(x/h) == floor(RN64(x/h)) (pin P1); x == 0 gives 0.
+// Returns whether the exact division is needed (also for non-finite x).
+__device__ __forceinline__ bool gs_bin_floor_f32(float x, float ihf, int& k) {
+  const float t = __fmul_rn(x, ihf);
+  const float fl = floorf(t);
+  const float fr = __fsub_rn(t, fl);
+  const float eps = __fmaf_rn(fabsf(t), 0x1p-20f, 0x1p-23f);  // a margin, not a result
+  k = __float2int_rz(fl);
+  return !((fr > eps && fr < __fsub_rn(1.0f, eps) && fabsf(t) < 0x1p22f) || x == 0.0f);
+}
+
+// The binning front of one point: cell key per coordinate (box-relative), the linear index
+// within the frame, fixed-point offsets q = RN(RN(x - RN(k*h)) * 2^F) (== gs_fixq).
 template <int D, typename T>
-__global__ void __launch_bounds__(768, 1) k_bin_priv(const T* __restrict__ pts, int64_t ntot,
-                                                   const GsBox* __restrict__ pb,
-                                                   uint32_t* __restrict__ cnt,
-                                                   unsigned long long* __restrict__ qs,
-                                                   uint32_t* __restrict__ slot, int* err,
-                                                   int TBL, int img_w, int rep_log2) {
+struct BinPt {
+  uint32_t loc;    // frame-local dense grid index (valid when ok)
+  uint32_t dloc;   // index within the frame's data box (dense tables)
+  bool ok, miss, nonfinite;
+  long long q[D];
+};
+
+struct BinGeo {
+  double h, inv_h, scale, magic;
+  float ihf;
+  bool f32fast, magic_ok;
+  int kmin32[GS_DMAX];
+  double kminD[GS_DMAX];
+  uint32_t span[GS_DMAX], strd[GS_DMAX], dstrd[GS_DMAX];
+};
+
+template <int D, typename T>
+__device__ __forceinline__ void bin_point(const T* xc, int64_t pl, const GsImg& im,
+                                          const BinGeo& g, BinPt<D, T>& o) {
+  double fl[D], xs[D];
+  int rel[D];
+  bool slow = false;
+  if constexpr (sizeof(T) == 4) {
+    if (g.f32fast) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        int k;
+        slow |= gs_bin_floor_f32(xc[c], g.ihf, k);
+        rel[c] = k - g.kmin32[c];
+        fl[c] = (double)k;
+        xs[c] = (double)xc[c];
+      }
+    } else {
+      slow = true;
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs[c] = (double)xc[c];
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      xs[c] = gs_feature<T, D>(xc, c, pl, im);
+      slow |= gs_bin_floor(xs[c], g.inv_h, fl[c]);
+      rel[c] = __double2int_rz(__dsub_rn(fl[c], g.kminD[c]));
+    }
+  }
+  o.nonfinite = false;
+  if (slow) {  // rare: the exact IEEE quotient (and the non-finite check) for every coordinate
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      o.nonfinite |= !isfinite(xs[c]);
+      fl[c] = floor(gs_ddiv_slow(xs[c], g.h));
+      const double r = __dsub_rn(fl[c], g.kminD[c]);
+      rel[c] = (r > -4.0 && r < 2147483647.0) ? __double2int_rz(r) : -4;
+    }
+  }
+  bool bad = o.nonfinite;
+  uint32_t loc = 0, dloc = 0;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const uint32_t dr = (uint32_t)(rel[c] - GS_APRON);
+    bad |= dr >= g.span[c];
+    loc += (uint32_t)rel[c] * g.strd[c];
+    dloc += dr * g.dstrd[c];
+    const double d = __dsub_rn(xs[c], __dmul_rn(fl[c], g.h));
+    const double v = __dmul_rn(d, g.scale);
+    // RN to an integer: the 1.5*2^52 trick is exact for |v| < 2^51 (F keeps |q| below it
+    // when n >= 513), else the conversion instruction
+    o.q[c] = g.magic_ok ? __double_as_longlong(__dadd_rn(v, g.magic)) - __double_as_longlong(g.magic)
+                        : __double2ll_rn(v);
+  }
+  o.ok = !bad;
+  o.miss = bad && !o.nonfinite;
+  o.loc = loc;
+  o.dloc = dloc;
+}
+
+// Warp aggregation over runs of equal keys (pixel-ordered images put most of a warp into 1-4
+// runs): a run's sums reduce to its first lane with REDUX before any atomic.  Runs come from
+// one shuffle + ballot (MATCH.ANY costs 2 cycles per distinct key).  A warp of many runs
+// (shuffled clouds, noisy backgrounds) skips it.  Returns whether this lane carries atomics
+// and its count.
+template <int D>
+__device__ __forceinline__ bool warp_runs(uint32_t key, bool act, long long* q, bool two_piece,
+                                          uint32_t& my_cnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(kFull, key, 1);
+  const bool head = lane == 0 || key != prev;
+  const unsigned heads = __ballot_sync(kFull, head);
+  my_cnt = 1;
+  if (__popc(heads) > kAggRuns) return act;
+  const unsigned upto = heads & (0xffffffffu >> (31 - lane));    // heads <= lane
+  const unsigned after = heads & ~(0xffffffffu >> (31 - lane));  // heads > lane
+  const int s = 31 - __clz(upto);
+  const int e = after ? __ffs(after) - 1 : 32;
+  const unsigned gm = (e == 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((1u << s) - 1u);
+  my_cnt = (uint32_t)__popc(gm);
+  unsigned rem = heads;
+  while (rem) {
+    const int ld = __ffs(rem) - 1;
+    rem &= rem - 1u;
+    if (ld == s) {
+      if (two_piece) {  // per-point |q| <= 2^51: 26-bit unsigned + signed high piece
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const long long u = q[c];
+          const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffff));
+          const long long s1 = __reduce_add_sync(gm, (int)(u >> 26));
+          q[c] = (long long)s0 + s1 * 67108864ll;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const unsigned long long u = (unsigned long long)q[c];
+          const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
+          const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
+          const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
+          q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
+        }
+      }
+    }
+  }
+  return act && head;  // only the run's first lane carries the run's sums
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(kBinThreads, 1)
+    k_bin(const T* __restrict__ pts, int64_t ntot, const GsBox* __restrict__ pb,
+          uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs, void* __restrict__ slot,
+          int* err, int img_w, int predicted, int max_reps, int hash_rep_log2) {
   constexpr int RC = gs_raw_cols<T, D>();
-  // TBL: table entries (a multiple of 32, <= bin_table_entries<D>()) sized to the CTA's points
-  // (initialising and flushing a table costs O(TBL) per CTA).  rep_log2: each cell gets
-  // 2^rep_log2 replica entries, chosen by lane (batched image frames: a frame's noisy
-  // background puts few distinct cells in a warp, many lanes each, and same-address shared
-  // atomics serialise); the replicas are summed by the flush.
   constexpr uint32_t EMPTY = 0xffffffffu;
-  // the first round's coordinates, the error word and the box are all requested before any
-  // of them is waited for (after an L2 flush each is a cold HBM round trip)
   const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
   const int64_t p0 = (int64_t)blockIdx.x * per;
   const int64_t p1 = min(ntot, p0 + per);
-  T xn[RC];
-#pragma unroll
-  for (int c = 0; c < RC; ++c) xn[c] = (p0 + threadIdx.x < p1) ? pts[(p0 + threadIdx.x) * RC + c] : T(0);
   __shared__ GsBox b;
   __shared__ int s_err;
   if (threadIdx.x == 0) {
     s_err = *err;
     b = *pb;
   }
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* ts = (unsigned long long*)smem;      // TBL * D sums
-  uint32_t* tk = (uint32_t*)(ts + (size_t)TBL * D);        // TBL keys
-  uint32_t* tc = tk + TBL;                                 // TBL counts
-  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
-    tk[j] = EMPTY;
-    tc[j] = 0u;
-#pragma unroll
-    for (int c = 0; c < D; ++c) ts[j * D + c] = 0ull;
-  }
   __syncthreads();
-  if (s_err & (1 | 32 | 64)) return;  // non-finite input / box beyond the grid: nothing to bin
+  if (s_err & GS_ERR_SKIP) return;  // non-finite input / box beyond the grid: nothing to bin
+  extern __shared__ __align__(16) unsigned char smem[];
   const unsigned lane = threadIdx.x & 31;
   const GsImg im = gs_img(img_w, b.n);
-  // per-dimension constants in registers; 32-bit cell arithmetic (the grid holds <= 2^28 cells)
-  const double h = b.h, inv_h = b.inv_h, scale = b.scale;
-  // per-point |q| <= h*2^F < 2^(ilogb(h)+1+F): when that is <= 2^51 (n >= 513 points per frame)
-  // a 32-lane sum splits into a 26-bit unsigned piece and a signed high piece, neither of which
-  // can overflow 32 bits
-  const bool two_piece = ilogb(h) + 1 + b.F <= 51;
-  double kminD[D];
-  uint32_t span[D], strd[D];
+  BinGeo g;
+  g.h = b.h;
+  g.inv_h = b.inv_h;
+  g.scale = b.scale;
+  g.magic = 0x1.8p52;
+  // per-point |q| <= h*2^F < 2^(ilogb(h)+1+F): <= 2^51 (n >= 513 points per frame) keeps the
+  // RN-to-integer trick exact and lets a 32-lane sum split into two 32-bit pieces
+  const bool two_piece = ilogb(b.h) + 1 + b.F <= 51;
+  g.magic_ok = two_piece;
+  g.ihf = __double2float_rn(b.inv_h);
+  g.f32fast = true;
+  uint32_t vd = 1;
 #pragma unroll
-  for (int c = 0; c < D; ++c) {
-    kminD[c] = (double)b.kmin[c];
-    span[c] = (uint32_t)(b.ext[c] - 2 * GS_APRON);
-    strd[c] = (uint32_t)b.stride[c];
+  for (int c = D - 1; c >= 0; --c) {
+    g.kminD[c] = (double)b.kmin[c];
+    g.f32fast &= b.kmin[c] > -(1ll << 30) && b.kmin[c] < (1ll << 30);
+    g.kmin32[c] = (int)b.kmin[c];
+    g.span[c] = (uint32_t)(b.ext[c] - 2 * GS_APRON);
+    g.strd[c] = (uint32_t)b.stride[c];
+    g.dstrd[c] = vd;
+    vd *= g.span[c];
   }
-  // frame of this thread's point, tracked incrementally (no 64-bit division per point)
-  int64_t fr = (p0 + threadIdx.x) / b.n, fr_end = (fr + 1) * b.n;
-  uint32_t Lf = (uint32_t)(fr * b.vol_frame);
   const uint32_t vf = (uint32_t)b.vol_frame;
-  // warp-uniform trip count so every lane takes part in the warp aggregation; the next
-  // round's coordinates are loaded before this round is processed (twice the bytes in flight)
-  for (int64_t pb = p0; pb < p1; pb += blockDim.x) {
-    const int64_t p = pb + threadIdx.x;
-    const bool valid = p < p1;
-    T xc[RC];
+  const bool s16 = b.vol_frame <= 65536;
+  uint16_t* slot16 = (uint16_t*)slot;
+  uint32_t* slot32 = (uint32_t*)slot;
+  const int errbit_box = predicted ? 128 : 2;
+  // table plan: dense data box (with replicas) when it fits, else the hash table
+  constexpr int EB = 4 + 8 * D;  // count + D x (lo, hi)
+  const bool dense = (int64_t)vd * EB <= kBinSmemBytes;
+  const int reps = dense ? max(1, min(max_reps, (int)(kBinSmemBytes / ((int64_t)vd * EB)))) : 1;
+  const int rep_log2 = dense ? 0 : hash_rep_log2;
+  const int TBL = dense ? (int)vd * reps : ((kBinSmemBytes / (EB + 4)) & ~31);
+  unsigned* tc = (unsigned*)smem;                  // TBL counts
+  unsigned* tlo = tc + TBL;                        // D x TBL low words
+  unsigned* thi = tlo + (size_t)D * TBL;           // D x TBL high words
+  uint32_t* tk = thi + (size_t)D * TBL;            // TBL keys (hash)
+  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
+    tc[j] = 0u;
 #pragma unroll
-    for (int c = 0; c < RC; ++c) xc[c] = xn[c];
-    const int64_t pn = p + blockDim.x;
-#pragma unroll
-    for (int c = 0; c < RC; ++c) xn[c] = pn < p1 ? pts[pn * RC + c] : T(0);
-    while (p >= fr_end) {
-      ++fr;
-      fr_end += b.n;
-      Lf += vf;
-    }
-    uint32_t key = EMPTY;
-    long long q[D];
-    {
-      // keys: floor(x/h) per coordinate with one (rare) exact-division branch per point;
-      // rel = fl - kmin is exact in fp64; fixed-point offset q = RN(RN(x - RN(fl*h)) * 2^F)
-      // (== gs_fixq: fl is (double)k) -- bit-identical to the oracle's build mode 1
-      double xs[D], fl[D];
-      bool slow = false;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        xs[c] = gs_feature<T, D>(xc, c, (sizeof(T) == 1 && D > 3) ? p - fr * b.n : 0, im);
-        slow |= gs_bin_floor(xs[c], inv_h, fl[c]);
-      }
-      if (slow) {
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          double f;
-          if (gs_bin_floor(xs[c], inv_h, f)) fl[c] = floor(gs_ddiv_slow(xs[c], h));
-        }
-      }
-      uint32_t L = Lf;
-      bool bad = false;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const int rel = __double2int_rz(__dsub_rn(fl[c], kminD[c]));
-        bad |= (uint32_t)(rel - GS_APRON) >= span[c];
-        L += (uint32_t)rel * strd[c];
-        q[c] = __double2ll_rn(__dmul_rn(__dsub_rn(xs[c], __dmul_rn(fl[c], h)), scale));
-      }
-      if (valid) {
-        if (bad) atomicOr(err, 2);
-        else {
-          slot[p] = L;
-          key = L;
-        }
-      }
-    }
-    // ---- warp aggregation over runs of equal keys (pixel-ordered images put most of a warp
-    // into 1-4 runs): a run's sums reduce to its first lane with hardware reductions (REDUX)
-    // before any atomic.  Runs come from one shuffle + ballot (MATCH.ANY costs 2 cycles per
-    // distinct key).  A warp of many runs (shuffled clouds, noisy backgrounds) skips it: its
-    // lanes' atomics hardly contend.
-    const uint32_t prev = __shfl_up_sync(kFull, key, 1);
-    const bool head = lane == 0 || key != prev;
-    const unsigned heads = __ballot_sync(kFull, head);
-    uint32_t my_cnt = 1;
-    bool act = key != EMPTY;
-    if (__popc(heads) <= kAggRuns) {
-      // my run: lanes [s, e) with s = my head, e = the next head (or 32)
-      const unsigned upto = heads & (0xffffffffu >> (31 - lane));      // heads <= lane
-      const unsigned after = heads & ~(0xffffffffu >> (31 - lane));    // heads > lane
-      const int s = 31 - __clz(upto);
-      const int e = after ? __ffs(after) - 1 : 32;
-      const unsigned gm = (e == 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((1u << s) - 1u);
-      my_cnt = (uint32_t)__popc(gm);
-      unsigned rem = heads;
-      while (rem) {
-        const int ld = __ffs(rem) - 1;
-        rem &= rem - 1u;
-        if (ld == s) {
-          if (two_piece) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const long long u = q[c];
-              const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffff));
-              const long long s1 = __reduce_add_sync(gm, (int)(u >> 26));
-              q[c] = (long long)s0 + s1 * 67108864ll;
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const unsigned long long u = (unsigned long long)q[c];
-              const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
-              const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
-              const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
-              q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
-            }
-          }
-        }
-      }
-      act = act && head;  // only the run's first lane carries the run's sums
-    }
-    // ---- table update.  The probe loop is predicated (no early exit) and the active lanes
-    // reconverge before the atomics, so the warp issues each atomic once (an early-exit loop
-    // let the compiler replay the whole atomic sequence once per exit group).
-    const unsigned am = __ballot_sync(kFull, act);
-    if (act) {
-      const uint32_t tkey = (key << rep_log2) | (lane & ((1u << rep_log2) - 1u));
-      uint32_t hsh = __umulhi(tkey * 2654435761u, (unsigned)TBL);
-      int hit = -1;
-#pragma unroll
-      for (int probe = 0; probe < kBinProbes; ++probe) {
-        if (hit < 0) {
-          uint32_t k = tk[hsh];
-          if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, tkey);
-          if (k == EMPTY || k == tkey) hit = (int)hsh;
-          hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
-        }
-      }
-      __syncwarp(am);
-      if (hit >= 0) {
-        atomicAdd(&tc[hit], my_cnt);
-#pragma unroll
-        for (int c = 0; c < D; ++c) smem_add_u64(&ts[hit * D + c], (unsigned long long)q[c]);
-      } else {
-        atomicAdd(&cnt[key], my_cnt);
-#pragma unroll
-        for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)q[c]);
-      }
-    }
+    for (int c = 0; c < D; ++c) tlo[c * TBL + j] = thi[c * TBL + j] = 0u;
+    if (!dense) tk[j] = EMPTY;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
-    const uint32_t key = tk[j];
-    if (key == EMPTY) continue;
-    const int64_t L = key >> rep_log2;
-    atomicAdd(&cnt[L], tc[j]);
+  bool saw_miss = false, saw_nan = false;
+  // segments: dense tables hold one frame, so the range is cut at frame boundaries
+  int64_t s0 = p0;
+  while (s0 < p1) {
+    const int64_t fr = s0 / b.n;
+    const int64_t s1 = dense ? min(p1, (fr + 1) * b.n) : p1;
+    const uint32_t fbase = (uint32_t)(fr * b.vol_frame);
+    // frame tracking inside a hash segment (several frames)
+    int64_t hfr = (s0 + threadIdx.x) / b.n, hfr_end = (hfr + 1) * b.n;
+    uint32_t hbase = (uint32_t)(hfr * b.vol_frame);
+    T xn[RC];
 #pragma unroll
-    for (int c = 0; c < D; ++c) atomicAdd(&qs[L * D + c], ts[j * D + c]);
+    for (int c = 0; c < RC; ++c) xn[c] = (s0 + threadIdx.x < s1) ? pts[(s0 + threadIdx.x) * RC + c] : T(0);
+    // warp-uniform trip count so every lane takes part in the warp aggregation; the next
+    // round's coordinates are loaded before this round is processed
+    for (int64_t pr = s0; pr < s1; pr += blockDim.x) {
+      const int64_t p = pr + threadIdx.x;
+      const bool valid = p < s1;
+      T xc[RC];
+#pragma unroll
+      for (int c = 0; c < RC; ++c) xc[c] = xn[c];
+      const int64_t pn = p + blockDim.x;
+#pragma unroll
+      for (int c = 0; c < RC; ++c) xn[c] = pn < s1 ? pts[pn * RC + c] : T(0);
+      if (!dense) {
+        while (p >= hfr_end) {
+          ++hfr;
+          hfr_end += b.n;
+          hbase += vf;
+        }
+      }
+      const uint32_t base = dense ? fbase : hbase;
+      BinPt<D, T> o;
+      bin_point<D, T>(xc, (sizeof(T) == 1 && D > 3) ? p - (dense ? fr : hfr) * b.n : 0, im, g, o);
+      uint32_t key = EMPTY;
+      if (valid) {
+        if (o.ok) {
+          if (s16) slot16[p] = (uint16_t)o.loc;
+          else slot32[p] = base + o.loc;
+          key = dense ? o.dloc : base + o.loc;
+        } else {
+          saw_nan |= o.nonfinite;
+          saw_miss |= o.miss;
+        }
+      }
+      uint32_t my_cnt;
+      const bool act = warp_runs<D>(key, key != EMPTY, o.q, two_piece, my_cnt);
+      const unsigned am = __ballot_sync(kFull, act);
+      if (dense) {
+        if (act) {
+          const uint32_t e = (lane % (unsigned)reps) * vd + key;
+          atomicAdd(&tc[e], my_cnt);
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            smem_add64(&tlo[c * TBL + e], &thi[c * TBL + e], (unsigned long long)o.q[c]);
+        }
+      } else if (act) {
+        // predicated probe loop, then the active lanes reconverge before the atomics (an
+        // early-exit loop let the compiler replay the atomic sequence once per exit group)
+        const uint32_t tkey = (key << rep_log2) | (lane & ((1u << rep_log2) - 1u));
+        uint32_t hsh = __umulhi(tkey * 2654435761u, (unsigned)TBL);
+        int hit = -1;
+#pragma unroll
+        for (int probe = 0; probe < kBinProbes; ++probe) {
+          if (hit < 0) {
+            uint32_t k = tk[hsh];
+            if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, tkey);
+            if (k == EMPTY || k == tkey) hit = (int)hsh;
+            hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
+          }
+        }
+        __syncwarp(am);
+        if (hit >= 0) {
+          atomicAdd(&tc[hit], my_cnt);
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            smem_add64(&tlo[c * TBL + hit], &thi[c * TBL + hit], (unsigned long long)o.q[c]);
+        } else {
+          atomicAdd(&cnt[key], my_cnt);
+#pragma unroll
+          for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)o.q[c]);
+        }
+      }
+    }
+    __syncthreads();
+    if (dense) {  // flush this frame's table (replicas summed) and leave it zeroed
+      for (uint32_t j = threadIdx.x; j < vd; j += blockDim.x) {
+        unsigned cn = 0;
+        for (int r = 0; r < reps; ++r) cn += tc[r * vd + j];
+        if (!cn) continue;
+        uint32_t L = fbase, rem = j;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const uint32_t dr = rem / g.dstrd[c];
+          rem -= dr * g.dstrd[c];
+          L += (dr + GS_APRON) * g.strd[c];
+        }
+        atomicAdd(&cnt[L], cn);
+        for (int r = 0; r < reps; ++r) tc[r * vd + j] = 0u;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          unsigned long long sq = 0ull;
+          for (int r = 0; r < reps; ++r) {
+            const uint32_t e = r * vd + j;
+            sq += ((unsigned long long)thi[c * TBL + e] << 32) | tlo[c * TBL + e];
+            tlo[c * TBL + e] = thi[c * TBL + e] = 0u;
+          }
+          atomicAdd(&qs[(size_t)L * D + c], sq);
+        }
+      }
+      __syncthreads();
+    }
+    s0 = s1;
   }
+  if (saw_nan) atomicOr(err, 1);
+  if (saw_miss) atomicOr(err, errbit_box);
+  if (!dense) {
+    for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
+      const uint32_t key = tk[j];
+      if (key == EMPTY) continue;
+      const int64_t L = key >> rep_log2;
+      atomicAdd(&cnt[L], tc[j]);
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        atomicAdd(&qs[L * D + c], ((unsigned long long)thi[c * TBL + j] << 32) | tlo[c * TBL + j]);
+    }
+  }
+}
+
+
+// Predicted key box (no bounds pass): the box of the previous run of this shape.
+__global__ void k_box_set(GsBox b, GsBox* __restrict__ out, unsigned* epoch) {
+  *out = b;
+  *epoch += 1u;
 }
 
 // ---------------------------------------------------------------- K3: compaction by scan
@@ -492,7 +633,7 @@ __global__ void __launch_bounds__(256) k_occ(
     const int* __restrict__ err, long long* __restrict__ xsum = nullptr) {
   // xsum != null: export mode (a shard's partial cells for the multi-GPU exchange): keys,
   // counts and the raw fixed-point sums, no centroids, no index / root / label entries
-  if (*err & (1 | 32 | 64)) return;
+  if (*err & GS_ERR_SKIP) return;
   __shared__ int sh[8];
   __shared__ GsBox b;
   __shared__ int s_tile, s_excl;
@@ -806,23 +947,50 @@ __global__ void k_compose(int m0, const int32_t* __restrict__ parent, int32_t* _
   if (i < m0) root[i] = parent[root[i]];
 }
 
-// K7: labels[p] = lab[slot[p]]
-// K7.  Block 0 also hands the run's control block to the host: it stores the words into
-// mapped pinned memory (no copy node, ~12 us per run on the graph path) and then re-zeroes
-// the part every run starts from zero, so the next run needs no memset node either.
-__global__ void __launch_bounds__(256) k_label(int64_t ntot, const uint32_t* __restrict__ slot,
+// K7: labels[p] = lab[cell of p].  Frames are blockIdx.y-strided, so a point's frame base is
+// known without a division; u16 slots are read 8 at a time (16-byte loads).  Block (0, 0) also
+// hands the run's control block to the host: it stores the words into mapped pinned memory (no
+// copy node, ~12 us per run on the graph path) and then re-zeroes the part every run starts
+// from zero, so the next run needs no memset node either.
+__global__ void __launch_bounds__(256) k_label(int64_t n, int64_t nf, const void* __restrict__ slot,
+                                               const GsBox* __restrict__ pb,
                                                const int32_t* __restrict__ lab,
                                                int32_t* __restrict__ labels,
                                                unsigned* __restrict__ ctl, unsigned* ctl_host,
                                                int ctl_words, int zero_words) {
-  if (blockIdx.x == 0 && ctl_host) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && ctl_host) {
     for (int w = threadIdx.x; w < ctl_words; w += blockDim.x) ctl_host[w] = ctl[w];
     __syncthreads();
     for (int w = threadIdx.x; w < zero_words; w += blockDim.x) ctl[w] = 0u;
   }
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ntot;
-       p += (int64_t)gridDim.x * blockDim.x)
-    labels[p] = __ldg(&lab[slot[p]]);
+  const int64_t vf = pb->vol_frame;
+  const bool s16 = vf <= 65536;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = s16 && (n % 8) == 0 && (((uintptr_t)slot | (uintptr_t)labels) & 15) == 0;
+  for (int64_t f = blockIdx.y; f < nf; f += gridDim.y) {
+    const int64_t p0 = f * n;
+    const uint32_t fbase = (uint32_t)(f * vf);
+    if (vec) {
+      const uint4* s8 = reinterpret_cast<const uint4*>((const uint16_t*)slot + p0);
+      int4* o8 = reinterpret_cast<int4*>(labels + p0);
+      for (int64_t i = tid; i < n / 8; i += nth) {
+        const uint4 w = s8[i];
+        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+        int l[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          l[2 * k] = __ldg(&lab[fbase + (u[k] & 0xffffu)]);
+          l[2 * k + 1] = __ldg(&lab[fbase + (u[k] >> 16)]);
+        }
+        o8[2 * i] = make_int4(l[0], l[1], l[2], l[3]);
+        o8[2 * i + 1] = make_int4(l[4], l[5], l[6], l[7]);
+      }
+    } else {
+      for (int64_t i = tid; i < n; i += nth)
+        labels[p0 + i] = __ldg(&lab[gs_slot_cell(slot, s16, p0 + i, fbase)]);
+    }
+  }
 }
 
 // Segmentation render: a segment's colour is its centroid's first three
@@ -841,13 +1009,16 @@ __global__ void k_segment_colours(int64_t k, int d, const double* __restrict__ c
 }
 
 // every pixel -> its segment's colour (label = lab[slot[p]], as K7)
-__global__ void __launch_bounds__(256) k_render(int64_t n, const uint32_t* __restrict__ slot,
+__global__ void __launch_bounds__(256) k_render(int64_t n, const void* __restrict__ slot,
+                                                int64_t frame, const GsBox* __restrict__ pb,
                                                 const int32_t* __restrict__ lab,
                                                 const uint32_t* __restrict__ rgb,
                                                 uint8_t* __restrict__ out) {
+  const bool s16 = pb->vol_frame <= 65536;
+  const uint32_t fbase = (uint32_t)(frame * pb->vol_frame);
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = rgb[lab[slot[p]]];
+    const uint32_t v = rgb[lab[gs_slot_cell(slot, s16, frame * n + p, fbase)]];
     out[3 * p] = (uint8_t)(v & 0xffu);
     out[3 * p + 1] = (uint8_t)((v >> 8) & 0xffu);
     out[3 * p + 2] = (uint8_t)((v >> 16) & 0xffu);
@@ -855,10 +1026,11 @@ __global__ void __launch_bounds__(256) k_render(int64_t n, const uint32_t* __res
 }
 
 // test hook: rank of every point's initial cell
-__global__ void k_slot_rank(int64_t ntot, const uint32_t* __restrict__ slot,
-                            const int32_t* __restrict__ idx, int64_t* __restrict__ out) {
+__global__ void k_slot_rank(int64_t ntot, const void* __restrict__ slot,
+                            const GsBox* __restrict__ pb, const int32_t* __restrict__ idx,
+                            int64_t* __restrict__ out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < ntot) out[p] = idx[slot[p]];
+  if (p < ntot) out[p] = idx[gs_slot_cell(slot, pb->vol_frame <= 65536, p, 0u)];
 }
 
 }  // namespace gs

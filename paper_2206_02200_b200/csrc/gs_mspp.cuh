@@ -67,14 +67,15 @@ __global__ void k_mspp_jacobi(int m, const GsBox* __restrict__ pb, const uint32_
 // max over points of |S'(cell of p) - x_p| (pin M3), as the bits of a non-negative double
 template <int D, typename T>
 __global__ void __launch_bounds__(256) k_mspp_disp0(int64_t n, const T* __restrict__ pts,
-                                                     const uint32_t* __restrict__ slot,
+                                                     const void* __restrict__ slot,
+                                                     const GsBox* __restrict__ pb,
                                                      const int32_t* __restrict__ idx,
                                                      const double* __restrict__ Snew,
                                                      unsigned long long* __restrict__ dmax) {
   unsigned long long best = 0ull;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const int r = idx[slot[p]];
+    const int r = idx[gs_slot_cell(slot, pb->vol_frame <= 65536, p, 0u)];
     double acc = 0.0;
 #pragma unroll
     for (int c = 0; c < D; ++c) {

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
   __syncthreads();
   // non-finite input / key box beyond the grid or the int64 range: binning did not run and the
   // box is not valid (the host reports the error; on the optimistic path K8 is already queued)
-  if (s_err0 & (1 | 32 | 64)) return;
+  if (s_err0 & GS_ERR_SKIP) return;
   const GsBox& b = sbox;
   // dense cell index of this frame: smem int16 table when the host reserved room for this
   // box's frame volume, else the global grid (L2-resident)

@@ -88,7 +88,12 @@ STATUS_NAMES = {
 GS_F32, GS_F64, GS_U8 = 0, 1, 2
 GS_RECORD_HISTORY, GS_DEVICE_OUTPUTS = 0x1, 0x2
 GS_TIME_PHASES, GS_TIME_KERNEL = 0x4, 0x8
+GS_NO_PIPELINE = 0x10
 GS_DEBUG_GLOBAL_PATH = 0x80000000
+GS_DEBUG_PIPELINE = 0x40000000
+GS_DEBUG_SWEEP_FLOW = 0x20000000
+GS_DEBUG_SWEEP_LEVELS = 0x10000000
+GS_DEBUG_SWEEP_SINGLE = 0x08000000
 
 # every symbol include/gridshift_c.h declares (checked by tests/test_abi.py)
 EXPORTED = [
@@ -123,7 +128,8 @@ class GsStats(C.Structure):
                 ("kernel_launches", C.c_int64), ("max_iterations", C.c_int32),
                 ("fixed_shift", C.c_int32), ("dense_cells", C.c_int64),
                 ("ms_k_bin", C.c_double), ("ms_k_label", C.c_double), ("lib_calls", C.c_int64),
-                ("sweep_modes", C.c_int64 * 3), ("resident_cycles", C.c_int64 * 8)]
+                ("sweep_modes", C.c_int64 * 3), ("resident_cycles", C.c_int64 * 8),
+                ("slot_bytes", C.c_int32), ("predicted_box", C.c_int32)]
 
 
 class GsSweepEntry(C.Structure):

@@ -7,8 +7,7 @@ def matched_agreement(a: np.ndarray, b: np.ndarray):
     (contingency table + Hungarian assignment), and the matching (a-id -> b-id)."""
     from scipy.optimize import linear_sum_assignment
     ka, kb = int(a.max()) + 1, int(b.max()) + 1
-    cont = np.zeros((ka, kb), np.int64)
-    np.add.at(cont, (a, b), 1)
+    cont = np.bincount(a.astype(np.int64) * kb + b, minlength=ka * kb).reshape(ka, kb)
     r, c = linear_sum_assignment(-cont)
     return cont[r, c].sum() / len(a), dict(zip(r.tolist(), c.tolist()))
 
