@@ -277,6 +277,15 @@ gs_status gs_debug_iterate_once(gs_ctx* ctx, int32_t d, double h, int64_t m,
                                 int64_t* parent_out, int32_t* changed_out,
                                 int32_t* converged_out, double* maxdisp_out);
 
+/* One iteration of K8 (the CTA-resident engine) on an injected lex-sorted state of <= its
+ * capacity: the cells after iterate_once (keys, counts, centroids in id order), parent_out[i] =
+ * the new cell of injected cell i, stop_out = converged-or-unchanged (the do-while exit of
+ * SPEC.md:141), maxdisp_out = the sweep's max displacement.  Mirrors oracle gso_iterate_once. */
+gs_status gs_debug_resident_once(gs_ctx* ctx, int32_t d, double h, int64_t m, const int64_t* keys,
+                                 const int64_t* counts, const double* centroids, int64_t* m_out,
+                                 int64_t* keys_out, int64_t* counts_out, double* centroids_out,
+                                 int64_t* parent_out, int32_t* stop_out, double* maxdisp_out);
+
 /* The fixed-point exponent F used for the binning sums of a frame of n points at bandwidth h. */
 int32_t gs_fixed_shift(int64_t n, double h);
 

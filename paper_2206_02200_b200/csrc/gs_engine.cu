@@ -2496,4 +2496,88 @@ gs_status gs_debug_iterate_once(gs_ctx* ctx, int32_t d, double h, int64_t m, con
   return GS_OK;
 }
 
+
+gs_status gs_debug_resident_once(gs_ctx* ctx, int32_t d, double h, int64_t m, const int64_t* keys,
+                                 const int64_t* counts, const double* centroids, int64_t* m_out,
+                                 int64_t* keys_out, int64_t* counts_out, double* centroids_out,
+                                 int64_t* parent_out, int32_t* stop_out, double* maxdisp_out) {
+  if (!ctx) return GS_E_INVALID_PARAMETER;
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(ctx, GS_E_INVALID_BANDWIDTH, "h");
+  if (m < 1) return fail(ctx, GS_E_EMPTY_INPUT, "m");
+  if (d < 1 || d > GS_MAX_DIM) return fail(ctx, GS_E_INVALID_PARAMETER, "d");
+  if (m > resident_capacity(d))
+    return fail(ctx, GS_E_INVALID_PARAMETER, "state larger than K8's capacity");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = ctx->stream;
+  ctx->have_run = false;
+  ctx->grouped = false;
+  ctx->img_w = 0;
+  GsBox b;
+  GS_TRY(make_box_from_cells(ctx, d, h, m, keys, centroids, &b));
+  ctx->box = b;
+  GS_TRY(ensure_dense(ctx, b.vol_total, d));
+  GS_TRY(ensure_cells(ctx, m, d));
+  GS_TRY(ensure_frames(ctx, 1));
+  GS_TRY(grow(ctx, ctx->hist, (sizeof(int64_t) + sizeof(double)) * 1));
+  GS_TRY(grow(ctx, ctx->dbox, sizeof(GsBox)));
+  GS_TRY(grow(ctx, ctx->labels, 16));
+  Readback rb;
+  GS_TRY(map_readback(ctx, 1, 1, &rb));
+  std::vector<uint32_t> hk(m), hc(m);
+  std::vector<int32_t> r0(m), first{0, (int32_t)m};
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t L = 0;
+    for (int c = 0; c < d; ++c) L += (keys[i * d + c] - b.kmin[c]) * b.stride[c];
+    hk[i] = (uint32_t)L;
+    hc[i] = (uint32_t)counts[i];
+    r0[i] = (int32_t)i;
+    if (i > 0 && hk[i] <= hk[i - 1])
+      return fail(ctx, GS_E_INVALID_INPUT, "injected keys must be strictly lex-sorted");
+  }
+  // the state K3 leaves for K8: lex-sorted initial cells, the dense index, identity roots
+  ctx->cur = 0;
+  GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
+  GS_CK(cudaMemcpyAsync(ctx->dbox.p, &b, sizeof(GsBox), cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->ckey[0].p, hk.data(), 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->initkey.p, hk.data(), 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->ccnt[0].p, hc.data(), 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->S[0].p, centroids, sizeof(double) * m * d, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->root.p, r0.data(), 4 * m, cudaMemcpyHostToDevice, st));
+  GS_CK(cudaMemcpyAsync(ctx->ifirst.p, first.data(), 8, cudaMemcpyHostToDevice, st));
+  gs::k_idx_set<<<blocks_for(m, 256), 256, 0, st>>>((int)m, ctx->ckey[0].as<uint32_t>(),
+                                                    ctx->idx.as<int32_t>());
+  GS_CK(cudaGetLastError());
+  ctx->ctl_clean = false;
+  int ms_run = 32;
+  while (ms_run < m) ms_run <<= 1;
+  gs_config cfg{h, 1, GS_RECORD_HISTORY};
+  ctx->ev_mask = 0;
+  GS_TRY(launch_tail(ctx, &cfg, 1, 0, d, ms_run, false, true, ctx->labels.as<int32_t>(), true,
+                     true, rb));
+  GS_CK(cudaStreamSynchronize(st));
+  if (rb.err[0] & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep schedule watchdog fired");
+  if (rb.err[0] & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
+  if (rb.err[0] & 16) return fail(ctx, GS_E_INTERNAL_INVARIANT, "state beyond K8's capacity");
+  const int64_t k = rb.fk[0], f0 = rb.fout[0];
+  const int fin = 1 - ctx->cur;
+  std::vector<uint32_t> nk(k), nc(k);
+  std::vector<int32_t> lab(b.vol_total);
+  GS_CK(cudaMemcpyAsync(nk.data(), ctx->ckey[fin].as<uint32_t>() + f0, 4 * k, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(nc.data(), ctx->ccnt[fin].as<uint32_t>() + f0, 4 * k, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(centroids_out, ctx->S[fin].as<double>() + (size_t)f0 * d,
+                        sizeof(double) * k * d, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaMemcpyAsync(lab.data(), ctx->lab.p, 4 * b.vol_total, cudaMemcpyDeviceToHost, st));
+  GS_CK(cudaStreamSynchronize(st));
+  *m_out = k;
+  for (int64_t g = 0; g < k; ++g) {
+    for (int c = 0; c < d; ++c) keys_out[g * d + c] = (nk[g] / b.stride[c]) % b.ext[c] + b.kmin[c];
+    counts_out[g] = nc[g];
+  }
+  for (int64_t i = 0; i < m; ++i) parent_out[i] = lab[hk[i]];
+  *stop_out = rb.fconv[0];
+  *maxdisp_out = rb.hd[0];
+  ctx->ctl_clean = true;  // K7 re-zeroed the control block
+  return GS_OK;
+}
+
 }  // extern "C"

@@ -696,6 +696,26 @@ __device__ __forceinline__ int ld_acquire_cluster_s32(const int* p) {
   return v;
 }
 
+// Release side of the dataflow sweep, on a peer CTA's shared memory (generic DSMEM address):
+// the pending-count decrement is acq_rel at cluster scope (it orders this warp's row stores,
+// made visible to this lane by the warp barrier, before the count, and acquires the other
+// releasers' rows through the count's RMW chain); the last releaser publishes the queue slot
+// with a release exchange that the owner's ld.acquire pairs with.
+__device__ __forceinline__ unsigned atom_sub_acq_rel_cluster(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cluster.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "l"(p), "r"(0u - v)
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void atom_exch_release_cluster(int* p, int v) {
+  int old;
+  asm volatile("atom.release.cluster.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  (void)old;
+}
+
 template <int D>
 __host__ __device__ constexpr size_t sweep_flow_smem(int mloc) {
   return (((size_t)8 * mloc + 15) & ~(size_t)15) + (size_t)(512 / 32) * 128 * D * 8;
@@ -744,6 +764,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
       }
     }
     i = __shfl_sync(0xffffffffu, i, 0);
+    __syncwarp();  // lane 0's acquire is ordered before every lane's operand-row loads
     if (i < 0) {
       dead = true;
       break;
@@ -796,11 +817,11 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
     auto release_one = [&](int j) {
       const int own = j % NC;
       unsigned* pj = cluster.map_shared_rank(pend + j / NC, own);
-      if (atomicSub(pj, 1u) == 1u) {
+      if (atom_sub_acq_rel_cluster(pj, 1u) == 1u) {
         unsigned* tl = cluster.map_shared_rank(&tail, own);
         int* qd = cluster.map_shared_rank(queue, own);
-        const unsigned slot = atomicAdd(tl, 1u);
-        atomicExch(&qd[slot], j);
+        const unsigned slot = atomicAdd(tl, 1u);  // slot uniqueness only: relaxed
+        atom_exch_release_cluster(&qd[slot], j);
       }
     };
     // successors: entries e < t < n; the last chunk's from registers, earlier chunks reloaded

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
 constexpr int kBinThreads = 1024;
 constexpr int kBinProbes = 4;  // hash probe budget before the point takes the global atomics
 constexpr int kAggRuns = 4;    // warp aggregation when the warp's keys form <= this many runs
-constexpr int kBinSmemBytes = 200 * 1024;
+constexpr int kBinSmemBytes = 224 * 1024;
 
 __device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned long long v) {
   const unsigned l = (unsigned)v;
@@ -967,24 +967,20 @@ __global__ void __launch_bounds__(256) k_label(int64_t n, int64_t nf, const void
   const bool s16 = vf <= 65536;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  const bool vec = s16 && (n % 8) == 0 && (((uintptr_t)slot | (uintptr_t)labels) & 15) == 0;
+  // u16 slots: a lane takes 4 consecutive points (8-byte slot load, 16-byte label store), so a
+  // warp instruction reads 256 contiguous bytes and writes 512 (whole lines: also for labels
+  // written straight into pinned host memory)
+  const bool vec = s16 && (n % 4) == 0 && (((uintptr_t)slot | (uintptr_t)labels) & 15) == 0;
   for (int64_t f = blockIdx.y; f < nf; f += gridDim.y) {
     const int64_t p0 = f * n;
     const uint32_t fbase = (uint32_t)(f * vf);
     if (vec) {
-      const uint4* s8 = reinterpret_cast<const uint4*>((const uint16_t*)slot + p0);
-      int4* o8 = reinterpret_cast<int4*>(labels + p0);
-      for (int64_t i = tid; i < n / 8; i += nth) {
-        const uint4 w = s8[i];
-        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
-        int l[8];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          l[2 * k] = __ldg(&lab[fbase + (u[k] & 0xffffu)]);
-          l[2 * k + 1] = __ldg(&lab[fbase + (u[k] >> 16)]);
-        }
-        o8[2 * i] = make_int4(l[0], l[1], l[2], l[3]);
-        o8[2 * i + 1] = make_int4(l[4], l[5], l[6], l[7]);
+      const uint2* s4 = reinterpret_cast<const uint2*>((const uint16_t*)slot + p0);
+      int4* o4 = reinterpret_cast<int4*>(labels + p0);
+      for (int64_t i = tid; i < n / 4; i += nth) {
+        const uint2 w = s4[i];
+        o4[i] = make_int4(__ldg(&lab[fbase + (w.x & 0xffffu)]), __ldg(&lab[fbase + (w.x >> 16)]),
+                          __ldg(&lab[fbase + (w.y & 0xffffu)]), __ldg(&lab[fbase + (w.y >> 16)]));
       }
     } else {
       for (int64_t i = tid; i < n; i += nth)

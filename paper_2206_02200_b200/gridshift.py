@@ -99,7 +99,7 @@ GS_DEBUG_SWEEP_SINGLE = 0x08000000
 EXPORTED = [
     "gs_validate", "gs_create", "gs_destroy", "gs_run", "gs_get_centroids", "gs_get_history",
     "gs_get_stats", "gs_last_error", "gs_status_string", "gs_debug_build",
-    "gs_debug_iterate_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
+    "gs_debug_iterate_once", "gs_debug_resident_once", "gs_fixed_shift", "gs_shard_keybounds", "gs_shard_bin",
     "gs_shard_run", "gs_render", "gs_tuner_create", "gs_tuner_destroy", "gs_tuner_last_error",
     "gs_tune_bandwidth", "gs_silhouette_subsampled", "gs_tracker_create", "gs_tracker_destroy",
     "gs_tracker_last_error", "gs_track_init", "gs_track_sequence", "gs_mspp_run",
@@ -174,6 +174,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.gs_status_string.restype = C.c_char_p
     lib.gs_debug_build.argtypes = [P, C.POINTER(GsInput), D, I64, P, P, P, P, P]
     lib.gs_debug_iterate_once.argtypes = [P, I32, D, I64, P, P, P, P, P, P, P, P, P, P, P, P]
+    lib.gs_debug_resident_once.argtypes = [P, I32, D, I64, P, P, P, P, P, P, P, P, P, P]
     lib.gs_fixed_shift.argtypes = [I64, D]
     lib.gs_fixed_shift.restype = I32
     lib.gs_render.argtypes = [P, I64, P, I32]
@@ -510,6 +511,27 @@ class Engine:
         mn = mo.value
         return dict(keys=ko[:mn], counts=co[:mn], centroids=so[:mn], swept=sw, parent=par,
                     changed=bool(ch.value), converged=bool(cv.value), maxdisp=md.value)
+
+    def debug_resident_once(self, keys: np.ndarray, counts: np.ndarray, cent: np.ndarray,
+                            h: float) -> dict:
+        """One iteration of K8 (the CTA-resident engine) on an injected state."""
+        keys = np.ascontiguousarray(keys, np.int64)
+        counts = np.ascontiguousarray(counts, np.int64)
+        cent = np.ascontiguousarray(cent, np.float64)
+        m, d = keys.shape
+        ko = np.zeros((m, d), np.int64)
+        co = np.zeros(m, np.int64)
+        so = np.zeros((m, d), np.float64)
+        par = np.zeros(m, np.int64)
+        mo = C.c_int64()
+        stop = C.c_int32()
+        md = C.c_double()
+        self._check(self._lib.gs_debug_resident_once(
+            self._ctx, d, h, m, _ptr(keys), _ptr(counts), _ptr(cent), C.byref(mo), _ptr(ko),
+            _ptr(co), _ptr(so), _ptr(par), C.byref(stop), C.byref(md)))
+        mn = mo.value
+        return dict(keys=ko[:mn], counts=co[:mn], centroids=so[:mn], parent=par,
+                    stop=bool(stop.value), maxdisp=md.value)
 
 
 _default_engine: Optional[Engine] = None

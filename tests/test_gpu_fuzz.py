@@ -82,3 +82,62 @@ def test_fuzz_batched_frames_global_path(engine, d):
         assert rb.iterations[f] == o["iterations"], f
         assert np.array_equal(rb.labels[f], o["labels"]), f
         assert np.array_equal(_bits(rb.centroids[f]), _bits(o["centroids"])), f
+
+
+def _high_d_cases():
+    """d = 7..12 (SPEC.md:96's documented limit): the dense cell grid holds the key box (apron 2
+    per side), so the data spans few cells per dimension -- 3 (d 7), 2 (d 8-10), 2 in one
+    dimension (d 11), one cell (d 12: 5^12 cells)."""
+    out = []
+    for d, span, seeds in ((7, 3, 3), (8, 2, 3), (9, 2, 2), (10, 2, 2), (11, 1, 1), (12, 0, 1)):
+        for s in range(seeds):
+            out.append((f"d{d}-s{s}", d, span, 700 + 10 * d + s))
+    return out
+
+
+@pytest.mark.parametrize("name,d,span,seed", _high_d_cases(), ids=[c[0] for c in _high_d_cases()])
+def test_fuzz_high_dimensions(engine, name, d, span, seed):
+    """K2/K3/K8/K7 and the global path's census/scan/Kahn sweep (d >= 7) bit-exact vs the oracle."""
+    rng = np.random.default_rng(seed)
+    h = 1.0
+    n = 600
+    k = 3
+    centres = rng.uniform(0.3, 0.7, (k, d))
+    if span >= 2:
+        centres[:, :] = rng.uniform(0.3, span - 0.3, (k, d))
+    elif span == 1:
+        centres[:, 0] = rng.uniform(0.3, 1.7, k)
+    lab = rng.integers(0, k, n)
+    X = centres[lab] + 0.08 * rng.standard_normal((n, d))
+    lo = 0.01
+    hi = np.full(d, 0.99) if span == 0 else np.full(d, max(span, 1) - 0.01)
+    if span == 1:
+        hi[:] = 0.99
+        hi[0] = 1.99
+    X = np.clip(X, lo, hi)
+    _check(engine, X, h, 0, name)
+    _check(engine, X, h, G.GS_DEBUG_GLOBAL_PATH, name + "-global")
+
+
+def test_high_dimension_key_range_refused(engine):
+    """A d = 12 dataset whose key box exceeds the dense grid is refused loudly (KEY_RANGE ->
+    InvalidParameterError), never approximated."""
+    rng = np.random.default_rng(5)
+    X = rng.uniform(0.0, 3.0, (200, 12))
+    with pytest.raises(G.InvalidParameterError):
+        engine.run(X, G.EngineConfig(1.0, 50))
+
+
+@pytest.mark.parametrize("flags", ["flow", "levels", "single"])
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_fuzz_sweep_schedules(engine, d, flags):
+    """Every global-path sweep variant (dataflow cluster sweep, level-synchronous cluster sweep,
+    single-CTA sweep) on the same inputs, bit-exact vs the oracle."""
+    fl = {"flow": G.GS_DEBUG_SWEEP_FLOW, "levels": G.GS_DEBUG_SWEEP_LEVELS,
+          "single": G.GS_DEBUG_SWEEP_SINGLE}[flags]
+    for seed in range(3):
+        rng = np.random.default_rng(4000 + 10 * d + seed)
+        n = 4000 if d <= 3 else 2000
+        X = _mixture(rng, n, d).astype(np.float32)
+        h = 0.3 if d <= 3 else 0.5
+        _check(engine, X, h, G.GS_DEBUG_GLOBAL_PATH | fl, f"d{d}-{flags}-{seed}")

@@ -78,6 +78,29 @@ def test_state_injection_bit_exact(engine, case):
         assert g["maxdisp"] == o["maxdisp"]
 
 
+@pytest.mark.parametrize("case", small_inputs(), ids=lambda c: c[0])
+def test_state_injection_resident_bit_exact(engine, case):
+    """K8 state injection: the oracle's iteration-t state fed to ONE iteration of the
+    CTA-resident engine (capacity permitting) must give the oracle's iteration t+1 bitwise --
+    cells, parent map, max displacement and the do-while exit flag."""
+    name, X, h = case
+    states = oracle_states(X.astype(np.float64), h, steps=30)
+    done = 0
+    for t, (keys, cnt, cen) in enumerate(states):
+        try:
+            g = engine.debug_resident_once(keys, cnt, cen, h)
+        except G.InvalidParameterError:  # beyond K8's capacity: the global path's state
+            continue
+        o = O.iterate_once(keys, cnt, cen, h)
+        assert_state_equal((g["keys"], g["counts"], g["centroids"]),
+                           (o["keys"], o["counts"], o["centroids"]), f"{name} t={t}")
+        assert np.array_equal(g["parent"], o["parent"]), f"{name} t={t}: parent"
+        assert g["stop"] == (o["converged"] or not o["changed"]), f"{name} t={t}: exit flag"
+        assert g["maxdisp"] == o["maxdisp"], f"{name} t={t}: max displacement"
+        done += 1
+    assert done > 0
+
+
 def _check_run(engine, X, h, max_iter, name, flags=0):
     cfg = G.EngineConfig(h, max_iter, record_history=True, debug_flags=flags)
     g = engine.run(X, cfg)
