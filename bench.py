@@ -565,6 +565,8 @@ def main():
     ap.add_argument("--input", default="features", choices=["features", "u8"],
                     help="u8: the image workloads (cfg2, cfg4) as 8-bit RGB pixels, features "
                          "formed on the device (segmentation front end, SURVEY.md §8(f)1)")
+    ap.add_argument("--profile-device", action="store_true",
+                    help="profiling aid: device-resident steps only (no e2e / phase passes)")
     args = ap.parse_args()
     if args.workload == "tune":
         return run_tune(args)
@@ -643,6 +645,12 @@ def main():
         ms = [a.elapsed_time(b) for a, b in ev]
         return ms, stats
 
+    if args.profile_device:  # ncu launch lists / captures of the device-resident step alone
+        for _ in range(args.warmup + args.steps):
+            step(True)
+        torch.cuda.synchronize()
+        eng.close()
+        return 0
     for _ in range(args.warmup):
         step(True)
         step(False)

@@ -501,15 +501,15 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
         ctx->epoch_dev.as<unsigned>(), img_w, copy);
     GS_LAUNCHED("k_bounds_box");
   } else {
-    // privatised binning: one 1024-thread CTA per SM at most, >= 1024 points per CTA
+    // privatised binning: one 1024-thread CTA per SM at most, >= 1024 points per CTA; the
+    // geometry comes from the host copy of the key box (ctx->box) as kernel parameters
     const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
     static std::atomic<uint64_t> done{0};
     GS_CK(attr_once(done, ctx->device, gs::k_bin<D, T>, gs::kBinSmemBytes));
-    const int hash_rep = ctx->bin_rep_log2;
+    const gs::BinParams P = gs::make_bin_params<D>(ctx->box, 4, ctx->bin_rep_log2, ctx->predicted);
     gs::k_bin<D, T><<<grid, gs::kBinThreads, gs::kBinSmemBytes, ctx->stream>>>(
-        (const T*)pts, ntot, ctx->dbox.as<GsBox>(), ctx->cnt.as<uint32_t>(),
-        ctx->qs.as<unsigned long long>(), ctx->slot.p, ctx->errflag.as<int>(), img_w,
-        ctx->predicted, 4, hash_rep);
+        (const T*)pts, ntot, P, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+        ctx->slot.p, ctx->errflag.as<int>(), img_w);
     GS_LAUNCHED("k_bin");
   }
   return GS_OK;
@@ -606,10 +606,19 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   GS_TRY(clean_ctl(ctx));
   ctx->ctl_clean = false;  // until K7 of this run re-zeroes it
   if (pbox) {  // the predicted box: no bounds pass (K2 checks every point against it)
+    if (ctx->host_src)  // zero-copy pinned input: K1 is the copy (its box is not used)
+      GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
     gs::k_box_set<<<1, 1, 0, st>>>(*pbox, ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>());
     GS_LAUNCHED("k_box_set");
+    ctx->box = *pbox;
   } else {
+    // bounds pass, then the box to the host: K2's geometry is kernel parameters
     GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
+    int hdr[8];
+    GS_CK(cudaMemcpyAsync(hdr, ctx->errflag.p, 32, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaMemcpyAsync(&ctx->box, ctx->dbox.p, sizeof(GsBox), cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaStreamSynchronize(st));
+    if (hdr[0] & GS_ERR_SKIP) return GS_OK;  // the caller reads the error bits
   }
   ctx->predicted = pbox ? 1 : 0;
   GS_TRY(rec_event(ctx, 6));
@@ -1347,16 +1356,14 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   int64_t vol_hint = 0;  // the cached shape's grid volume (sizes the compaction launch)
   ctx->sweep_flags = cfg->flags & (GS_DEBUG_SWEEP_FLOW | GS_DEBUG_SWEEP_LEVELS | GS_DEBUG_SWEEP_SINGLE);
   // the predicted key box (no bounds pass): the last box at this (d, dtype, h, image width),
-  // re-based to this call's point and frame counts; not for pinned inputs small enough for the
-  // zero-copy bounds pass (it is the copy) or the shard / debug entry points
+  // re-based to this call's point and frame counts (not for the shard / debug entry points;
+  // a pinned input small enough for the zero-copy pass still runs K1, as the copy)
   GsBox pbox_run{};
   const GsBox* pb = nullptr;
   auto choose_pbox = [&]() -> gs_status {
     pb = nullptr;
     if (ctx->shard_front || force_global || !ctx->pbox_valid || ctx->pbox_d != d ||
         ctx->pbox_dtype != in->dtype || ctx->pbox_h != cfg->h || ctx->pbox_w != ctx->img_w)
-      return GS_OK;
-    if (!in->on_device && input_bytes(in) <= kZeroCopyMaxBytes && pinned_device_ptr(in->points))
       return GS_OK;
     pbox_run = ctx->pbox;
     pbox_run.n = n;
@@ -1405,7 +1412,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
   std::vector<int32_t> g_iters(nf, 0);
   int64_t swept = 0;
   GS_TRY(choose_pbox());
-  if (!force_global && !ctx->shard_front && ctx->shape_ms > 0 && key == ctx->shape) {
+  if (!force_global && !ctx->shard_front && ctx->shape_ms > 0 && key == ctx->shape && pb) {
     // ---- optimistic path: the whole run with no host round trip, replayed from a CUDA graph
     //      when the caller's buffers allow it (pinned or device memory)
     const bool graphed = ctx->use_graphs && (in->on_device || graph_safe(in->points)) &&
@@ -2265,6 +2272,7 @@ gs_status gs_shard_bin(gs_ctx* ctx, const gs_input* in, double h, int64_t n_glob
   GS_CK(cudaMemsetAsync(ctx->ctl.p, 0, ctl_zero_bytes(ctx->ctl_nf), st));
   ctx->ctl_clean = false;
   GS_CK(cudaMemcpyAsync(ctx->dbox.p, &b, sizeof(GsBox), cudaMemcpyHostToDevice, st));
+  ctx->box = b;
   GS_TRY(dispatch_bounds_bin(ctx, dpts, in->dtype, d, n, false, 0));
   k_epoch_bump<<<1, 1, 0, st>>>(ctx->epoch_dev.as<unsigned>());
   GS_LAUNCHED("k_epoch_bump");

@@ -681,10 +681,15 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
 // processed, so a warp waiting on position k only waits for cells at earlier positions of some
 // queue: no deadlock).  A warp updates one cell (lane l loads list word l of each 128-entry
 // chunk, the operand rows are staged per warp, lanes c < D add them in list order), stores the
-// row, fences it (__threadfence: visible GPU-wide before the release), and releases the
-// successors with remote atomics on their owners' pending counts; the last releaser appends
-// the successor with an atomic on the owner's tail and a store of the cell id into the owner's
-// queue slot (initialised to -1; the consumer polls it with an acquire load).  No barrier, no
+// row, and releases the successors with remote atomics on their owners' pending counts; the
+// last releaser appends the successor with an atomic on the owner's tail and a store of the
+// cell id into the owner's queue slot (initialised to -1; the consumer polls it with an
+// acquire load).  Memory ordering (PTX model, cluster scope): after the warp barrier every
+// lane -- the row writers included -- executes fence.acq_rel.cluster, so each successor's
+// relaxed decrement is a release pattern over the rows; the last releaser's fence after its
+// decrement acquires the other releasers' rows through the count's RMW chain and releases them
+// with the queue-slot store; the consumer's ld.acquire pairs with it, and a warp barrier
+// carries it to the lanes that load the rows.  No barrier, no
 // level skew: the critical path is the DAG depth x one update + one release.  A spin watchdog
 // sets err bit 8 instead of hanging.  Operands and add order are the serial sweep's.
 __device__ __forceinline__ int ld_acquire_cluster_s32(const int* p) {
@@ -696,24 +701,8 @@ __device__ __forceinline__ int ld_acquire_cluster_s32(const int* p) {
   return v;
 }
 
-// Release side of the dataflow sweep, on a peer CTA's shared memory (generic DSMEM address):
-// the pending-count decrement is acq_rel at cluster scope (it orders this warp's row stores,
-// made visible to this lane by the warp barrier, before the count, and acquires the other
-// releasers' rows through the count's RMW chain); the last releaser publishes the queue slot
-// with a release exchange that the owner's ld.acquire pairs with.
-__device__ __forceinline__ unsigned atom_sub_acq_rel_cluster(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.cluster.add.u32 %0, [%1], %2;"
-               : "=r"(old)
-               : "l"(p), "r"(0u - v)
-               : "memory");
-  return old;
-}
-
-__device__ __forceinline__ void atom_exch_release_cluster(int* p, int v) {
-  int old;
-  asm volatile("atom.release.cluster.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  (void)old;
+__device__ __forceinline__ void fence_acq_rel_cluster() {
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
 }
 
 template <int D>
@@ -808,20 +797,19 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
       const double s1 = gl_div(num, (double)dn, rd);
       __stcg(&Q[((int64_t)P1ROW + i) * D + lane], __dmul_rn((double)cn, s1));
       __stcg(&Q[(int64_t)i * D + lane], s1);
-      if (flow_fence)  // the row is visible before any successor is released
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-      else
-        __threadfence();
     }
     __syncwarp();
+    if (flow_fence) __threadfence();  // (diagnostic variant: GPU-scope fence as well)
+    fence_acq_rel_cluster();  // every lane: the rows precede any release of a successor
     auto release_one = [&](int j) {
       const int own = j % NC;
       unsigned* pj = cluster.map_shared_rank(pend + j / NC, own);
-      if (atom_sub_acq_rel_cluster(pj, 1u) == 1u) {
+      if (atomicSub(pj, 1u) == 1u) {
+        fence_acq_rel_cluster();  // acquire the other releasers' rows, release them all
         unsigned* tl = cluster.map_shared_rank(&tail, own);
         int* qd = cluster.map_shared_rank(queue, own);
-        const unsigned slot = atomicAdd(tl, 1u);  // slot uniqueness only: relaxed
-        atom_exch_release_cluster(&qd[slot], j);
+        const unsigned slot = atomicAdd(tl, 1u);  // slot uniqueness only
+        atomicExch(&qd[slot], j);
       }
     };
     // successors: entries e < t < n; the last chunk's from registers, earlier chunks reloaded

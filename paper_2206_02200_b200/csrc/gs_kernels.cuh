@@ -11,6 +11,9 @@
 // K8 (the CTA-resident iteration engine) is gs_resident.cuh.
 #pragma once
 
+#include <cmath>
+#include <cstring>
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -241,106 +244,142 @@ __device__ __forceinline__ bool gs_bin_floor(double x, double inv_h, double& fl)
   return !(fabs(t) < 0.5 - 0x1p-30 && fabs(qd) < 0x1p20) && x != 0.0;
 }
 
-// fp32 inputs: the same floor from fp32 arithmetic.  t = RN32(x * RN32(1/h)) is within
-// |t| 2^-22.9 of x/h, so when t's fractional part is farther than |t| 2^-20 + 2^-23 from 0 and
-// from 1 (and |t| < 2^22), floor(t) == floor(x/h) == floor(RN64(x/h)) (pin P1); x == 0 gives 0.
-// Returns whether the exact division is needed (also for non-finite x).
-__device__ __forceinline__ bool gs_bin_floor_f32(float x, float ihf, int& k) {
-  const float t = __fmul_rn(x, ihf);
-  const float fl = floorf(t);
-  const float fr = __fsub_rn(t, fl);
-  const float eps = __fmaf_rn(fabsf(t), 0x1p-20f, 0x1p-23f);  // a margin, not a result
-  k = __float2int_rz(fl);
-  return !((fr > eps && fr < __fsub_rn(1.0f, eps) && fabsf(t) < 0x1p22f) || x == 0.0f);
+// fp32 inputs: the same floor from fp32 arithmetic, with no FRND/F2I (16 lanes/clk/SM on
+// sm_100, measured: profiles/r2_microbench_conv.txt).  u = RN(x*ihf + C) with C = 1.5*2^23 - kmin
+// is rint(v) - kmin + 1.5*2^23 for the exact product v = x*ihf (ihf = RN32(1/h), |v - x/h| <=
+// |x/h| 2^-23.9) while |v - kmin| < 2^22; nr = C - u = -rint(v) exactly; d = RN(v - rint(v)).
+// When |d| > |rint(v)| 2^-20, x/h lies on v's side of the integer rint(v), so floor(x/h) ==
+// floor(RN64(x/h)) == rint(v) - (d < 0) (pin P1); x == +-0 gives 0.  Outside the magic range the
+// decoded key lies beyond the box (the host enables this path only for extents < 2^21), so the
+// point is flagged, never mis-binned.  Returns the key relative to the box origin.
+__device__ __forceinline__ int gs_bin_rel_f32(float x, float ihf, float C, bool& fine) {
+  const float u = __fmaf_rn(x, ihf, C);
+  const float nr = __fsub_rn(C, u);
+  const float d = __fmaf_rn(x, ihf, nr);  // (-0 + +0 = +0: x == -0 gives key 0)
+  fine = fabsf(d) > __fmul_rn(fabsf(nr), 0x1p-20f) || x == 0.0f;
+  return (__float_as_int(u) - 0x4B400000) + (__float_as_int(d) >> 31);
 }
 
-// The binning front of one point: cell key per coordinate (box-relative), the linear index
-// within the frame, fixed-point offsets q = RN(RN(x - RN(k*h)) * 2^F) (== gs_fixq).
-template <int D, typename T>
-struct BinPt {
-  uint32_t loc;    // frame-local dense grid index (valid when ok)
-  uint32_t dloc;   // index within the frame's data box (dense tables)
-  bool ok, miss, nonfinite;
-  long long q[D];
-};
-
-struct BinGeo {
-  double h, inv_h, scale, magic;
+// Launch geometry of K2, computed on the host from the key box (kernel parameters live in the
+// constant bank: no registers for the per-dimension constants).
+struct BinParams {
+  double h, inv_h, scale, Mq;  // Mq = 1.5*2^(52-F): RN(d + Mq) - Mq = RN to the 2^-F grid
+  long long Mbits;             // bits of Mq: table sums carry count * Mbits, removed at flush
+  long long n, vol_frame;
   float ihf;
-  bool f32fast, magic_ok;
+  int magic_ok, two_piece, f32fast, dense, reps, TBL, rep_log2, s16, predicted;
+  uint32_t vd;                 // cells of a frame's data box
+  float Cf[GS_DMAX];           // 1.5*2^23 - kmin (fp32 fast key)
   int kmin32[GS_DMAX];
   double kminD[GS_DMAX];
   uint32_t span[GS_DMAX], strd[GS_DMAX], dstrd[GS_DMAX];
 };
 
-template <int D, typename T>
-__device__ __forceinline__ void bin_point(const T* xc, int64_t pl, const GsImg& im,
-                                          const BinGeo& g, BinPt<D, T>& o) {
+template <int D>
+inline BinParams make_bin_params(const GsBox& b, int max_reps, int hash_rep_log2, int predicted) {
+  BinParams P;
+  memset(&P, 0, sizeof(P));
+  P.h = b.h;
+  P.inv_h = b.inv_h;
+  P.scale = b.scale;
+  P.n = b.n;
+  P.vol_frame = b.vol_frame;
+  P.two_piece = (std::ilogb(b.h) + 1 + b.F) <= 51;
+  P.magic_ok = P.two_piece;
+  P.Mq = std::ldexp(1.5, 52 - b.F);
+  std::memcpy(&P.Mbits, &P.Mq, 8);
+  P.ihf = (float)b.inv_h;
+  P.f32fast = P.magic_ok;
+  uint32_t vd = 1;
+  for (int c = D - 1; c >= 0; --c) {
+    P.kminD[c] = (double)b.kmin[c];
+    P.f32fast &= b.kmin[c] > -(1ll << 21) && b.kmin[c] < (1ll << 21) && b.ext[c] < (1ll << 21);
+    P.kmin32[c] = (int)b.kmin[c];
+    P.Cf[c] = 12582912.0f - (float)P.kmin32[c];
+    P.span[c] = (uint32_t)(b.ext[c] - 2 * GS_APRON);
+    P.strd[c] = (uint32_t)b.stride[c];
+    P.dstrd[c] = vd;
+    vd *= P.span[c];
+  }
+  P.vd = vd;
+  P.s16 = b.vol_frame <= 65536;
+  // dense data box (with replicas) when it fits and the frame's cells fit u16 slots
+  constexpr int EW = 1 + 2 * D;
+  P.dense = P.s16 && (int64_t)vd * EW * 4 <= kBinSmemBytes;
+  P.reps = P.dense ? std::max(1, std::min(max_reps, (int)(kBinSmemBytes / ((int64_t)vd * EW * 4)))) : 1;
+  P.TBL = P.dense ? (int)vd * P.reps : ((kBinSmemBytes / (EW * 4 + 4)) & ~31);
+  P.rep_log2 = P.dense ? 0 : hash_rep_log2;
+  P.predicted = predicted;
+  return P;
+}
+
+// The binning front of one point: cell key per coordinate (box-relative), the linear index
+// within the frame (loc) and within the frame's data box (dloc), and the fixed-point offsets
+// q = RN(RN(x - RN(k*h)) * 2^F) (== gs_fixq) as w = q + Mbits when magic_ok (the 1.5*2^(52-F)
+// trick: |q| <= 2^51), else q itself.  Returns 0 ok, 1 outside the box, 2 non-finite.
+template <int D, typename T, bool FAST>
+__device__ __forceinline__ int bin_point(const T* xc, int64_t pl, const GsImg& im,
+                                         const BinParams& P, uint32_t& loc, uint32_t& dloc,
+                                         long long* w) {
   double fl[D], xs[D];
   int rel[D];
   bool slow = false;
-  if constexpr (sizeof(T) == 4) {
-    if (g.f32fast) {
+  if constexpr (FAST) {
+    bool fine = true;
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        int k;
-        slow |= gs_bin_floor_f32(xc[c], g.ihf, k);
-        rel[c] = k - g.kmin32[c];
-        fl[c] = (double)k;
-        xs[c] = (double)xc[c];
-      }
-    } else {
-      slow = true;
-#pragma unroll
-      for (int c = 0; c < D; ++c) xs[c] = (double)xc[c];
+    for (int c = 0; c < D; ++c) {
+      bool f;
+      rel[c] = gs_bin_rel_f32(xc[c], P.ihf, P.Cf[c], f);
+      fine &= f;
+      fl[c] = (double)(rel[c] + P.kmin32[c]);
+      xs[c] = (double)xc[c];
     }
+    slow = !fine;
   } else {
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       xs[c] = gs_feature<T, D>(xc, c, pl, im);
-      slow |= gs_bin_floor(xs[c], g.inv_h, fl[c]);
-      rel[c] = __double2int_rz(__dsub_rn(fl[c], g.kminD[c]));
+      slow |= gs_bin_floor(xs[c], P.inv_h, fl[c]);
+      rel[c] = __double2int_rz(__dsub_rn(fl[c], P.kminD[c]));
     }
   }
-  o.nonfinite = false;
+  bool nonfinite = false;
   if (slow) {  // rare: the exact IEEE quotient (and the non-finite check) for every coordinate
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      o.nonfinite |= !isfinite(xs[c]);
-      fl[c] = floor(gs_ddiv_slow(xs[c], g.h));
-      const double r = __dsub_rn(fl[c], g.kminD[c]);
+      nonfinite |= !isfinite(xs[c]);
+      fl[c] = floor(gs_ddiv_slow(xs[c], P.h));
+      const double r = __dsub_rn(fl[c], P.kminD[c]);
       rel[c] = (r > -4.0 && r < 2147483647.0) ? __double2int_rz(r) : -4;
     }
   }
-  bool bad = o.nonfinite;
-  uint32_t loc = 0, dloc = 0;
+  bool bad = false;
+  uint32_t l = 0, dl = 0;
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const uint32_t dr = (uint32_t)(rel[c] - GS_APRON);
-    bad |= dr >= g.span[c];
-    loc += (uint32_t)rel[c] * g.strd[c];
-    dloc += dr * g.dstrd[c];
-    const double d = __dsub_rn(xs[c], __dmul_rn(fl[c], g.h));
-    const double v = __dmul_rn(d, g.scale);
-    // RN to an integer: the 1.5*2^52 trick is exact for |v| < 2^51 (F keeps |q| below it
-    // when n >= 513), else the conversion instruction
-    o.q[c] = g.magic_ok ? __double_as_longlong(__dadd_rn(v, g.magic)) - __double_as_longlong(g.magic)
-                        : __double2ll_rn(v);
+    bad |= dr >= P.span[c];
+    l += (uint32_t)rel[c] * P.strd[c];
+    dl += dr * P.dstrd[c];
+    const double dd = __dsub_rn(xs[c], __dmul_rn(fl[c], P.h));
+    if (FAST || P.magic_ok)  // (the fast path is only taken with magic_ok)
+      w[c] = __double_as_longlong(__dadd_rn(dd, P.Mq));
+    else
+      w[c] = __double2ll_rn(__dmul_rn(dd, P.scale));
   }
-  o.ok = !bad;
-  o.miss = bad && !o.nonfinite;
-  o.loc = loc;
-  o.dloc = dloc;
+  loc = l;
+  dloc = dl;
+  return nonfinite ? 2 : bad ? 1 : 0;
 }
 
 // Warp aggregation over runs of equal keys (pixel-ordered images put most of a warp into 1-4
 // runs): a run's sums reduce to its first lane with REDUX before any atomic.  Runs come from
 // one shuffle + ballot (MATCH.ANY costs 2 cycles per distinct key).  A warp of many runs
-// (shuffled clouds, noisy backgrounds) skips it.  Returns whether this lane carries atomics
-// and its count.
+// (shuffled clouds, noisy backgrounds) skips it.  w holds q + off per lane; the run head gets
+// sum(q) + count * off.  Returns whether this lane carries atomics and its count.
 template <int D>
-__device__ __forceinline__ bool warp_runs(uint32_t key, bool act, long long* q, bool two_piece,
-                                          uint32_t& my_cnt) {
+__device__ __forceinline__ bool warp_runs(uint32_t key, bool act, long long* w, long long off,
+                                          bool two_piece, uint32_t& my_cnt) {
   const unsigned lane = threadIdx.x & 31;
   const uint32_t prev = __shfl_up_sync(kFull, key, 1);
   const bool head = lane == 0 || key != prev;
@@ -361,19 +400,19 @@ __device__ __forceinline__ bool warp_runs(uint32_t key, bool act, long long* q, 
       if (two_piece) {  // per-point |q| <= 2^51: 26-bit unsigned + signed high piece
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const long long u = q[c];
+          const long long u = w[c] - off;
           const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffff));
           const long long s1 = __reduce_add_sync(gm, (int)(u >> 26));
-          q[c] = (long long)s0 + s1 * 67108864ll;
+          w[c] = (long long)s0 + s1 * 67108864ll + (long long)my_cnt * off;
         }
       } else {
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const unsigned long long u = (unsigned long long)q[c];
+          const unsigned long long u = (unsigned long long)(w[c] - off);
           const unsigned long long s0 = __reduce_add_sync(gm, (unsigned)(u & 0x3ffffffu));
           const unsigned long long s1 = __reduce_add_sync(gm, (unsigned)((u >> 26) & 0x3ffffffu));
           const unsigned long long s2 = __reduce_add_sync(gm, (unsigned)(u >> 52));
-          q[c] = (long long)(s0 + (s1 << 26) + (s2 << 52));
+          w[c] = (long long)(s0 + (s1 << 26) + (s2 << 52)) + (long long)my_cnt * off;
         }
       }
     }
@@ -381,132 +420,94 @@ __device__ __forceinline__ bool warp_runs(uint32_t key, bool act, long long* q, 
   return act && head;  // only the run's first lane carries the run's sums
 }
 
-template <int D, typename T>
-__global__ void __launch_bounds__(kBinThreads, 1)
-    k_bin(const T* __restrict__ pts, int64_t ntot, const GsBox* __restrict__ pb,
-          uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs, void* __restrict__ slot,
-          int* err, int img_w, int predicted, int max_reps, int hash_rep_log2) {
+// Shared-memory atomics on 32-bit shared addresses (no generic-to-shared conversion per use).
+// A table entry is EW = 1 + 2D words: [count, lo_0, hi_0, ..., lo_{D-1}, hi_{D-1}] (an odd word
+// stride, so random entries spread over the banks); the 64-bit sums are two 32-bit atomics, the
+// low word's carry added into the high word.
+__device__ __forceinline__ void reds_add(uint32_t a, unsigned v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void reds_add64(uint32_t a, unsigned long long v) {
+  asm volatile(
+      "{\n\t.reg .u32 o, t;\n\t"
+      "atom.shared.add.u32 o, [%0], %1;\n\t"
+      "add.cc.u32 t, o, %1;\n\t"
+      "addc.u32 t, %2, 0;\n\t"
+      "red.shared.add.u32 [%0+4], t;\n\t}" ::"r"(a),
+      "r"((unsigned)v), "r"((unsigned)(v >> 32))
+      : "memory");
+}
+
+// the (offset) sum of coordinate c held by a table entry
+__device__ __forceinline__ unsigned long long bin_entry_sum(const unsigned* ent, int c) {
+  return ((unsigned long long)ent[2 + 2 * c] << 32) | ent[1 + 2 * c];
+}
+
+// One frame segment [s0, s0 + cnt) of the CTA's range: bin every point into the table (entries
+// at shared address ent_s; hash keys at tk).  DENSE: the table is the frame's data box (x reps
+// replicas by lane; slots are u16); else the hash table (keys = global cell index; a point
+// whose probes fail takes the global atomics).  Coordinates are prefetched two rounds ahead
+// (two rounds of 1024 points in flight per SM).
+template <int D, typename T, bool FAST, bool DENSE>
+__device__ __forceinline__ void bin_segment(const T* __restrict__ pts, int64_t s0, uint32_t cnt,
+                                            uint32_t fbase, int64_t fpos0, const GsImg& im,
+                                            const BinParams& P, uint32_t ent_s, uint32_t* tk,
+                                            uint32_t rep_off, void* __restrict__ slot,
+                                            uint32_t* __restrict__ gcnt,
+                                            unsigned long long* __restrict__ gqs, int& saw) {
   constexpr int RC = gs_raw_cols<T, D>();
+  constexpr int EW = 1 + 2 * D;
   constexpr uint32_t EMPTY = 0xffffffffu;
-  const int64_t per = (ntot + gridDim.x - 1) / gridDim.x;
-  const int64_t p0 = (int64_t)blockIdx.x * per;
-  const int64_t p1 = min(ntot, p0 + per);
-  __shared__ GsBox b;
-  __shared__ int s_err;
-  if (threadIdx.x == 0) {
-    s_err = *err;
-    b = *pb;
-  }
-  __syncthreads();
-  if (s_err & GS_ERR_SKIP) return;  // non-finite input / box beyond the grid: nothing to bin
-  extern __shared__ __align__(16) unsigned char smem[];
   const unsigned lane = threadIdx.x & 31;
-  const GsImg im = gs_img(img_w, b.n);
-  BinGeo g;
-  g.h = b.h;
-  g.inv_h = b.inv_h;
-  g.scale = b.scale;
-  g.magic = 0x1.8p52;
-  // per-point |q| <= h*2^F < 2^(ilogb(h)+1+F): <= 2^51 (n >= 513 points per frame) keeps the
-  // RN-to-integer trick exact and lets a 32-lane sum split into two 32-bit pieces
-  const bool two_piece = ilogb(b.h) + 1 + b.F <= 51;
-  g.magic_ok = two_piece;
-  g.ihf = __double2float_rn(b.inv_h);
-  g.f32fast = true;
-  uint32_t vd = 1;
+  const T* __restrict__ src = pts + s0 * RC;
+  uint16_t* __restrict__ slot16 = (uint16_t*)slot + s0;
+  uint32_t* __restrict__ slot32 = (uint32_t*)slot + s0;
+  const uint32_t B = blockDim.x;
+  const long long off = (FAST || P.magic_ok) ? P.Mbits : 0ll;
+  T xa[RC], xb[RC];
+  {
+    const uint32_t i = threadIdx.x;
+    const T* pa = src + (size_t)i * RC;
+    const T* pb = src + (size_t)(i + B) * RC;
 #pragma unroll
-  for (int c = D - 1; c >= 0; --c) {
-    g.kminD[c] = (double)b.kmin[c];
-    g.f32fast &= b.kmin[c] > -(1ll << 30) && b.kmin[c] < (1ll << 30);
-    g.kmin32[c] = (int)b.kmin[c];
-    g.span[c] = (uint32_t)(b.ext[c] - 2 * GS_APRON);
-    g.strd[c] = (uint32_t)b.stride[c];
-    g.dstrd[c] = vd;
-    vd *= g.span[c];
+    for (int c = 0; c < RC; ++c) {
+      xa[c] = i < cnt ? pa[c] : T(0);
+      xb[c] = i + B < cnt ? pb[c] : T(0);
+    }
   }
-  const uint32_t vf = (uint32_t)b.vol_frame;
-  const bool s16 = b.vol_frame <= 65536;
-  uint16_t* slot16 = (uint16_t*)slot;
-  uint32_t* slot32 = (uint32_t*)slot;
-  const int errbit_box = predicted ? 128 : 2;
-  // table plan: dense data box (with replicas) when it fits, else the hash table
-  constexpr int EB = 4 + 8 * D;  // count + D x (lo, hi)
-  const bool dense = (int64_t)vd * EB <= kBinSmemBytes;
-  const int reps = dense ? max(1, min(max_reps, (int)(kBinSmemBytes / ((int64_t)vd * EB)))) : 1;
-  const int rep_log2 = dense ? 0 : hash_rep_log2;
-  const int TBL = dense ? (int)vd * reps : ((kBinSmemBytes / (EB + 4)) & ~31);
-  unsigned* tc = (unsigned*)smem;                  // TBL counts
-  unsigned* tlo = tc + TBL;                        // D x TBL low words
-  unsigned* thi = tlo + (size_t)D * TBL;           // D x TBL high words
-  uint32_t* tk = thi + (size_t)D * TBL;            // TBL keys (hash)
-  for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
-    tc[j] = 0u;
-#pragma unroll
-    for (int c = 0; c < D; ++c) tlo[c * TBL + j] = thi[c * TBL + j] = 0u;
-    if (!dense) tk[j] = EMPTY;
-  }
-  __syncthreads();
-  bool saw_miss = false, saw_nan = false;
-  // segments: dense tables hold one frame, so the range is cut at frame boundaries
-  int64_t s0 = p0;
-  while (s0 < p1) {
-    const int64_t fr = s0 / b.n;
-    const int64_t s1 = dense ? min(p1, (fr + 1) * b.n) : p1;
-    const uint32_t fbase = (uint32_t)(fr * b.vol_frame);
-    // frame tracking inside a hash segment (several frames)
-    int64_t hfr = (s0 + threadIdx.x) / b.n, hfr_end = (hfr + 1) * b.n;
-    uint32_t hbase = (uint32_t)(hfr * b.vol_frame);
-    T xn[RC];
-#pragma unroll
-    for (int c = 0; c < RC; ++c) xn[c] = (s0 + threadIdx.x < s1) ? pts[(s0 + threadIdx.x) * RC + c] : T(0);
-    // warp-uniform trip count so every lane takes part in the warp aggregation; the next
-    // round's coordinates are loaded before this round is processed
-    for (int64_t pr = s0; pr < s1; pr += blockDim.x) {
-      const int64_t p = pr + threadIdx.x;
-      const bool valid = p < s1;
-      T xc[RC];
-#pragma unroll
-      for (int c = 0; c < RC; ++c) xc[c] = xn[c];
-      const int64_t pn = p + blockDim.x;
-#pragma unroll
-      for (int c = 0; c < RC; ++c) xn[c] = pn < s1 ? pts[pn * RC + c] : T(0);
-      if (!dense) {
-        while (p >= hfr_end) {
-          ++hfr;
-          hfr_end += b.n;
-          hbase += vf;
-        }
+  auto point = [&](const T* xc, uint32_t i) {
+    uint32_t loc, dloc;
+    long long w[D];
+    const int st = bin_point<D, T, FAST>(xc, (sizeof(T) == 1 && D > 3) ? fpos0 + i : 0, im, P,
+                                         loc, dloc, w);
+    uint32_t key = EMPTY;
+    if (i < cnt) {
+      if (st == 0) {
+        if (DENSE || P.s16) slot16[i] = (uint16_t)loc;
+        else slot32[i] = fbase + loc;
+        key = DENSE ? dloc : fbase + loc;
+      } else {
+        saw |= st;
       }
-      const uint32_t base = dense ? fbase : hbase;
-      BinPt<D, T> o;
-      bin_point<D, T>(xc, (sizeof(T) == 1 && D > 3) ? p - (dense ? fr : hfr) * b.n : 0, im, g, o);
-      uint32_t key = EMPTY;
-      if (valid) {
-        if (o.ok) {
-          if (s16) slot16[p] = (uint16_t)o.loc;
-          else slot32[p] = base + o.loc;
-          key = dense ? o.dloc : base + o.loc;
-        } else {
-          saw_nan |= o.nonfinite;
-          saw_miss |= o.miss;
-        }
+    }
+    uint32_t my_cnt;
+    const bool act = warp_runs<D>(key, key != EMPTY, w, off, P.two_piece, my_cnt);
+    if constexpr (DENSE) {
+      if (act) {
+        const uint32_t a = ent_s + (rep_off + key) * (4 * EW);
+        reds_add(a, my_cnt);
+#pragma unroll
+        for (int c = 0; c < D; ++c) reds_add64(a + 4 + 8 * c, (unsigned long long)w[c]);
       }
-      uint32_t my_cnt;
-      const bool act = warp_runs<D>(key, key != EMPTY, o.q, two_piece, my_cnt);
+    } else {
       const unsigned am = __ballot_sync(kFull, act);
-      if (dense) {
-        if (act) {
-          const uint32_t e = (lane % (unsigned)reps) * vd + key;
-          atomicAdd(&tc[e], my_cnt);
-#pragma unroll
-          for (int c = 0; c < D; ++c)
-            smem_add64(&tlo[c * TBL + e], &thi[c * TBL + e], (unsigned long long)o.q[c]);
-        }
-      } else if (act) {
+      if (act) {
         // predicated probe loop, then the active lanes reconverge before the atomics (an
         // early-exit loop let the compiler replay the atomic sequence once per exit group)
-        const uint32_t tkey = (key << rep_log2) | (lane & ((1u << rep_log2) - 1u));
-        uint32_t hsh = __umulhi(tkey * 2654435761u, (unsigned)TBL);
+        const int rl = P.rep_log2;
+        const uint32_t tkey = (key << rl) | (lane & ((1u << rl) - 1u));
+        uint32_t hsh = __umulhi(tkey * 2654435761u, (unsigned)P.TBL);
         int hit = -1;
 #pragma unroll
         for (int probe = 0; probe < kBinProbes; ++probe) {
@@ -514,67 +515,154 @@ __global__ void __launch_bounds__(kBinThreads, 1)
             uint32_t k = tk[hsh];
             if (k == EMPTY) k = atomicCAS(&tk[hsh], EMPTY, tkey);
             if (k == EMPTY || k == tkey) hit = (int)hsh;
-            hsh = (hsh + 1 == (unsigned)TBL) ? 0u : hsh + 1;
+            hsh = (hsh + 1 == (unsigned)P.TBL) ? 0u : hsh + 1;
           }
         }
         __syncwarp(am);
         if (hit >= 0) {
-          atomicAdd(&tc[hit], my_cnt);
+          const uint32_t a = ent_s + (uint32_t)hit * (4 * EW);
+          reds_add(a, my_cnt);
+#pragma unroll
+          for (int c = 0; c < D; ++c) reds_add64(a + 4 + 8 * c, (unsigned long long)w[c]);
+        } else {
+          atomicAdd(&gcnt[key], my_cnt);
 #pragma unroll
           for (int c = 0; c < D; ++c)
-            smem_add64(&tlo[c * TBL + hit], &thi[c * TBL + hit], (unsigned long long)o.q[c]);
-        } else {
-          atomicAdd(&cnt[key], my_cnt);
-#pragma unroll
-          for (int c = 0; c < D; ++c) atomicAdd(&qs[(size_t)key * D + c], (unsigned long long)o.q[c]);
+            atomicAdd(&gqs[(size_t)key * D + c],
+                      (unsigned long long)(w[c] - (long long)my_cnt * off));
         }
       }
     }
+  };
+  auto load = [&](T* x, uint32_t i) {
+    const T* pp = src + (size_t)i * RC;
+#pragma unroll
+    for (int c = 0; c < RC; ++c) x[c] = i < cnt ? pp[c] : T(0);
+  };
+  // two rounds per trip (the prefetch registers swap roles instead of being copied); every
+  // lane runs both halves, so the warp aggregation always sees the whole warp
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 2 * B) {
+    const uint32_t i = i0 + threadIdx.x;
+    T xc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) xc[c] = xa[c];
+    load(xa, i + 2 * B);
+    point(xc, i);
+#pragma unroll
+    for (int c = 0; c < RC; ++c) xc[c] = xb[c];
+    load(xb, i + 3 * B);
+    point(xc, i + B);
+  }
+}
+
+template <int D, typename T, bool FAST, bool DENSE>
+__device__ __forceinline__ void bin_range(const T* __restrict__ pts, int64_t p0, int64_t p1,
+                                          const GsImg& im, const BinParams& P, unsigned* ent,
+                                          uint32_t* tk, void* __restrict__ slot,
+                                          uint32_t* __restrict__ gcnt,
+                                          unsigned long long* __restrict__ gqs, int& saw) {
+  constexpr int EW = 1 + 2 * D;
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t vd = P.vd;
+  const int reps = P.reps;
+  const uint32_t rep_off = DENSE ? (lane % (unsigned)reps) * vd : 0u;
+  const uint32_t ent_s = (uint32_t)__cvta_generic_to_shared(ent);
+  const unsigned long long off = (FAST || P.magic_ok) ? (unsigned long long)P.Mbits : 0ull;
+  // segments: one frame each (the dense table holds one frame; a segment's frame base is one
+  // constant), also cut every 2^28 points (32-bit offsets inside a segment)
+  int64_t s0 = p0;
+  int64_t fr = p0 / P.n;
+  while (s0 < p1) {
+    const int64_t s1 = min(min(p1, (int64_t)((fr + 1) * P.n)), s0 + (int64_t(1) << 28));
+    const uint32_t fbase = (uint32_t)(fr * P.vol_frame);
+    bin_segment<D, T, FAST, DENSE>(pts, s0, (uint32_t)(s1 - s0), fbase, s0 - fr * P.n, im, P,
+                                   ent_s, tk, rep_off, slot, gcnt, gqs, saw);
     __syncthreads();
-    if (dense) {  // flush this frame's table (replicas summed) and leave it zeroed
+    if (DENSE) {  // flush this frame's table (replicas summed) and leave it zeroed
       for (uint32_t j = threadIdx.x; j < vd; j += blockDim.x) {
         unsigned cn = 0;
-        for (int r = 0; r < reps; ++r) cn += tc[r * vd + j];
+        for (int r = 0; r < reps; ++r) cn += ent[(size_t)(r * vd + j) * EW];
         if (!cn) continue;
         uint32_t L = fbase, rem = j;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const uint32_t dr = rem / g.dstrd[c];
-          rem -= dr * g.dstrd[c];
-          L += (dr + GS_APRON) * g.strd[c];
+          const uint32_t dr = rem / P.dstrd[c];
+          rem -= dr * P.dstrd[c];
+          L += (dr + GS_APRON) * P.strd[c];
         }
-        atomicAdd(&cnt[L], cn);
-        for (int r = 0; r < reps; ++r) tc[r * vd + j] = 0u;
+        atomicAdd(&gcnt[L], cn);
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          unsigned long long sq = 0ull;
-          for (int r = 0; r < reps; ++r) {
-            const uint32_t e = r * vd + j;
-            sq += ((unsigned long long)thi[c * TBL + e] << 32) | tlo[c * TBL + e];
-            tlo[c * TBL + e] = thi[c * TBL + e] = 0u;
-          }
-          atomicAdd(&qs[(size_t)L * D + c], sq);
+          unsigned long long sq = 0ull - (unsigned long long)cn * off;  // sum(w) - count * off
+          for (int r = 0; r < reps; ++r) sq += bin_entry_sum(ent + (size_t)(r * vd + j) * EW, c);
+          atomicAdd(&gqs[(size_t)L * D + c], sq);
         }
+        for (int r = 0; r < reps; ++r)
+#pragma unroll
+          for (int k = 0; k < EW; ++k) ent[(size_t)(r * vd + j) * EW + k] = 0u;
       }
       __syncthreads();
     }
     s0 = s1;
-  }
-  if (saw_nan) atomicOr(err, 1);
-  if (saw_miss) atomicOr(err, errbit_box);
-  if (!dense) {
-    for (int j = threadIdx.x; j < TBL; j += blockDim.x) {
-      const uint32_t key = tk[j];
-      if (key == EMPTY) continue;
-      const int64_t L = key >> rep_log2;
-      atomicAdd(&cnt[L], tc[j]);
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-        atomicAdd(&qs[L * D + c], ((unsigned long long)thi[c * TBL + j] << 32) | tlo[c * TBL + j]);
-    }
+    if (s0 == (fr + 1) * P.n) ++fr;
   }
 }
 
+template <int D, typename T>
+__global__ void __launch_bounds__(kBinThreads, 1)
+    k_bin(const T* __restrict__ pts, int64_t ntot, const __grid_constant__ BinParams P,
+          uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs, void* __restrict__ slot,
+          int* err, int img_w) {
+  constexpr uint32_t EMPTY = 0xffffffffu;
+  constexpr int EW = 1 + 2 * D;
+  // CTA ranges start on multiples of 4 points (16-byte aligned rows of fp32 d = 3 features)
+  const int64_t per = ((ntot + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
+  const int64_t p0 = min(ntot, (int64_t)blockIdx.x * per);
+  const int64_t p1 = min(ntot, p0 + per);
+  __shared__ int s_err;
+  if (threadIdx.x == 0) s_err = *err;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* ent = (unsigned*)smem;
+  uint32_t* tk = ent + (size_t)EW * P.TBL;
+  for (int j = threadIdx.x; j < EW * P.TBL; j += blockDim.x) ent[j] = 0u;
+  if (!P.dense)
+    for (int j = threadIdx.x; j < P.TBL; j += blockDim.x) tk[j] = EMPTY;
+  __syncthreads();
+  if (s_err & GS_ERR_SKIP) return;  // non-finite input / box beyond the grid: nothing to bin
+  const GsImg im = gs_img(img_w, P.n);
+  int saw = 0;
+  bool done = false;
+  if constexpr (sizeof(T) == 4) {
+    if (P.f32fast) {
+      if (P.dense)
+        bin_range<D, T, true, true>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
+      else
+        bin_range<D, T, true, false>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
+      done = true;
+    }
+  }
+  if (!done) {
+    if (P.dense)
+      bin_range<D, T, false, true>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
+    else
+      bin_range<D, T, false, false>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
+  }
+  if (saw & 2) atomicOr(err, 1);
+  if (saw & 1) atomicOr(err, P.predicted ? 128 : 2);
+  if (!P.dense) {
+    const unsigned long long off = P.magic_ok ? (unsigned long long)P.Mbits : 0ull;
+    for (int j = threadIdx.x; j < P.TBL; j += blockDim.x) {
+      const uint32_t key = tk[j];
+      if (key == EMPTY) continue;
+      const int64_t L = key >> P.rep_log2;
+      const unsigned* e = ent + (size_t)j * EW;
+      atomicAdd(&cnt[L], e[0]);
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+        atomicAdd(&qs[L * D + c], bin_entry_sum(e, c) - (unsigned long long)e[0] * off);
+    }
+  }
+}
 
 // Predicted key box (no bounds pass): the box of the previous run of this shape.
 __global__ void k_box_set(GsBox b, GsBox* __restrict__ out, unsigned* epoch) {

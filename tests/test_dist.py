@@ -1,7 +1,6 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the frame-sharded driver: the sharded
-result must equal the single-process result frame for frame.  The per-rank clustering here
-is the CPU oracle (test infrastructure) so the test runs without a GPU; on the GPU box the
-same driver calls the engine (bench.py under torchrun)."""
+"""Multi-process (gloo) tests of the multi-GPU drivers: the sharded result must equal the
+single-process result frame for frame / point for point.  The CPU tests use the oracle (test
+infrastructure) as each rank's clusterer; the GPU tests run the engine on every rank."""
 import os
 import socket
 
@@ -60,6 +59,48 @@ def _worker(rank, world, port, nframes, outdir):
     np.savez(os.path.join(outdir, f"r{rank}.npz"), labels=out["labels"], first=out["first"],
              count=out["count"], k_all=out["k_all"], it_all=out["iterations_all"], tmax=t)
     dist.destroy_process_group()
+
+
+def _cluster_engine(X):
+    from paper_2206_02200_b200 import gridshift as G
+    eng = G.Engine(0)
+    r = eng.run_batch(X, G.EngineConfig(0.08, 50))
+    eng.close()
+    return r.labels, np.asarray(r.k), np.asarray(r.iterations)
+
+
+def _engine_worker(rank, world, port, nframes, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2206_02200_b200.dist import run_frames
+    out = run_frames(_frames, _cluster_engine, nframes)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), labels=out["labels"], first=out["first"],
+             count=out["count"], k_all=out["k_all"], it_all=out["iterations_all"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_frames_multi_rank_engine_matches_oracle(tmp_path, world):
+    """Frame sharding with the ENGINE as each rank's clusterer (all ranks on cuda:0: frames
+    are independent, so the ranks' kernels never wait on each other): every frame of every
+    shard equals the oracle, and the gathered per-frame k / iterations are complete."""
+    import torch.multiprocessing as mp
+    nframes = 7
+    mp.spawn(_engine_worker, args=(world, _free_port(), nframes, str(tmp_path)), nprocs=world,
+             join=True)
+    ref_labels, ref_k, ref_it = _cluster(_frames(0, nframes))
+    seen = 0
+    for r in range(world):
+        z = np.load(tmp_path / f"r{r}.npz")
+        f0, c = int(z["first"]), int(z["count"])
+        assert np.array_equal(z["labels"], ref_labels[f0:f0 + c])
+        assert np.array_equal(z["k_all"], ref_k)
+        assert np.array_equal(z["it_all"], ref_it)
+        seen += c
+    assert seen == nframes
 
 
 def test_two_rank_gloo_matches_single_process(tmp_path):

@@ -50,6 +50,14 @@ def small_inputs():
     out.append(("d4", rng.normal(0, 1, size=(4000, 4)), 0.6))
     out.append(("d6", rng.normal(0, 1, size=(3000, 6)), 0.9))
     out.append(("single", np.array([[1.0, 2.0, 3.0]]), 0.3))
+    # fp32 corner cases of the fast key path: signed zeros, exact multiples of h and their
+    # fp32 neighbours, values whose x/h lands within an ulp of an integer
+    z = np.array([-0.0, 0.0, -0.0, 0.0], np.float32)
+    m = (np.arange(-40, 41) * np.float32(0.08)).astype(np.float32)
+    near = np.concatenate([m, np.nextafter(m, np.float32(1e9)), np.nextafter(m, np.float32(-1e9))])
+    g3 = np.stack([np.resize(np.concatenate([z, near]), 400)] * 3, 1)
+    g3[:, 1] = g3[::-1, 1]
+    out.append(("f32_corners", np.ascontiguousarray(g3.astype(np.float32)), 0.08))
     return out
 
 
