@@ -178,6 +178,28 @@ gs_status gs_shard_run(gs_ctx* ctx, int64_t m_all, const uint32_t* keys, const u
                        const int64_t* sums, int64_t n_shard, const gs_config* cfg,
                        gs_result* out);
 
+/* ---- multi-GPU drivers: one host thread drives R ranks, each an engine
+ * context on its own device (devices may repeat: loopback ranks share a GPU).
+ *  gs_dist_run_frames: independent frames in contiguous blocks per rank (one host thread per
+ *    rank), no exchange -- replaces engine.run over a frame batch.
+ *  gs_dist_run_slabs: ONE cloud (batch 1, host memory, d <= 6) split into R contiguous point
+ *    shards; cells owned by dim-0 slabs of the global key box; per iteration the first key
+ *    layer of each slab goes to the rank below (old centroids), the sweep runs slab after slab
+ *    with the lower neighbour's swept last layer (the in-place lex sweep of SPEC.md:117-125
+ *    across slabs), cells whose new key leaves the slab migrate to its owner and every owner
+ *    folds its members in old global lex order (Eq. 3), has_converged sees the neighbours'
+ *    new boundary layers.  Labels, centroids, iterations and history are bit-identical to one
+ *    GPU clustering the whole cloud (gs_run).  Data moves are device-to-device peer copies.
+ * Results: out as gs_run's (labels of all points); centroids / history by gs_dist_get_*. */
+typedef struct gs_dist gs_dist;
+gs_status gs_dist_create(int ndev, const int* devices, gs_dist** out);
+void gs_dist_destroy(gs_dist* D);
+const char* gs_dist_last_error(const gs_dist* D);
+gs_status gs_dist_run_frames(gs_dist* D, const gs_input* in, const gs_config* cfg, gs_result* out);
+gs_status gs_dist_run_slabs(gs_dist* D, const gs_input* in, const gs_config* cfg, gs_result* out);
+gs_status gs_dist_get_centroids(gs_dist* D, int64_t frame, double* out, int64_t cap_k);
+gs_status gs_dist_get_history(gs_dist* D, int64_t* m_t, double* maxdisp_t, int32_t cap);
+
 /* ---- bandwidth sweep (reference module `metrics`) ----
  * gs_tune_bandwidth replaces tune_bandwidth(X, clusterer, h_grid) with the
  * GridShift engine as the clusterer and silhouette_subsampled as the score:

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <climits>
+#include <functional>
 #include <chrono>
 #include <mutex>
 #include <cmath>
@@ -143,7 +145,7 @@ struct gs_ctx {
   const uint32_t* shard_keys = nullptr;
   const uint32_t* shard_counts = nullptr;
   const int64_t* shard_sums = nullptr;
-  DevBuf xsum, pkeys, pcounts, psums;
+  DevBuf xsum, pkeys, pcounts, psums, npend;
   // pinned, device-mapped readback area: K7 stores the control block there (zero copy)
   void* pin = nullptr;
   void* pin_dev = nullptr;
@@ -685,8 +687,17 @@ gs_status launch_sweep_levels(gs_ctx* ctx, int d, int64_t m, const int32_t* eoff
 
 // Global path, d <= 6: neighbour lists at a fixed stride, then the single-CTA Kahn sweep with
 // the operand rows in L2 (gs_global.cuh).  Q = ctx->S1: rows [0, m) = S1 after the sweep.
+// own_lo/own_hi/halo (multi-GPU slabs, gs_dist): cells outside [own_lo, own_hi) are the
+// neighbouring slabs' boundary layers, frozen in the lists; `halo` writes their Q / P1 rows
+// between the lists and the sweep
+struct SweepHalo {
+  int own_lo = 0, own_hi = INT_MAX;
+  std::function<gs_status(double*)> rows;
+};
+
 template <int D>
-gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
+gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K, const SweepHalo* halo = nullptr) {
+  if (halo) GS_TRY(grow(ctx, ctx->npend, 4 * (size_t)m));
   cudaStream_t st = ctx->stream;
   const GsBox& b = ctx->box;
   const int KP = (K + 3) & ~3;
@@ -702,8 +713,11 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
       (int)m, b, K, KP, ctx->ckey[cur].as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(),
       ctx->S[cur].as<double>(), ctx->idx.as<int32_t>(), ctx->fdone.as<int32_t>(), lists,
       ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(), ctx->den.as<uint32_t>(),
-      ctx->rden.as<double>(), Q, ctx->fm.as<int32_t>());
+      ctx->rden.as<double>(), Q, ctx->fm.as<int32_t>(), halo ? halo->own_lo : 0,
+      halo ? halo->own_hi : INT_MAX, halo ? ctx->npend.as<int32_t>() : nullptr);
+  const int32_t* pinit = halo ? ctx->npend.as<int32_t>() : nullptr;
   GS_LAUNCHED("k_nbr_lists");
+  if (halo && halo->rows) GS_TRY(halo->rows(Q));
   constexpr size_t kBudget = 220 * 1024;
   const size_t smem = 4 * ((size_t)(m + 3) / 4 + 1) + 2 * (size_t)m;
   const int in_smem = (m < 65536 && smem <= kBudget) ? 1 : 0;
@@ -743,7 +757,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
             (const int32_t*)ctx->nbn.as<int32_t>(), (const int32_t*)ctx->nbe.as<int32_t>(),
             (const uint32_t*)ctx->ccnt[cur].as<uint32_t>(),
             (const uint32_t*)ctx->den.as<uint32_t>(), (const double*)ctx->rden.as<double>(), Q,
-            ctx->errflag.as<int>(), flow_sleep, flow_fence);
+            ctx->errflag.as<int>(), flow_sleep, flow_fence, pinit);
         if (le == cudaSuccess) {
           GS_LAUNCHED("k_sweep_flow");
           return GS_OK;
@@ -792,7 +806,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
                                           (const int32_t*)ctx->nbe.as<int32_t>(),
                                           (const uint32_t*)ctx->ccnt[cur].as<uint32_t>(),
                                           (const uint32_t*)ctx->den.as<uint32_t>(),
-                                          (const double*)ctx->rden.as<double>(), Q, cprof);
+                                          (const double*)ctx->rden.as<double>(), Q, cprof, pinit);
       if (le == cudaSuccess) {
         GS_LAUNCHED("k_sweep_cluster");
         if (ctrace) {  // diagnostics: per-level split, max over CTAs
@@ -838,7 +852,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
   gs::k_sweep_global<D><<<1, gs::sweep_global_threads<D>(), in_smem ? smem : 0, st>>>(
       (int)m, KP, lists, ctx->nbn.as<int32_t>(), ctx->nbe.as<int32_t>(),
       ctx->ccnt[cur].as<uint32_t>(), ctx->den.as<uint32_t>(), ctx->rden.as<double>(), Q,
-      ctx->lvl.as<unsigned>(), ctx->order.as<unsigned>(), in_smem, prof);
+      ctx->lvl.as<unsigned>(), ctx->order.as<unsigned>(), in_smem, prof, pinit);
   GS_LAUNCHED("k_sweep_global");
   if (trace) {  // diagnostics: per-level update / release / barrier split of this sweep
     std::vector<long long> h(2000 * 66 + 8);
@@ -870,11 +884,12 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K) {
   return GS_OK;
 }
 
-gs_status launch_global_sweep(gs_ctx* ctx, int d, int64_t m, int K) {
+gs_status launch_global_sweep(gs_ctx* ctx, int d, int64_t m, int K,
+                              const SweepHalo* halo = nullptr) {
   switch (d) {
 #define GS_CASE(D) \
   case D:          \
-    return launch_global_sweep_d<D>(ctx, m, K);
+    return launch_global_sweep_d<D>(ctx, m, K, halo);
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
 #undef GS_CASE
   }
@@ -1402,7 +1417,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     }
     GS_TRY(rec_event(ctx, 1));
     const gs_status sf = launch_nscale(ctx, dpts, in->dtype, d, n, nf, cfg->h, vol_hint,
-                                       ctx->host_src ? nullptr : pb);
+                                       pb);
     ctx->host_src = nullptr;
     GS_TRY(sf);
     GS_TRY(rec_event(ctx, 2));
@@ -2064,7 +2079,7 @@ void gs_destroy(gs_ctx* ctx) {
                     &ctx->bpart, &ctx->cub_tmp, &ctx->dbg, &ctx->modes, &ctx->tiles,
                     &ctx->dbox, &ctx->erec, &ctx->lprod, &ctx->rden, &ctx->lvl,
                     &ctx->lsucc, &ctx->order, &ctx->xsum, &ctx->pkeys, &ctx->pcounts,
-                    &ctx->psums, &ctx->epoch_dev, &ctx->fswept, &ctx->fout, &ctx->ctl})
+                    &ctx->psums, &ctx->npend, &ctx->epoch_dev, &ctx->fswept, &ctx->fout, &ctx->ctl})
     b->release();
   for (auto& b : ctx->stage) b.release();
   if (ctx->copy_stream) {
@@ -2589,3 +2604,6 @@ gs_status gs_debug_resident_once(gs_ctx* ctx, int32_t d, double h, int64_t m, co
 }
 
 }  // extern "C"
+
+// ---- multi-GPU drivers (gs_dist_*)
+#include "gs_dist.cuh"

@@ -14,6 +14,8 @@
 
 #include <cooperative_groups.h>
 
+#include <climits>
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -53,9 +55,14 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
                             uint32_t* __restrict__ lists, int32_t* __restrict__ nbn,
                             int32_t* __restrict__ nbe, uint32_t* __restrict__ den,
                             double* __restrict__ rden, double* __restrict__ Q,
-                            int32_t* __restrict__ fm) {
+                            int32_t* __restrict__ fm, int own_lo = 0, int own_hi = INT_MAX,
+                            int32_t* __restrict__ npend = nullptr) {
   // probes in batches of 27 from a shared offset table: the loads of a batch are independent
   // (one L2 round trip per batch instead of one per probe behind the odometer and the stores)
+  // own_lo/own_hi (multi-GPU slabs, gs_dist): cells outside [own_lo, own_hi) are halo cells
+  // of the neighbouring slabs -- frozen here (their rows are written by the caller); npend =
+  // the own earlier neighbours, the sweep's pending counts (an own cell does not wait on the
+  // lower halo: it is final before this slab's sweep starts)
   constexpr int KMAX = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 : 729;
   constexpr int B = KMAX < 27 ? KMAX : 27;
   __shared__ int offs[KMAX];
@@ -68,14 +75,15 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
   const int64_t L = ckey[i];
   const int64_t f = L / b.vol_frame;
   uint32_t* li = lists + (int64_t)i * KP;
-  if (fdone[f]) {
+  if (fdone[f] || i < own_lo || i >= own_hi) {
     nbn[i] = nbe[i] = 0;
+    if (npend) npend[i] = 0;
     den[i] = ccnt[i];
     for (int c = 0; c < D; ++c) Q[(int64_t)i * D + c] = S0[(int64_t)i * D + c];
     return;
   }
   atomicAdd(&fm[f], 1);
-  int n = 0, e = 0;
+  int n = 0, e = 0, eo = 0;
   uint32_t s = 0;
   const uint32_t P1ROW = (uint32_t)m + 1u, ZROW = (uint32_t)m;
   for (int t0 = 0; t0 < KMAX; t0 += B) {
@@ -92,11 +100,13 @@ __global__ void k_nbr_lists(int m, GsBox b, int K, int KP, const uint32_t* __res
       s += cb[u];
       li[n++] = j < i ? P1ROW + (uint32_t)j : (uint32_t)j;
       e += j < i;
+      eo += j < i && j >= own_lo;
     }
   }
   for (int t = n; t < KP; ++t) li[t] = ZROW;
   nbn[i] = n;
   nbe[i] = e;
+  if (npend) npend[i] = eo;
   den[i] = s;
   rden[i] = __drcp_rn((double)s);
   const double ci = (double)ccnt[i];
@@ -120,7 +130,8 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
     const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
     const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q,
-    unsigned* pend_g, unsigned* queue_g, int in_smem, long long* prof = nullptr) {
+    unsigned* pend_g, unsigned* queue_g, int in_smem, long long* prof = nullptr,
+    const int32_t* __restrict__ pinit = nullptr) {
   // prof (diagnostics, GS_TRACE_GLOBAL): per level [width, start, per-warp update end x 32,
   // per-warp release end x 32] clock stamps, plain stores (no atomics on the path)
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -140,7 +151,7 @@ __global__ void __launch_bounds__(sweep_global_threads<D>(), 1) k_sweep_global(
   for (int w = tid; w < (m + 3) / 4; w += T) pend[w] = 0u;
   __syncthreads();
   for (int i = tid; i < m; i += T) {
-    const int e = nbe[i];
+    const int e = pinit ? pinit[i] : nbe[i];  // pending predecessors
     if (e > 0) atomicAdd(&pend[i >> 2], (unsigned)e << (8 * (i & 3)));
     else q_put(atomicAdd(&tail, 1), i);
   }
@@ -439,7 +450,7 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
     const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
     const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q,
-    long long* prof = nullptr) {
+    long long* prof = nullptr, const int32_t* __restrict__ pinit = nullptr) {
   // prof (diagnostics, GS_TRACE_GLOBAL): per level and CTA [width, start, update end,
   // release end, barrier end] clock stamps (an extra block barrier after the update)
   namespace cg = cooperative_groups;
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(sweep_cluster_threads<D>(), 1) k_sweep_cluster
   for (int t = tid; t < mloc; t += T) {
     const int i = rank + NC * t;
     if (i >= m) break;
-    const int e = nbe[i];
+    const int e = pinit ? pinit[i] : nbe[i];  // pending predecessors
     pend[t] = (unsigned)e;
     if (e == 0) qbuf0[atomicAdd(&tails[0], 1u)] = (unsigned)i;
   }
@@ -715,7 +726,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
     int m, int KP, const uint32_t* __restrict__ lists, const int32_t* __restrict__ nbn,
     const int32_t* __restrict__ nbe, const uint32_t* __restrict__ ccnt,
     const uint32_t* __restrict__ den, const double* __restrict__ rden, double* Q, int* err,
-    int flow_sleep, int flow_fence) {
+    int flow_sleep, int flow_fence, const int32_t* __restrict__ pinit = nullptr) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int NC = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
@@ -733,7 +744,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
   __syncthreads();
   for (int t = tid; t < own_n; t += T) {
     const int i = rank + NC * t;
-    const int e = nbe[i];
+    const int e = pinit ? pinit[i] : nbe[i];  // pending predecessors
     pend[t] = (unsigned)e;
     if (e == 0) queue[atomicAdd(&tail, 1u)] = i;
   }

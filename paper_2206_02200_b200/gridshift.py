@@ -103,6 +103,8 @@ EXPORTED = [
     "gs_shard_run", "gs_render", "gs_tuner_create", "gs_tuner_destroy", "gs_tuner_last_error",
     "gs_tune_bandwidth", "gs_silhouette_subsampled", "gs_tracker_create", "gs_tracker_destroy",
     "gs_tracker_last_error", "gs_track_init", "gs_track_sequence", "gs_mspp_run",
+    "gs_dist_create", "gs_dist_destroy", "gs_dist_last_error", "gs_dist_run_frames",
+    "gs_dist_run_slabs", "gs_dist_get_centroids", "gs_dist_get_history",
 ]
 
 
@@ -191,6 +193,15 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.gs_silhouette_subsampled.argtypes = [P, C.POINTER(GsInput), P, I32, I64, C.c_uint64,
                                              C.POINTER(D)]
     lib.gs_mspp_run.argtypes = [P, C.POINTER(GsInput), D, D, I32, C.POINTER(GsResult), P]
+    lib.gs_dist_create.argtypes = [C.c_int, P, C.POINTER(P)]
+    lib.gs_dist_destroy.argtypes = [P]
+    lib.gs_dist_destroy.restype = None
+    lib.gs_dist_last_error.argtypes = [P]
+    lib.gs_dist_last_error.restype = C.c_char_p
+    lib.gs_dist_run_frames.argtypes = [P, C.POINTER(GsInput), C.POINTER(GsConfig), C.POINTER(GsResult)]
+    lib.gs_dist_run_slabs.argtypes = [P, C.POINTER(GsInput), C.POINTER(GsConfig), C.POINTER(GsResult)]
+    lib.gs_dist_get_centroids.argtypes = [P, I64, P, I64]
+    lib.gs_dist_get_history.argtypes = [P, P, P, I32]
     lib.gs_tracker_create.argtypes = [C.c_int, C.POINTER(P)]
     lib.gs_tracker_destroy.argtypes = [P]
     lib.gs_tracker_destroy.restype = None
@@ -532,6 +543,85 @@ class Engine:
         mn = mo.value
         return dict(keys=ko[:mn], counts=co[:mn], centroids=so[:mn], parent=par,
                     stop=bool(stop.value), maxdisp=md.value)
+
+
+class Dist:
+    """Multi-GPU driver (gridshift_c.h gs_dist_*): one host thread drives R ranks, each an
+    engine context on devices[r] (a device may repeat: loopback ranks share a GPU)."""
+
+    def __init__(self, devices):
+        self._lib = load_library()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _raise(self._lib.gs_dist_create(len(devices), devs, C.byref(h)), "gs_dist_create")
+        self._d = h
+        self.R = len(devices)
+
+    def close(self) -> None:
+        if getattr(self, "_d", None):
+            self._lib.gs_dist_destroy(self._d)
+            self._d = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, status: int) -> None:
+        _raise(status, self._lib.gs_dist_last_error(self._d).decode() if self._d else "")
+
+    @staticmethod
+    def _input(X):
+        X = np.ascontiguousarray(X)
+        dt = GS_F32 if X.dtype == np.float32 else GS_F64
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        return X, dt
+
+    def run_slabs(self, X: np.ndarray, cfg: EngineConfig) -> ClusterLabeling:
+        """ONE cloud X[n, d] over the ranks: point shards, dim-0 slab ownership of the cells,
+        per-iteration halo exchange; equal to Engine.run on one GPU."""
+        X, dt = self._input(X)
+        n, d = X.shape
+        labels = np.zeros(n, np.int32)
+        k = np.zeros(1, np.int64)
+        it = np.zeros(1, np.int32)
+        cv = np.zeros(1, np.int32)
+        flags = (GS_RECORD_HISTORY if cfg.record_history else 0) | cfg.debug_flags
+        inp = GsInput(X.ctypes.data, n, d, dt, 1, 0, 0)
+        c = GsConfig(cfg.h, cfg.max_iterations, flags)
+        res = GsResult(labels.ctypes.data, k.ctypes.data, it.ctypes.data, cv.ctypes.data)
+        self._check(self._lib.gs_dist_run_slabs(self._d, C.byref(inp), C.byref(c), C.byref(res)))
+        cen = np.zeros((int(k[0]), d), np.float64)
+        self._check(self._lib.gs_dist_get_centroids(self._d, 0, cen.ctypes.data, int(k[0])))
+        hist = None
+        if cfg.record_history:
+            mt = np.zeros(int(it[0]), np.int64)
+            md = np.zeros(int(it[0]), np.float64)
+            self._check(self._lib.gs_dist_get_history(self._d, mt.ctypes.data, md.ctypes.data,
+                                                      int(it[0])))
+            hist = [(int(a), float(b)) for a, b in zip(mt, md)]
+        return ClusterLabeling(labels, cen, int(it[0]), bool(cv[0]), hist)
+
+    def run_frames(self, X: np.ndarray, cfg: EngineConfig) -> BatchLabeling:
+        """Independent frames X[batch, n, d] in contiguous blocks per rank."""
+        X, dt = self._input(X)
+        b, n, d = X.shape
+        labels = np.zeros((b, n), np.int32)
+        k = np.zeros(b, np.int64)
+        it = np.zeros(b, np.int32)
+        cv = np.zeros(b, np.int32)
+        inp = GsInput(X.ctypes.data, n, d, dt, b, 0, 0)
+        c = GsConfig(cfg.h, cfg.max_iterations, cfg.debug_flags)
+        res = GsResult(labels.ctypes.data, k.ctypes.data, it.ctypes.data, cv.ctypes.data)
+        self._check(self._lib.gs_dist_run_frames(self._d, C.byref(inp), C.byref(c), C.byref(res)))
+        out = BatchLabeling(labels, k, it, cv)
+        for f in range(b):
+            cen = np.zeros((int(k[f]), d), np.float64)
+            self._check(self._lib.gs_dist_get_centroids(self._d, f, cen.ctypes.data, int(k[f])))
+            out.centroids.append(cen)
+        return out
 
 
 _default_engine: Optional[Engine] = None

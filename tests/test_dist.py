@@ -245,3 +245,53 @@ def test_cloud_multi_rank_engine_matches_single_gpu(tmp_path, kind, world):
     ref = eng.run(_cloud(kind=kind), G.EngineConfig(1.0, 100))
     _check_cloud(str(tmp_path), world, ref.labels, ref.centroids, ref.iterations)
     eng.close()
+
+
+# ---------------------------------------------------------------- gs_dist (one process, R ranks)
+def _blobs2(n=5000, seed=9):
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(0, 8, size=(5, 2))
+    return c[rng.integers(0, 5, n)] + rng.normal(0, 0.5, size=(n, 2))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,world", [("small", 2), ("small", 3), ("blobs2", 2), ("blobs2", 4),
+                                        ("cfg5", 2), ("cfg5", 3)])
+def test_dist_slabs_match_single_gpu(kind, world):
+    """gs_dist_run_slabs: one cloud, points sharded over R loopback ranks on cuda:0, cells owned
+    by dim-0 slabs with the per-iteration halo exchange (swept lower layer, old upper layer),
+    migration of rehomed cells and the ordered merge -- labels, centroid bits, iterations and
+    history equal to one GPU clustering the whole cloud."""
+    from paper_2206_02200_b200 import gridshift as G
+    X = _blobs2() if kind == "blobs2" else _cloud(kind=kind)
+    h = 0.4 if kind == "blobs2" else 1.0
+    cfg = G.EngineConfig(h, 100, record_history=True)
+    eng = G.Engine(0)
+    ref = eng.run(X, cfg)
+    eng.close()
+    D = G.Dist([0] * world)
+    got = D.run_slabs(X, cfg)
+    D.close()
+    assert got.iterations == ref.iterations
+    assert got.converged == ref.converged
+    assert np.array_equal(got.labels, ref.labels)
+    assert np.array_equal(got.centroids.view(np.int64), ref.centroids.view(np.int64))
+    assert got.history == ref.history
+
+
+@pytest.mark.gpu
+def test_dist_frames_match_single_gpu():
+    """gs_dist_run_frames: frame blocks per rank (one host thread each), equal to one batch."""
+    from paper_2206_02200_b200 import gridshift as G
+    X = _frames(0, 7)
+    cfg = G.EngineConfig(0.08, 50)
+    eng = G.Engine(0)
+    ref = eng.run_batch(X, cfg)
+    eng.close()
+    D = G.Dist([0, 0, 0])
+    got = D.run_frames(X, cfg)
+    D.close()
+    assert np.array_equal(got.labels, ref.labels)
+    assert np.array_equal(got.k, ref.k) and np.array_equal(got.iterations, ref.iterations)
+    for f in range(X.shape[0]):
+        assert np.array_equal(got.centroids[f].view(np.int64), ref.centroids[f].view(np.int64))
