@@ -728,6 +728,9 @@ def main():
                         f"replicated iteration)") if shard_cloud else
                        (f"{B} of the {cfg.batch} frames on this rank (frame shards x{world})"
                         if args.workload == "cfg4" else f"replicas x{world}"),
+        "step_ms_dist": {"min": float(np.min(ms_dev)), "median": float(np.median(ms_dev)),
+                         "max": float(np.max(ms_dev)),
+                         "e2e_median": float(np.median(ms_e2e))},
         "cell_updates_per_s": cells / (it_ms / 1e3) if it_ms > 0 else None,
         "cells_swept_per_step": s0["cells_swept"], "m0": s0["m0"], "k": s0["k_total"],
         "iterations": s0["max_iterations"],

@@ -169,6 +169,16 @@ struct gs_ctx {
   int shape_ms = 0;
   GsBox shape_box{};
   int64_t shape_vol_frame = 0;
+  // a few recent shapes (a whole-batch call and the frame groups of a host batch alternate)
+  struct ShapeEntry {
+    ShapeKey key;
+    int ms = 0;
+    GsBox box{};
+    int64_t vol_frame = 0;
+    uint64_t used = 0;
+  };
+  ShapeEntry shapes[4];
+  uint64_t shape_tick = 0;
   // CUDA graph of the optimistic run for one (shape, caller buffers) combination
   struct GraphKey {
     ShapeKey shape;
@@ -1424,6 +1434,18 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
     return GS_OK;
   };
   const gs_ctx::ShapeKey key{n, nf, d, in->dtype, cfg->h, cfg->max_iter, ctx->img_w};
+  gs_ctx::ShapeEntry* sent = nullptr;  // this shape's cache entry, if any
+  for (auto& e : ctx->shapes)
+    if (e.ms > 0 && e.key == key) sent = &e;
+  if (sent) {
+    ctx->shape = key;
+    ctx->shape_ms = sent->ms;
+    ctx->shape_box = sent->box;
+    ctx->shape_vol_frame = sent->vol_frame;
+    sent->used = ++ctx->shape_tick;
+  } else {
+    ctx->shape_ms = 0;
+  }
   std::vector<int32_t> g_iters(nf, 0);
   int64_t swept = 0;
   GS_TRY(choose_pbox());
@@ -1484,6 +1506,7 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       // a point outside the predicted box: redo the run with the bounds pass (below)
     } else if ((rb.err[0] & 32) || rb.ctr[4] != 0) {  // grid too small / a frame too big: redo it
       ctx->shape_ms = 0;                        // synchronously below
+      if (sent) sent->ms = 0;
       if (rb.err[0] & 32) GS_TRY(grow_dense_for(ctx, *(long long*)(rb.err + 2), d));
     } else {
       goto results;
@@ -1602,6 +1625,13 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
       ctx->shape_ms = std::min(ms_cap, 2 * ms_run);  // headroom for data-dependent m0
       ctx->shape_box = b;
       ctx->shape_vol_frame = b.vol_frame;
+      gs_ctx::ShapeEntry* e = sent;
+      if (!e) {  // least recently used entry
+        e = &ctx->shapes[0];
+        for (auto& x : ctx->shapes)
+          if (x.used < e->used) e = &x;
+      }
+      *e = gs_ctx::ShapeEntry{key, ctx->shape_ms, b, b.vol_frame, ++ctx->shape_tick};
     }
     GS_TRY(launch_tail(ctx, cfg, nf, ntot, d, ms_run, false, iter == 0, out->labels, dev_out,
                        rec, rb));

@@ -249,14 +249,18 @@ __device__ __forceinline__ bool gs_bin_floor(double x, double inv_h, double& fl)
 // is rint(v) - kmin + 1.5*2^23 for the exact product v = x*ihf (ihf = RN32(1/h), |v - x/h| <=
 // |x/h| 2^-23.9) while |v - kmin| < 2^22; nr = C - u = -rint(v) exactly; d = RN(v - rint(v)).
 // When |d| > |rint(v)| 2^-20, x/h lies on v's side of the integer rint(v), so floor(x/h) ==
-// floor(RN64(x/h)) == rint(v) - (d < 0) (pin P1); x == +-0 gives 0.  Outside the magic range the
-// decoded key lies beyond the box (the host enables this path only for extents < 2^21), so the
-// point is flagged, never mis-binned.  Returns the key relative to the box origin.
-__device__ __forceinline__ int gs_bin_rel_f32(float x, float ihf, float C, bool& fine) {
+// floor(RN64(x/h)) == rint(v) - (d < 0) (pin P1); x == +-0 gives 0.  The test uses the launch
+// constant thr = (max |key of the box| + 2) * 2^-20 >= |rint(v)| 2^-20 for every point in or
+// next to the box (one compare instead of a multiply and two compares); a point farther out
+// may take a key off by one, which is still outside the box and flagged.  Outside the magic
+// range the decoded key lies beyond the box (the host enables this path only for extents
+// < 2^21), so the point is flagged, never mis-binned.  Returns the key relative to the box
+// origin.
+__device__ __forceinline__ int gs_bin_rel_f32(float x, float ihf, float C, float thr, bool& fine) {
   const float u = __fmaf_rn(x, ihf, C);
   const float nr = __fsub_rn(C, u);
   const float d = __fmaf_rn(x, ihf, nr);  // (-0 + +0 = +0: x == -0 gives key 0)
-  fine = fabsf(d) > __fmul_rn(fabsf(nr), 0x1p-20f) || x == 0.0f;
+  fine = (fabsf(d) > thr) | (x == 0.0f);
   return (__float_as_int(u) - 0x4B400000) + (__float_as_int(d) >> 31);
 }
 
@@ -266,7 +270,7 @@ struct BinParams {
   double h, inv_h, scale, Mq;  // Mq = 1.5*2^(52-F): RN(d + Mq) - Mq = RN to the 2^-F grid
   long long Mbits;             // bits of Mq: table sums carry count * Mbits, removed at flush
   long long n, vol_frame;
-  float ihf;
+  float ihf, thr;               // thr: fp32 key fineness threshold (gs_bin_rel_f32)
   int magic_ok, two_piece, f32fast, dense, reps, TBL, rep_log2, s16, predicted;
   uint32_t vd;                 // cells of a frame's data box
   float Cf[GS_DMAX];           // 1.5*2^23 - kmin (fp32 fast key)
@@ -302,6 +306,10 @@ inline BinParams make_bin_params(const GsBox& b, int max_reps, int hash_rep_log2
     vd *= P.span[c];
   }
   P.vd = vd;
+  int64_t kmax = 0;
+  for (int c = 0; c < D; ++c)
+    kmax = std::max<int64_t>(kmax, std::max(std::llabs(b.kmin[c]), std::llabs(b.kmin[c] + b.ext[c])));
+  P.thr = std::ldexp((float)(kmax + 2), -20);
   P.s16 = b.vol_frame <= 65536;
   // dense data box (with replicas) when it fits and the frame's cells fit u16 slots
   constexpr int EW = 1 + 2 * D;
@@ -329,7 +337,7 @@ __device__ __forceinline__ int bin_point(const T* xc, int64_t pl, const GsImg& i
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       bool f;
-      rel[c] = gs_bin_rel_f32(xc[c], P.ihf, P.Cf[c], f);
+      rel[c] = gs_bin_rel_f32(xc[c], P.ihf, P.Cf[c], P.thr, f);
       fine &= f;
       fl[c] = (double)(rel[c] + P.kmin32[c]);
       xs[c] = (double)xc[c];
