@@ -216,13 +216,16 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
 //  * hash: open addressing over (global cell index), bounded probes, global atomics on a miss
 //    (clouds whose box is far larger than a CTA's table: cfg5).
 // 64-bit shared adds are two native 32-bit atomics with the carry of the low word (sm_100 has no
-// 64-bit shared add; atomicAdd(u64) compiles to a CAS loop).  Low and high words live in
-// separate arrays (SoA), so a warp's entries spread over the banks.
+// 64-bit shared add; atomicAdd(u64) compiles to a CAS loop).  An entry is EW = 1 + 2D words
+// [count, lo_0, hi_0, ...]: an odd word stride, so random entries spread over the banks.
 //
 // Predicted box (`predicted` != 0): the key box is the one the previous run of this shape used
 // (no bounds pass); a point outside it sets err bit 128 (the host clears the grid and reruns
 // with the bounds pass) and a non-finite coordinate sets bit 1.
-constexpr int kBinThreads = 1024;
+#ifndef GS_BIN_THREADS
+#define GS_BIN_THREADS 1024  // (experiments override it at build time)
+#endif
+constexpr int kBinThreads = GS_BIN_THREADS;
 constexpr int kBinProbes = 4;  // hash probe budget before the point takes the global atomics
 constexpr int kAggRuns = 4;    // warp aggregation when the warp's keys form <= this many runs
 constexpr int kBinSmemBytes = 224 * 1024;
