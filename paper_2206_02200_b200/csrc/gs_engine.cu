@@ -146,6 +146,9 @@ struct gs_ctx {
   const uint32_t* shard_counts = nullptr;
   const int64_t* shard_sums = nullptr;
   DevBuf xsum, pkeys, pcounts, psums, npend;
+  // component sweep of the global path (gs_global.cuh k_cc_* / k_sweep_comp)
+  DevBuf ccpar, ccsize, cccur, ccoff, ccmem, ccloc, ccdesc, ccctr, ccgs;
+  bool comp_ok = true;  // the component sweep can be launched on this device
   // pinned, device-mapped readback area: K7 stores the control block there (zero copy)
   void* pin = nullptr;
   void* pin_dev = nullptr;
@@ -728,6 +731,68 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K, const SweepHalo* 
   const int32_t* pinit = halo ? ctx->npend.as<int32_t>() : nullptr;
   GS_LAUNCHED("k_nbr_lists");
   if (halo && halo->rows) GS_TRY(halo->rows(Q));
+  const uint32_t dbg0 = ctx->sweep_flags;
+  if constexpr (D <= 3) {
+    // the component sweep (r2): connected components of the active cells swept independently,
+    // one CTA each with everything in shared memory, when every component fits a CTA
+    if (!halo && ctx->comp_ok &&
+        !(dbg0 & (GS_DEBUG_SWEEP_FLOW | GS_DEBUG_SWEEP_LEVELS | GS_DEBUG_SWEEP_SINGLE)) &&
+        m <= gs::kCcMaxCells) {
+      for (DevBuf* bb : {&ctx->ccpar, &ctx->cccur, &ctx->ccoff, &ctx->ccmem})
+        GS_TRY(grow(ctx, *bb, 4 * (size_t)m));
+      GS_TRY(grow(ctx, ctx->ccloc, 4 * (size_t)m * D));   // box min corners (per root)
+      GS_TRY(grow(ctx, ctx->ccsize, 4 * (size_t)m * D));  // box max corners (per root)
+      GS_TRY(grow(ctx, ctx->ccgs, 4 * (size_t)m));        // component sizes (per root)
+      GS_TRY(grow(ctx, ctx->ccdesc, 16 * (size_t)m));
+      GS_TRY(grow(ctx, ctx->ccctr, 32));
+      int32_t* root = ctx->ccpar.as<int32_t>();
+      static std::atomic<uint64_t> done_s{0};
+      const unsigned mb0 = blocks_for(m, 256);
+      gs::k_cc_init<D><<<mb0, 256, 0, st>>>((int)m, KP, lists, ctx->nbe.as<int32_t>(), root,
+                                            ctx->ccgs.as<int32_t>(), ctx->cccur.as<int32_t>(),
+                                            ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>());
+      GS_LAUNCHED("k_cc_init");
+      for (int jp = 0; jp < 2; ++jp) {
+        gs::k_cc_jump<<<mb0, 256, 0, st>>>((int)m, root);
+        GS_LAUNCHED("k_cc_jump");
+      }
+      gs::k_cc_hook<D><<<mb0, 256, 0, st>>>((int)m, KP, lists, ctx->nbe.as<int32_t>(), root);
+      GS_LAUNCHED("k_cc_hook");
+      gs::k_cc_count<D><<<mb0, 256, 0, st>>>((int)m, b, ctx->ckey[cur].as<uint32_t>(), root,
+                                             ctx->ccgs.as<int32_t>(), ctx->ccloc.as<int32_t>(),
+                                             ctx->ccsize.as<int32_t>());
+      GS_LAUNCHED("k_cc_count");
+      gs::k_cc_plan<D><<<1, 1024, 0, st>>>((int)m, ctx->ccgs.as<int32_t>(),
+                                           ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>(),
+                                           ctx->ccoff.as<int32_t>(), ctx->ccdesc.as<int32_t>(),
+                                           ctx->ccctr.as<long long>());
+      GS_LAUNCHED("k_cc_plan");
+      long long plan[3] = {0, 0, 0};
+      GS_CK(cudaMemcpyAsync(plan, ctx->ccctr.p, sizeof(plan), cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaStreamSynchronize(st));
+      const int ncomp = (int)plan[0], maxsz = (int)plan[1];
+      const size_t csm = (size_t)plan[2];
+      constexpr size_t kCompBudget = 224 * 1024;
+      if (ncomp == 0) return GS_OK;  // every cell isolated or frozen: Q rows are final (P3)
+      if (csm <= kCompBudget && maxsz < 65535) {
+        const unsigned mb = blocks_for(m, 256);
+        gs::k_cc_scatter<<<mb, 256, 0, st>>>((int)m, root, ctx->ccoff.as<int32_t>(),
+                                             ctx->cccur.as<int32_t>(), ctx->ccmem.as<int32_t>());
+        GS_LAUNCHED("k_cc_scatter");
+        GS_CK(attr_once(done_s, ctx->device, gs::k_sweep_comp<D>, (int)kCompBudget));
+        gs::k_sweep_comp<D><<<(unsigned)ncomp, 256, csm, st>>>(
+            (int)m, b, ctx->ccdesc.as<int32_t>(), ctx->ccmem.as<int32_t>(),
+            ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>(), ctx->ckey[cur].as<uint32_t>(),
+            ctx->ccnt[cur].as<uint32_t>(), Q);
+        const cudaError_t le = cudaGetLastError();
+        if (le == cudaSuccess) {
+          GS_LAUNCHED("k_sweep_comp");
+          return GS_OK;
+        }
+        ctx->comp_ok = false;  // cannot be launched here: the cluster sweeps from now on
+      }
+    }
+  }
   constexpr size_t kBudget = 220 * 1024;
   const size_t smem = 4 * ((size_t)(m + 3) / 4 + 1) + 2 * (size_t)m;
   const int in_smem = (m < 65536 && smem <= kBudget) ? 1 : 0;

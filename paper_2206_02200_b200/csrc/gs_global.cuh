@@ -839,4 +839,374 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
   cluster.sync();  // no CTA exits while others may still touch its shared memory
 }
 
+// ---------------------------------------------------------------- component sweep (r2)
+// Eq. (5)'s sweep couples a cell only to its active neighbours, so the connected components
+// of the active cells (adjacency = the 3^d neighbourhood) are swept independently: the
+// sequential lexicographic sweep restricted to one component performs exactly the same
+// updates, with the same operands in the same order, as the sweep over all cells.  cfg5's
+// first iteration has 62 components of <= 4,095 cells and a 125-level DAG; the cluster sweep
+// pays ~8.6 K cycles per level (operands in L2, a cluster barrier); here one CTA per component
+// holds everything in shared memory and pays one block barrier per level.
+//   k_cc_init / k_cc_jump / k_cc_hook / k_cc_count   union-find over each cell's lex-earlier
+//                neighbours (the lists of k_nbr_lists) in global memory on all SMs; roots,
+//                component sizes and bounding boxes
+//   k_cc_plan    one CTA: offsets of the components of >= 2 cells, count, largest
+//                shared-memory need (cells + bounding box)
+//   k_cc_scatter member lists per component (any order: the sweep's result does not depend on
+//                the order of a level's cells)
+//   k_sweep_comp one CTA per component: the cells' rows (C'*S, replaced by C'*S_new when the
+//                cell is updated -- every reader of the old row is a predecessor, finished
+//                before), a u16 index over the component's bounding box (+1 margin), per cell
+//                its box position, neighbour mask, count and ΣC', the pending counts and two
+//                frontier queues, all in shared memory.  Per level, a lane per (cell,
+//                coordinate) resolves the active neighbours through the box index in lex
+//                offset order (the serial sweep's operands and order, pin P2), divides with
+//                RN(1/ΣC') (Markstein), stores S_new to Q's row and C'*S_new to its shared row,
+//                then the warp releases the lex-later neighbours (every decrement in flight
+//                together, ONE tail atomic per warp); one block barrier per level.  Singleton
+//                cells (isolated or frozen) keep the Q row k_nbr_lists wrote (S_old, pin P3).
+constexpr int kCcMaxCells = 1 << 20;  // (u16 local indices limit a component, not m)
+
+template <int D>
+__host__ __device__ constexpr int comp_K() { return D == 1 ? 3 : D == 2 ? 9 : 27; }
+
+// shared-memory bytes of one component: rows (sz + 1 with the zero row) 8D; per cell its box
+// position, C', ΣC' (4 B each), a u16 pending count and a u16 queue slot (20 B); the u16 box
+// index (2 B per box cell)
+template <int D>
+__host__ __device__ constexpr size_t sweep_comp_smem(long long sz, long long box) {
+  return (size_t)(sz + 1) * D * 8 + (size_t)sz * 16 + (size_t)((sz + 1) & ~1ll) * 2 +
+         (size_t)box * 2 + 64;
+}
+
+// Connected components in global memory, all SMs (ECL-CC style): every cell hooked to its
+// smallest lex-earlier neighbour (list entry 0: lists are in lex offset order over lex-sorted
+// cells), pointer jumping to shorten the chains, then the other lex-earlier neighbours united
+// (finds with path halving; a hook puts a root under a smaller root, so pointers only ever go
+// to smaller indices and every root ends as its component's smallest cell).
+__device__ __forceinline__ int cc_find_g(int32_t* par, int x) {
+  int cur = __ldcg(&par[x]);
+  if (cur == x) return x;
+  int prev = x, nxt;
+  while (cur > (nxt = __ldcg(&par[cur]))) {
+    __stcg(&par[prev], nxt);
+    prev = cur;
+    cur = nxt;
+  }
+  return cur;
+}
+
+template <int D>
+__global__ void k_cc_init(int m, int KP, const uint32_t* __restrict__ lists,
+                          const int32_t* __restrict__ nbe, int32_t* __restrict__ par,
+                          int32_t* __restrict__ gsize, int32_t* __restrict__ cur,
+                          int32_t* __restrict__ bmin, int32_t* __restrict__ bmax) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  par[i] = nbe[i] > 0 ? (int)(__ldg(&lists[(int64_t)i * KP]) - ((uint32_t)m + 1u)) : i;
+  gsize[i] = 0;
+  cur[i] = 0;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    bmin[(size_t)i * D + c] = INT_MAX;
+    bmax[(size_t)i * D + c] = INT_MIN;
+  }
+}
+
+__global__ void k_cc_jump(int m, int32_t* par) {  // par[i] <- its great-grandparent
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int p = __ldcg(&par[i]);
+  p = __ldcg(&par[p]);
+  p = __ldcg(&par[p]);
+  __stcg(&par[i], p);
+}
+
+template <int D>
+__global__ void k_cc_hook(int m, int KP, const uint32_t* __restrict__ lists,
+                          const int32_t* __restrict__ nbe, int32_t* par) {
+  constexpr int KE = comp_K<D>() / 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int e = nbe[i];
+  const uint32_t P1ROW = (uint32_t)m + 1u;
+  int jj[KE];
+#pragma unroll
+  for (int t = 1; t < KE; ++t) jj[t] = t < e ? (int)(__ldg(&lists[(int64_t)i * KP + t]) - P1ROW) : -1;
+#pragma unroll
+  for (int t = 1; t < KE; ++t) {
+    if (jj[t] < 0) continue;
+    int a = cc_find_g(par, i), bb = cc_find_g(par, jj[t]);
+    while (a != bb) {
+      if (a < bb) {
+        const int t2 = a;
+        a = bb;
+        bb = t2;
+      }
+      const int old = atomicCAS(&par[a], a, bb);
+      if (old == a) break;
+      a = cc_find_g(par, old);
+      bb = cc_find_g(par, bb);
+    }
+  }
+}
+
+// roots; sizes and bounding boxes reduced per group of equal roots in a warp
+template <int D>
+__global__ void k_cc_count(int m, GsBox b, const uint32_t* __restrict__ ckey, int32_t* par,
+                           int32_t* __restrict__ gsize, int32_t* __restrict__ bmin,
+                           int32_t* __restrict__ bmax) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = i < m;
+  int r = -1, x[D];
+  if (in) {
+    r = cc_find_g(par, i);
+    const uint32_t L = ckey[i] % (uint32_t)b.vol_frame;
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = (int)((L / (uint32_t)b.stride[c]) % (uint32_t)b.ext[c]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; ++c) x[c] = 0;
+  }
+  const unsigned g = __match_any_sync(0xffffffffu, r);
+  const int n = __popc(g);
+  int lo[D], hi[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    lo[c] = __reduce_min_sync(g, x[c]);
+    hi[c] = __reduce_max_sync(g, x[c]);
+  }
+  if (in && (int)(threadIdx.x & 31) == __ffs(g) - 1) {
+    atomicAdd(&gsize[r], n);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      atomicMin(&bmin[(size_t)r * D + c], lo[c]);
+      atomicMax(&bmax[(size_t)r * D + c], hi[c]);
+    }
+  }
+  if (in) __stcg(&par[i], r);  // (roots are final: compress)
+}
+
+// one CTA: components of >= 2 cells in root order -> coff (per root, -1 otherwise), desc[c] =
+// {offset, size, root, -}; ctr[0] = components, ctr[1] = largest size, ctr[2] = largest
+// shared-memory need of k_sweep_comp.  The sizes stream through shared memory in chunks of
+// 8 per thread (coalesced loads), each thread scanning 8 consecutive roots.
+template <int D>
+__global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __restrict__ gsize,
+                                                      const int32_t* __restrict__ bmin,
+                                                      const int32_t* __restrict__ bmax,
+                                                      int32_t* __restrict__ coff,
+                                                      int32_t* __restrict__ desc,
+                                                      long long* __restrict__ ctr) {
+  constexpr int PER = 8;
+  __shared__ int s_a[1024], s_b[1024], s_g[1024 * PER];
+  __shared__ unsigned long long s_need;
+  __shared__ int s_max;
+  const int T = blockDim.x, tid = threadIdx.x;
+  if (tid == 0) {
+    s_need = 0;
+    s_max = 0;
+  }
+  int base_off = 0, base_c = 0;
+  for (int c0 = 0; c0 < m; c0 += T * PER) {
+    for (int k = tid; k < T * PER; k += T) s_g[k] = c0 + k < m ? gsize[c0 + k] : 0;
+    __syncthreads();
+    int v = 0, cf = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int sz = s_g[tid * PER + k];
+      if (sz >= 2) {
+        v += sz;
+        ++cf;
+      }
+    }
+    s_a[tid] = v;
+    s_b[tid] = cf;
+    __syncthreads();
+    for (int o = 1; o < T; o <<= 1) {
+      const int x = tid >= o ? s_a[tid - o] : 0, y = tid >= o ? s_b[tid - o] : 0;
+      __syncthreads();
+      s_a[tid] += x;
+      s_b[tid] += y;
+      __syncthreads();
+    }
+    int off = base_off + s_a[tid] - v, c = base_c + s_b[tid] - cf;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = c0 + tid * PER + k;
+      if (i >= m) break;
+      const int sz = s_g[tid * PER + k];
+      coff[i] = sz >= 2 ? off : -1;
+      if (sz >= 2) {
+        long long box = 1;
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+          box *= (long long)(bmax[(size_t)i * D + q] - bmin[(size_t)i * D + q] + 3);
+        desc[4 * c] = off;
+        desc[4 * c + 1] = sz;
+        desc[4 * c + 2] = i;
+        desc[4 * c + 3] = 0;
+        atomicMax(&s_max, sz);
+        atomicMax(&s_need, (unsigned long long)sweep_comp_smem<D>(sz, box));
+        off += sz;
+        ++c;
+      }
+    }
+    base_off += s_a[T - 1];
+    base_c += s_b[T - 1];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    ctr[0] = base_c;
+    ctr[1] = s_max;
+    ctr[2] = (long long)s_need;
+  }
+}
+
+__global__ void k_cc_scatter(int m, const int32_t* __restrict__ root,
+                             const int32_t* __restrict__ coff, int32_t* __restrict__ cur,
+                             int32_t* __restrict__ mem) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int r = root[i];
+  const int o = coff[r];
+  if (o < 0) return;
+  mem[o + atomicAdd(&cur[r], 1)] = i;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_sweep_comp(
+    int m, GsBox b, const int32_t* __restrict__ desc, const int32_t* __restrict__ mem,
+    const int32_t* __restrict__ bmin, const int32_t* __restrict__ bmax,
+    const uint32_t* __restrict__ ckey, const uint32_t* __restrict__ ccnt, double* Q) {
+  constexpr int K = comp_K<D>(), KE = K / 2;  // offsets t < KE are lex-earlier, t == KE self
+  constexpr int CPW = 32 / D;
+  extern __shared__ __align__(16) unsigned char csm[];
+  const int off = desc[4 * blockIdx.x], sz = desc[4 * blockIdx.x + 1];
+  const int r0 = desc[4 * blockIdx.x + 2];
+  int blo[D], bst[D];
+  int V = 1;
+#pragma unroll
+  for (int c = D - 1; c >= 0; --c) {  // the component's box with one empty layer per side
+    blo[c] = bmin[(size_t)r0 * D + c] - 1;
+    bst[c] = V;
+    V *= bmax[(size_t)r0 * D + c] - blo[c] + 2;
+  }
+  __shared__ int s_offs[K];
+  __shared__ unsigned s_cnt[3];  // cells appended by level L live in s_cnt[(L + 1) % 3]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  double* row = (double*)csm;                               // (sz + 1) x D, zero row sz
+  uint32_t* bpos = (uint32_t*)(row + (size_t)(sz + 1) * D);  // box position per cell
+  uint32_t* cnt = bpos + sz;                                 // C'
+  uint32_t* dsum = cnt + sz;                                 // ΣC'
+  uint32_t* pend = dsum + sz;                                // u16 pending counts, in pairs
+  uint16_t* queue = (uint16_t*)(pend + ((sz + 1) >> 1));     // every cell appended once
+  uint16_t* bidx = queue + ((sz + 1) & ~1);                  // box index (0xffff: none)
+  if (tid == 0) s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+  for (int t = tid; t < K; t += blockDim.x) {  // lex offsets (dim 0 most significant)
+    int r = t, o = 0;
+#pragma unroll
+    for (int c = D - 1; c >= 0; --c) {
+      o += (r % 3 - 1) * bst[c];
+      r /= 3;
+    }
+    s_offs[t] = o;
+  }
+  for (int t = tid; t < V; t += blockDim.x) bidx[t] = 0xffffu;
+  for (int t = tid; t < ((sz + 1) >> 1); t += blockDim.x) pend[t] = 0u;
+  __syncthreads();
+  for (int l = tid; l < sz; l += blockDim.x) {
+    const int g = mem[off + l];
+    const int64_t L = (int64_t)(ckey[g] % (uint32_t)b.vol_frame);
+    uint32_t p = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) p += (uint32_t)((int)((L / b.stride[c]) % b.ext[c]) - blo[c]) * bst[c];
+    bpos[l] = p;
+    bidx[p] = (uint16_t)l;
+    cnt[l] = ccnt[g];
+#pragma unroll
+    for (int c = 0; c < D; ++c) row[(size_t)l * D + c] = __ldcg(&Q[(int64_t)g * D + c]);
+  }
+  if (tid < D) row[(size_t)sz * D + tid] = 0.0;
+  __syncthreads();
+  for (int l = tid; l < sz; l += blockDim.x) {  // ΣC', pending counts, first frontier
+    const uint32_t p = bpos[l];
+    uint32_t s = 0;
+    int e = 0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const uint32_t j = bidx[p + s_offs[t]];
+      if (j != 0xffffu) {
+        s += cnt[j];
+        e += t < KE;
+      }
+    }
+    dsum[l] = s;
+    if (e) atomicAdd(&pend[l >> 1], (unsigned)e << (16 * (l & 1)));
+    else queue[atomicAdd(&s_cnt[0], 1u)] = (uint16_t)l;
+  }
+  __syncthreads();
+  const int q = lane / D, c = lane - (lane / D) * D;
+  int offs[K];  // the lex offsets in registers
+#pragma unroll
+  for (int t = 0; t < K; ++t) offs[t] = s_offs[t];
+  int h0 = 0, t0 = 0;  // the frontier: queue[h0, t0)
+  for (int L = 0;; ++L) {
+    h0 = t0;
+    t0 += (int)*(volatile unsigned*)&s_cnt[L % 3];
+    if (h0 == t0) break;
+    if (tid == 0) s_cnt[(L + 2) % 3] = 0u;  // its last readers passed the previous barrier
+    unsigned* nct = &s_cnt[(L + 1) % 3];
+    for (int base = h0 + warp * CPW; base < t0; base += nwarps * CPW) {
+      const int k = base + q;
+      const bool act = q < CPW && k < t0;
+      const int l = act ? (int)queue[k] : sz;
+      const uint32_t p = act ? bpos[l] : 0u;
+      uint32_t jn[K];
+#pragma unroll
+      for (int t = 0; t < K; ++t) jn[t] = act ? (uint32_t)bidx[p + offs[t]] : 0xffffu;
+      // release the lex-later neighbours first (their updates run after this level's barrier,
+      // which orders this cell's row store before them): lane c of the cell takes offsets
+      // KE+1+c, +D, ...; every decrement in flight before any result is used
+      constexpr int RMAX = (K - KE - 1 + D - 1) / D;
+      uint32_t js[RMAX], od[RMAX];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) js[r] = 0xffffu;
+#pragma unroll
+      for (int t = KE + 1; t < K; ++t)  // (static indices: the lane's share selected by predicate)
+        if ((t - KE - 1) % D == c) js[(t - KE - 1) / D] = jn[t];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r)
+        od[r] = js[r] != 0xffffu
+                    ? (atomicSub(&pend[js[r] >> 1], 1u << (16 * (js[r] & 1))) >> (16 * (js[r] & 1))) & 0xffffu
+                    : 0u;
+      int nr = 0;
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) nr += od[r] == 1u;
+      if (nr) {
+        int at = t0 + (int)atomicAdd(nct, (unsigned)nr);
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+          if (od[r] == 1u) queue[at++] = (uint16_t)js[r];
+      }
+      if (act) {  // (a component cell always has an active neighbour besides itself)
+        const int g = mem[off + l];
+        const uint32_t dn = dsum[l], cn = cnt[l];
+        const double rd = __drcp_rn((double)dn);
+        double t2[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) t2[t] = row[(size_t)(jn[t] != 0xffffu ? jn[t] : (uint32_t)sz) * D + c];
+        double num = 0.0;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+          if (jn[t] != 0xffffu) num = __dadd_rn(num, t2[t]);
+        const double s1 = gl_div(num, (double)dn, rd);
+        Q[(int64_t)g * D + c] = s1;
+        row[(size_t)l * D + c] = __dmul_rn((double)cn, s1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace gs
