@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __res
                                                       int32_t* __restrict__ desc,
                                                       long long* __restrict__ ctr) {
   constexpr int PER = 8;
-  __shared__ int s_a[1024], s_b[1024], s_g[1024 * PER];
+  __shared__ int s_a[64], s_b[64], s_g[1024 * PER];
   __shared__ unsigned long long s_need;
   __shared__ int s_max;
   const int T = blockDim.x, tid = threadIdx.x;
@@ -1020,17 +1020,38 @@ __global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __res
         ++cf;
       }
     }
-    s_a[tid] = v;
-    s_b[tid] = cf;
-    __syncthreads();
-    for (int o = 1; o < T; o <<= 1) {
-      const int x = tid >= o ? s_a[tid - o] : 0, y = tid >= o ? s_b[tid - o] : 0;
-      __syncthreads();
-      s_a[tid] += x;
-      s_b[tid] += y;
-      __syncthreads();
+    // block scan of (v, cf): warp shuffles, then the warp totals by warp 0
+    const int lane = tid & 31, wid = tid >> 5;
+    int xv = v, xc = cf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, xv, o), b2 = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) {
+        xv += a;
+        xc += b2;
+      }
     }
-    int off = base_off + s_a[tid] - v, c = base_c + s_b[tid] - cf;
+    if (lane == 31) {
+      s_a[wid] = xv;
+      s_b[wid] = xc;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int a = lane < (T >> 5) ? s_a[lane] : 0, b2 = lane < (T >> 5) ? s_b[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int pa = __shfl_up_sync(0xffffffffu, a, o), pb = __shfl_up_sync(0xffffffffu, b2, o);
+        if (lane >= o) {
+          a += pa;
+          b2 += pb;
+        }
+      }
+      s_a[32 + lane] = a;  // inclusive warp prefixes
+      s_b[32 + lane] = b2;
+    }
+    __syncthreads();
+    int off = base_off + (wid ? s_a[32 + wid - 1] : 0) + xv - v;
+    int c = base_c + (wid ? s_b[32 + wid - 1] : 0) + xc - cf;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int i = c0 + tid * PER + k;
@@ -1052,8 +1073,8 @@ __global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __res
         ++c;
       }
     }
-    base_off += s_a[T - 1];
-    base_c += s_b[T - 1];
+    base_off += s_a[32 + (T >> 5) - 1];
+    base_c += s_b[32 + (T >> 5) - 1];
     __syncthreads();
   }
   if (tid == 0) {
