@@ -524,7 +524,9 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
     const gs::BinParams P = gs::make_bin_params<D>(ctx->box, 4, ctx->bin_rep_log2, ctx->predicted);
     gs::k_bin<D, T><<<grid, gs::kBinThreads, gs::kBinSmemBytes, ctx->stream>>>(
         (const T*)pts, ntot, P, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
-        ctx->slot.p, ctx->errflag.as<int>(), img_w);
+        ctx->slot.p, ctx->errflag.as<int>(), img_w,
+        ctx->predicted ? ctx->dbox.as<GsBox>() : nullptr,
+        ctx->predicted ? ctx->epoch_dev.as<unsigned>() : nullptr, ctx->box);
     GS_LAUNCHED("k_bin");
   }
   return GS_OK;
@@ -623,9 +625,7 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   if (pbox) {  // the predicted box: no bounds pass (K2 checks every point against it)
     if (ctx->host_src)  // zero-copy pinned input: K1 is the copy (its box is not used)
       GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));
-    gs::k_box_set<<<1, 1, 0, st>>>(*pbox, ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>());
-    GS_LAUNCHED("k_box_set");
-    ctx->box = *pbox;
+    ctx->box = *pbox;  // K2's block 0 stores it as the device box and bumps the run epoch
   } else {
     // bounds pass, then the box to the host: K2's geometry is kernel parameters
     GS_TRY(dispatch_bounds_bin(ctx, dpts, dtype, d, ntot, true, nblk, h, n, nf));

@@ -623,7 +623,13 @@ template <int D, typename T>
 __global__ void __launch_bounds__(kBinThreads, 1)
     k_bin(const T* __restrict__ pts, int64_t ntot, const __grid_constant__ BinParams P,
           uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs, void* __restrict__ slot,
-          int* err, int img_w) {
+          int* err, int img_w, GsBox* __restrict__ pbox_out = nullptr,
+          unsigned* __restrict__ epoch = nullptr, const __grid_constant__ GsBox pbox = GsBox{}) {
+  // the predicted box (no bounds pass) becomes the device box here, for K3 (one launch less)
+  if (pbox_out && blockIdx.x == 0 && threadIdx.x == 0) {
+    *pbox_out = pbox;
+    *epoch += 1u;
+  }
   constexpr uint32_t EMPTY = 0xffffffffu;
   constexpr int EW = 1 + 2 * D;
   // CTA ranges start on multiples of 4 points (16-byte aligned rows of fp32 d = 3 features)
@@ -675,11 +681,6 @@ __global__ void __launch_bounds__(kBinThreads, 1)
   }
 }
 
-// Predicted key box (no bounds pass): the box of the previous run of this shape.
-__global__ void k_box_set(GsBox b, GsBox* __restrict__ out, unsigned* epoch) {
-  *out = b;
-  *epoch += 1u;
-}
 
 // ---------------------------------------------------------------- K3: compaction by scan
 // The dense grid is in lexicographic order, so scanning its occupancy yields the cell list

@@ -102,51 +102,61 @@ __device__ __forceinline__ double gs_dist(const double* a, const double* b, int 
   return __dsqrt_rn(acc);
 }
 
-// silhouette per sample point (pin S2).  Thread u owns the sorted position u (sample point
-// ord[u]); every thread walks the same (cluster, member) sequence, so the staged tile is read
-// as a broadcast.  seg[0..kc] = cluster starts in sorted order; cid[u] = u's cluster.
+// silhouette (pin S2), parallel over (sample point, cluster) pairs: CTA (x, c) gives its
+// kSilThreads sorted positions the mean distance to the members of cluster c, summed in the
+// members' sorted order (the pinned order: each pair's sum is the same chain as the serial
+// walk's), with u itself skipped in its own cluster.  The own cluster's mean is a(u); the other
+// clusters' means meet in an atomic min on the bits of b(u) (non-negative doubles order as
+// their bit patterns), so b(u) is the exact minimum in any order.  Members are staged in shared
+// memory and read as a broadcast.  seg[0..kc] = cluster starts in sorted order; cid[u] = u's
+// cluster.  (One thread per point walking every cluster left 97 % of the warp slots idle.)
 template <int D>
 __global__ void __launch_bounds__(kSilThreads) k_silhouette(
     const double* __restrict__ xo, int64_t s, int d_rt, const int32_t* __restrict__ seg, int kc,
-    const int32_t* __restrict__ ord, const int32_t* __restrict__ cid, double* __restrict__ sil) {
+    const int32_t* __restrict__ cid, double* __restrict__ amean,
+    unsigned long long* __restrict__ bmin, int c0) {
   constexpr int DD = D > 0 ? D : 12;
-  constexpr int kSilTile = 4096 / DD;  // sample points staged in shared memory per round (32 KB)
+  constexpr int kSilTile = 4096 / DD;  // members staged per round (32 KB)
   const int d = D > 0 ? D : d_rt;
   __shared__ double tile[kSilTile * DD];
+  const int c = c0 + (int)blockIdx.y;
+  const int64_t cs = seg[c], ce = seg[c + 1], size = ce - cs;
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = u < s;
   double xi[DD];
-  for (int c = 0; c < d; ++c) xi[c] = live ? xo[u * d + c] : 0.0;
+  for (int k = 0; k < d; ++k) xi[k] = live ? xo[u * d + k] : 0.0;
   const int own = live ? cid[u] : -1;
-  double a = 0.0, b = INFINITY, sum = 0.0;
-  bool single = false;
-  int c = 0;
-  int64_t cs = 0, ce = seg[1];
-  for (int64_t t0 = 0; t0 < s; t0 += kSilTile) {
-    const int64_t nt = min((int64_t)kSilTile, s - t0);
+  double sum = 0.0;
+  for (int64_t t0 = cs; t0 < ce; t0 += kSilTile) {
+    const int64_t nt = min((int64_t)kSilTile, ce - t0);
     __syncthreads();
     for (int64_t e = threadIdx.x; e < nt * d; e += blockDim.x) tile[e] = xo[t0 * d + e];
     __syncthreads();
-    for (int64_t tt = 0; tt < nt; ++tt) {
-      const int64_t t = t0 + tt;
-      if (t != u) sum = __dadd_rn(sum, gs_dist(xi, tile + tt * d, d));
-      if (t + 1 == ce) {  // end of cluster c (uniform across threads)
-        const int64_t size = ce - cs;
-        if (c == own) {
-          if (size == 1) single = true;
-          else a = __ddiv_rn(sum, (double)(size - 1));
-        } else {
-          const double mean = __ddiv_rn(sum, (double)size);
-          if (mean < b) b = mean;
-        }
-        sum = 0.0;
-        ++c;
-        cs = ce;
-        if (c < kc) ce = seg[c + 1];
-      }
-    }
+    for (int64_t tt = 0; tt < nt; ++tt)
+      if (t0 + tt != u) sum = __dadd_rn(sum, gs_dist(xi, tile + tt * d, d));
   }
   if (!live) return;
+  if (c == own) {
+    amean[u] = size == 1 ? -1.0 : __ddiv_rn(sum, (double)(size - 1));  // -1: a singleton
+  } else {
+    atomicMin(&bmin[u], (unsigned long long)__double_as_longlong(__ddiv_rn(sum, (double)size)));
+  }
+}
+
+__global__ void k_sil_init(int64_t s, unsigned long long* __restrict__ bmin) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u < s) bmin[u] = 0x7ff0000000000000ull;  // +inf
+}
+
+__global__ void k_sil_combine(int64_t s, const int32_t* __restrict__ ord,
+                              const double* __restrict__ amean,
+                              const unsigned long long* __restrict__ bmin,
+                              double* __restrict__ sil) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= s) return;
+  const double a0 = amean[u], b = __longlong_as_double((long long)bmin[u]);
+  const bool single = a0 < 0.0;
+  const double a = single ? 0.0 : a0;
   const double mx = a > b ? a : b;
   sil[ord[u]] = (single || mx == 0.0) ? 0.0 : __ddiv_rn(__dsub_rn(b, a), mx);
 }
@@ -174,7 +184,7 @@ struct DevMem {
 struct Worker {
   gs_ctx* eng = nullptr;
   cudaStream_t st = nullptr;
-  DevMem labels, ls, ord, seg, cid, xo, sil;
+  DevMem labels, ls, ord, seg, cid, xo, sil, amean, bmin;
   std::vector<int32_t> h_ls, h_ord, h_seg, h_cid;
   std::vector<double> h_sil;
 };
@@ -242,10 +252,12 @@ gs_status stage(gs_tuner* t, const gs_input* in, int64_t cap, uint64_t seed, int
 
 template <int D>
 void launch_sil(const Worker& w, int64_t s, int d, int kc) {
-  const unsigned nb = (unsigned)((s + kSilThreads - 1) / kSilThreads);
-  k_silhouette<D><<<nb, kSilThreads, 0, w.st>>>(w.xo.as<double>(), s, d, w.seg.as<int32_t>(), kc,
-                                               w.ord.as<int32_t>(), w.cid.as<int32_t>(),
-                                               w.sil.as<double>());
+  for (int c0 = 0; c0 < kc; c0 += 65535) {  // (grid.y limit)
+    const dim3 grid((unsigned)((s + kSilThreads - 1) / kSilThreads), (unsigned)min(65535, kc - c0));
+    k_silhouette<D><<<grid, kSilThreads, 0, w.st>>>(w.xo.as<double>(), s, d, w.seg.as<int32_t>(),
+                                                   kc, w.cid.as<int32_t>(), w.amean.as<double>(),
+                                                   w.bmin.as<unsigned long long>(), c0);
+  }
 }
 
 // silhouette (pin S2) of the sample under the device labels `dlabels` (n entries).
@@ -279,12 +291,15 @@ gs_status silhouette_dev(gs_tuner* t, Worker& w, const int32_t* dlabels, int64_t
   TCK(w.seg.grow(sizeof(int32_t) * (kc + 1)));
   TCK(w.xo.grow(sizeof(double) * s * d));
   TCK(w.sil.grow(sizeof(double) * s));
+  TCK(w.amean.grow(sizeof(double) * s));
+  TCK(w.bmin.grow(sizeof(unsigned long long) * s));
   TCK(cudaMemcpyAsync(w.ord.p, w.h_ord.data(), sizeof(int32_t) * s, cudaMemcpyHostToDevice, w.st));
   TCK(cudaMemcpyAsync(w.cid.p, w.h_cid.data(), sizeof(int32_t) * s, cudaMemcpyHostToDevice, w.st));
   TCK(cudaMemcpyAsync(w.seg.p, w.h_seg.data(), sizeof(int32_t) * (kc + 1), cudaMemcpyHostToDevice,
                       w.st));
   k_permute<<<nb, 256, 0, w.st>>>(t->xs.as<double>(), w.ord.as<int32_t>(), s, d,
                                   w.xo.as<double>());
+  k_sil_init<<<nb, 256, 0, w.st>>>(s, w.bmin.as<unsigned long long>());
   switch (d) {
     case 1: launch_sil<1>(w, s, d, kc); break;
     case 2: launch_sil<2>(w, s, d, kc); break;
@@ -293,6 +308,8 @@ gs_status silhouette_dev(gs_tuner* t, Worker& w, const int32_t* dlabels, int64_t
     case 5: launch_sil<5>(w, s, d, kc); break;
     default: launch_sil<0>(w, s, d, kc); break;
   }
+  k_sil_combine<<<nb, 256, 0, w.st>>>(s, w.ord.as<int32_t>(), w.amean.as<double>(),
+                                      w.bmin.as<unsigned long long>(), w.sil.as<double>());
   TCK(cudaGetLastError());
   w.h_sil.resize(s);
   TCK(cudaMemcpyAsync(w.h_sil.data(), w.sil.p, sizeof(double) * s, cudaMemcpyDeviceToHost, w.st));
