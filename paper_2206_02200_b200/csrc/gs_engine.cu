@@ -1799,7 +1799,21 @@ int64_t group_frames(const gs_input* in, const gs_config* cfg) {
 
 gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_result* out) {
   const int64_t nf = in->batch, n = in->n, gf = group_frames(in, cfg);
-  const int64_t G = (nf + gf - 1) / gf;
+  // group schedule: a short first group (the pipeline fill: its copy is not overlapped), then
+  // groups of gf frames, the remainder last (three group shapes at most: the shape cache keeps
+  // every group on the optimistic path)
+  std::vector<int64_t> g0s, gcs;
+  {
+    int64_t f = 0;
+    const int64_t first = (cfg->flags & GS_DEBUG_PIPELINE) ? gf : std::max<int64_t>(1, gf / 4);
+    while (f < nf) {
+      const int64_t c = std::min(f == 0 ? first : gf, nf - f);
+      g0s.push_back(f);
+      gcs.push_back(c);
+      f += c;
+    }
+  }
+  const int64_t G = (int64_t)g0s.size();
   const size_t fb = input_bytes(in) / (size_t)nf;
   const int d = in->d;
   cudaStream_t st = ctx->stream;
@@ -1810,7 +1824,7 @@ gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_
   for (auto& b : ctx->stage) GS_TRY(grow(ctx, b, fb * (size_t)gf));
   const char* src = static_cast<const char*>(in->points);
   auto stage_in = [&](int64_t g) -> gs_status {
-    const int64_t f0 = g * gf, cnt = std::min(gf, nf - f0);
+    const int64_t f0 = g0s[g], cnt = gcs[g];
     GS_CK(cudaMemcpyAsync(ctx->stage[g & 1].p, src + (size_t)f0 * fb, fb * (size_t)cnt,
                           cudaMemcpyHostToDevice, ctx->copy_stream));
     GS_CK(cudaEventRecord(ctx->ev_copy[g & 1], ctx->copy_stream));
@@ -1833,8 +1847,8 @@ gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_
   gs_status s = stage_in(0);
   int64_t f0 = 0;
   for (int64_t g = 0; g < G && s == GS_OK; ++g) {
-    f0 = g * gf;
-    const int64_t cnt = std::min(gf, nf - f0);
+    f0 = g0s[g];
+    const int64_t cnt = gcs[g];
     // the other staging buffer was last read by group g-1, which has completed (synchronous)
     if (g + 1 < G && (s = stage_in(g + 1)) != GS_OK) break;
     if (cudaStreamWaitEvent(st, ctx->ev_copy[g & 1], 0) != cudaSuccess) {
