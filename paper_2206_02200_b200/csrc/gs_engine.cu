@@ -149,6 +149,8 @@ struct gs_ctx {
   // component sweep of the global path (gs_global.cuh k_cc_* / k_sweep_comp)
   DevBuf ccpar, ccsize, cccur, ccoff, ccmem, ccloc, ccdesc, ccctr, ccgs;
   bool comp_ok = true;  // the component sweep can be launched on this device
+  // MS++ all-SM loop (first grids beyond one CTA): particles, their keys, initial-cell roots
+  DevBuf mpos, mpc, mkey, mroot, msnew;
   // pinned, device-mapped readback area: K7 stores the control block there (zero copy)
   void* pin = nullptr;
   void* pin_dev = nullptr;
@@ -1945,6 +1947,104 @@ gs_status mspp_launch(gs_ctx* ctx, const void* dpts, int64_t n, int64_t m0, doub
   gs::k_mspp_disp0<D, T><<<blocks_for(n, 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
       n, (const T*)dpts, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->idx.as<int32_t>(), snew0, disp0);
   GS_LAUNCHED("k_mspp_disp0");
+  if (m0 > MS) {  // ---- the first grid exceeds one CTA: later iterations on all SMs
+    const int64_t V = ctx->box.vol_total;
+    GS_TRY(grow(ctx, ctx->mpos, sizeof(double) * (size_t)m0 * D));
+    GS_TRY(grow(ctx, ctx->mpc, sizeof(uint32_t) * (size_t)m0));
+    GS_TRY(grow(ctx, ctx->mkey, sizeof(uint32_t) * (size_t)m0));
+    GS_TRY(grow(ctx, ctx->mroot, sizeof(int32_t) * (size_t)m0));
+    GS_TRY(grow(ctx, ctx->msnew, sizeof(double) * (size_t)m0 * D));
+    unsigned* cnt32 = ctx->counters.as<unsigned>();
+    // particles = the initial cells at iteration 0's positions; the first grid's index released
+    GS_CK(cudaMemcpyAsync(ctx->mpos.p, snew0, sizeof(double) * (size_t)m0 * D,
+                          cudaMemcpyDeviceToDevice, st));
+    GS_CK(cudaMemcpyAsync(ctx->mpc.p, ctx->ccnt[0].p, sizeof(uint32_t) * (size_t)m0,
+                          cudaMemcpyDeviceToDevice, st));
+    gs::k_iota<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->mroot.as<int32_t>());
+    GS_LAUNCHED("k_iota");
+    gs::k_idx_clear<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->ckey[0].as<uint32_t>(),
+                                                          ctx->idx.as<int32_t>());
+    GS_LAUNCHED("k_idx_clear");
+    std::vector<double> hd((size_t)max_iter, 0.0);
+    unsigned long long d0b = 0;
+    GS_CK(cudaMemcpyAsync(&d0b, disp0, 8, cudaMemcpyDeviceToHost, st));
+    GS_CK(cudaStreamSynchronize(st));
+    double dsp;
+    std::memcpy(&dsp, &d0b, 8);
+    hd[0] = dsp;
+    int it = 1;
+    bool conv = dsp < tol;
+    bool final_pass = conv || it >= max_iter;
+    int64_t mp = m0;
+    const unsigned tg = (unsigned)std::min<int64_t>(V / gs::kOccTile + 1, (int64_t)ctx->num_sms * 4);
+    unsigned long long* dmax = disp0;  // reused: the displacement of the current iteration
+    for (;;) {
+      // re-grid the particles (pins M1, M4)
+      gs::k_mspp_bin_g<D><<<blocks_for(mp, 256), 256, 0, st>>>(
+          (int)mp, ctx->mpos.as<double>(), ctx->mpc.as<uint32_t>(), ctx->dbox.as<GsBox>(),
+          ctx->box.scale, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+          ctx->mkey.as<uint32_t>(), ctx->epoch_dev.as<unsigned>(), cnt32 + 5,
+          ctx->errflag.as<int>());
+      GS_LAUNCHED("k_mspp_bin_g");
+      gs::k_occ<<<tg, 256, 0, st>>>(
+          ctx->dbox.as<GsBox>(), ctx->epoch_dev.as<unsigned>(), ctx->tiles.as<unsigned long long>(),
+          cnt32 + 5, cnt32, ctx->cnt.as<uint32_t>(), ctx->qs.as<unsigned long long>(),
+          ctx->ckey[1].as<uint32_t>(), ctx->ccnt[1].as<uint32_t>(), ctx->S[1].as<double>(),
+          ctx->idx.as<int32_t>(), ctx->root.as<int32_t>(), ctx->initkey.as<uint32_t>(),
+          ctx->ifirst.as<int32_t>(), ctx->errflag.as<int>());
+      GS_LAUNCHED("k_occ");
+      if (final_pass) {  // pin M5: the final cells, ids = lex ranks
+        gs::k_mspp_root_g<<<blocks_for(m0, 256), 256, 0, st>>>(
+            (int)m0, ctx->mroot.as<int32_t>(), ctx->mkey.as<uint32_t>(), ctx->idx.as<int32_t>(),
+            ctx->ckey[0].as<uint32_t>(), ctx->lab.as<int32_t>());
+        GS_LAUNCHED("k_mspp_root_g");
+        unsigned mfin = 0;
+        GS_CK(cudaMemcpyAsync(&mfin, cnt32, 4, cudaMemcpyDeviceToHost, st));
+        GS_CK(cudaStreamSynchronize(st));
+        gs::k_idx_clear<<<blocks_for(mfin, 256), 256, 0, st>>>(
+            (int)mfin, ctx->ckey[1].as<uint32_t>(), ctx->idx.as<int32_t>());
+        GS_LAUNCHED("k_idx_clear");
+        const int ow[4] = {(int)mfin, it, conv ? 1 : 0, 0};
+        GS_CK(cudaMemcpyAsync(outw, ow, sizeof(ow), cudaMemcpyHostToDevice, st));
+        if (dhist)
+          GS_CK(cudaMemcpyAsync(dhist, hd.data(), sizeof(double) * hd.size(),
+                                cudaMemcpyHostToDevice, st));
+        GS_CK(cudaStreamSynchronize(st));  // (hd and ow are host stack memory)
+        return GS_OK;
+      }
+      // update (pin M2), displacement (M3), particle -> cell of the initial roots (M4)
+      GS_CK(cudaMemsetAsync(dmax, 0, 8, st));
+      gs::k_mspp_jacobi_g<D><<<blocks_for(mp, 128), 128, 0, st>>>(
+          cnt32, ctx->dbox.as<GsBox>(), ctx->ckey[1].as<uint32_t>(), ctx->ccnt[1].as<uint32_t>(),
+          ctx->S[1].as<double>(), ctx->idx.as<int32_t>(), ctx->msnew.as<double>());
+      GS_LAUNCHED("k_mspp_jacobi_g");
+      gs::k_mspp_disp_g<D><<<blocks_for(mp, 256), 256, 0, st>>>(
+          (int)mp, ctx->mpos.as<double>(), ctx->mkey.as<uint32_t>(), ctx->idx.as<int32_t>(),
+          ctx->msnew.as<double>(), dmax);
+      GS_LAUNCHED("k_mspp_disp_g");
+      gs::k_mspp_root_g<<<blocks_for(m0, 256), 256, 0, st>>>(
+          (int)m0, ctx->mroot.as<int32_t>(), ctx->mkey.as<uint32_t>(), ctx->idx.as<int32_t>(),
+          nullptr, nullptr);
+      GS_LAUNCHED("k_mspp_root_g");
+      gs::k_mspp_next_g<D><<<blocks_for(mp, 256), 256, 0, st>>>(
+          cnt32, ctx->msnew.as<double>(), ctx->ccnt[1].as<uint32_t>(), ctx->ckey[1].as<uint32_t>(),
+          ctx->mpos.as<double>(), ctx->mpc.as<uint32_t>(), ctx->idx.as<int32_t>());
+      GS_LAUNCHED("k_mspp_next_g");
+      unsigned long long rb[2] = {0, 0};
+      GS_CK(cudaMemcpyAsync(&rb[0], dmax, 8, cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaMemcpyAsync(&rb[1], cnt32, 4, cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaStreamSynchronize(st));
+      int err = 0;
+      GS_CK(cudaMemcpy(&err, ctx->errflag.p, sizeof(int), cudaMemcpyDeviceToHost));
+      if (err & 2) return fail(ctx, GS_E_INTERNAL_INVARIANT, "an MS++ particle left the key box");
+      std::memcpy(&dsp, &rb[0], 8);
+      mp = (int64_t)(unsigned)rb[1];
+      hd[(size_t)it] = dsp;
+      ++it;
+      conv = dsp < tol;
+      final_pass = conv || it >= max_iter;
+    }
+  }
   gs::MsppArgs a;
   a.m0 = (int)m0;
   a.MS = MS;
@@ -1996,6 +2096,7 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
   ctx->have_run = false;
   ctx->grouped = false;
   ctx->img_w = 0;
+  ctx->stats = gs_stats{};  // (kernel_launches of this MS++ run)
   cudaGetLastError();
   const int d = in->d;
   const int64_t n = in->n;
@@ -2043,15 +2144,8 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
     MS /= 2;
     vol_small = 1;
   }
-  if (m0 > MS) {  // restore the clean grid (K3 indexed the first grid's cells) before refusing
-    gs::k_idx_clear<<<blocks_for(m0, 256), 256, 0, ctx->stream>>>(
-        (int)m0, ctx->ckey[0].as<uint32_t>(), ctx->idx.as<int32_t>());
-    GS_CK(cudaStreamSynchronize(ctx->stream));
-    return fail(ctx, GS_E_INVALID_PARAMETER,
-                "MS++ baseline: the first grid (" + std::to_string((long long)m0) +
-                    " cells) exceeds one CTA's shared memory (" + std::to_string(MS) + ")");
-  }
   GS_TRY(grow(ctx, ctx->S1, sizeof(double) * (size_t)m0 * d));
+  GS_TRY(ensure_cells(ctx, m0, d));  // (the all-SM loop re-grids into the second cell buffers)
   GS_TRY(grow(ctx, ctx->dbg, 64 + sizeof(double) * (size_t)max_iter));
   GS_CK(cudaMemsetAsync(ctx->dbg.p, 0, 64, ctx->stream));
   unsigned long long* disp0 = (unsigned long long*)ctx->dbg.p;

@@ -13,6 +13,15 @@
 //                                       displacement; then the final cells (M5), the label
 //                                       table and the centroids
 //   K7 k_label                          labels[p] = lab[slot[p]]
+// A first grid larger than one CTA's shared memory (r2: cfg3, cfg5) runs the later iterations
+// on all SMs instead, host-driven, one round trip per iteration:
+//   k_mspp_bin_g    particles -> the dense grid (count and count * q fixed-point sums, integer
+//                   atomics: any order gives the same bits, pin M1/M4)
+//   k_occ           the engine's compaction: lex-sorted cells, centroids, idx
+//   k_mspp_jacobi_g Eq. (6) per cell (pin M2, as k_mspp_jacobi)
+//   k_mspp_disp_g   displacement of every particle (pin M3) and the particle -> cell map of
+//                   the initial cells' roots (M4)
+//   k_mspp_next_g   the cells become the particles; the grid index is released
 // Every fp64 step is the oracle's expression with _rn intrinsics: bit-identical labels,
 // centroids, iteration counts and displacements.
 #pragma once
@@ -286,6 +295,112 @@ __global__ void __launch_bounds__(512, 1) k_mspp_loop(MsppArgs a) {
     final_pass = conv || it >= a.max_iter;
     __syncthreads();
   }
+}
+
+// ---- the all-SM loop (first grids beyond one CTA)
+__global__ void k_iota(int m, int32_t* __restrict__ v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) v[i] = i;
+}
+
+template <int D>
+__global__ void k_mspp_bin_g(int mp, const double* __restrict__ pos,
+                             const uint32_t* __restrict__ pc, const GsBox* __restrict__ pb,
+                             double scale, uint32_t* __restrict__ cnt,
+                             unsigned long long* __restrict__ qs, uint32_t* __restrict__ pkey,
+                             unsigned* __restrict__ epoch, unsigned* __restrict__ ticket,
+                             int* __restrict__ err) {
+  const GsBox b = *pb;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {  // a fresh compaction epoch and tile ticket for the k_occ that follows
+    *epoch += 1u;
+    *ticket = 0u;
+  }
+  if (i >= mp) return;
+  int64_t L = 0, kc[D];
+  bool out = false;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    kc[c] = gs_grid_coord(pos[(int64_t)i * D + c], b.h, b.inv_h);
+    const int64_t r = kc[c] - b.kmin[c];
+    out |= r < 0 || r >= b.ext[c];
+    L += r * b.stride[c];
+  }
+  if (out) {  // (a mean of points of the box stays in it)
+    atomicOr(err, 2);
+    return;
+  }
+  pkey[i] = (uint32_t)L;
+  atomicAdd(&cnt[L], pc[i]);
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const long long q = gs_fixq(pos[(int64_t)i * D + c], kc[c], b.h, scale);
+    atomicAdd(&qs[L * D + c], (unsigned long long)((long long)pc[i] * q));
+  }
+}
+
+template <int D>
+__global__ void k_mspp_jacobi_g(const unsigned* __restrict__ m_ptr, const GsBox* __restrict__ pb,
+                                const uint32_t* __restrict__ ckey,
+                                const uint32_t* __restrict__ ccnt, const double* __restrict__ S,
+                                const int32_t* __restrict__ idx, double* __restrict__ Snew) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int)*m_ptr) return;
+  const GsBox b = *pb;
+  double o[D];
+  mspp_update_cell<D>(
+      b, (int64_t)ckey[i], i, [&](int64_t L) { return idx[L]; },
+      [&](int j) { return ccnt[j]; }, [&](int j, int c) { return S[(int64_t)j * D + c]; }, o);
+#pragma unroll
+  for (int c = 0; c < D; ++c) Snew[(int64_t)i * D + c] = o[c];
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_mspp_disp_g(int mp, const double* __restrict__ pos,
+                                                      const uint32_t* __restrict__ pkey,
+                                                      const int32_t* __restrict__ idx,
+                                                      const double* __restrict__ Snew,
+                                                      unsigned long long* __restrict__ dmax) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long best = 0ull;
+  if (i < mp) {
+    const int g = idx[pkey[i]];
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double t = __dsub_rn(Snew[(int64_t)g * D + c], pos[(int64_t)i * D + c]);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+    best = (unsigned long long)__double_as_longlong(__dsqrt_rn(acc));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(dmax, best);
+}
+
+// root[c0] <- the cell (rank) of the initial cell's particle; final: lab[initial key] = it
+__global__ void k_mspp_root_g(int m0, int32_t* __restrict__ root, const uint32_t* __restrict__ pkey,
+                              const int32_t* __restrict__ idx, const uint32_t* __restrict__ ckey0,
+                              int32_t* __restrict__ lab) {
+  const int c0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c0 >= m0) return;
+  const int g = idx[pkey[root[c0]]];
+  if (lab) lab[ckey0[c0]] = g;
+  else root[c0] = g;
+}
+
+// the m cells become the particles (positions Snew, counts); the grid index is released
+template <int D>
+__global__ void k_mspp_next_g(const unsigned* __restrict__ m_ptr, const double* __restrict__ Snew,
+                              const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ ckey,
+                              double* __restrict__ pos, uint32_t* __restrict__ pc,
+                              int32_t* __restrict__ idx) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int)*m_ptr) return;
+#pragma unroll
+  for (int c = 0; c < D; ++c) pos[(int64_t)g * D + c] = Snew[(int64_t)g * D + c];
+  pc[g] = ccnt[g];
+  idx[ckey[g]] = -1;
 }
 
 }  // namespace gs

@@ -78,6 +78,11 @@ CASES = [
     ("maxiter2", lambda: CF.generate("cfg2")[0], 0.08, dict(max_iter=2)),
     ("bigtol", lambda: CF.generate("cfg1")[0], 0.5, dict(tol=10.0)),
     ("cells1700", lambda: np.random.default_rng(6).random((20000, 3)), 0.09, {}),
+    # first grids beyond one CTA (r2): the later iterations run on all SMs
+    ("cells8000", lambda: np.random.default_rng(7).random((50000, 3)), 0.05, {}),
+    ("cfg5_small", lambda: CF.generate("cfg5", scale=1 / 64)[0], 1.0, {}),
+    ("cfg3_small", lambda: CF.generate("cfg3", scale=0.05)[0], 0.06, {}),
+    ("big_maxiter3", lambda: np.random.default_rng(8).random((60000, 2)), 0.01, dict(max_iter=3)),
 ]
 
 
@@ -109,10 +114,9 @@ def test_gpu_mspp_errors(engine):
     bad[1, 1] = np.inf
     with pytest.raises(G.InvalidInputError):
         engine.mspp(bad, 0.5)
-    # a first grid beyond one CTA (8,000 cells at d = 3) is refused, never approximated
-    with pytest.raises(G.InvalidParameterError):
-        engine.mspp(np.random.default_rng(7).random((50000, 3)), 0.05)
-    # ... and leaves the context's grid clean for the next run
+    # a first grid beyond one CTA runs on all SMs and leaves the context's grid clean for the
+    # next engine run
+    engine.mspp(np.random.default_rng(7).random((50000, 3)), 0.05)
     X = CF.generate("cfg2")[0]
     r = engine.run(X, G.EngineConfig(0.08, 100))
     assert np.array_equal(r.labels, O.run(X.astype(np.float64), 0.08, 100, O.BUILD_FIXED)["labels"])
