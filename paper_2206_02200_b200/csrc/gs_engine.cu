@@ -520,7 +520,7 @@ gs_status launch_bounds_bin_t(gs_ctx* ctx, const void* pts, int64_t ntot, bool b
   } else {
     // privatised binning: one 1024-thread CTA per SM at most, >= 1024 points per CTA; the
     // geometry comes from the host copy of the key box (ctx->box) as kernel parameters
-    const unsigned grid = blocks_for(ntot, 1024, ctx->num_sms);
+    const unsigned grid = blocks_for(ntot, 1024, (int64_t)ctx->num_sms * gs::kBinCtas);
     static std::atomic<uint64_t> done{0};
     GS_CK(attr_once(done, ctx->device, gs::k_bin<D, T>, gs::kBinSmemBytes));
     const gs::BinParams P = gs::make_bin_params<D>(ctx->box, 4, ctx->bin_rep_log2, ctx->predicted);

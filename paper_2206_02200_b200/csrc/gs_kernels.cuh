@@ -225,10 +225,14 @@ __global__ void __launch_bounds__(256) k_bounds_box(const T* __restrict__ pts, i
 #ifndef GS_BIN_THREADS
 #define GS_BIN_THREADS 1024  // (experiments override it at build time)
 #endif
+#ifndef GS_BIN_CTAS
+#define GS_BIN_CTAS 1        // K2 CTAs per SM
+#endif
 constexpr int kBinThreads = GS_BIN_THREADS;
+constexpr int kBinCtas = GS_BIN_CTAS;
 constexpr int kBinProbes = 4;  // hash probe budget before the point takes the global atomics
 constexpr int kAggRuns = 4;    // warp aggregation when the warp's keys form <= this many runs
-constexpr int kBinSmemBytes = 224 * 1024;
+constexpr int kBinSmemBytes = (kBinCtas == 1 ? 224 : 112) * 1024;
 
 __device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, unsigned long long v) {
   const unsigned l = (unsigned)v;
@@ -274,7 +278,8 @@ struct BinParams {
   long long Mbits;             // bits of Mq: table sums carry count * Mbits, removed at flush
   long long n, vol_frame;
   float ihf, thr;               // thr: fp32 key fineness threshold (gs_bin_rel_f32)
-  int magic_ok, two_piece, f32fast, dense, reps, TBL, rep_log2, s16, predicted;
+  float s2F, xmin;              // X path: 2^F, and the least |x| whose x*2^F is an integer
+  int magic_ok, two_piece, f32fast, xpath, dense, reps, TBL, rep_log2, s16, predicted;
   uint32_t vd;                 // cells of a frame's data box
   float Cf[GS_DMAX];           // 1.5*2^23 - kmin (fp32 fast key)
   int kmin32[GS_DMAX];
@@ -319,6 +324,28 @@ inline BinParams make_bin_params(const GsBox& b, int max_reps, int hash_rep_log2
   P.dense = P.s16 && (int64_t)vd * EW * 4 <= kBinSmemBytes;
   P.reps = P.dense ? std::max(1, std::min(max_reps, (int)(kBinSmemBytes / ((int64_t)vd * EW * 4)))) : 1;
   P.TBL = P.dense ? (int)vd * P.reps : ((kBinSmemBytes / (EW * 4 + 4)) & ~31);
+  // The fp32 fast path sums X = x*2^F (an integer for |x| >= 2^(23-F)) instead of q: with
+  // c = RN(k*h), RN(x - c) is exact (Sterbenz for |k| >= 1 and for k = -1, |x| >= h/2; k = 0
+  // trivially; k = -1, |x| < h/2 because x is a multiple of 2^-F >= ulp(h)/2), so q =
+  // RHE((x - c)*2^F) = X - Cr with Cr = RHE(c*2^F), unless c*2^F has fraction exactly 1/2 (a
+  // tie: the path is refused for the whole box).  The table sums X; the flush takes count*Cr.
+  // |X| < 2^52 keeps the two-piece warp reduction and F2I exact.
+  if (P.f32fast && P.dense) {
+    const int F = b.F;
+    bool ok = F <= 53 - std::ilogb(b.h) && F <= 120 && F >= -100;
+    ok = ok && std::ldexp((double)(kmax + 2) * b.h, F) < 0x1p52;
+    int64_t tot = 0;
+    for (int c = 0; c < D; ++c) tot += b.ext[c];
+    ok = ok && tot <= 65536;
+    for (int c = 0; ok && c < D; ++c)
+      for (int64_t k = b.kmin[c]; ok && k < b.kmin[c] + b.ext[c]; ++k) {
+        const double C = std::ldexp((double)k * b.h, F);
+        ok = C - std::floor(C) != 0.5;
+      }
+    P.xpath = ok;
+    P.s2F = std::ldexp(1.0f, F);
+    P.xmin = std::ldexp(1.0f, 23 - F);
+  }
   P.rep_log2 = P.dense ? 0 : hash_rep_log2;
   P.predicted = predicted;
   return P;
@@ -327,13 +354,58 @@ inline BinParams make_bin_params(const GsBox& b, int max_reps, int hash_rep_log2
 // The binning front of one point: cell key per coordinate (box-relative), the linear index
 // within the frame (loc) and within the frame's data box (dloc), and the fixed-point offsets
 // q = RN(RN(x - RN(k*h)) * 2^F) (== gs_fixq) as w = q + Mbits when magic_ok (the 1.5*2^(52-F)
-// trick: |q| <= 2^51), else q itself.  Returns 0 ok, 1 outside the box, 2 non-finite.
-template <int D, typename T, bool FAST>
+// trick: |q| <= 2^51), else q itself; XP (the fp32 X path of dense tables): w = X = x*2^F, and
+// q = X - Cr (the table sums X, the flush takes count * Cr, bin_cr).  Returns 0 ok, 1 outside
+// the box, 2 non-finite.
+
+// X path: Cr = RHE(RN(k*h) * 2^F) of key k (q = X - Cr)
+__device__ __forceinline__ long long bin_cr(int k, const BinParams& P) {
+  return __double2ll_rn(__dmul_rn(__dmul_rn((double)k, P.h), P.scale));
+}
+
+template <int D, typename T, bool FAST, bool XP>
 __device__ __forceinline__ int bin_point(const T* xc, int64_t pl, const GsImg& im,
                                          const BinParams& P, uint32_t& loc, uint32_t& dloc,
                                          long long* w) {
-  double fl[D], xs[D];
   int rel[D];
+  if constexpr (XP) {  // the X path: w = x*2^F, no fp64 (see make_bin_params)
+    bool fine = true;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      bool f;
+      const float x = (float)xc[c];
+      rel[c] = gs_bin_rel_f32(x, P.ihf, P.Cf[c], P.thr, f);
+      fine &= f & ((fabsf(x) >= P.xmin) | (x == 0.0f));
+      w[c] = __float2ll_rn(__fmul_rn(x, P.s2F));
+    }
+    bool nonfinite = false;
+    if (!fine) {  // rare: the IEEE quotient, and w = q + Cr for an x that is not a multiple of 2^-F
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const double x = (double)xc[c];
+        nonfinite |= !isfinite(x);
+        const double f = floor(gs_ddiv_slow(x, P.h));
+        const double r = __dsub_rn(f, P.kminD[c]);
+        rel[c] = (r > -4.0 && r < 2147483647.0) ? __double2int_rz(r) : -4;
+        const double ck = __dmul_rn(f, P.h);
+        w[c] = __double2ll_rn(__dmul_rn(__dsub_rn(x, ck), P.scale)) +
+               __double2ll_rn(__dmul_rn(ck, P.scale));
+      }
+    }
+    bool bad = false;
+    uint32_t l = 0, dl = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const uint32_t dr = (uint32_t)(rel[c] - GS_APRON);
+      bad |= dr >= P.span[c];
+      l += (uint32_t)rel[c] * P.strd[c];
+      dl += dr * P.dstrd[c];
+    }
+    loc = l;
+    dloc = dl;
+    return nonfinite ? 2 : bad ? 1 : 0;
+  }
+  double fl[D], xs[D];
   bool slow = false;
   if constexpr (FAST) {
     bool fine = true;
@@ -373,7 +445,7 @@ __device__ __forceinline__ int bin_point(const T* xc, int64_t pl, const GsImg& i
     l += (uint32_t)rel[c] * P.strd[c];
     dl += dr * P.dstrd[c];
     const double dd = __dsub_rn(xs[c], __dmul_rn(fl[c], P.h));
-    if (FAST || P.magic_ok)  // (the fast path is only taken with magic_ok)
+    if (FAST || P.magic_ok)  // (the fast key path is only taken with magic_ok)
       w[c] = __double_as_longlong(__dadd_rn(dd, P.Mq));
     else
       w[c] = __double2ll_rn(__dmul_rn(dd, P.scale));
@@ -475,7 +547,8 @@ __device__ __forceinline__ void bin_segment(const T* __restrict__ pts, int64_t s
   uint16_t* __restrict__ slot16 = (uint16_t*)slot + s0;
   uint32_t* __restrict__ slot32 = (uint32_t*)slot + s0;
   const uint32_t B = blockDim.x;
-  const long long off = (FAST || P.magic_ok) ? P.Mbits : 0ll;
+  constexpr bool XP = FAST && DENSE;  // the X path (dense tables; the hash path keeps q)
+  const long long off = (!XP && (FAST || P.magic_ok)) ? P.Mbits : 0ll;
   T xa[RC], xb[RC];
   {
     const uint32_t i = threadIdx.x;
@@ -490,7 +563,7 @@ __device__ __forceinline__ void bin_segment(const T* __restrict__ pts, int64_t s
   auto point = [&](const T* xc, uint32_t i) {
     uint32_t loc, dloc;
     long long w[D];
-    const int st = bin_point<D, T, FAST>(xc, (sizeof(T) == 1 && D > 3) ? fpos0 + i : 0, im, P,
+    const int st = bin_point<D, T, FAST, XP>(xc, (sizeof(T) == 1 && D > 3) ? fpos0 + i : 0, im, P,
                                          loc, dloc, w);
     uint32_t key = EMPTY;
     if (i < cnt) {
@@ -503,7 +576,7 @@ __device__ __forceinline__ void bin_segment(const T* __restrict__ pts, int64_t s
       }
     }
     uint32_t my_cnt;
-    const bool act = warp_runs<D>(key, key != EMPTY, w, off, P.two_piece, my_cnt);
+    const bool act = warp_runs<D>(key, key != EMPTY, w, off, XP || P.two_piece, my_cnt);
     if constexpr (DENSE) {
       if (act) {
         const uint32_t a = ent_s + (rep_off + key) * (4 * EW);
@@ -578,7 +651,8 @@ __device__ __forceinline__ void bin_range(const T* __restrict__ pts, int64_t p0,
   const int reps = P.reps;
   const uint32_t rep_off = DENSE ? (lane % (unsigned)reps) * vd : 0u;
   const uint32_t ent_s = (uint32_t)__cvta_generic_to_shared(ent);
-  const unsigned long long off = (FAST || P.magic_ok) ? (unsigned long long)P.Mbits : 0ull;
+  constexpr bool XP = FAST && DENSE;
+  const unsigned long long off = (!XP && (FAST || P.magic_ok)) ? (unsigned long long)P.Mbits : 0ull;
   // segments: one frame each (the dense table holds one frame; a segment's frame base is one
   // constant), also cut every 2^28 points (32-bit offsets inside a segment)
   int64_t s0 = p0;
@@ -595,16 +669,20 @@ __device__ __forceinline__ void bin_range(const T* __restrict__ pts, int64_t p0,
         for (int r = 0; r < reps; ++r) cn += ent[(size_t)(r * vd + j) * EW];
         if (!cn) continue;
         uint32_t L = fbase, rem = j;
+        int kk[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
           const uint32_t dr = rem / P.dstrd[c];
           rem -= dr * P.dstrd[c];
           L += (dr + GS_APRON) * P.strd[c];
+          kk[c] = (int)dr + GS_APRON + P.kmin32[c];
         }
         atomicAdd(&gcnt[L], cn);
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          unsigned long long sq = 0ull - (unsigned long long)cn * off;  // sum(w) - count * off
+          // sum(w) - count * off (X path: sum(X) - count * Cr)
+          unsigned long long sq = 0ull - (unsigned long long)cn *
+                                             (XP ? (unsigned long long)bin_cr(kk[c], P) : off);
           for (int r = 0; r < reps; ++r) sq += bin_entry_sum(ent + (size_t)(r * vd + j) * EW, c);
           atomicAdd(&gqs[(size_t)L * D + c], sq);
         }
@@ -620,7 +698,7 @@ __device__ __forceinline__ void bin_range(const T* __restrict__ pts, int64_t p0,
 }
 
 template <int D, typename T>
-__global__ void __launch_bounds__(kBinThreads, 1)
+__global__ void __launch_bounds__(kBinThreads, kBinCtas)
     k_bin(const T* __restrict__ pts, int64_t ntot, const __grid_constant__ BinParams P,
           uint32_t* __restrict__ cnt, unsigned long long* __restrict__ qs, void* __restrict__ slot,
           int* err, int img_w, GsBox* __restrict__ pbox_out = nullptr,
@@ -651,11 +729,13 @@ __global__ void __launch_bounds__(kBinThreads, 1)
   bool done = false;
   if constexpr (sizeof(T) == 4) {
     if (P.f32fast) {
-      if (P.dense)
-        bin_range<D, T, true, true>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
-      else
+      if (!P.dense) {
         bin_range<D, T, true, false>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
-      done = true;
+        done = true;
+      } else if (P.xpath) {  // dense tables take the fast keys only with the X path
+        bin_range<D, T, true, true>(pts, p0, p1, im, P, ent, tk, slot, cnt, qs, saw);
+        done = true;
+      }
     }
   }
   if (!done) {

@@ -471,3 +471,36 @@ def test_misaligned_device_input(engine):
                    device_outputs=True)
     ref = engine.run_batch(X, cfg)
     assert np.array_equal(lab.cpu().numpy(), ref.labels)
+
+
+def _xpath_cases():
+    rng = np.random.default_rng(77)
+    # fp32 image-like frame with values below 2^(23-F) (x*2^F not an integer: the slow branch
+    # of the X path), denormals, signed zeros and small negatives (key -1, |x| < h/2)
+    X = rng.uniform(-0.3, 1.0, size=(20000, 3)).astype(np.float32)
+    X[::5, 0] = rng.uniform(0, 2.0 ** -20, size=X[::5, 0].shape).astype(np.float32)
+    X[1::7, 1] = -rng.uniform(0, 2.0 ** -24, size=X[1::7, 1].shape).astype(np.float32)
+    X[2::11, 2] = np.float32(1e-40)
+    X[3::13] = -0.0
+    yield "tiny", X, 0.08
+    # a key box whose RN(k h) 2^F has fraction exactly 1/2 (F = 45, h = 0.5 + 2^-46, k = 1): the
+    # X path is refused and the dense table takes the generic fp64 path
+    Y = rng.uniform(0.0, 3.0, size=(65536, 3)).astype(np.float32)
+    yield "tie_box", Y, 0.5 + 2.0 ** -46
+
+
+@pytest.mark.parametrize("case", list(_xpath_cases()), ids=lambda c: c[0])
+def test_binning_x_path_edges(engine, case):
+    """K2's fp32 X path (dense tables sum x*2^F and take count * RHE(RN(k h) 2^F) at the
+    flush) against the oracle's fixed-point build: its slow branch and its refusal."""
+    name, X, h = case
+    if name == "tie_box":
+        assert G.fixed_shift(len(X), h) == 45
+    g = engine.debug_build(X, h)
+    o = O.build_grid(X.astype(np.float64), h, O.BUILD_FIXED)
+    assert_state_equal(g[:3], o[:3], name)
+    assert np.array_equal(g[3], o[3]), "point -> cell rank differs"
+    r = engine.run(X, G.EngineConfig(h, 30))
+    ro = O.run(X.astype(np.float64), h, 30, O.BUILD_FIXED)
+    assert np.array_equal(r.labels, ro["labels"])
+    assert np.array_equal(_bits(r.centroids), _bits(ro["centroids"]))
