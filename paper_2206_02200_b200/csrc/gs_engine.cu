@@ -155,6 +155,11 @@ struct gs_ctx {
   void* pin = nullptr;
   void* pin_dev = nullptr;
   size_t pin_bytes = 0;
+  // global path: small pinned area for the per-iteration readbacks (plan, packed frame state)
+  void* hpin = nullptr;
+  size_t hpin_bytes = 0;
+  cudaEvent_t ev_plan = nullptr;
+  DevBuf iterpack;  // device side of the packed end-of-iteration readback
   // the control block's zero region is zero (K7 re-zeroes it at the end of every run; any
   // other user of the block, or a run that stopped early, clears this and a memset follows)
   bool ctl_clean = false;
@@ -656,6 +661,22 @@ gs_status launch_nscale(gs_ctx* ctx, const void* dpts, int dtype, int d, int64_t
   return GS_OK;
 }
 
+gs_status ensure_hpin(gs_ctx* ctx, size_t need) {
+  if (need > ctx->hpin_bytes) {
+    if (ctx->hpin) {
+      GS_CK(cudaStreamSynchronize(ctx->stream));
+      cudaFreeHost(ctx->hpin);
+    }
+    ctx->hpin = nullptr;
+    ctx->hpin_bytes = 0;
+    need = std::max<size_t>(need, 4096);
+    GS_CK(cudaHostAlloc(&ctx->hpin, need, cudaHostAllocDefault));
+    ctx->hpin_bytes = need;
+  }
+  if (!ctx->ev_plan) GS_CK(cudaEventCreateWithFlags(&ctx->ev_plan, cudaEventDisableTiming));
+  return GS_OK;
+}
+
 template <int D>
 gs_status launch_sweep_levels_d(gs_ctx* ctx, int64_t m, const int32_t* eoff,
                                 const int32_t* loff) {
@@ -769,29 +790,38 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K, const SweepHalo* 
                                            ctx->ccoff.as<int32_t>(), ctx->ccdesc.as<int32_t>(),
                                            ctx->ccctr.as<long long>());
       GS_LAUNCHED("k_cc_plan");
-      long long plan[3] = {0, 0, 0};
-      GS_CK(cudaMemcpyAsync(plan, ctx->ccctr.p, sizeof(plan), cudaMemcpyDeviceToHost, st));
-      GS_CK(cudaStreamSynchronize(st));
-      const int ncomp = (int)plan[0], maxsz = (int)plan[1];
-      const size_t csm = (size_t)plan[2];
+      // The plan goes to the host while the sweep already runs: k_cc_scatter and k_sweep_comp
+      // read it on the device (CTAs take components by ticket; a plan that does not fit a CTA
+      // makes the launch a no-op), so the host's wait for it overlaps the sweep.
       constexpr size_t kCompBudget = 224 * 1024;
-      if (ncomp == 0) return GS_OK;  // every cell isolated or frozen: Q rows are final (P3)
-      if (csm <= kCompBudget && maxsz < 65535) {
+      GS_TRY(ensure_hpin(ctx, 64));
+      long long* plan = (long long*)ctx->hpin;
+      GS_CK(cudaMemcpyAsync(plan, ctx->ccctr.p, 24, cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaEventRecord(ctx->ev_plan, st));
+      {
         const unsigned mb = blocks_for(m, 256);
         gs::k_cc_scatter<<<mb, 256, 0, st>>>((int)m, root, ctx->ccoff.as<int32_t>(),
                                              ctx->cccur.as<int32_t>(), ctx->ccmem.as<int32_t>());
         GS_LAUNCHED("k_cc_scatter");
         GS_CK(attr_once(done_s, ctx->device, gs::k_sweep_comp<D>, (int)kCompBudget));
-        gs::k_sweep_comp<D><<<(unsigned)ncomp, 256, csm, st>>>(
+        const unsigned cg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, m / 2));
+        gs::k_sweep_comp<D><<<cg, 256, kCompBudget, st>>>(
             (int)m, b, ctx->ccdesc.as<int32_t>(), ctx->ccmem.as<int32_t>(),
             ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>(), ctx->ckey[cur].as<uint32_t>(),
-            ctx->ccnt[cur].as<uint32_t>(), Q);
+            ctx->ccnt[cur].as<uint32_t>(), Q, ctx->ccctr.as<long long>(), (long long)kCompBudget);
         const cudaError_t le = cudaGetLastError();
+        GS_CK(cudaEventSynchronize(ctx->ev_plan));
+        const int ncomp = (int)plan[0], maxsz = (int)plan[1];
+        const size_t csm = (size_t)plan[2];
         if (le == cudaSuccess) {
           GS_LAUNCHED("k_sweep_comp");
-          return GS_OK;
+          if (ncomp == 0) return GS_OK;  // every cell isolated or frozen: Q rows are final (P3)
+          if (csm <= kCompBudget && maxsz < 65535) return GS_OK;
+          // (the launch was a no-op: some component does not fit a CTA)
+        } else {
+          ctx->comp_ok = false;  // cannot be launched here: the cluster sweeps from now on
+          if (ncomp == 0) return GS_OK;
         }
-        ctx->comp_ok = false;  // cannot be launched here: the cluster sweeps from now on
       }
     }
   }
@@ -975,17 +1005,22 @@ gs_status launch_global_sweep(gs_ctx* ctx, int d, int64_t m, int K,
 
 // One iterate_once over all frames (frozen frames excluded).  Cells in buffer `cur`; the new
 // cells land in buffer 1-cur.  Per-frame changed/adjacency/m/disp land in the f* arrays.
-gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
+// defer_mnew: the new cell count stays on the device (the later kernels read it there, their
+// grids sized for m) and the per-iteration accumulators are cleared by k_iter_pack, not here;
+// *mnew_out = -1 and the caller reads the count with the rest of the iteration's state.
+gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out, bool defer_mnew = false) {
   const GsBox& b = ctx->box;
   const int d = b.d;
   const int K = (int)ipow3(d);
   const int cur = ctx->cur, nxt = 1 - cur;
   const int64_t nf = b.nframes;
   cudaStream_t st = ctx->stream;
-  GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, st));
-  GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, st));
-  GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, st));
-  GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, st));
+  if (!defer_mnew) {
+    GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, st));
+  }
   const unsigned mb = blocks_for(m, 256);
   if (d <= 6) {
     // (1) fixed-stride neighbour lists (all SMs), (2) the single-CTA Kahn sweep over L2
@@ -1051,10 +1086,13 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
                                          ctx->sval.as<uint32_t>(), ctx->parent.as<int32_t>(),
                                          ctx->segstart.as<int32_t>());
   GS_LAUNCHED("k_seg");
-  int32_t mnew = 0;
-  GS_CK(cudaMemcpyAsync(&mnew, ctx->sid.as<int32_t>() + (m - 1), sizeof(int32_t),
-                        cudaMemcpyDeviceToHost, ctx->stream));
-  GS_CK(cudaStreamSynchronize(ctx->stream));
+  int32_t mnew = (int32_t)m;  // (deferred: the grids' upper bound)
+  const int32_t* mdev = defer_mnew ? ctx->sid.as<int32_t>() + (m - 1) : nullptr;
+  if (!defer_mnew) {
+    GS_CK(cudaMemcpyAsync(&mnew, ctx->sid.as<int32_t>() + (m - 1), sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CK(cudaStreamSynchronize(ctx->stream));
+  }
   const unsigned nb = blocks_for(mnew, 256);
   switch (d) {
 #define GS_CASE(D)                                                                            \
@@ -1062,7 +1100,8 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
     gs::k_fold<D><<<nb, 256, 0, ctx->stream>>>(                                               \
         mnew, (int)m, ctx->segstart.as<int32_t>(), ctx->skey.as<uint32_t>(),                 \
         ctx->sval.as<uint32_t>(), ctx->ccnt[cur].as<uint32_t>(), ctx->S1.as<double>(),       \
-        ctx->ckey[nxt].as<uint32_t>(), ctx->ccnt[nxt].as<uint32_t>(), ctx->S[nxt].as<double>()); \
+        ctx->ckey[nxt].as<uint32_t>(), ctx->ccnt[nxt].as<uint32_t>(), ctx->S[nxt].as<double>(), \
+        mdev);                                                                                 \
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6)
     GS_CASE(7) GS_CASE(8) GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12)
@@ -1073,7 +1112,7 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
                                                ctx->idx.as<int32_t>());
   GS_LAUNCHED("k_idx_clear");
   gs::k_idx_set<<<nb, 256, 0, ctx->stream>>>(mnew, ctx->ckey[nxt].as<uint32_t>(),
-                                             ctx->idx.as<int32_t>());
+                                             ctx->idx.as<int32_t>(), mdev);
   GS_LAUNCHED("k_idx_set");
   switch (d) {
 #define GS_ADJ(D)                                                                             \
@@ -1081,7 +1120,7 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
     gs::k_adjacent<D><<<nb, 256, 0, ctx->stream>>>(mnew, b, K, ctx->ckey[nxt].as<uint32_t>(), \
                                                    ctx->idx.as<int32_t>(),                    \
                                                    ctx->fdone.as<int32_t>(),                  \
-                                                   ctx->fadj.as<int32_t>());                  \
+                                                   ctx->fadj.as<int32_t>(), mdev);            \
     break;
     GS_ADJ(1) GS_ADJ(2) GS_ADJ(3) GS_ADJ(4) GS_ADJ(5) GS_ADJ(6) GS_ADJ(7) GS_ADJ(8) GS_ADJ(9)
     GS_ADJ(10) GS_ADJ(11) GS_ADJ(12)
@@ -1089,7 +1128,7 @@ gs_status iterate(gs_ctx* ctx, int64_t m, int64_t* mnew_out) {
   }
   GS_LAUNCHED("k_adjacent");
   ctx->cur = nxt;
-  *mnew_out = mnew;
+  *mnew_out = defer_mnew ? -1 : mnew;
   return GS_OK;
 }
 
@@ -1629,34 +1668,45 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
         if (!ctx->h_done[f]) mx = std::max<int64_t>(mx, fcnt[f]);
       return mx;
     };
+    // one packed device->host copy per iteration (new cell count, error bits, per-frame state):
+    // the accumulators start clean here and k_iter_pack leaves them clean
+    GS_CK(cudaMemsetAsync(ctx->fchanged.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fadj.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fm.p, 0, sizeof(int32_t) * nf, st));
+    GS_CK(cudaMemsetAsync(ctx->fdisp.p, 0, sizeof(unsigned long long) * nf, st));
+    const size_t pack_bytes = 16 + 24 * (size_t)nf;
+    GS_TRY(ensure_hpin(ctx, 64 + pack_bytes));
+    GS_TRY(grow(ctx, ctx->iterpack, pack_bytes));
+    int32_t* hpack = (int32_t*)((char*)ctx->hpin + 64);
     while (live > 0 && (force_global || max_live() > ms_cap)) {
       int64_t mnew = 0;
-      GS_TRY(iterate(ctx, m, &mnew));
+      GS_TRY(iterate(ctx, m, &mnew, true));
+      const int32_t* mdev = ctx->sid.as<int32_t>() + (m - 1);
       gs::k_compose<<<blocks_for(m0, 256), 256, 0, st>>>((int)m0, ctx->parent.as<int32_t>(),
                                                           ctx->root.as<int32_t>());
       GS_LAUNCHED("k_compose");
-      gs::k_frame_ranges<<<blocks_for(mnew, 256), 256, 0, st>>>(
-          (int)mnew, b.vol_frame, ctx->ckey[ctx->cur].as<uint32_t>(),
-          ctx->ffirst.as<int32_t>(), ctx->fcount.as<int32_t>());
+      gs::k_frame_ranges<<<blocks_for(m, 256), 256, 0, st>>>(
+          (int)m, b.vol_frame, ctx->ckey[ctx->cur].as<uint32_t>(),
+          ctx->ffirst.as<int32_t>(), ctx->fcount.as<int32_t>(), mdev);
       GS_LAUNCHED("k_frame_ranges");
-      gs::k_frame_counts<<<blocks_for(nf, 256), 256, 0, st>>>(nf, ctx->ffirst.as<int32_t>(),
-                                                              ctx->fcount.as<int32_t>());
-      GS_LAUNCHED("k_frame_counts");
-      GS_CK(cudaMemcpyAsync(fch.data(), ctx->fchanged.p, sizeof(int32_t) * nf,
-                            cudaMemcpyDeviceToHost, st));
-      GS_CK(cudaMemcpyAsync(fadj.data(), ctx->fadj.p, sizeof(int32_t) * nf,
-                            cudaMemcpyDeviceToHost, st));
-      GS_CK(cudaMemcpyAsync(fm.data(), ctx->fm.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
-                            st));
-      GS_CK(cudaMemcpyAsync(fcnt.data(), ctx->fcount.p, sizeof(int32_t) * nf,
-                            cudaMemcpyDeviceToHost, st));
-      GS_CK(cudaMemcpyAsync(fdisp.data(), ctx->fdisp.p, sizeof(unsigned long long) * nf,
-                            cudaMemcpyDeviceToHost, st));
-      int err = 0;
-      GS_TRY(read_err(ctx, &err));
+      gs::k_iter_pack<<<blocks_for(nf, 256), 256, 0, st>>>(
+          nf, ctx->ffirst.as<int32_t>(), ctx->fcount.as<int32_t>(), ctx->fchanged.as<int32_t>(),
+          ctx->fadj.as<int32_t>(), ctx->fm.as<int32_t>(), ctx->fdisp.as<unsigned long long>(),
+          mdev, ctx->errflag.as<int>(), ctx->iterpack.as<int32_t>());
+      GS_LAUNCHED("k_iter_pack");
+      GS_CK(cudaMemcpyAsync(hpack, ctx->iterpack.p, pack_bytes, cudaMemcpyDeviceToHost, st));
+      GS_CK(cudaStreamSynchronize(st));
+      mnew = hpack[0];
+      const int err = hpack[1];
+      std::memcpy(fch.data(), hpack + 4, 4 * (size_t)nf);
+      std::memcpy(fadj.data(), hpack + 4 + nf, 4 * (size_t)nf);
+      std::memcpy(fm.data(), hpack + 4 + 2 * nf, 4 * (size_t)nf);
+      std::memcpy(fcnt.data(), hpack + 4 + 3 * nf, 4 * (size_t)nf);
+      std::memcpy(fdisp.data(), hpack + 4 + 4 * nf, 8 * (size_t)nf);
       if (err & 8) return fail(ctx, GS_E_INTERNAL_INVARIANT, "sweep dataflow watchdog fired");
       if (err & 4) return fail(ctx, GS_E_INTERNAL_INVARIANT, "centroid left the key box");
       ++iter;
+      bool newly_done = false;
       for (int64_t f = 0; f < nf; ++f) {
         if (ctx->h_done[f]) continue;
         swept += fm[f];
@@ -1672,11 +1722,13 @@ gs_status run_impl(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_res
           ctx->h_done[f] = 1;
           ctx->h_conv[f] = conv ? 1 : 0;
           --live;
+          newly_done = true;
         }
       }
       m = mnew;
-      GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
-                            cudaMemcpyHostToDevice, st));
+      if (newly_done)
+        GS_CK(cudaMemcpyAsync(ctx->fdone.p, ctx->h_done.data(), sizeof(int32_t) * nf,
+                              cudaMemcpyHostToDevice, st));
     }
     g_iters = ctx->h_iters;
     GS_CK(cudaMemcpyAsync(ctx->fiters.p, ctx->h_iters.data(), sizeof(int32_t) * nf,
@@ -2292,6 +2344,9 @@ void gs_destroy(gs_ctx* ctx) {
   for (auto& e : ctx->ev_copy)
     if (e) cudaEventDestroy(e);
   if (ctx->pin) cudaFreeHost(ctx->pin);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  if (ctx->ev_plan) cudaEventDestroy(ctx->ev_plan);
+  ctx->iterpack.release();
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);

@@ -1081,6 +1081,7 @@ __global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __res
     ctr[0] = base_c;
     ctr[1] = s_max;
     ctr[2] = (long long)s_need;
+    ctr[3] = 0;  // k_sweep_comp's component ticket
   }
 }
 
@@ -1099,12 +1100,25 @@ template <int D>
 __global__ void __launch_bounds__(256) k_sweep_comp(
     int m, GsBox b, const int32_t* __restrict__ desc, const int32_t* __restrict__ mem,
     const int32_t* __restrict__ bmin, const int32_t* __restrict__ bmax,
-    const uint32_t* __restrict__ ckey, const uint32_t* __restrict__ ccnt, double* Q) {
+    const uint32_t* __restrict__ ckey, const uint32_t* __restrict__ ccnt, double* Q,
+    long long* __restrict__ plan, long long budget) {
   constexpr int K = comp_K<D>(), KE = K / 2;  // offsets t < KE are lex-earlier, t == KE self
   constexpr int CPW = 32 / D;
   extern __shared__ __align__(16) unsigned char csm[];
-  const int off = desc[4 * blockIdx.x], sz = desc[4 * blockIdx.x + 1];
-  const int r0 = desc[4 * blockIdx.x + 2];
+  // The plan is read here, not by the host (which reads it while this kernel runs): CTAs take
+  // components by ticket; a plan that does not fit a CTA makes the whole launch a no-op and
+  // the host, seeing the same plan, runs the cluster sweep instead.
+  const long long ncomp = plan[0];
+  if (ncomp == 0 || plan[1] >= 65535 || plan[2] > budget) return;
+  __shared__ int s_ci;
+  for (;;) {
+  __syncthreads();  // the previous component's shared state is dead
+  if (threadIdx.x == 0) s_ci = (int)atomicAdd((unsigned long long*)&plan[3], 1ull);
+  __syncthreads();
+  const int ci = s_ci;
+  if (ci >= ncomp) return;
+  const int off = desc[4 * ci], sz = desc[4 * ci + 1];
+  const int r0 = desc[4 * ci + 2];
   int blo[D], bst[D];
   int V = 1;
 #pragma unroll
@@ -1228,6 +1242,7 @@ __global__ void __launch_bounds__(256) k_sweep_comp(
     }
     __syncthreads();
   }
+  }  // next component
 }
 
 }  // namespace gs

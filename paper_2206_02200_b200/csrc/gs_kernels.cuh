@@ -996,7 +996,8 @@ __global__ void k_fold(int mnew, int m, const int32_t* __restrict__ segstart,
                        const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sval,
                        const uint32_t* __restrict__ ccnt, const double* __restrict__ S1,
                        uint32_t* __restrict__ okey, uint32_t* __restrict__ ocnt,
-                       double* __restrict__ oS) {
+                       double* __restrict__ oS, const int32_t* __restrict__ mnew_dev = nullptr) {
+  if (mnew_dev) mnew = *mnew_dev;  // the new cell count straight from the scan (no host read)
   int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= mnew) return;
   const int start = segstart[g];
@@ -1063,7 +1064,9 @@ __global__ void k_idx_clear(int m, const uint32_t* __restrict__ key, int32_t* __
   if (i < m) idx[key[i]] = -1;
 }
 
-__global__ void k_idx_set(int m, const uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
+__global__ void k_idx_set(int m, const uint32_t* __restrict__ key, int32_t* __restrict__ idx,
+                          const int32_t* __restrict__ m_dev = nullptr) {
+  if (m_dev) m = *m_dev;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) idx[key[i]] = i;
 }
@@ -1073,7 +1076,8 @@ __global__ void k_idx_set(int m, const uint32_t* __restrict__ key, int32_t* __re
 template <int D>
 __global__ void k_adjacent(int m, GsBox b, int K, const uint32_t* __restrict__ key,
                            const int32_t* __restrict__ idx, const int32_t* __restrict__ fdone,
-                           int32_t* __restrict__ fadj) {
+                           int32_t* __restrict__ fadj, const int32_t* __restrict__ m_dev = nullptr) {
+  if (m_dev) m = *m_dev;
   if constexpr (D <= 6) {
     constexpr int KMAX = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : D == 5 ? 243 : 729;
     constexpr int B = KMAX < 27 ? KMAX : 27;

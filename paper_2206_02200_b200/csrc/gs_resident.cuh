@@ -1058,7 +1058,9 @@ __global__ void __launch_bounds__(512, 1) k_resident(ResidentArgs a) {
 
 // current cell range of every frame (cells are frame-major)
 __global__ void k_frame_ranges(int m, int64_t vol_frame, const uint32_t* __restrict__ key,
-                               int32_t* __restrict__ first, int32_t* __restrict__ count) {
+                               int32_t* __restrict__ first, int32_t* __restrict__ count,
+                               const int32_t* __restrict__ m_dev = nullptr) {
+  if (m_dev) m = *m_dev;
   int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= m) return;
   const int64_t f = key[g] / vol_frame;
@@ -1070,6 +1072,35 @@ __global__ void k_frame_counts(int64_t nf, const int32_t* __restrict__ first,
                                int32_t* __restrict__ count) {
   int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (f < nf) count[f] -= first[f];
+}
+
+// End of a global-path iteration: frame cell counts (k_frame_counts), then everything the host
+// loop reads, packed for ONE device->host copy -- [mnew, err, -, -] then per frame changed,
+// adjacent, swept cells, cell count (int32 each) and the max displacement bits (u64) -- and the
+// per-iteration accumulators cleared for the next iteration.
+__global__ void k_iter_pack(int64_t nf, const int32_t* __restrict__ first, int32_t* __restrict__ count,
+                            int32_t* __restrict__ fchanged, int32_t* __restrict__ fadj,
+                            int32_t* __restrict__ fm, unsigned long long* __restrict__ fdisp,
+                            const int32_t* __restrict__ mnew_dev, const int* __restrict__ err,
+                            int32_t* __restrict__ out) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (f == 0) {
+    out[0] = *mnew_dev;
+    out[1] = *err;
+  }
+  if (f >= nf) return;
+  const int32_t c = count[f] - first[f];
+  count[f] = c;
+  int32_t* o = out + 4;
+  o[f] = fchanged[f];
+  o[nf + f] = fadj[f];
+  o[2 * nf + f] = fm[f];
+  o[3 * nf + f] = c;
+  ((unsigned long long*)(o + 4 * nf))[f] = fdisp[f];
+  fchanged[f] = 0;
+  fadj[f] = 0;
+  fm[f] = 0;
+  fdisp[f] = 0ull;
 }
 
 
