@@ -91,3 +91,20 @@ def test_no_device_is_loud():
         pytest.skip("a device is present")
     with pytest.raises(G.Error):
         G.Engine(0)
+
+
+def test_cmake_project_configures(tmp_path):
+    """The CMake build (CMakeLists.txt: CUDA language, sm_100a only, the gridshift::cuda target a
+    reference-side CMake links) configures with the toolchain in this image; the full build is
+    the same sources and flags as the Makefile's and is not repeated here."""
+    import shutil
+    import subprocess
+    cmake = shutil.which("cmake")
+    if cmake is None or not os.path.exists("/usr/local/cuda/bin/nvcc"):
+        pytest.skip("cmake or nvcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([cmake, "-S", root, "-B", str(tmp_path), "-G", "Ninja"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    ninja = (tmp_path / "build.ninja").read_text()
+    assert "libgridshift_cuda.so" in ninja and "sm_100a" in ninja and "--fmad=false" in ninja

@@ -504,3 +504,31 @@ def test_binning_x_path_edges(engine, case):
     ro = O.run(X.astype(np.float64), h, 30, O.BUILD_FIXED)
     assert np.array_equal(r.labels, ro["labels"])
     assert np.array_equal(_bits(r.centroids), _bits(ro["centroids"]))
+
+
+def _component_clouds():
+    rng = np.random.default_rng(2206)
+    # 600 small separated clumps (3-D, h = 1): far more components of >= 2 cells than SMs, so
+    # k_sweep_comp's CTAs take several components each from the device-side ticket
+    cen = rng.choice(40 ** 3, size=600, replace=False)
+    cen = np.stack([cen // 1600, (cen // 40) % 40, cen % 40], 1) * 6.0
+    many = (cen[:, None, :] + rng.normal(0, 0.7, size=(600, 40, 3))).reshape(-1, 3)
+    yield "many_components", many, 1.0
+    # one connected slab of ~70 K cells next to a few clumps: the plan does not fit a CTA, the
+    # component launch is a no-op and the cluster sweep runs instead
+    slab = rng.uniform(0, 1, size=(400000, 3)) * [260.0, 260.0, 1.0]
+    yield "oversized_component", np.concatenate([slab, many[:4000] + [0, 0, 40.0]]), 1.0
+
+
+@pytest.mark.parametrize("case", list(_component_clouds()), ids=lambda c: c[0])
+def test_component_sweep_tickets_and_fallback(engine, case):
+    """The global path's component sweep reads its plan on the device (the host reads it while
+    the sweep runs): more components than CTAs, and a component too large for a CTA."""
+    name, X, h = case
+    cfg = G.EngineConfig(h, 60, record_history=True, debug_flags=G.GS_DEBUG_GLOBAL_PATH)
+    g = engine.run(X, cfg)
+    o = O.run(X, h, 60, O.BUILD_FIXED)
+    assert g.iterations == o["iterations"], name
+    assert np.array_equal(g.labels, o["labels"]), name
+    assert np.array_equal(_bits(g.centroids), _bits(o["centroids"])), name
+    assert g.history == o["history"], name
