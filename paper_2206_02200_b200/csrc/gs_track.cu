@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(kTrackThreads, 1) k_track(TrackParams P) {
           mxx = max(mxx, x);
           mny = min(mny, y);
           mxy = max(mxy, y);
-          atomicOr(&NB[cell >> 5], 1u << (cell & 31));
+          // (a solid object puts the whole window into a few cells: test before the atomic, so
+          // only the first pixels of a cell pay the same-address serialisation)
+          const unsigned bitm = 1u << (cell & 31);
+          if (!(*(volatile unsigned*)&NB[cell >> 5] & bitm)) atomicOr(&NB[cell >> 5], bitm);
         }
       }
 #pragma unroll
