@@ -632,7 +632,7 @@ gs_status slab_run(gs_dist* D, const gs_input* in, const gs_config* cfg, gs_resu
                                                        RR.mem_idx.as<int32_t>(), c->lab.as<int32_t>());
     GS_DCK(cudaGetLastError());
     GS_DTRY(r, grow(c, c->labels, 4 * (size_t)pc[r]));
-    gs::k_label<<<label_grid(c, pc[r], 1), 256, 0, st>>>(pc[r], 1, c->slot.p,
+    gs::k_label<true><<<label_grid(c, pc[r], 1), 256, 0, st>>>(pc[r], 1, c->slot.p,
                                                           c->dbox.as<GsBox>(), c->lab.as<int32_t>(),
                                                           c->labels.as<int32_t>(), nullptr,
                                                           nullptr, 0, 0);

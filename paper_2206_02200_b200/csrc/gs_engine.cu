@@ -222,6 +222,10 @@ struct gs_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {};
   DevBuf stage[2];
+  // labels of a frame group leave by DMA on their own stream while the next groups run
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t ev_d2h[2] = {};
+  DevBuf lab_stage[2];
   bool grouped = false;
   int64_t group_f0 = 0;
   // predicted key box: the box of the last successful run of this (n, frames, d, dtype, h)
@@ -1312,7 +1316,8 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
   }
-  gs::k_label<<<label_grid(ctx, ntot / nf, nf), 256, 0, st>>>(
+  auto* klab = vf > 65536 ? gs::k_label<true> : gs::k_label<false>;  // (tuning only, see K7)
+  klab<<<label_grid(ctx, ntot / nf, nf), 256, 0, st>>>(
       ntot / nf, nf, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->lab.as<int32_t>(), dlabels,
       ctx->ctl.as<unsigned>(), (unsigned*)ctx->pin_dev, (int)(ctl_bytes(ctx->ctl_nf) / 4),
       (int)(ctl_zero_bytes(ctx->ctl_nf) / 4));
@@ -1876,6 +1881,18 @@ gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_
     for (auto& e : ctx->ev_copy) GS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& b : ctx->stage) GS_TRY(grow(ctx, b, fb * (size_t)gf));
+  // Pinned caller labels: K7 writes a group's labels to a device staging buffer at HBM speed
+  // and the copy engine moves them out on a third stream while later groups are copied in and
+  // run (zero-copy label stores from the SMs made K7 itself PCIe-bound and slowed the
+  // concurrent input copies); pageable labels keep the in-stream copy of run_impl.
+  const bool dma_out = !(cfg->flags & GS_DEVICE_OUTPUTS) && graph_safe(out->labels);
+  if (dma_out) {
+    if (!ctx->d2h_stream) {
+      GS_CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->ev_d2h) GS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (auto& b : ctx->lab_stage) GS_TRY(grow(ctx, b, sizeof(int32_t) * (size_t)n * (size_t)gf));
+  }
   const char* src = static_cast<const char*>(in->points);
   auto stage_in = [&](int64_t g) -> gs_status {
     const int64_t f0 = g0s[g], cnt = gcs[g];
@@ -1917,10 +1934,28 @@ gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_
                 out->converged + f0};
     gs_config c = *cfg;
     c.flags &= ~(uint32_t)(GS_DEBUG_PIPELINE | GS_DEVICE_OUTPUTS);
+    if (dma_out) {
+      // the staging buffer was last drained by group g-2's copy
+      if (g >= 2 && cudaStreamWaitEvent(st, ctx->ev_d2h[g & 1], 0) != cudaSuccess) {
+        s = fail(ctx, GS_E_CUDA, "cudaStreamWaitEvent");
+        break;
+      }
+      r.labels = ctx->lab_stage[g & 1].as<int32_t>();
+      c.flags |= GS_DEVICE_OUTPUTS;
+    }
     if ((s = run_impl(ctx, &sub, &c, &r)) != GS_OK) {
       ctx->err = "frames " + std::to_string((long long)f0) + "-" +
                  std::to_string((long long)(f0 + cnt - 1)) + ": " + ctx->err;
       break;
+    }
+    if (dma_out) {  // (run_impl has synchronised: the group's labels are in the staging buffer)
+      if (cudaMemcpyAsync(out->labels + (size_t)f0 * n, ctx->lab_stage[g & 1].p,
+                          sizeof(int32_t) * (size_t)n * (size_t)cnt, cudaMemcpyDeviceToHost,
+                          ctx->d2h_stream) != cudaSuccess ||
+          cudaEventRecord(ctx->ev_d2h[g & 1], ctx->d2h_stream) != cudaSuccess) {
+        s = fail(ctx, GS_E_CUDA, "label copy");
+        break;
+      }
     }
     // this group's centroids (rows h_ffirst[f] .. + h_k[f] of the final cell buffer)
     int64_t lo = INT64_MAX, hi = 0;
@@ -1962,6 +1997,8 @@ gs_status run_grouped(gs_ctx* ctx, const gs_input* in, const gs_config* cfg, gs_
   }
   ctx->use_graphs = graphs;
   cudaStreamSynchronize(ctx->copy_stream);  // no staging copy outlives the call
+  if (ctx->d2h_stream && cudaStreamSynchronize(ctx->d2h_stream) != cudaSuccess && s == GS_OK)
+    s = fail(ctx, GS_E_CUDA, "label copy");
   if (s != GS_OK) {
     ctx->have_run = false;
     ctx->grouped = false;
@@ -2221,7 +2258,7 @@ extern "C" gs_status gs_mspp_run(gs_ctx* ctx, const gs_input* in, double h, doub
   GS_TRY(ls);
   GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * n));
   int32_t* dl = ctx->labels.as<int32_t>();
-  gs::k_label<<<label_grid(ctx, n, 1), 256, 0, ctx->stream>>>(
+  gs::k_label<false><<<label_grid(ctx, n, 1), 256, 0, ctx->stream>>>(
       n, 1, ctx->slot.p, ctx->dbox.as<GsBox>(), ctx->lab.as<int32_t>(), dl, nullptr, nullptr, 0,
       0);
   GS_LAUNCHED("k_label");
@@ -2343,6 +2380,13 @@ void gs_destroy(gs_ctx* ctx) {
   }
   for (auto& e : ctx->ev_copy)
     if (e) cudaEventDestroy(e);
+  if (ctx->d2h_stream) {
+    cudaStreamSynchronize(ctx->d2h_stream);
+    cudaStreamDestroy(ctx->d2h_stream);
+  }
+  for (auto& e : ctx->ev_d2h)
+    if (e) cudaEventDestroy(e);
+  for (auto& b : ctx->lab_stage) b.release();
   if (ctx->pin) cudaFreeHost(ctx->pin);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   if (ctx->ev_plan) cudaEventDestroy(ctx->ev_plan);

@@ -1136,6 +1136,9 @@ __global__ void k_compose(int m0, const int32_t* __restrict__ parent, int32_t* _
 // hands the run's control block to the host: it stores the words into mapped pinned memory (no
 // copy node, ~12 us per run on the graph path) and then re-zeroes the part every run starts
 // from zero, so the next run needs no memset node either.
+// WIDE picks the tuned path (false: u16 frame-local slots of image frames; true: u32 global
+// slots of clouds); either instantiation is correct for either slot width (scalar fallback).
+template <bool WIDE>
 __global__ void __launch_bounds__(256) k_label(int64_t n, int64_t nf, const void* __restrict__ slot,
                                                const GsBox* __restrict__ pb,
                                                const int32_t* __restrict__ lab,
@@ -1157,10 +1160,11 @@ __global__ void __launch_bounds__(256) k_label(int64_t n, int64_t nf, const void
   // flight (their slot loads issued before any gather): one load per lane left the kernel
   // latency-bound (long_scoreboard 95 % of the stalls, 4.5 TB/s)
   const bool vec = s16 && (n % 4) == 0 && (((uintptr_t)slot | (uintptr_t)labels) & 15) == 0;
+  const bool vec32 = !s16 && (n % 4) == 0 && (((uintptr_t)slot | (uintptr_t)labels) & 15) == 0;
   for (int64_t f = blockIdx.y; f < nf; f += gridDim.y) {
     const int64_t p0 = f * n;
     const uint32_t fbase = (uint32_t)(f * vf);
-    if (vec) {
+    if (!WIDE && vec) {
       const uint2* s4 = reinterpret_cast<const uint2*>((const uint16_t*)slot + p0);
       int4* o4 = reinterpret_cast<int4*>(labels + p0);
       const int64_t n4 = n / 4;
@@ -1171,6 +1175,25 @@ __global__ void __launch_bounds__(256) k_label(int64_t n, int64_t nf, const void
       int64_t i = tid;
       for (; i + 3 * nth < n4; i += 4 * nth) {
         const uint2 w0 = __ldcs(&s4[i]), w1 = __ldcs(&s4[i + nth]), w2 = __ldcs(&s4[i + 2 * nth]),
+                    w3 = __ldcs(&s4[i + 3 * nth]);
+        put(i, w0);
+        put(i + nth, w1);
+        put(i + 2 * nth, w2);
+        put(i + 3 * nth, w3);
+      }
+      for (; i < n4; i += nth) put(i, __ldcs(&s4[i]));
+    } else if (WIDE && vec32) {
+      // u32 slots (global cell indices: clouds): the same shape -- 16-byte slot loads, four
+      // groups in flight, 16-byte label stores (one scalar chain per lane ran at 1.7 TB/s)
+      const uint4* s4 = reinterpret_cast<const uint4*>((const uint32_t*)slot + p0);
+      int4* o4 = reinterpret_cast<int4*>(labels + p0);
+      const int64_t n4 = n / 4;
+      auto put = [&](int64_t i, const uint4& w) {
+        o4[i] = make_int4(__ldg(&lab[w.x]), __ldg(&lab[w.y]), __ldg(&lab[w.z]), __ldg(&lab[w.w]));
+      };
+      int64_t i = tid;
+      for (; i + 3 * nth < n4; i += 4 * nth) {
+        const uint4 w0 = __ldcs(&s4[i]), w1 = __ldcs(&s4[i + nth]), w2 = __ldcs(&s4[i + 2 * nth]),
                     w3 = __ldcs(&s4[i + 3 * nth]);
         put(i, w0);
         put(i + nth, w1);
