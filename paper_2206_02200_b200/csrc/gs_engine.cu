@@ -1311,7 +1311,10 @@ gs_status launch_tail(gs_ctx* ctx, const gs_config* cfg, int64_t nf, int64_t nto
   // ---- labels: K8 wrote lab[initial cell key] = final frame-local id; label[p] = lab[slot[p]]
   //      (straight into pinned caller memory when it is graph-safe host memory)
   int32_t* dlabels = user_labels;
-  const bool direct = dev_out || graph_safe(user_labels);
+  // (large label arrays leave by DMA: the copy engine's bursts beat SM-issued stores over the
+  // bus, as for the inputs past kZeroCopyMaxBytes)
+  const bool direct = dev_out || (graph_safe(user_labels) &&
+                                  sizeof(int32_t) * (size_t)ntot <= (size_t(16) << 20));
   if (!direct) {
     GS_TRY(grow(ctx, ctx->labels, sizeof(int32_t) * ntot));
     dlabels = ctx->labels.as<int32_t>();
