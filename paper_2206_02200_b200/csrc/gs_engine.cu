@@ -771,7 +771,7 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K, const SweepHalo* 
       GS_TRY(grow(ctx, ctx->ccsize, 4 * (size_t)m * D));  // box max corners (per root)
       GS_TRY(grow(ctx, ctx->ccgs, 4 * (size_t)m));        // component sizes (per root)
       GS_TRY(grow(ctx, ctx->ccdesc, 16 * (size_t)m));
-      GS_TRY(grow(ctx, ctx->ccctr, 32));
+      GS_TRY(grow(ctx, ctx->ccctr, 64));
       int32_t* root = ctx->ccpar.as<int32_t>();
       static std::atomic<uint64_t> done_s{0};
       const unsigned mb0 = blocks_for(m, 256);
@@ -789,10 +789,11 @@ gs_status launch_global_sweep_d(gs_ctx* ctx, int64_t m, int K, const SweepHalo* 
                                              ctx->ccgs.as<int32_t>(), ctx->ccloc.as<int32_t>(),
                                              ctx->ccsize.as<int32_t>());
       GS_LAUNCHED("k_cc_count");
-      gs::k_cc_plan<D><<<1, 1024, 0, st>>>((int)m, ctx->ccgs.as<int32_t>(),
-                                           ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>(),
-                                           ctx->ccoff.as<int32_t>(), ctx->ccdesc.as<int32_t>(),
-                                           ctx->ccctr.as<long long>());
+      GS_CK(cudaMemsetAsync(ctx->ccctr.p, 0, 48, st));
+      gs::k_cc_plan_par<D><<<mb0, 256, 0, st>>>(
+          (int)m, ctx->ccgs.as<int32_t>(), ctx->ccloc.as<int32_t>(), ctx->ccsize.as<int32_t>(),
+          ctx->ccoff.as<int32_t>(), ctx->ccdesc.as<int32_t>(),
+          ctx->ccctr.as<unsigned long long>());
       GS_LAUNCHED("k_cc_plan");
       // The plan goes to the host while the sweep already runs: k_cc_scatter and k_sweep_comp
       // read it on the device (CTAs take components by ticket; a plan that does not fit a CTA

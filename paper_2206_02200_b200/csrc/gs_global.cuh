@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(512, 1) k_sweep_flow(
 //   k_cc_init / k_cc_jump / k_cc_hook / k_cc_count   union-find over each cell's lex-earlier
 //                neighbours (the lists of k_nbr_lists) in global memory on all SMs; roots,
 //                component sizes and bounding boxes
-//   k_cc_plan    one CTA: offsets of the components of >= 2 cells, count, largest
+//   k_cc_plan_par offsets of the components of >= 2 cells, count, largest (block scans + atomics)
 //                shared-memory need (cells + bounding box)
 //   k_cc_scatter member lists per component (any order: the sweep's result does not depend on
 //                the order of a level's cells)
@@ -987,102 +987,84 @@ __global__ void k_cc_count(int m, GsBox b, const uint32_t* __restrict__ ckey, in
   if (in) __stcg(&par[i], r);  // (roots are final: compress)
 }
 
-// one CTA: components of >= 2 cells in root order -> coff (per root, -1 otherwise), desc[c] =
-// {offset, size, root, -}; ctr[0] = components, ctr[1] = largest size, ctr[2] = largest
-// shared-memory need of k_sweep_comp.  The sizes stream through shared memory in chunks of
-// 8 per thread (coalesced loads), each thread scanning 8 consecutive roots.
+// The plan: components of >= 2 cells -> coff (per root, -1 otherwise), desc[c] = {offset, size,
+// root, -}; ctr[0] = components, ctr[1] = largest size, ctr[2] = largest shared-memory need of
+// k_sweep_comp, ctr[3] = its component ticket, ctr[4] = cells in components (the member array's
+// fill); ctr is zeroed before the launch.  On all SMs (r2, session 4; one CTA scanning all roots
+// took 19 us on cfg5): the offsets only have to be disjoint, not in root order (member lists in
+// any order give the same sweep), so every block scans its 256 roots and takes its share of the
+// member array and of the descriptor list with two atomics.
 template <int D>
-__global__ void __launch_bounds__(1024, 1) k_cc_plan(int m, const int32_t* __restrict__ gsize,
-                                                      const int32_t* __restrict__ bmin,
-                                                      const int32_t* __restrict__ bmax,
-                                                      int32_t* __restrict__ coff,
-                                                      int32_t* __restrict__ desc,
-                                                      long long* __restrict__ ctr) {
-  constexpr int PER = 8;
-  __shared__ int s_a[64], s_b[64], s_g[1024 * PER];
-  __shared__ unsigned long long s_need;
-  __shared__ int s_max;
-  const int T = blockDim.x, tid = threadIdx.x;
-  if (tid == 0) {
-    s_need = 0;
-    s_max = 0;
+__global__ void __launch_bounds__(256) k_cc_plan_par(int m, const int32_t* __restrict__ gsize,
+                                                     const int32_t* __restrict__ bmin,
+                                                     const int32_t* __restrict__ bmax,
+                                                     int32_t* __restrict__ coff,
+                                                     int32_t* __restrict__ desc,
+                                                     unsigned long long* __restrict__ ctr) {
+  __shared__ int s_v[8], s_c[8];
+  __shared__ int s_base_off, s_base_c;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int i = blockIdx.x * blockDim.x + tid;
+  const int sz = i < m ? gsize[i] : 0;
+  const bool comp = sz >= 2;
+  long long box = 1;
+  if (comp) {
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      box *= (long long)(bmax[(size_t)i * D + q] - bmin[(size_t)i * D + q] + 3);
   }
-  int base_off = 0, base_c = 0;
-  for (int c0 = 0; c0 < m; c0 += T * PER) {
-    for (int k = tid; k < T * PER; k += T) s_g[k] = c0 + k < m ? gsize[c0 + k] : 0;
-    __syncthreads();
-    int v = 0, cf = 0;
+  int xv = comp ? sz : 0, xc = comp ? 1 : 0;
+  const int v = xv, cf = xc;
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int sz = s_g[tid * PER + k];
-      if (sz >= 2) {
-        v += sz;
-        ++cf;
-      }
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, xv, o), b2 = __shfl_up_sync(0xffffffffu, xc, o);
+    if (lane >= o) {
+      xv += a;
+      xc += b2;
     }
-    // block scan of (v, cf): warp shuffles, then the warp totals by warp 0
-    const int lane = tid & 31, wid = tid >> 5;
-    int xv = v, xc = cf;
+  }
+  if (lane == 31) {
+    s_v[wid] = xv;
+    s_c[wid] = xc;
+  }
+  unsigned long long need = comp ? (unsigned long long)sweep_comp_smem<D>(sz, box) : 0ull;
+  int mx = comp ? sz : 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, xv, o), b2 = __shfl_up_sync(0xffffffffu, xc, o);
-      if (lane >= o) {
-        xv += a;
-        xc += b2;
-      }
-    }
-    if (lane == 31) {
-      s_a[wid] = xv;
-      s_b[wid] = xc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      int a = lane < (T >> 5) ? s_a[lane] : 0, b2 = lane < (T >> 5) ? s_b[lane] : 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncthreads();
+  int pv = 0, pc = 0, tv = 0, tc = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int pa = __shfl_up_sync(0xffffffffu, a, o), pb = __shfl_up_sync(0xffffffffu, b2, o);
-        if (lane >= o) {
-          a += pa;
-          b2 += pb;
-        }
-      }
-      s_a[32 + lane] = a;  // inclusive warp prefixes
-      s_b[32 + lane] = b2;
+  for (int w = 0; w < 8; ++w) {
+    if (w < wid) {
+      pv += s_v[w];
+      pc += s_c[w];
     }
-    __syncthreads();
-    int off = base_off + (wid ? s_a[32 + wid - 1] : 0) + xv - v;
-    int c = base_c + (wid ? s_b[32 + wid - 1] : 0) + xc - cf;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = c0 + tid * PER + k;
-      if (i >= m) break;
-      const int sz = s_g[tid * PER + k];
-      coff[i] = sz >= 2 ? off : -1;
-      if (sz >= 2) {
-        long long box = 1;
-#pragma unroll
-        for (int q = 0; q < D; ++q)
-          box *= (long long)(bmax[(size_t)i * D + q] - bmin[(size_t)i * D + q] + 3);
-        desc[4 * c] = off;
-        desc[4 * c + 1] = sz;
-        desc[4 * c + 2] = i;
-        desc[4 * c + 3] = 0;
-        atomicMax(&s_max, sz);
-        atomicMax(&s_need, (unsigned long long)sweep_comp_smem<D>(sz, box));
-        off += sz;
-        ++c;
-      }
-    }
-    base_off += s_a[32 + (T >> 5) - 1];
-    base_c += s_b[32 + (T >> 5) - 1];
-    __syncthreads();
+    tv += s_v[w];
+    tc += s_c[w];
   }
   if (tid == 0) {
-    ctr[0] = base_c;
-    ctr[1] = s_max;
-    ctr[2] = (long long)s_need;
-    ctr[3] = 0;  // k_sweep_comp's component ticket
+    s_base_off = tc ? (int)atomicAdd(&ctr[4], (unsigned long long)tv) : 0;
+    s_base_c = tc ? (int)atomicAdd(&ctr[0], (unsigned long long)tc) : 0;
   }
+  if (lane == 0 && mx) {
+    atomicMax(&ctr[1], (unsigned long long)mx);
+    atomicMax(&ctr[2], need);
+  }
+  __syncthreads();
+  if (i >= m) return;
+  if (!comp) {
+    coff[i] = -1;
+    return;
+  }
+  const int off = s_base_off + pv + xv - v, c = s_base_c + pc + xc - cf;
+  coff[i] = off;
+  desc[4 * c] = off;
+  desc[4 * c + 1] = sz;
+  desc[4 * c + 2] = i;
+  desc[4 * c + 3] = 0;
 }
 
 __global__ void k_cc_scatter(int m, const int32_t* __restrict__ root,
